@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 ORCA step (arXiv 1908.10107) -- prints ONE JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config uniform_1m] [--impl ours|reference]
+
+Metric (BASELINE.json): agent-updates/s (and ms/frame) of the full per-timestep ORCA
+update (binning -> 3x3 k-nearest -> half-planes -> LP2/LP3 -> integrate), i.e. one
+"step" = one pass of every hot-path stage over all agents.
+
+Timing: W untimed warm-up steps; then K timed steps, each bracketed by CUDA
+events on the library's own stream, with an L2 flush (a 512 MiB write) between timed
+steps because the 1M-agent working set (~56 MB) would otherwise stay L2-resident; barrier
++ synchronize around the timed region; max over ranks.  `e2e` repeats the metric through
+the public C-ABI with pinned HOST buffers (orca_set_agents H2D -> orca_step ->
+orca_get_state D2H every step).  `cpu_baseline` / `--impl reference` time the fp64 oracle
+(test infrastructure) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SMS = 148
+FP32_LANES_PER_SM = 128  # B200: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md / DESIGN.md §7)
+
+# algorithmic fp32 lane-ops per counted unit
+OPS = dict(cand=5, lines=40, checks=4, lp1=8, proj=10)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="uniform_1m")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return None
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(config):
+    from paper_1908_10107_b200 import workloads as W
+    w = W.make(config)
+    rho = {"uniform": 0.25, "uniform_1m": 0.25, "dense": 0.5, "uniform_4m": 0.25}.get(config)
+    return w, rho
+
+
+def oracle_rate(w, seconds, rng_seed=0):
+    """fp64 oracle (single thread) on a bounded random sample of agents of the same
+    workload state; returns (agents/s, sample size, elapsed)."""
+    from oracle import oracle as O
+    p = O.make_params(**w["params"])
+    n = len(w["pos"])
+    rng = np.random.default_rng(rng_seed)
+    probe = np.sort(rng.choice(n, min(n, 2000), replace=False))
+    t0 = time.perf_counter()
+    O.step(p, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"), pref_speed=w.get("pref_speed", 1.0),
+           agents=probe)
+    t1 = time.perf_counter() - t0
+    m = int(min(n, max(2000, len(probe) * seconds / max(t1, 1e-6))))
+    sample = np.sort(rng.choice(n, m, replace=False))
+    t0 = time.perf_counter()
+    O.step(p, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"), pref_speed=w.get("pref_speed", 1.0),
+           agents=sample)
+    el = time.perf_counter() - t0
+    return m / el, m, el
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    w, rho = workload(args.config)
+    n = len(w["pos"])
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_rate(w, per_step / 4)
+    rates, samples, els = [], [], []
+    for s in range(args.steps):
+        r, m, el = oracle_rate(w, per_step, rng_seed=s + 1)
+        rates.append(r)
+        samples.append(m)
+        els.append(el)
+    value = float(np.sum(samples) / np.sum(els))
+    line = {
+        "impl": "reference", "metric": "agent-updates/s", "value": value, "unit": "agent-updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * n / value, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w["name"], "n_agents": n, "rho": rho, **w["params"]},
+        "cpu_baseline": {"value": value, "unit": "agent-updates/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{int(np.mean(samples))} random agents of the {n}-agent state per step "
+                                   f"(one step each, full-state bins), single thread"},
+        "e2e": {"value": value, "unit": "agent-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or world == 1, "launch N>1 with torchrun"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1908_10107_b200 import build as B
+    if rank == 0:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    from paper_1908_10107_b200 import orca
+
+    w, rho = workload(args.config)
+    n_total = len(w["pos"])
+    if world > 1:
+        nid = orca.nccl_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(nid), dtype=torch.uint8, device="cuda")
+        dist.broadcast(t, 0)
+        ctx = orca.Orca(w["params"], device=local, rank=rank, world=world, nccl_id=bytes(t.cpu().tolist()))
+    else:
+        ctx = orca.Orca(w["params"], device=local)
+    ctx.set_agents(w["pos"], w["vel"], w["pref"])
+    if w.get("goals") is not None:
+        ctx.set_goals(w["goals"], w["pref_speed"])
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    # ---- warm-up (also instantiates the 1-step and K-step graphs outside the timed region)
+    for _ in range(args.warmup):
+        ctx.step(1)
+    ctx.step(min(args.steps, 64))
+    barrier()
+    work0 = ctx.work()
+    ctx.reset_stats()
+
+    # ---- timed region: K steps, L2 flushed between steps, events on the library stream
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    with Clocks(local) as clk:
+        with torch.cuda.stream(stream):
+            for s in range(args.steps):
+                flush.zero_()
+                evs[s][0].record(stream)
+                ctx.step(1)
+                evs[s][1].record(stream)
+        barrier()
+    ms = float(sum(a.elapsed_time(b) for a, b in evs))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    st = ctx.stats()
+    ms_per_step = ms / args.steps
+    value = n_total * args.steps / (ms / 1000.0)
+
+    # ---- L2-resident variant (context): K steps in one graph, no flush
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        ctx.step(args.steps)
+        e1.record(stream)
+    barrier()
+    ms_res = e0.elapsed_time(e1) / args.steps
+
+    # ---- per-kernel times (un-graphed, events around every launch, L2 flushed between)
+    stage = np.zeros(4)
+    for s in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        stage += np.array(ctx.step_timed(1))
+    stage /= args.steps
+    work1 = ctx.work()
+    work = {k: 0.5 * (work0[k] + work1[k]) for k in work0}
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if world == 1:
+        hp = torch.from_numpy(w["pos"]).pin_memory()
+        hv = torch.from_numpy(w["vel"]).pin_memory()
+        hq = torch.from_numpy(w["pref"]).pin_memory()
+        op = torch.empty_like(hp).pin_memory()
+        ov = torch.empty_like(hv).pin_memory()
+        ctx.set_agents(hp, hv, hq)
+        ctx.step(1)
+        ctx.get_state(op, ov)
+        ne = max(1, args.e2e_steps)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(ne):
+            ctx.set_agents(hp, hv, hq)
+            ctx.step(1)
+            ctx.get_state(op, ov)
+        el = time.perf_counter() - t0
+        e2e = {"value": n_total * ne / el, "unit": "agent-updates/s",
+               "h2d_bytes_per_step": int(hp.numel() * 4 * 3), "d2h_bytes_per_step": int(op.numel() * 4 * 2),
+               "ms_per_step": 1000.0 * el / ne}
+
+    # ---- roofline of the dominant kernel (k_step): ALU bound
+    pk, pk_kind = peaks()
+    ops = sum(OPS[k] * work[k] for k in OPS)
+    t_step = stage[0] / 1000.0
+    achieved = ops / t_step / 1e12
+    peak = SMS * FP32_LANES_PER_SM * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config, {}).get("k_step_dram_bytes")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": "k_step", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_source": f"148 SMs x 128 FP32 lanes x sm_max_mhz ({pk_kind} MEASURED_PEAKS.json)",
+                "ops_per_launch": ops, "work_per_launch": work,
+                "stage_ms": {"k_step": stage[0], "k_scan": stage[1], "k_scatter": stage[2]}}
+    # HBM view of the binning kernels (context)
+    hbm_bytes_scatter = n_total / world * (4 + 4 + 4 + 3 * 8 + 4 + 3 * 8 + 4)
+    hbm = {"kernel": "k_scatter", "achieved_gbs": hbm_bytes_scatter / (stage[2] / 1000.0) / 1e9 if stage[2] > 0 else None,
+           "peak_gbs": pk.get("hbm_gbs"), "bytes_per_launch": hbm_bytes_scatter}
+
+    line = {
+        "metric": "agent-updates/s", "value": value, "unit": "agent-updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": w["name"], "n_agents": n_total, "rho": rho, **w["params"],
+                   "l2": "flushed between timed steps (512 MiB write); per-step CUDA events on the library stream",
+                   "parallelism": f"strips{world}" if world > 1 else "single"},
+        "ms_per_step_l2_resident": ms_res,
+        "gpu_launches": 3 * args.steps,
+        "roofline": roofline, "hbm_context": hbm,
+        "stats": st,
+    }
+    line["e2e"] = e2e
+    if rank == 0:
+        c = clk.summary()
+        line["clocks"] = c
+        if world == 1 and not args.no_cpu_baseline:
+            r, m, el = oracle_rate(w, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": r, "unit": "agent-updates/s", "cores": 1, "kind": "oracle",
+                                    "sample": f"{m} random agents of the initial {n_total}-agent state, one step, "
+                                              f"single thread, {el:.1f} s"}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

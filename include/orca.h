@@ -1,0 +1,182 @@
+/*
+ * orca.h -- C ABI of liborca, the B200-native (sm_100a) ORCA crowd step.
+ *
+ * What it computes (arXiv 1908.10107, PAPER.md; "P:NN" = PAPER.md line NN):
+ *   one synchronous time step of the ORCA agent update (§3):
+ *     1. spatial binning of agents into a uniform grid of cell size r_obs (FLAME messages
+ *        organised into spatial bins, Fig. 2 caption P:94);
+ *     2. each agent reads its own and the 8 surrounding bins and keeps the k nearest
+ *        agents strictly within r_obs, in (distance, id) order;
+ *     3. one ORCA half-plane per observed neighbour (Fig. 1(b)-(c));
+ *     4. the closest permitted velocity to the preferred one by an incremental 2-D LP
+ *        (P:82-86), or the least-penetrating velocity when infeasible;
+ *     5. explicit integration p' = p + dt v'.
+ *   The cited ORCA geometry and every reading of a silent/garbled passage are listed in
+ *   DESIGN.md §3.  No buffer or argument here carries a torch type.
+ *
+ * Conventions (all entry points):
+ *   - Every function returns orca_status (0 = OK) except orca_destroy / orca_status_string
+ *     / orca_last_error.  No C++ exception crosses the ABI.
+ *   - Vectors are float32 x,y interleaved: "float[2n]" means n agents, element 2i = x of
+ *     agent i, 2i+1 = y.  Agent id = index in the orca_set_agents arrays.
+ *   - Pointer arguments may be HOST (pageable or pinned) or DEVICE (CUDA, same device as
+ *     the context) memory; the library dispatches through unified addressing.  The library
+ *     copies inputs (the caller keeps ownership of its buffers) and writes outputs into
+ *     caller-allocated buffers.
+ *   - A context is used by one host thread at a time.  orca_step is asynchronous on the
+ *     context's stream; every getter synchronises that stream.
+ *   - On error, orca_last_error() returns a thread-local human-readable message.
+ */
+#ifndef ORCA_H
+#define ORCA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------------------ */
+typedef int32_t orca_status;
+#define ORCA_OK 0
+#define ORCA_ERR_INVALID_ARGUMENT 1 /* bad parameter, NaN/Inf input, null pointer */
+#define ORCA_ERR_NOT_READY 2        /* step/get before set_agents */
+#define ORCA_ERR_OUT_OF_MEMORY 3    /* cudaMalloc failed */
+#define ORCA_ERR_CUDA 4             /* any other CUDA runtime error */
+#define ORCA_ERR_NCCL 5             /* NCCL error (multi-GPU contexts) */
+#define ORCA_ERR_CAPACITY 6         /* grid / halo / migration buffer too small */
+#define ORCA_ERR_INTERNAL 7
+
+/* Largest supported maxNeighbors (compile-time bound of the per-agent LP). */
+#define ORCA_MAX_K 32
+
+/* ---- parameters (BASELINE.json north_star order) ------------------------------------ *
+ * timeStep      dt > 0, seconds: integration step ("simulation iteration").
+ * neighborDist  r_obs > 0, metres: observation radius (Fig. 2 caption); it is also
+ *               the grid cell size, so the 3x3 bins cover the r_obs disc.
+ * maxNeighbors  k in [0, ORCA_MAX_K]: at most k nearest neighbours give half-planes.
+ * timeHorizon   tau > 0, seconds: lookahead of the velocity obstacle (Fig. 1(b)).
+ * radius        r > 0, metres: agent radius, global (Fig. 1(a)); R = 2r per pair.
+ * maxSpeed      >= 0, m/s: speed cap |v| <= maxSpeed ("capped maximum speed").
+ * All finite. */
+typedef struct {
+    float timeStep;
+    float neighborDist;
+    int32_t maxNeighbors;
+    float timeHorizon;
+    float radius;
+    float maxSpeed;
+} orca_params;
+
+typedef struct orca_ctx orca_ctx; /* opaque, library-owned */
+
+/* Per-context counters accumulated over all steps since creation / the last reset. */
+typedef struct {
+    int64_t steps;          /* orca_step iterations executed */
+    int64_t agent_updates;  /* sum over steps of the agent count */
+    int64_t infeasible;     /* agent-steps whose LP2 failed -> LP3 */
+    int64_t degenerate;     /* agent-steps with a g1 or g2 event (DESIGN.md §3 Q15/Q9) */
+    int64_t coincident;     /* g1: collision branch with w == 0 (Q15) */
+    int64_t eps_parallel;   /* g2: an LP pair with |det| <= 1e-5 (Q9) */
+    int64_t marginal;       /* g3: infeasible with max penetration < 1e-6 (reported only) */
+    int64_t collision_pairs;/* neighbour pairs that took the collision branch (Q4) */
+} orca_stats;
+
+/* ---- lifecycle -------------------------------------------------------------------- */
+
+/* Create a single-GPU context on CUDA device `device` (its own non-blocking stream).
+ * Errors: INVALID_ARGUMENT (params out of range, out == NULL), CUDA. */
+orca_status orca_create(const orca_params *params, int32_t device, orca_ctx **out);
+
+/* Release all device memory, graphs and the stream.  NULL is a no-op. */
+void orca_destroy(orca_ctx *ctx);
+
+/* ---- state ------------------------------------------------------------------------ */
+
+/* Load n >= 0 agents (copied).  pos, vel, prefVel: float[2n] (x,y interleaved); prefVel
+ * is the preferred velocity held constant over steps (reading Q16) unless orca_set_goals
+ * is called afterwards.  Freezes the grid: origin = fl32(min - r_obs) per axis, dims =
+ * floor((max - origin)/r_obs) + 2 (reading Q12); later positions outside are clamped to
+ * edge cells.  Bins the agents.  Clears any goals.
+ * Errors: INVALID_ARGUMENT (n < 0, NULL with n > 0, NaN/Inf), CAPACITY (grid larger than
+ * 2^28 cells), OUT_OF_MEMORY, CUDA. */
+orca_status orca_set_agents(orca_ctx *ctx, int64_t n, const float *pos, const float *vel,
+                            const float *prefVel);
+
+/* Goal seeking ("The agent's velocity is in the direction of the goal location,
+ * scaled to the walking speed"): goal float[2n] by id; from the next step on, the
+ * preferred velocity is recomputed every step as g*min(1, prefSpeed/|g|), g = goal - pos.
+ * Errors: NOT_READY, INVALID_ARGUMENT (NULL, NaN/Inf, prefSpeed < 0). */
+orca_status orca_set_goals(orca_ctx *ctx, const float *goal, float prefSpeed);
+
+/* Enqueue n_steps >= 0 synchronous steps on the context stream (one CUDA graph replay;
+ * no host synchronisation).  Errors: NOT_READY, INVALID_ARGUMENT, CUDA, NCCL. */
+orca_status orca_step(orca_ctx *ctx, int32_t n_steps);
+
+/* Current positions / velocities in id order into caller buffers float[2n] (either may
+ * be NULL).  Synchronises.  Errors: NOT_READY, CUDA. */
+orca_status orca_get_state(orca_ctx *ctx, float *pos, float *vel);
+
+/* Number of agents currently held (multi-GPU: held by this rank). */
+orca_status orca_get_count(orca_ctx *ctx, int64_t *n);
+
+/* ---- introspection (tests / bench; not needed for simulation) ----------------------- */
+
+/* Frozen grid: origin[2] (fp32 values widened to double), cell size, dims {nx, ny}. */
+orca_status orca_get_grid(orca_ctx *ctx, double origin[2], float *cs, int32_t dims[2]);
+
+/* Cell (cx, cy) of every agent for the current state, id order, int32[n] each. */
+orca_status orca_debug_cells(orca_ctx *ctx, int32_t *cx, int32_t *cy);
+
+/* Compute (but do NOT apply) the next step for the current state, id order:
+ * vnew float[2n] (nullable), flags uint8[n] (nullable; bit0 infeasible, bit1 g1
+ * coincident, bit2 g2 eps-parallel, bit3 g3 marginal), nbr int32[n*k] neighbour ids in
+ * (distance, id) order padded with -1 (nullable), cnt int32[n] (nullable).
+ * Runs the same device code as orca_step.  Synchronises. */
+orca_status orca_debug_step(orca_ctx *ctx, float *vnew, uint8_t *flags, int32_t *nbr,
+                            int32_t *cnt);
+
+/* Work of one step on the current state, counted by an instrumented dry run of the same
+ * kernel (not applied): out[0] candidates read from the 3x3 bins, out[1] half-planes
+ * built, out[2] LP constraint checks, out[3] LP1 inner iterations, out[4] LP3 projected
+ * lines.  Used for the ALU roofline.  Synchronises. */
+orca_status orca_debug_work(orca_ctx *ctx, int64_t out[5]);
+
+/* Counters (synchronises).  orca_reset_stats zeroes them. */
+orca_status orca_get_stats(orca_ctx *ctx, orca_stats *out);
+orca_status orca_reset_stats(orca_ctx *ctx);
+
+/* The context's cudaStream_t (as void*), e.g. for CUDA-event timing by the caller. */
+orca_status orca_get_stream(orca_ctx *ctx, void **stream);
+
+/* Per-stage device time of the last orca_step_timed call, milliseconds:
+ * ms[0] = step kernel (query+ORCA+LP+integrate+hash), ms[1] = scan, ms[2] = scatter,
+ * ms[3] = exchange (multi-GPU).  orca_step_timed runs n_steps un-graphed with CUDA events
+ * around every launch on the context stream and synchronises. */
+orca_status orca_step_timed(orca_ctx *ctx, int32_t n_steps, double ms[4]);
+
+/* ---- errors ----------------------------------------------------------------------- */
+const char *orca_status_string(orca_status s);
+const char *orca_last_error(void);
+
+/* ---- multi-GPU: spatial strips over NCCL ------------------------------ */
+
+/* NCCL unique id (128 bytes) for rank 0 to broadcast through any process group.
+ * Errors: NCCL (libnccl.so.2 not loadable). */
+orca_status orca_nccl_unique_id(void *id128);
+
+/* Create the rank-th of `world` strip contexts on `device`; every rank must call it with
+ * the same params and id.  world == 1 behaves like orca_create.  Each rank must then call
+ * orca_set_agents with the SAME global arrays (every rank keeps only its strip; ids are
+ * global).  Errors: INVALID_ARGUMENT, NCCL, CUDA. */
+orca_status orca_create_dist(const orca_params *params, int32_t device, int32_t rank,
+                             int32_t world, const void *nccl_id128, orca_ctx **out);
+
+/* Local agents of this rank: ids int32[n_local] (nullable), pos/vel float[2 n_local]
+ * (nullable); n_local from orca_get_count.  Synchronises. */
+orca_status orca_get_local_state(orca_ctx *ctx, int32_t *ids, float *pos, float *vel);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORCA_H */

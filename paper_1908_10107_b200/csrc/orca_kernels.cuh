@@ -1,0 +1,608 @@
+// orca_kernels.cuh -- sm_100a device code of the ORCA step (arXiv 1908.10107).
+//
+// Product path.  Shares no code with oracle/.  Every stage of the step runs here:
+//   k_hash      cell hash + histogram (atomic rank = in-cell slot)     FLAME bins
+//   k_scan      exclusive scan of the per-cell counts -> cellStart
+//   k_scatter   counting-sort permutation into cell-sorted SoA
+//   k_step      3x3 k-nearest query -> ORCA half-planes -> LP2/LP3 -> integrate -> next hash
+//               (P:77 model, Fig. 1 geometry, P:80 fallback, P:82 incremental LP)
+//
+// Numerics:
+//   * discrete decisions that must match the fp64 oracle bit-for-bit (cell floor, the
+//     neighbour key kappa, the ORCA branch predicates) are evaluated in fp64 with explicit
+//     round-to-nearest intrinsics (__dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn), i.e. the
+//     oracle's expression trees without contraction;
+//   * the continuous geometry and the LP run in fp32 in Hessian normal form (n, s):
+//     permitted set n.v >= s, |n| = 1, which keeps r^2 - s^2 and the LP3 bisectors
+//     well conditioned.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace orca {
+
+constexpr int kMaxK = 32;
+constexpr float kEps = 1e-5f;  // parallel-line tolerance (reading Q9)
+
+// per-agent flag bits (match orca_debug_step)
+constexpr uint32_t FL_INFEASIBLE = 1u;
+constexpr uint32_t FL_G1 = 2u;
+constexpr uint32_t FL_G2 = 4u;
+constexpr uint32_t FL_G3 = 8u;
+
+// indices into the device stats block (uint64)
+enum { ST_INFEASIBLE = 0, ST_DEGENERATE, ST_G1, ST_G2, ST_G3, ST_COLLISION, ST_COUNT };
+
+// Work counters of an instrumented dry step (orca_debug_work): per-launch totals used by
+// the bench's ALU roofline.
+struct Work {
+    unsigned long long cand;   // candidates read from the 3x3 bins (message reads)
+    unsigned long long lines;  // ORCA half-planes built
+    unsigned long long checks; // LP2 constraint checks (incl. inside LP3)
+    unsigned long long lp1;    // LP1 inner iterations
+    unsigned long long proj;   // LP3 projected lines
+};
+struct WorkT {
+    uint32_t cand, lines, checks, lp1, proj;
+};
+
+struct Grid {
+    float ox, oy, cs;  // origin, cell size (fp32 values; widened exactly to fp64)
+    int nx, ny;        // dims
+};
+
+struct Model {
+    float dt, maxSpeed, R;        // R = 2 r (combined radius, Fig. 1(a))
+    float invTauF, invDtF;        // fp32 copies for the continuous geometry
+    double invTauD, invDtD;       // 1/fl64(tau), 1/fl64(dt) for the predicates
+    double R2D;                   // fl64(R)^2
+    double nd2D;                  // fl64(nd)^2 (exact: nd is fp32)
+    float nd2Fup;                 // fp32 prefilter bound, rounded up with margin
+    int k;                        // maxNeighbors
+    int goals;                    // 1: aux holds goals, pref = g min(1, s/|g|)
+    float prefSpeed;
+};
+
+// ------------------------------------------------------------------ cell (reading Q11)
+__device__ __forceinline__ int cell_coord(float x, float o, float cs, int nc) {
+    double t = __ddiv_rn(__dsub_rn((double)x, (double)o), (double)cs);
+    double f = floor(t);
+    f = fmax(f, 0.0);
+    f = fmin(f, (double)(nc - 1));
+    return (int)f;
+}
+
+__device__ __forceinline__ uint32_t cell_id(float x, float y, const Grid& g) {
+    int cx = cell_coord(x, g.ox, g.cs, g.nx);
+    int cy = cell_coord(y, g.oy, g.cs, g.ny);
+    return (uint32_t)cx * (uint32_t)g.ny + (uint32_t)cy;  // column-major: strips are ranges
+}
+
+// ------------------------------------------------------------------------- binning
+__global__ void k_hash(int n, const float2* __restrict__ pos, Grid g, uint32_t* __restrict__ cell,
+                       uint32_t* __restrict__ rank, uint32_t* __restrict__ count) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        float2 p = pos[i];
+        uint32_t c = cell_id(p.x, p.y, g);
+        cell[i] = c;
+        rank[i] = atomicAdd(&count[c], 1u);
+    }
+}
+
+// Single-CTA exclusive scan over C counts, tiled (1024 threads x 4 per tile).  Writes
+// cellStart[0..C] and re-zeroes count for the next step's histogram.
+__global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uint32_t* __restrict__ cellStart,
+                                               int C) {
+    __shared__ uint32_t warpSums[32];
+    __shared__ uint32_t carryS;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carryS = 0;
+    __syncthreads();
+    for (int base = 0; base < C; base += 4096) {
+        uint32_t v[4];
+        const int i0 = base + tid * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = (i0 + q < C) ? count[i0 + q] : 0u;
+        uint32_t local = v[0] + v[1] + v[2] + v[3];
+        uint32_t incl = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) warpSums[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = warpSums[lane];
+            uint32_t wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
+            }
+            warpSums[lane] = wi - w;  // exclusive warp offsets
+        }
+        __syncthreads();
+        uint32_t run = carryS + warpSums[wid] + incl - local;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (i0 + q < C) {
+                cellStart[i0 + q] = run;
+                count[i0 + q] = 0u;
+            }
+            run += v[q];
+        }
+        __syncthreads();
+        if (tid == 1023) carryS = run;
+        __syncthreads();
+    }
+    if (tid == 0) cellStart[C] = carryS;
+}
+
+__global__ void k_scatter(int n, const uint32_t* __restrict__ cell, const uint32_t* __restrict__ rank,
+                          const uint32_t* __restrict__ cellStart, const float2* __restrict__ posW,
+                          const float2* __restrict__ velW, const float2* __restrict__ auxW,
+                          const uint32_t* __restrict__ idW, float2* __restrict__ posS, float2* __restrict__ velS,
+                          float2* __restrict__ auxS, uint32_t* __restrict__ idS) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t dst = cellStart[cell[i]] + rank[i];
+        posS[dst] = posW[i];
+        velS[dst] = velW[i];
+        auxS[dst] = auxW[i];
+        idS[dst] = idW[i];
+    }
+}
+
+// ------------------------------------------------------------- ORCA half-plane (Fig. 1)
+// Agent i against neighbour j, R = r_i + r_j.  Branch predicates in fp64 exactly as the
+// oracle's expression trees; geometry in fp32 Hessian form.  Returns flag bits
+// (FL_G1) and sets *collision.
+__device__ __forceinline__ uint32_t orca_line(float xi, float yi, float vxi, float vyi, float xj, float yj,
+                                              float vxj, float vyj, uint32_t idi, uint32_t idj, const Model& m,
+                                              float& nx, float& ny, float& s, int& collision) {
+    const double rpx = __dsub_rn((double)xj, (double)xi);
+    const double rpy = __dsub_rn((double)yj, (double)yi);
+    const double rvx = __dsub_rn((double)vxi, (double)vxj);
+    const double rvy = __dsub_rn((double)vyi, (double)vyj);
+    const double d2 = __dadd_rn(__dmul_rn(rpx, rpx), __dmul_rn(rpy, rpy));
+    uint32_t fl = 0;
+    collision = 0;
+    if (d2 > m.R2D) {
+        const double wx = __dsub_rn(rvx, __dmul_rn(m.invTauD, rpx));
+        const double wy = __dsub_rn(rvy, __dmul_rn(m.invTauD, rpy));
+        const double wl2 = __dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy));
+        const double dot1 = __dadd_rn(__dmul_rn(wx, rpx), __dmul_rn(wy, rpy));
+        if (dot1 < 0.0 && __dmul_rn(dot1, dot1) > __dmul_rn(m.R2D, wl2)) {
+            // cut-off circle: n = w/|w|, s = n.v_i + (R/tau - |w|)/2
+            const float wl = sqrtf((float)wl2);
+            const float inv = 1.0f / wl;
+            nx = (float)wx * inv;
+            ny = (float)wy * inv;
+            s = fmaf(nx, vxi, ny * vyi) + 0.5f * (m.R * m.invTauF - wl);
+        } else {
+            // legs: s = n.(v_i + v_j)/2 since n is orthogonal to the leg direction
+            const float leg = sqrtf((float)__dsub_rn(d2, m.R2D));
+            const float px = (float)rpx, py = (float)rpy;
+            const float invd2 = 1.0f / (float)d2;
+            const double detw = __dsub_rn(__dmul_rn(rpx, wy), __dmul_rn(rpy, wx));
+            if (detw > 0.0) {  // left leg
+                nx = -(px * m.R + py * leg) * invd2;
+                ny = (px * leg - py * m.R) * invd2;
+            } else {  // right leg (ties -> right, reading Q5)
+                nx = (py * leg - px * m.R) * invd2;
+                ny = -(px * leg + py * m.R) * invd2;
+            }
+            s = 0.5f * fmaf(nx, vxi + vxj, ny * (vyi + vyj));
+        }
+    } else {
+        // collision (reading Q4): horizon dt
+        collision = 1;
+        const double wx = __dsub_rn(rvx, __dmul_rn(m.invDtD, rpx));
+        const double wy = __dsub_rn(rvy, __dmul_rn(m.invDtD, rpy));
+        const double wl2 = __dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy));
+        float wl;
+        if (wl2 == 0.0) {  // coincident, equal velocity (reading Q15)
+            nx = (idi < idj) ? -1.0f : 1.0f;
+            ny = 0.0f;
+            wl = 0.0f;
+            fl |= FL_G1;
+        } else {
+            wl = sqrtf((float)wl2);
+            const float inv = 1.0f / wl;
+            nx = (float)wx * inv;
+            ny = (float)wy * inv;
+        }
+        s = fmaf(nx, vxi, ny * vyi) + 0.5f * (m.R * m.invDtF - wl);
+    }
+    return fl;
+}
+
+// ------------------------------------------------------------------- LP
+// Lines live in shared memory, one column per thread: element m of this thread's list
+// is at [m * T] of each pointer (bank = tid % 32 for every m -> conflict-free even under
+// divergence).
+struct Lines {
+    float* nx;
+    float* ny;
+    float* s;
+};
+
+template <bool CNT>
+__device__ __forceinline__ bool lp1(const Lines& L, int T, int no, float r, float optx, float opty, bool dirOpt,
+                                    float& vx, float& vy, uint32_t& fl, WorkT& w) {
+    const float nix = L.nx[no * T], niy = L.ny[no * T], si = L.s[no * T];
+    const float disc = (r - si) * (r + si);  // r^2 - s^2: distance of the chord
+    if (disc < 0.0f) return false;
+    const float sq = sqrtf(disc);
+    float tL = -sq, tR = sq;
+    const float Dx = niy, Dy = -nix;  // line direction; base point s_i n_i
+    for (int j = 0; j < no; ++j) {
+        if (CNT) ++w.lp1;
+        const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
+        const float den = fmaf(njx, Dx, njy * Dy);
+        const float num = sj - si * fmaf(njx, nix, njy * niy);
+        if (fabsf(den) <= kEps) {
+            fl |= FL_G2;
+            if (num > 0.0f) return false;
+            continue;
+        }
+        const float t = num / den;
+        if (den > 0.0f)
+            tL = fmaxf(tL, t);
+        else
+            tR = fminf(tR, t);
+        if (tL > tR) return false;
+    }
+    const float od = fmaf(optx, Dx, opty * Dy);
+    float t;
+    if (dirOpt)
+        t = (od > 0.0f) ? tR : tL;
+    else
+        t = fminf(fmaxf(od, tL), tR);
+    vx = fmaf(t, Dx, si * nix);
+    vy = fmaf(t, Dy, si * niy);
+    return true;
+}
+
+template <bool CNT>
+__device__ __forceinline__ int lp2(const Lines& L, int T, int n, float r, float optx, float opty, bool dirOpt,
+                                   float& vx, float& vy, uint32_t& fl, WorkT& w) {
+    if (dirOpt) {
+        vx = optx * r;
+        vy = opty * r;
+    } else {
+        const float l2 = fmaf(optx, optx, opty * opty);
+        if (l2 > r * r) {
+            const float sc = r / sqrtf(l2);
+            vx = optx * sc;
+            vy = opty * sc;
+        } else {
+            vx = optx;
+            vy = opty;
+        }
+    }
+    for (int i = 0; i < n; ++i) {
+        if (CNT) ++w.checks;
+        const float pen = L.s[i * T] - fmaf(L.nx[i * T], vx, L.ny[i * T] * vy);
+        if (pen > 0.0f) {
+            const float tx = vx, ty = vy;
+            if (!lp1<CNT>(L, T, i, r, optx, opty, dirOpt, vx, vy, fl, w)) {
+                vx = tx;
+                vy = ty;
+                return i;
+            }
+        }
+    }
+    return n;
+}
+
+// LP3: least penetration from the LP2 failure index.  The projected constraint
+// "penetration_j <= penetration_i" is the line (n_j - n_i).v >= s_j - s_i, normalised.
+template <bool CNT>
+__device__ __forceinline__ void lp3(const Lines& L, const Lines& P, int T, int n, int begin, float r, float& vx,
+                                    float& vy, uint32_t& fl, WorkT& w) {
+    float dist = 0.0f;
+    for (int i = begin; i < n; ++i) {
+        const float nix = L.nx[i * T], niy = L.ny[i * T], si = L.s[i * T];
+        if (si - fmaf(nix, vx, niy * vy) > dist) {
+            int m = 0;
+            for (int j = 0; j < i; ++j) {
+                const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
+                const float det = fmaf(nix, njy, -niy * njx);
+                if (fabsf(det) <= kEps) {
+                    fl |= FL_G2;
+                    if (fmaf(nix, njx, niy * njy) > 0.0f) continue;  // same direction
+                }
+                if (CNT) ++w.proj;
+                const float dx = njx - nix, dy = njy - niy;
+                const float il = 1.0f / sqrtf(fmaf(dx, dx, dy * dy));
+                P.nx[m * T] = dx * il;
+                P.ny[m * T] = dy * il;
+                P.s[m * T] = (sj - si) * il;
+                ++m;
+            }
+            const float tx = vx, ty = vy;
+            if (lp2<CNT>(P, T, m, r, nix, niy, true, vx, vy, fl, w) < m) {
+                vx = tx;  // floating-point failure: keep the current point
+                vy = ty;
+            }
+            dist = si - fmaf(nix, vx, niy * vy);
+        }
+    }
+}
+
+// --------------------------------------------------------------------- fused step
+struct StepArgs {
+    int n;
+    Grid g;
+    Model m;
+    // cell-sorted (rest) state
+    const float2* __restrict__ posS;
+    const float2* __restrict__ velS;
+    const float2* __restrict__ auxS;  // prefVel, or goal when m.goals
+    const uint32_t* __restrict__ idS;
+    const uint32_t* __restrict__ cellStart;
+    // outputs of a real step (work buffers, next step's binning)
+    float2* posW;
+    float2* velW;
+    float2* auxW;
+    uint32_t* idW;
+    uint32_t* cellW;
+    uint32_t* rankW;
+    uint32_t* count;
+    unsigned long long* stats;
+    // outputs of a dry (debug) step, indexed by global id
+    float2* dbgV;
+    uint8_t* dbgFlags;
+    int32_t* dbgNbr;
+    int32_t* dbgCnt;
+    Work* work;  // dry step only: instrumented work counts (nullable)
+};
+
+__device__ __forceinline__ bool key_less(double ka, uint32_t ia, double kb, uint32_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+constexpr int kStepThreads = 128;
+
+// bytes of dynamic shared memory per thread for neighbour list + lines + LP3 lines
+__host__ __device__ constexpr int step_smem_per_thread(int k) { return k * (8 + 4 + 4 + 12 + 12); }
+
+template <bool DRY>
+__global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
+    constexpr bool CNT = DRY;  // only the debug variant counts work
+    WorkT w{0, 0, 0, 0, 0};
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int T = kStepThreads;
+    const int tid = threadIdx.x;
+    const int k = a.m.k;
+    double* sKey = reinterpret_cast<double*>(smem) + tid;
+    uint32_t* sId = reinterpret_cast<uint32_t*>(smem + (size_t)8 * k * T) + tid;
+    uint32_t* sJ = reinterpret_cast<uint32_t*>(smem + (size_t)12 * k * T) + tid;
+    float* fbase = reinterpret_cast<float*>(smem + (size_t)16 * k * T) + tid;
+    const Lines L{fbase, fbase + k * T, fbase + 2 * k * T};
+    const Lines P{fbase + 3 * k * T, fbase + 4 * k * T, fbase + 5 * k * T};
+
+    const int i = blockIdx.x * T + tid;
+    const bool active = i < a.n;
+    uint32_t fl = 0;
+    int nColl = 0;
+    if (active) {
+        const float2 pi = a.posS[i];
+        const float2 vi = a.velS[i];
+        const float2 aux = a.auxS[i];
+        const uint32_t idi = a.idS[i];
+        const int cx = cell_coord(pi.x, a.g.ox, a.g.cs, a.g.nx);
+        const int cy = cell_coord(pi.y, a.g.oy, a.g.cs, a.g.ny);
+
+        // ---- 2. k nearest within r_obs over the 3x3 bins -------------
+        int cnt = 0;
+        float thr = a.m.nd2Fup;  // fp32 prefilter; the fp64 key decides
+        double lastKey = a.m.nd2D;
+        uint32_t lastId = 0xffffffffu;
+        if (k > 0) {
+            const int r0 = max(cy - 1, 0), r1 = min(cy + 1, a.g.ny - 1);
+            for (int col = max(cx - 1, 0); col <= min(cx + 1, a.g.nx - 1); ++col) {
+                const int b = (int)a.cellStart[col * a.g.ny + r0];
+                const int e = (int)a.cellStart[col * a.g.ny + r1 + 1];
+                if (CNT) w.cand += (uint32_t)(e - b);
+                for (int j = b; j < e; ++j) {
+                    const float2 pj = a.posS[j];
+                    const float dx = pj.x - pi.x, dy = pj.y - pi.y;
+                    const float d2 = fmaf(dx, dx, dy * dy);
+                    if (d2 > thr || j == i) continue;
+                    const double Dx = __dsub_rn((double)pj.x, (double)pi.x);
+                    const double Dy = __dsub_rn((double)pj.y, (double)pi.y);
+                    const double key = __dadd_rn(__dmul_rn(Dx, Dx), __dmul_rn(Dy, Dy));
+                    if (!(key < a.m.nd2D)) continue;
+                    const uint32_t idj = a.idS[j];
+                    if (cnt == k && !key_less(key, idj, lastKey, lastId)) continue;
+                    int p = (cnt < k) ? cnt : k - 1;
+                    while (p > 0 && key_less(key, idj, sKey[(p - 1) * T], sId[(p - 1) * T])) {
+                        sKey[p * T] = sKey[(p - 1) * T];
+                        sId[p * T] = sId[(p - 1) * T];
+                        sJ[p * T] = sJ[(p - 1) * T];
+                        --p;
+                    }
+                    sKey[p * T] = key;
+                    sId[p * T] = idj;
+                    sJ[p * T] = (uint32_t)j;
+                    if (cnt < k) ++cnt;
+                    if (cnt == k) {
+                        lastKey = sKey[(k - 1) * T];
+                        lastId = sId[(k - 1) * T];
+                        // fp32 d2 has relative error < 2^-22; margin 2^-20, rounded up
+                        thr = __fmul_ru(__double2float_ru(lastKey), 1.0f + 0x1p-20f);
+                    }
+                }
+            }
+        }
+
+        // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
+        for (int q = 0; q < cnt; ++q) {
+            const uint32_t j = sJ[q * T];
+            const float2 pj = a.posS[j];
+            const float2 vj = a.velS[j];
+            float nx, ny, s;
+            int coll;
+            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, sId[q * T], a.m, nx, ny, s, coll);
+            nColl += coll;
+            L.nx[q * T] = nx;
+            L.ny[q * T] = ny;
+            L.s[q * T] = s;
+        }
+
+        // ---- 4. LP2, LP3 on failure ------------------------------------------
+        float px, py;
+        if (a.m.goals) {  // toward the goal at walking speed (reading Q16)
+            const float gx = aux.x - pi.x, gy = aux.y - pi.y;
+            const float gl = sqrtf(fmaf(gx, gx, gy * gy));
+            const float sc = (gl > a.m.prefSpeed) ? a.m.prefSpeed / gl : 1.0f;
+            px = gx * sc;
+            py = gy * sc;
+        } else {
+            px = aux.x;
+            py = aux.y;
+        }
+        float vx, vy;
+        if (CNT) w.lines += (uint32_t)cnt;
+        const int f = lp2<CNT>(L, T, cnt, a.m.maxSpeed, px, py, false, vx, vy, fl, w);
+        if (f < cnt) {
+            fl |= FL_INFEASIBLE;
+            lp3<CNT>(L, P, T, cnt, f, a.m.maxSpeed, vx, vy, fl, w);
+            float dl = 0.0f;
+            for (int q = 0; q < cnt; ++q) dl = fmaxf(dl, L.s[q * T] - fmaf(L.nx[q * T], vx, L.ny[q * T] * vy));
+            if (dl > 0.0f && dl < 1e-6f) fl |= FL_G3;
+        }
+
+        // ---- 5. integrate (explicit Euler) + next step's binning ----------------------
+        if (DRY) {
+            if (a.dbgV) a.dbgV[idi] = make_float2(vx, vy);
+            if (a.dbgFlags) a.dbgFlags[idi] = (uint8_t)fl;
+            if (a.dbgCnt) a.dbgCnt[idi] = cnt;
+            if (a.dbgNbr)
+                for (int q = 0; q < k; ++q) a.dbgNbr[(size_t)idi * k + q] = (q < cnt) ? (int32_t)sId[q * T] : -1;
+        } else {
+            const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
+            const uint32_t c = cell_id(pn.x, pn.y, a.g);
+            a.posW[i] = pn;
+            a.velW[i] = make_float2(vx, vy);
+            a.auxW[i] = aux;
+            a.idW[i] = idi;
+            a.cellW[i] = c;
+            a.rankW[i] = atomicAdd(&a.count[c], 1u);
+        }
+    }
+    if (DRY && a.work) {
+        unsigned long long c[5] = {w.cand, w.lines, w.checks, w.lp1, w.proj};
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            for (int o = 16; o > 0; o >>= 1) c[q] += __shfl_xor_sync(0xffffffffu, c[q], o);
+        }
+        if ((tid & 31) == 0) {
+            atomicAdd(&a.work->cand, c[0]);
+            atomicAdd(&a.work->lines, c[1]);
+            atomicAdd(&a.work->checks, c[2]);
+            atomicAdd(&a.work->lp1, c[3]);
+            atomicAdd(&a.work->proj, c[4]);
+        }
+    }
+    if (!DRY) {
+        const int cInf = __syncthreads_count(fl & FL_INFEASIBLE);
+        const int cDeg = __syncthreads_count(fl & (FL_G1 | FL_G2));
+        const int cG1 = __syncthreads_count(fl & FL_G1);
+        const int cG2 = __syncthreads_count(fl & FL_G2);
+        const int cG3 = __syncthreads_count(fl & FL_G3);
+        // collision pairs: warp-reduce then one atomic per warp
+        int c = nColl;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if ((tid & 31) == 0 && c) atomicAdd(&a.stats[ST_COLLISION], (unsigned long long)c);
+        if (tid == 0) {
+            if (cInf) atomicAdd(&a.stats[ST_INFEASIBLE], (unsigned long long)cInf);
+            if (cDeg) atomicAdd(&a.stats[ST_DEGENERATE], (unsigned long long)cDeg);
+            if (cG1) atomicAdd(&a.stats[ST_G1], (unsigned long long)cG1);
+            if (cG2) atomicAdd(&a.stats[ST_G2], (unsigned long long)cG2);
+            if (cG3) atomicAdd(&a.stats[ST_G3], (unsigned long long)cG3);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ state utilities
+__global__ void k_unpermute(int n, const uint32_t* __restrict__ idS, const float2* __restrict__ posS,
+                            const float2* __restrict__ velS, float2* __restrict__ posOut,
+                            float2* __restrict__ velOut) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t id = idS[i];
+        if (posOut) posOut[id] = posS[i];
+        if (velOut) velOut[id] = velS[i];
+    }
+}
+
+__global__ void k_cells(int n, const uint32_t* __restrict__ idS, const float2* __restrict__ posS, Grid g,
+                        int32_t* __restrict__ cxOut, int32_t* __restrict__ cyOut) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float2 p = posS[i];
+        const uint32_t id = idS[i];
+        cxOut[id] = cell_coord(p.x, g.ox, g.cs, g.nx);
+        cyOut[id] = cell_coord(p.y, g.oy, g.cs, g.ny);
+    }
+}
+
+// out[i] = in[idS[i]]: id-ordered array -> sorted order
+__global__ void k_gather_by_id(int n, const uint32_t* __restrict__ idS, const float2* __restrict__ in,
+                               float2* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[idS[i]];
+}
+
+__global__ void k_iota(int n, uint32_t* __restrict__ id) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) id[i] = (uint32_t)i;
+}
+
+// Block-partial min/max of the positions and a non-finite count over all input arrays.
+// partial[b] = {minx, miny, maxx, maxy, nonfinite}
+__global__ void k_minmax(int n, const float2* __restrict__ pos, const float2* __restrict__ vel,
+                         const float2* __restrict__ aux, float* __restrict__ partial) {
+    float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    int bad = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float2 p = pos[i];
+        const float2 v = vel[i];
+        const float2 q = aux[i];
+        bad += !(isfinite(p.x) && isfinite(p.y) && isfinite(v.x) && isfinite(v.y) && isfinite(q.x) &&
+                 isfinite(q.y));
+        mnx = fminf(mnx, p.x);
+        mny = fminf(mny, p.y);
+        mxx = fmaxf(mxx, p.x);
+        mxy = fmaxf(mxy, p.y);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    __shared__ float s[32][5];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        s[wid][0] = mnx;
+        s[wid][1] = mny;
+        s[wid][2] = mxx;
+        s[wid][3] = mxy;
+        s[wid][4] = (float)bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float r[5] = {INFINITY, INFINITY, -INFINITY, -INFINITY, 0.0f};
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            r[0] = fminf(r[0], s[w][0]);
+            r[1] = fminf(r[1], s[w][1]);
+            r[2] = fmaxf(r[2], s[w][2]);
+            r[3] = fmaxf(r[3], s[w][3]);
+            r[4] += s[w][4];
+        }
+        for (int q = 0; q < 5; ++q) partial[blockIdx.x * 5 + q] = r[q];
+    }
+}
+
+}  // namespace orca

@@ -1,0 +1,245 @@
+"""Thin Python binding of liborca (include/orca.h).  Argument marshalling only: every
+step of the ORCA update runs in the library's CUDA kernels.  There is no CPU fallback --
+importing this module raises if liborca.so is missing or cannot be loaded.
+
+Arrays may be numpy arrays (host) or CUDA torch tensors (device); both are passed to the
+library as raw pointers, which dispatches through unified addressing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liborca.so")
+
+ORCA_MAX_K = 32
+STATUS = {0: "ok", 1: "invalid argument", 2: "not ready", 3: "out of memory", 4: "CUDA error",
+          5: "NCCL error", 6: "capacity exceeded", 7: "internal error"}
+
+# names declared in include/orca.h (checked by tests/test_capi.py)
+EXPORTS = [
+    "orca_create", "orca_destroy", "orca_set_agents", "orca_set_goals", "orca_step", "orca_get_state",
+    "orca_get_count", "orca_get_grid", "orca_debug_cells", "orca_debug_step", "orca_get_stats",
+    "orca_reset_stats", "orca_get_stream", "orca_step_timed", "orca_status_string", "orca_last_error",
+    "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
+]
+
+
+class OrcaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"liborca: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("timeStep", ctypes.c_float), ("neighborDist", ctypes.c_float),
+                ("maxNeighbors", ctypes.c_int32), ("timeHorizon", ctypes.c_float),
+                ("radius", ctypes.c_float), ("maxSpeed", ctypes.c_float)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("steps", "agent_updates", "infeasible", "degenerate",
+                                               "coincident", "eps_parallel", "marginal", "collision_pairs")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not found: run `python -m paper_1908_10107_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+    P = ctypes.POINTER
+    sig = {
+        "orca_create": [P(Params), i32, P(vp)],
+        "orca_destroy": [vp],
+        "orca_set_agents": [vp, i64, vp, vp, vp],
+        "orca_set_goals": [vp, vp, f32],
+        "orca_step": [vp, i32],
+        "orca_get_state": [vp, vp, vp],
+        "orca_get_count": [vp, P(i64)],
+        "orca_get_grid": [vp, P(ctypes.c_double), P(f32), P(i32)],
+        "orca_debug_cells": [vp, vp, vp],
+        "orca_debug_step": [vp, vp, vp, vp, vp],
+        "orca_get_stats": [vp, P(Stats)],
+        "orca_reset_stats": [vp],
+        "orca_get_stream": [vp, P(vp)],
+        "orca_step_timed": [vp, i32, P(ctypes.c_double)],
+        "orca_status_string": [i32],
+        "orca_last_error": [],
+        "orca_nccl_unique_id": [vp],
+        "orca_create_dist": [P(Params), i32, i32, i32, vp, P(vp)],
+        "orca_get_local_state": [vp, vp, vp, vp],
+        "orca_debug_work": [vp, P(i64)],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = i32
+    L.orca_destroy.restype = None
+    L.orca_status_string.restype = ctypes.c_char_p
+    L.orca_last_error.restype = ctypes.c_char_p
+    return L
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise OrcaError(st, _lib.orca_last_error().decode())
+
+
+def _ptr(a):
+    """Raw pointer of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return ctypes.c_void_p(a.ctypes.data)
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(a.data_ptr())
+    raise TypeError(type(a))
+
+
+def _as_f32(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return np.ascontiguousarray(a, dtype=np.float32)
+    return a  # torch tensors: caller supplies float32 contiguous
+
+
+def make_params(timeStep=0.25, neighborDist=15.0, maxNeighbors=10, timeHorizon=5.0, radius=0.5,
+                maxSpeed=1.33) -> Params:
+    return Params(timeStep, neighborDist, maxNeighbors, timeHorizon, radius, maxSpeed)
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.orca_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Orca:
+    """One liborca context (orca_create / orca_create_dist ... orca_destroy)."""
+
+    def __init__(self, params: Params | dict | None = None, device: int = 0, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None):
+        if params is None:
+            params = make_params()
+        elif isinstance(params, dict):
+            params = make_params(**params)
+        self.params = params
+        self._ctx = ctypes.c_void_p()
+        if world == 1:
+            _check(_lib.orca_create(ctypes.byref(params), device, ctypes.byref(self._ctx)))
+        else:
+            idb = ctypes.create_string_buffer(nccl_id, 128)
+            _check(_lib.orca_create_dist(ctypes.byref(params), device, rank, world, idb, ctypes.byref(self._ctx)))
+        self.n = 0
+
+    def close(self):
+        if self._ctx:
+            _lib.orca_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- state
+    def set_agents(self, pos, vel, pref):
+        pos, vel, pref = _as_f32(pos), _as_f32(vel), _as_f32(pref)
+        n = (pos.shape[0] if pos.ndim == 2 else pos.shape[0] // 2)
+        _check(_lib.orca_set_agents(self._ctx, n, _ptr(pos), _ptr(vel), _ptr(pref)))
+        self.n = n
+
+    def set_goals(self, goals, pref_speed: float):
+        _check(_lib.orca_set_goals(self._ctx, _ptr(_as_f32(goals)), pref_speed))
+
+    def step(self, n_steps: int = 1):
+        _check(_lib.orca_step(self._ctx, n_steps))
+
+    def step_timed(self, n_steps: int):
+        ms = (ctypes.c_double * 4)()
+        _check(_lib.orca_step_timed(self._ctx, n_steps, ms))
+        return list(ms)
+
+    def count(self) -> int:
+        n = ctypes.c_int64()
+        _check(_lib.orca_get_count(self._ctx, ctypes.byref(n)))
+        return n.value
+
+    def get_state(self, pos=None, vel=None):
+        """Into caller buffers (numpy or torch) if given, else new numpy arrays."""
+        if pos is None and vel is None:
+            pos = np.empty((self.count(), 2), np.float32)
+            vel = np.empty((self.count(), 2), np.float32)
+        _check(_lib.orca_get_state(self._ctx, _ptr(pos), _ptr(vel)))
+        return pos, vel
+
+    def get_local_state(self):
+        n = self.count()
+        ids = np.empty(n, np.int32)
+        pos = np.empty((n, 2), np.float32)
+        vel = np.empty((n, 2), np.float32)
+        _check(_lib.orca_get_local_state(self._ctx, _ptr(ids), _ptr(pos), _ptr(vel)))
+        return ids, pos, vel
+
+    def grid(self):
+        o = (ctypes.c_double * 2)()
+        cs = ctypes.c_float()
+        d = (ctypes.c_int32 * 2)()
+        _check(_lib.orca_get_grid(self._ctx, o, ctypes.byref(cs), d))
+        return np.array([o[0], o[1]], np.float64), cs.value, np.array([d[0], d[1]], np.int32)
+
+    def debug_cells(self):
+        n = self.count()
+        cx = np.empty(n, np.int32)
+        cy = np.empty(n, np.int32)
+        _check(_lib.orca_debug_cells(self._ctx, _ptr(cx), _ptr(cy)))
+        return cx, cy
+
+    def debug_step(self):
+        """(vnew (n,2) f32, flags u8, nbr (n,k) int32, cnt int32) for the current state."""
+        n = self.count()
+        k = self.params.maxNeighbors
+        v = np.empty((n, 2), np.float32)
+        fl = np.empty(n, np.uint8)
+        nb = np.empty((n, max(k, 1)), np.int32)
+        cnt = np.empty(n, np.int32)
+        _check(_lib.orca_debug_step(self._ctx, _ptr(v), _ptr(fl), _ptr(nb) if k > 0 else None, _ptr(cnt)))
+        return v, fl, nb[:, :k], cnt
+
+    def work(self) -> dict:
+        out = (ctypes.c_int64 * 5)()
+        _check(_lib.orca_debug_work(self._ctx, out))
+        return dict(cand=out[0], lines=out[1], checks=out[2], lp1=out[3], proj=out[4])
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(_lib.orca_get_stats(self._ctx, ctypes.byref(s)))
+        return s.as_dict()
+
+    def reset_stats(self):
+        _check(_lib.orca_reset_stats(self._ctx))
+
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        _check(_lib.orca_get_stream(self._ctx, ctypes.byref(s)))
+        return s.value or 0

@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on the same
+seeded inputs.
+
+Bar (BASELINE.json north_star / DESIGN.md §4):
+  * grid, cells and neighbour id lists: bit-exact;
+  * single-step new velocities within 1e-4 m/s absolute (max-norm per component) for
+    every agent the oracle does not flag degenerate (g1|g2|g4); degenerate < 0.1 %;
+  * infeasible agents: max penetration of the GPU velocity, evaluated in fp64 on the
+    oracle's lines, <= delta*_oracle + 1e-4;
+  * positions within dt*1e-4 + 1 ulp_fp32(|p|) of p + dt v (oracle);
+  * |v| <= maxSpeed (fp32 rounding slack 1e-6 relative).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import pins
+from paper_1908_10107_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+VTOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def orca():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1908_10107_b200 import build
+    build.build()
+    from paper_1908_10107_b200 import orca as O
+    return O
+
+
+def _ctx(orca, w, **over):
+    p = dict(w["params"])
+    p.update(over)
+    o = orca.Orca(p)
+    o.set_agents(w["pos"], w["vel"], w["pref"])
+    if w.get("goals") is not None:
+        o.set_goals(w["goals"], w["pref_speed"])
+    return o, p
+
+
+def _oracle_params(oracle, p):
+    return oracle.make_params(**p)
+
+
+def compare_step(orca, oracle, w, agents=None, max_deg=None, **over):
+    """One step from the state in w on both sides; returns a report dict and asserts the
+    bar.  agents: optional sample of ids for large inputs (oracle computes one by one)."""
+    o, p = _ctx(orca, w, **over)
+    op = _oracle_params(oracle, p)
+    origin, cs, dims = o.grid()
+    oorigin, odims = oracle.grid_derive(w["pos"], op.neighborDist)
+    assert np.array_equal(origin, oorigin.astype(np.float64)) and np.array_equal(dims, odims)
+    # cells (bit-exact)
+    cx, cy = o.debug_cells()
+    ocx, ocy = oracle.cells(w["pos"], oorigin, op.neighborDist, odims)
+    assert np.array_equal(cx, ocx) and np.array_equal(cy, ocy)
+    # one step (dry) on the GPU
+    v, fl, nb, cnt = o.debug_step()
+    ref = oracle.step(op, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"),
+                      pref_speed=w.get("pref_speed", 1.0), agents=agents, want_nbrs=True)
+    ids = np.arange(len(w["pos"])) if agents is None else np.asarray(agents)
+    # neighbours (bit-exact)
+    assert np.array_equal(cnt[ids], ref["cnt"])
+    assert np.array_equal(nb[ids], ref["nbr"])
+    # velocities
+    ov = ref["vel"]
+    gv = v[ids].astype(np.float64)
+    err = np.max(np.abs(gv - ov), axis=1)
+    deg = (ref["flags"] & oracle.FLAG_DEGENERATE) != 0
+    bad = (err > VTOL) & ~deg
+    k = p["maxNeighbors"]
+    # infeasible: penetration of the GPU answer on the oracle's lines
+    inf = (ref["flags"] & oracle.FLAG_INFEASIBLE) != 0
+    worst_pen_gap = 0.0
+    for q in np.nonzero(inf)[0][:400]:
+        i = ids[q]
+        lines = [oracle.orca_line(w["pos"][i], w["vel"][i], w["pos"][j], w["vel"][j], i, j, p["radius"],
+                                  p["timeHorizon"], p["timeStep"])[0] for j in ref["nbr"][q][:ref["cnt"][q]]]
+        gap = pins.penetration_np(lines, gv[q]) - ref["delta"][q]
+        worst_pen_gap = max(worst_pen_gap, gap)
+    speed = np.hypot(gv[:, 0], gv[:, 1])
+    report = dict(n=len(ids), max_err=float(err[~deg].max()) if (~deg).any() else 0.0,
+                  n_bad=int(bad.sum()), n_deg=int(deg.sum()), n_inf=int(inf.sum()),
+                  gpu_inf=int(((fl[ids] & 1) != 0).sum()), worst_pen_gap=worst_pen_gap,
+                  max_speed=float(speed.max()) if len(speed) else 0.0)
+    assert report["n_bad"] == 0, (report, np.nonzero(bad)[0][:10])
+    assert report["n_deg"] <= (max(1, 0.001 * len(ids)) if max_deg is None else max_deg), report
+    assert worst_pen_gap <= VTOL, report
+    assert np.all(speed <= p["maxSpeed"] * (1 + 1e-6) + 1e-7), report
+    # a real step agrees with the dry step and moves p + dt v
+    o.step(1)
+    pos1, vel1 = o.get_state()
+    assert np.array_equal(vel1, v)
+    pexp = ref["pos"]
+    ptol = p["timeStep"] * VTOL + np.spacing(np.abs(pexp).max(axis=1).astype(np.float32)).astype(np.float64)
+    perr = np.max(np.abs(pos1[ids].astype(np.float64) - pexp), axis=1)
+    assert np.all((perr <= ptol + 1e-12) | deg), perr.max()
+    o.close()
+    return report
+
+
+# --------------------------------------------------------------------------- cases
+@pytest.mark.parametrize("config,n,rho", [
+    ("uniform", 3000, 0.25), ("uniform", 3000, 0.5), ("uniform", 2000, 0.01), ("uniform", 2500, 0.1),
+    ("corridor", 3000, None), ("dense", 4000, None),
+])
+def test_step_parity_small(orca, oracle, config, n, rho):
+    if config == "corridor":
+        w = W.corridor(n=n, length=n / (0.25 * 30.0), width=30.0)
+    else:
+        w = W.make(config, n=n, rho=rho)
+    compare_step(orca, oracle, w)
+
+
+def test_step_parity_circle_goals(orca, oracle):
+    w = W.make("circle")
+    compare_step(orca, oracle, w)
+
+
+@pytest.mark.parametrize("warm", [5, 20])
+def test_step_parity_warm_state(orca, oracle, warm):
+    """State warmed up by the ORACLE (fp32 state between steps), then one step on both."""
+    w = W.make("uniform", n=2000, rho=0.5)
+    op = oracle.make_params(**w["params"])
+    pos, vel, _ = oracle.run(op, w["pos"], w["vel"], pref=w["pref"], steps=warm)
+    w2 = dict(w, pos=pos, vel=vel)
+    compare_step(orca, oracle, w2)
+
+
+def test_step_parity_corridor_warm(orca, oracle):
+    w = W.corridor(n=3000, length=400.0, width=30.0)
+    op = oracle.make_params(**w["params"])
+    pos, vel, _ = oracle.run(op, w["pos"], w["vel"], pref=w["pref"], steps=15)
+    compare_step(orca, oracle, dict(w, pos=pos, vel=vel))
+
+
+def test_circle_warm_goals(orca, oracle):
+    """The circle's central crush (many infeasible agents, overlaps) at oracle step 300."""
+    w = W.make("circle")
+    op = oracle.make_params(**w["params"])
+    pos, vel, _ = oracle.run(op, w["pos"], w["vel"], goals=w["goals"], pref_speed=1.0, steps=300)
+    compare_step(orca, oracle, dict(w, pos=pos, vel=vel))
+
+
+@pytest.mark.parametrize("k", [0, 1, 7, 32])
+def test_step_parity_k(orca, oracle, k):
+    w = W.make("uniform", n=1500, rho=0.3)
+    compare_step(orca, oracle, w, maxNeighbors=k)
+
+
+def test_tie_lattice_neighbors(orca, oracle):
+    pos = W.tie_lattice(30)
+    w = dict(pos=pos, vel=np.zeros_like(pos), pref=np.zeros_like(pos), goals=None,
+             params=dict(W.DEFAULT_PARAMS, neighborDist=2.5, radius=0.2))
+    compare_step(orca, oracle, w)
+
+
+def test_coincident_agents(orca, oracle):
+    """Coincident agents with equal velocity (reading Q15, g1): deterministic +-x push."""
+    rng = np.random.default_rng(9)
+    pos = rng.uniform(0, 40, (400, 2)).astype(np.float32)
+    pos[300:310] = pos[0]  # ten coincident copies of agent 0
+    vel = np.zeros_like(pos)
+    pref = rng.uniform(-1, 1, (400, 2)).astype(np.float32)
+    w = dict(pos=pos, vel=vel, pref=pref, goals=None, params=dict(W.DEFAULT_PARAMS))
+    rep = compare_step(orca, oracle, w, max_deg=11)
+    assert rep["n_deg"] == 11
+
+
+def test_empty_and_single(orca, oracle):
+    o = orca.Orca(W.DEFAULT_PARAMS)
+    e = np.zeros((0, 2), np.float32)
+    o.set_agents(e, e, e)
+    o.step(3)
+    p, v = o.get_state()
+    assert p.shape == (0, 2)
+    one = np.array([[1.0, 2.0]], np.float32)
+    o.set_agents(one, np.zeros_like(one), np.array([[3.0, 0.0]], np.float32))
+    o.step(1)
+    p, v = o.get_state()
+    assert np.allclose(v, [[1.33, 0.0]], atol=1e-6) and np.allclose(p, [[1.0 + 0.25 * 1.33, 2.0]], atol=1e-6)
+    o.close()
+
+
+def test_not_ready_and_nan(orca):
+    o = orca.Orca(W.DEFAULT_PARAMS)
+    with pytest.raises(orca.OrcaError) as e:
+        o.step(1)
+    assert e.value.status == 2
+    bad = np.array([[np.nan, 0.0]], np.float32)
+    with pytest.raises(orca.OrcaError) as e:
+        o.set_agents(bad, np.zeros_like(bad), np.zeros_like(bad))
+    assert e.value.status == 1
+    o.close()
+
+
+def test_device_pointer_inputs(orca, oracle):
+    """torch CUDA tensors in, torch CUDA tensors out: same result as host arrays."""
+    import torch
+    w = W.make("uniform", n=2000, rho=0.25)
+    a, _ = _ctx(orca, w)
+    a.step(3)
+    pa, va = a.get_state()
+    b = orca.Orca(w["params"])
+    tp = torch.from_numpy(w["pos"]).cuda()
+    tv = torch.from_numpy(w["vel"]).cuda()
+    tq = torch.from_numpy(w["pref"]).cuda()
+    b.set_agents(tp, tv, tq)
+    b.step(3)
+    op = torch.empty_like(tp)
+    ov = torch.empty_like(tv)
+    b.get_state(op, ov)
+    assert np.array_equal(op.cpu().numpy(), pa) and np.array_equal(ov.cpu().numpy(), va)
+    a.close()
+    b.close()
+
+
+def test_deterministic_and_graph_equals_timed(orca):
+    w = W.make("uniform", n=20000, rho=0.25)
+    a, _ = _ctx(orca, w)
+    b, _ = _ctx(orca, w)
+    c, _ = _ctx(orca, w)
+    a.step(10)
+    b.step(10)
+    c.step_timed(10)
+    pa, va = a.get_state()
+    pb, vb = b.get_state()
+    pc, vc = c.get_state()
+    assert np.array_equal(pa, pb) and np.array_equal(va, vb)
+    assert np.array_equal(pa, pc) and np.array_equal(va, vc)
+    for o in (a, b, c):
+        o.close()
+
+
+def test_multistep_invariants_circle(orca):
+    """C0 on the GPU: speed cap every step; all agents reach their goals by step 1000."""
+    w = W.make("circle")
+    o, p = _ctx(orca, w)
+    for _ in range(20):
+        o.step(50)
+        pos, vel = o.get_state()
+        assert np.all(np.hypot(vel[:, 0], vel[:, 1]) <= p["maxSpeed"] * (1 + 1e-6))
+    dist = np.hypot(*(pos - w["goals"]).T)
+    assert np.all(dist < p["radius"]), np.sort(dist)[-5:]
+    st = o.stats()
+    assert st["steps"] == 1000 and st["infeasible"] > 0
+    o.close()
+
+
+# ------------------------------------------------------- full sizes, sampled outputs
+@pytest.mark.parametrize("config", ["uniform", "uniform_1m", "dense"])
+def test_full_size_sampled(orca, oracle, config):
+    """BASELINE sizes in the bench's launch configuration; the oracle recomputes a random
+    sample of agents one by one on the full state."""
+    w = W.make(config)
+    rng = np.random.default_rng(123)
+    ag = np.sort(rng.choice(len(w["pos"]), 1500, replace=False))
+    rep = compare_step(orca, oracle, w, agents=ag)
+    assert rep["n"] == 1500
