@@ -359,29 +359,77 @@ struct StepArgs {
     Work* work;  // dry step only: instrumented work counts (nullable)
 };
 
-__device__ __forceinline__ bool key_less(double ka, uint32_t ia, double kb, uint32_t ib) {
-    return ka < kb || (ka == kb && ia < ib);
-}
-
 constexpr int kStepThreads = 128;
 
-// bytes of dynamic shared memory per thread for neighbour list + lines + LP3 lines
-__host__ __device__ constexpr int step_smem_per_thread(int k) { return k * (8 + 4 + 4 + 12 + 12); }
+// Per-thread shared memory (32-bit words, one column per thread, stride kStepThreads):
+//   region L: 3k words -- the top-k list as (key.lo, key.hi, j) during selection, then
+//             overwritten in place by the half-planes (nx, ny, s) in the same slots;
+//   region B: max(k + 24, 3k) words -- candidate buffer during the scan, then the LP3
+//             projected lines (3k words).
+__host__ __device__ constexpr int step_buf_words(int k) { return (k + 24 > 3 * k) ? k + 24 : 3 * k; }
+__host__ __device__ constexpr int step_smem_per_thread(int k) { return 4 * (3 * k + step_buf_words(k)); }
+
+// Exact (kappa, id) order of candidate j against list slot key/j (ids loaded only on
+// an exact key tie).
+__device__ __forceinline__ bool cand_less(double ka, uint32_t ja, double kb, uint32_t jb,
+                                          const uint32_t* __restrict__ idS) {
+    if (ka != kb) return ka < kb;
+    return idS[ja] < idS[jb];
+}
+
+__device__ __forceinline__ double exact_key(float2 pj, float2 pi) {
+    const double Dx = __dsub_rn((double)pj.x, (double)pi.x);
+    const double Dy = __dsub_rn((double)pj.y, (double)pi.y);
+    return __dadd_rn(__dmul_rn(Dx, Dx), __dmul_rn(Dy, Dy));
+}
+
+// Merge the nb buffered candidates into the sorted top-k list (exact keys, ties by id).
+// Returns the new list length; the list is (key.lo, key.hi, j) in L0/L1/L2.
+__device__ __forceinline__ int merge_candidates(uint32_t* L0, uint32_t* L1, uint32_t* L2, int cnt, int k,
+                                                const uint32_t* Bf, int nb, float2 pi, double nd2,
+                                                const float2* __restrict__ posS, const uint32_t* __restrict__ idS) {
+    constexpr int T = kStepThreads;
+    for (int b = 0; b < nb; ++b) {
+        const uint32_t j = Bf[b * T];
+        const double key = exact_key(posS[j], pi);
+        if (!(key < nd2)) continue;  // strictly within r_obs (reading Q10)
+        if (cnt == k) {
+            const double lk = __hiloint2double((int)L1[(k - 1) * T], (int)L0[(k - 1) * T]);
+            if (!cand_less(key, j, lk, L2[(k - 1) * T], idS)) continue;
+        }
+        int p = (cnt < k) ? cnt : k - 1;
+        while (p > 0) {
+            const double pk = __hiloint2double((int)L1[(p - 1) * T], (int)L0[(p - 1) * T]);
+            if (!cand_less(key, j, pk, L2[(p - 1) * T], idS)) break;
+            L0[p * T] = L0[(p - 1) * T];
+            L1[p * T] = L1[(p - 1) * T];
+            L2[p * T] = L2[(p - 1) * T];
+            --p;
+        }
+        L0[p * T] = (uint32_t)__double2loint(key);
+        L1[p * T] = (uint32_t)__double2hiint(key);
+        L2[p * T] = j;
+        if (cnt < k) ++cnt;
+    }
+    return cnt;
+}
 
 template <bool DRY>
 __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
     constexpr bool CNT = DRY;  // only the debug variant counts work
     WorkT w{0, 0, 0, 0, 0};
     extern __shared__ __align__(16) unsigned char smem[];
-    const int T = kStepThreads;
+    constexpr int T = kStepThreads;
     const int tid = threadIdx.x;
     const int k = a.m.k;
-    double* sKey = reinterpret_cast<double*>(smem) + tid;
-    uint32_t* sId = reinterpret_cast<uint32_t*>(smem + (size_t)8 * k * T) + tid;
-    uint32_t* sJ = reinterpret_cast<uint32_t*>(smem + (size_t)12 * k * T) + tid;
-    float* fbase = reinterpret_cast<float*>(smem + (size_t)16 * k * T) + tid;
-    const Lines L{fbase, fbase + k * T, fbase + 2 * k * T};
-    const Lines P{fbase + 3 * k * T, fbase + 4 * k * T, fbase + 5 * k * T};
+    const int capB = step_buf_words(k);
+    uint32_t* L0 = reinterpret_cast<uint32_t*>(smem) + tid;
+    uint32_t* L1 = L0 + k * T;
+    uint32_t* L2 = L1 + k * T;
+    uint32_t* Bf = L2 + k * T;
+    const Lines L{reinterpret_cast<float*>(L0), reinterpret_cast<float*>(L1), reinterpret_cast<float*>(L2)};
+    const Lines P{reinterpret_cast<float*>(Bf), reinterpret_cast<float*>(Bf) + k * T,
+                  reinterpret_cast<float*>(Bf) + 2 * k * T};
 
     const int i = blockIdx.x * T + tid;
     const bool active = i < a.n;
@@ -396,56 +444,97 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
         const int cy = cell_coord(pi.y, a.g.oy, a.g.cs, a.g.ny);
 
         // ---- 2. k nearest within r_obs over the 3x3 bins -------------
+        // Five contiguous runs of the cell-sorted arrays: own cell first (tightest
+        // neighbours), then the rest of the own column, then the two side columns.
+        int rb[5], re[5];
+        {
+            const int ny = a.g.ny;
+            const int r0 = max(cy - 1, 0), r1 = min(cy + 1, ny - 1);
+            const int c = cx * ny + cy;
+            const int s0 = (int)a.cellStart[cx * ny + r0], s1 = (int)a.cellStart[c];
+            const int s2 = (int)a.cellStart[c + 1], s3 = (int)a.cellStart[cx * ny + r1 + 1];
+            rb[0] = s1; re[0] = s2;
+            rb[1] = s0; re[1] = s1;
+            rb[2] = s2; re[2] = s3;
+            if (cx > 0) {
+                rb[3] = (int)a.cellStart[(cx - 1) * ny + r0];
+                re[3] = (int)a.cellStart[(cx - 1) * ny + r1 + 1];
+            } else {
+                rb[3] = re[3] = 0;
+            }
+            if (cx + 1 < a.g.nx) {
+                rb[4] = (int)a.cellStart[(cx + 1) * ny + r0];
+                re[4] = (int)a.cellStart[(cx + 1) * ny + r1 + 1];
+            } else {
+                rb[4] = re[4] = 0;
+            }
+        }
         int cnt = 0;
-        float thr = a.m.nd2Fup;  // fp32 prefilter; the fp64 key decides
-        double lastKey = a.m.nd2D;
-        uint32_t lastId = 0xffffffffu;
         if (k > 0) {
-            const int r0 = max(cy - 1, 0), r1 = min(cy + 1, a.g.ny - 1);
-            for (int col = max(cx - 1, 0); col <= min(cx + 1, a.g.nx - 1); ++col) {
-                const int b = (int)a.cellStart[col * a.g.ny + r0];
-                const int e = (int)a.cellStart[col * a.g.ny + r1 + 1];
-                if (CNT) w.cand += (uint32_t)(e - b);
-                for (int j = b; j < e; ++j) {
-                    const float2 pj = a.posS[j];
-                    const float dx = pj.x - pi.x, dy = pj.y - pi.y;
-                    const float d2 = fmaf(dx, dx, dy * dy);
-                    if (d2 > thr || j == i) continue;
-                    const double Dx = __dsub_rn((double)pj.x, (double)pi.x);
-                    const double Dy = __dsub_rn((double)pj.y, (double)pi.y);
-                    const double key = __dadd_rn(__dmul_rn(Dx, Dx), __dmul_rn(Dy, Dy));
-                    if (!(key < a.m.nd2D)) continue;
-                    const uint32_t idj = a.idS[j];
-                    if (cnt == k && !key_less(key, idj, lastKey, lastId)) continue;
-                    int p = (cnt < k) ? cnt : k - 1;
-                    while (p > 0 && key_less(key, idj, sKey[(p - 1) * T], sId[(p - 1) * T])) {
-                        sKey[p * T] = sKey[(p - 1) * T];
-                        sId[p * T] = sId[(p - 1) * T];
-                        sJ[p * T] = sJ[(p - 1) * T];
-                        --p;
-                    }
-                    sKey[p * T] = key;
-                    sId[p * T] = idj;
-                    sJ[p * T] = (uint32_t)j;
-                    if (cnt < k) ++cnt;
-                    if (cnt == k) {
-                        lastKey = sKey[(k - 1) * T];
-                        lastId = sId[(k - 1) * T];
-                        // fp32 d2 has relative error < 2^-22; margin 2^-20, rounded up
-                        thr = __fmul_ru(__double2float_ru(lastKey), 1.0f + 0x1p-20f);
-                    }
+            int ncand = 0;
+#pragma unroll
+            for (int r = 0; r < 5; ++r) ncand += re[r] - rb[r];
+            // Radius guess from the 3x3 density: r^2 = 2.2 k / (pi rho), rho = ncand / (9 cs^2)
+            // (about 22 expected hits for k = 10).  Exactness does not depend on it: a too
+            // small guess that yields < k neighbours triggers a full-radius rescan.
+            float thr = a.m.nd2Fup;
+            bool guessed = false;
+            if (ncand > 4 * k) {
+                const float g = 2.2f * (float)k * 9.0f * a.g.cs * a.g.cs / (3.14159265f * (float)ncand);
+                if (g < thr) {
+                    thr = g;
+                    guessed = true;
                 }
             }
+            for (int pass = 0; pass < 2; ++pass) {
+                const float thrPass = thr;
+                int nb = 0;
+#pragma unroll
+                for (int r = 0; r < 5; ++r) {
+                    for (int j = rb[r]; j < re[r]; ++j) {
+                        const float2 pj = a.posS[j];
+                        const float dx = pj.x - pi.x, dy = pj.y - pi.y;
+                        const float d2 = fmaf(dx, dx, dy * dy);
+                        if (d2 <= thr && j != i) {
+                            Bf[nb * T] = (uint32_t)j;
+                            if (++nb == capB) {  // buffer full: merge, tighten the bound
+                                cnt = merge_candidates(L0, L1, L2, cnt, k, Bf, nb, pi, a.m.nd2D, a.posS, a.idS);
+                                nb = 0;
+                                if (cnt == k) {
+                                    const double lk = __hiloint2double((int)L1[(k - 1) * T], (int)L0[(k - 1) * T]);
+                                    // fp32 d2 has relative error < 2^-22: margin 2^-20, rounded up
+                                    thr = fminf(thr, __fmul_ru(__double2float_ru(lk), 1.0f + 0x1p-20f));
+                                }
+                            }
+                        }
+                    }
+                }
+                cnt = merge_candidates(L0, L1, L2, cnt, k, Bf, nb, pi, a.m.nd2D, a.posS, a.idS);
+                if (!guessed) break;
+                // Exact only if every candidate rejected by the guessed radius is strictly
+                // beyond the k-th key: rejected => key > thrPass (1 - 2^-22).
+                if (cnt == k) {
+                    const double lk = __hiloint2double((int)L1[(k - 1) * T], (int)L0[(k - 1) * T]);
+                    if (lk < (double)thrPass * (1.0 - 0x1p-20)) break;
+                }
+                cnt = 0;  // rescan at the full radius
+                thr = a.m.nd2Fup;
+                guessed = false;
+            }
+            if (CNT) w.cand += (uint32_t)ncand;
         }
 
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
+        // (half-plane q overwrites list slot q in place: j is read before the write)
         for (int q = 0; q < cnt; ++q) {
-            const uint32_t j = sJ[q * T];
+            const uint32_t j = L2[q * T];
             const float2 pj = a.posS[j];
             const float2 vj = a.velS[j];
+            const uint32_t idj = a.idS[j];
+            if (DRY && a.dbgNbr) a.dbgNbr[(size_t)idi * k + q] = (int32_t)idj;
             float nx, ny, s;
             int coll;
-            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, sId[q * T], a.m, nx, ny, s, coll);
+            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, idj, a.m, nx, ny, s, coll);
             nColl += coll;
             L.nx[q * T] = nx;
             L.ny[q * T] = ny;
@@ -481,7 +570,7 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
             if (a.dbgFlags) a.dbgFlags[idi] = (uint8_t)fl;
             if (a.dbgCnt) a.dbgCnt[idi] = cnt;
             if (a.dbgNbr)
-                for (int q = 0; q < k; ++q) a.dbgNbr[(size_t)idi * k + q] = (q < cnt) ? (int32_t)sId[q * T] : -1;
+                for (int q = cnt; q < k; ++q) a.dbgNbr[(size_t)idi * k + q] = -1;
         } else {
             const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
             const uint32_t c = cell_id(pn.x, pn.y, a.g);
