@@ -25,6 +25,7 @@
 /* g2 flag threshold: pairs whose |det| is this small may be decided differently by an
  * fp32 solver that uses a 1e-5 tolerance (reading Q9 + fp32 rounding slack). */
 #define OR_G2_DET 2e-5
+#define OR_G2_SLACK 1e-6 /* fp32 rounding slack on line offsets */
 /* g3 thresholds (SURVEY §8(c) degenerate class g3). */
 #define OR_G3_EPS 1e-6
 
@@ -270,7 +271,11 @@ static int lp1(const or_line *L, int no, double r, const double opt[2], int dirO
     for (int i = 0; i < no; ++i) {
         const double den = det2(L[no].dx, L[no].dy, L[i].dx, L[i].dy);
         const double num = det2(L[i].dx, L[i].dy, L[no].px - L[i].px, L[no].py - L[i].py);
-        if (fabs(den) <= OR_G2_DET && diag) *diag |= OR_FLAG_G2_PARALLEL;
+        /* g2: nearly parallel AND the crossing t = num/den lies inside the chord's reach,
+         * i.e. an fp32 solver's "parallel -> fail if pointing away, else skip" rule could
+         * decide differently from the exact crossing (reading Q9) */
+        if (fabs(den) <= OR_G2_DET && fabs(num) <= OR_G2_DET * r + OR_G2_SLACK && diag)
+            *diag |= OR_FLAG_G2_PARALLEL;
         if (fabs(den) <= OR_EPS) {
             if (num < 0.0) return 0; /* parallel and pointing away */
             continue;
@@ -333,7 +338,12 @@ void or_lp3(const or_line *L, int n, int begin, double r, double v[2], uint32_t 
             for (int j = 0; j < i; ++j) {
                 or_line q;
                 const double determinant = det2(L[i].dx, L[i].dy, L[j].dx, L[j].dy);
-                if (fabs(determinant) <= OR_G2_DET && diag) *diag |= OR_FLAG_G2_PARALLEL;
+                /* g2: nearly parallel, same direction (an fp32 solver skips the pair) and the
+                 * lines so close that their bisector still crosses the speed disc (reading Q9) */
+                if (fabs(determinant) <= OR_G2_DET && L[i].dx * L[j].dx + L[i].dy * L[j].dy > 0.0 &&
+                    fabs(det2(L[i].dx, L[i].dy, L[j].px - L[i].px, L[j].py - L[i].py)) <= OR_G2_DET * r + OR_G2_SLACK &&
+                    diag)
+                    *diag |= OR_FLAG_G2_PARALLEL;
                 if (fabs(determinant) <= OR_EPS) {
                     if (L[i].dx * L[j].dx + L[i].dy * L[j].dy > 0.0) continue; /* same direction */
                     q.px = 0.5 * (L[i].px + L[j].px);                            /* opposite */

@@ -20,6 +20,10 @@ using namespace orca;
 
 namespace {
 
+constexpr int kSubRowsLog2 = 3;  // 8 sort sub-rows per cell
+
+int scan_tiles(int64_t C) { return (int)((C + kScanTile - 1) / kScanTile); }
+
 thread_local std::string g_last_error;
 
 orca_status fail(orca_status s, const std::string& msg) {
@@ -70,13 +74,14 @@ struct orca_ctx {
     bool goals = false;
     float prefSpeed = 0.0f;
     Grid g{};
-    int64_t C = 0;
+    int64_t C = 0;     // sort bins = cells x 2^lgS sub-rows
     // sorted (rest) state and work buffers
     float2 *posS = nullptr, *velS = nullptr, *auxS = nullptr;
     uint32_t* idS = nullptr;
     float2 *posW = nullptr, *velW = nullptr, *auxW = nullptr;
     uint32_t *idW = nullptr, *cellW = nullptr, *rankW = nullptr;
-    uint32_t *count = nullptr, *cellStart = nullptr;
+    uint32_t *count = nullptr, *binStart = nullptr;
+    unsigned long long* scanStatus = nullptr;  // look-back status words + ticket (zeroed per scan)
     unsigned long long* stats = nullptr;
     float* partial = nullptr;  // k_minmax partials
     float2* tmp2 = nullptr;    // id-ordered scratch (get_state / set_goals)
@@ -122,7 +127,7 @@ StepArgs make_args(orca_ctx* c) {
     a.velS = c->velS;
     a.auxS = c->auxS;
     a.idS = c->idS;
-    a.cellStart = c->cellStart;
+    a.binStart = c->binStart;
     a.posW = c->posW;
     a.velW = c->velW;
     a.auxW = c->auxW;
@@ -147,12 +152,24 @@ orca_status ensure_capacity(orca_ctx* c, int64_t n, int64_t C) {
     }
     if (C > c->cellCap) {
         dfree(c->count);
-        dfree(c->cellStart);
-        CK(cudaMalloc(&c->count, C * sizeof(uint32_t)));
-        CK(cudaMalloc(&c->cellStart, (C + 1) * sizeof(uint32_t)));
+        dfree(c->binStart);
+        dfree(c->scanStatus);
+        CK(cudaMalloc(&c->count, (C + 4) * sizeof(uint32_t)));
+        CK(cudaMalloc(&c->binStart, (C + 1) * sizeof(uint32_t)));
+        CK(cudaMalloc(&c->scanStatus, (scan_tiles(C) + 1) * sizeof(unsigned long long)));
         c->cellCap = C;
     }
     return ORCA_OK;
+}
+
+// exclusive scan of the bin counts (memset of the look-back status + one launch)
+cudaError_t enqueue_scan(orca_ctx* c) {
+    const int tiles = scan_tiles(c->C);
+    cudaError_t e = cudaMemsetAsync(c->scanStatus, 0, (tiles + 1) * sizeof(unsigned long long), c->stream);
+    if (e != cudaSuccess) return e;
+    k_scan<<<tiles, 1024, 0, c->stream>>>(c->count, c->binStart, (int)c->C, c->scanStatus,
+                                          reinterpret_cast<unsigned int*>(c->scanStatus + tiles));
+    return cudaGetLastError();
 }
 
 void drop_graph(orca_ctx* c) {
@@ -170,10 +187,10 @@ cudaError_t enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
         k_step<false><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
     }
     if (ev) cudaEventRecord(ev[1], c->stream);
-    k_scan<<<1, 1024, 0, c->stream>>>(c->count, c->cellStart, (int)c->C);
+    enqueue_scan(c);
     if (ev) cudaEventRecord(ev[2], c->stream);
     if (n > 0)
-        k_scatter<<<grid_blocks(n, 256), 256, 0, c->stream>>>(n, c->cellW, c->rankW, c->cellStart, c->posW, c->velW,
+        k_scatter<<<grid_blocks(n, 256), 256, 0, c->stream>>>(n, c->cellW, c->rankW, c->binStart, c->posW, c->velW,
                                                               c->auxW, c->idW, c->posS, c->velS, c->auxS, c->idS);
     if (ev) cudaEventRecord(ev[3], c->stream);
     return cudaGetLastError();
@@ -242,11 +259,12 @@ void orca_destroy(orca_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     drop_graph(c);
     float2** f2[] = {&c->posS, &c->velS, &c->auxS, &c->posW, &c->velW, &c->auxW, &c->tmp2, &c->tmp2b};
-    uint32_t** u4[] = {&c->idS, &c->idW, &c->cellW, &c->rankW, &c->count, &c->cellStart};
+    uint32_t** u4[] = {&c->idS, &c->idW, &c->cellW, &c->rankW, &c->count, &c->binStart};
     for (auto pp : f2) dfree(*pp);
     for (auto pp : u4) dfree(*pp);
     dfree(c->stats);
     dfree(c->partial);
+    dfree(c->scanStatus);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -293,6 +311,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     const float cs = c->p.neighborDist;
     Grid g{};
     g.cs = cs;
+    g.lgS = kSubRowsLog2;
     if (n == 0) {
         g.ox = g.oy = 0.0f;
         g.nx = g.ny = 1;
@@ -302,13 +321,13 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
         g.oy = oy;
         const double tx = std::floor(((double)mx[0] - (double)g.ox) / (double)cs);
         const double ty = std::floor(((double)mx[1] - (double)g.oy) / (double)cs);
-        if (tx + 2 > 1e9 || ty + 2 > 1e9 || (tx + 2) * (ty + 2) > (double)(1 << 28))
-            return fail(ORCA_ERR_CAPACITY, "grid would exceed 2^28 cells");
+        if (tx + 2 > 1e9 || ty + 2 > 1e9 || (tx + 2) * (ty + 2) * (double)(1 << kSubRowsLog2) > (double)(1 << 28))
+            return fail(ORCA_ERR_CAPACITY, "grid would exceed 2^28 sort bins");
         g.nx = (int)tx + 2;
         g.ny = (int)ty + 2;
     }
     c->g = g;
-    c->C = (int64_t)g.nx * g.ny;
+    c->C = ((int64_t)g.nx * g.ny) << g.lgS;
     st = ensure_capacity(c, n, c->C);
     if (st) return st;
     c->n = n;
@@ -318,9 +337,9 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
         k_iota<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->idW);
         k_hash<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->posW, c->g, c->cellW, c->rankW, c->count);
     }
-    k_scan<<<1, 1024, 0, c->stream>>>(c->count, c->cellStart, (int)c->C);
+    CK(enqueue_scan(c));
     if (n > 0)
-        k_scatter<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->cellW, c->rankW, c->cellStart, c->posW,
+        k_scatter<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->cellW, c->rankW, c->binStart, c->posW,
                                                               c->velW, c->auxW, c->idW, c->posS, c->velS, c->auxS,
                                                               c->idS);
     CK(cudaGetLastError());

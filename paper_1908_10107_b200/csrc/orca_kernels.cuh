@@ -2,7 +2,7 @@
 //
 // Product path.  Shares no code with oracle/.  Every stage of the step runs here:
 //   k_hash      cell hash + histogram (atomic rank = in-cell slot)     FLAME bins
-//   k_scan      exclusive scan of the per-cell counts -> cellStart
+//   k_scan      exclusive scan (decoupled look-back) of the per-bin counts -> binStart
 //   k_scatter   counting-sort permutation into cell-sorted SoA
 //   k_step      3x3 k-nearest query -> ORCA half-planes -> LP2/LP3 -> integrate -> next hash
 //               (P:77 model, Fig. 1 geometry, P:80 fallback, P:82 incremental LP)
@@ -48,7 +48,8 @@ struct WorkT {
 
 struct Grid {
     float ox, oy, cs;  // origin, cell size (fp32 values; widened exactly to fp64)
-    int nx, ny;        // dims
+    int nx, ny;        // dims (cells of size cs = r_obs)
+    int lgS;           // each cell is split into 2^lgS sub-rows for the sort order
 };
 
 struct Model {
@@ -72,10 +73,23 @@ __device__ __forceinline__ int cell_coord(float x, float o, float cs, int nc) {
     return (int)f;
 }
 
-__device__ __forceinline__ uint32_t cell_id(float x, float y, const Grid& g) {
-    int cx = cell_coord(x, g.ox, g.cs, g.nx);
-    int cy = cell_coord(y, g.oy, g.cs, g.ny);
-    return (uint32_t)cx * (uint32_t)g.ny + (uint32_t)cy;  // column-major: strips are ranges
+// Sub-row of y: floor(t * 2^lgS) with t the same fp64 quotient as cell_coord, clamped;
+// its >> lgS is exactly the clamped cell row (scaling by a power of two is exact).
+__device__ __forceinline__ int subrow_coord(float y, const Grid& g) {
+    const double t = __ddiv_rn(__dsub_rn((double)y, (double)g.oy), (double)g.cs);
+    double f = floor(t * (double)(1 << g.lgS));
+    f = fmax(f, 0.0);
+    f = fmin(f, (double)((g.ny << g.lgS) - 1));
+    return (int)f;
+}
+
+// Bin id of the sort order: column-major over (cx, sub-row), so a strip of columns is
+// one contiguous id range, a coarse cell is 2^lgS consecutive bins, and each column run
+// of the 3x3 stencil is ordered by y at sub-row granularity.
+__device__ __forceinline__ uint32_t bin_id(float x, float y, const Grid& g) {
+    const int cx = cell_coord(x, g.ox, g.cs, g.nx);
+    const int sy = subrow_coord(y, g);
+    return (uint32_t)cx * (uint32_t)(g.ny << g.lgS) + (uint32_t)sy;
 }
 
 // ------------------------------------------------------------------------- binning
@@ -83,69 +97,101 @@ __global__ void k_hash(int n, const float2* __restrict__ pos, Grid g, uint32_t* 
                        uint32_t* __restrict__ rank, uint32_t* __restrict__ count) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         float2 p = pos[i];
-        uint32_t c = cell_id(p.x, p.y, g);
+        uint32_t c = bin_id(p.x, p.y, g);
         cell[i] = c;
         rank[i] = atomicAdd(&count[c], 1u);
     }
 }
 
-// Single-CTA exclusive scan over C counts, tiled (1024 threads x 4 per tile).  Writes
-// cellStart[0..C] and re-zeroes count for the next step's histogram.
-__global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uint32_t* __restrict__ cellStart,
-                                               int C) {
+// Single-pass exclusive scan (decoupled look-back) over C bin counts: tiles of 4096
+// (1024 threads x 4).  status[] (64-bit: flag << 62 | value) and the tile ticket must be
+// zero at launch.  Writes binStart[0..C] and re-zeroes count for the next histogram.
+constexpr unsigned long long kAggFlag = 1ull << 62, kIncFlag = 2ull << 62, kValMask = (1ull << 62) - 1;
+constexpr int kScanTile = 4096;
+
+__global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uint32_t* __restrict__ binStart, int C,
+                                               unsigned long long* __restrict__ status,
+                                               unsigned int* __restrict__ ticket) {
     __shared__ uint32_t warpSums[32];
-    __shared__ uint32_t carryS;
+    __shared__ uint32_t tileS, prefixS;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) carryS = 0;
+    if (tid == 0) tileS = atomicAdd(ticket, 1u);
     __syncthreads();
-    for (int base = 0; base < C; base += 4096) {
-        uint32_t v[4];
-        const int i0 = base + tid * 4;
+    const int tile = (int)tileS;
+    const int base = tile * kScanTile;
+    uint32_t v[4];
+    const int i0 = base + tid * 4;
+    if (i0 + 3 < C) {
+        const uint4 q = *reinterpret_cast<const uint4*>(count + i0);
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) v[q] = (i0 + q < C) ? count[i0 + q] : 0u;
-        uint32_t local = v[0] + v[1] + v[2] + v[3];
-        uint32_t incl = local;
+    }
+    const uint32_t local = v[0] + v[1] + v[2] + v[3];
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warpSums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t w = warpSums[lane];
+        uint32_t wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
         }
-        if (lane == 31) warpSums[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t w = warpSums[lane];
-            uint32_t wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += y;
+        warpSums[lane] = wi - w;  // exclusive warp offsets
+        const uint32_t total = __shfl_sync(0xffffffffu, wi, 31);
+        if (lane == 0) {
+            // publish the aggregate, look back for the inclusive prefix of earlier tiles
+            volatile unsigned long long* st = status;
+            if (tile == 0) {
+                st[0] = kIncFlag | total;
+                prefixS = 0;
+            } else {
+                st[tile] = kAggFlag | total;
+                unsigned long long pre = 0;
+                int t = tile - 1;
+                while (true) {
+                    unsigned long long x;
+                    do {
+                        x = st[t];
+                    } while ((x >> 62) == 0);
+                    pre += x & kValMask;
+                    if ((x >> 62) == 2) break;
+                    --t;
+                }
+                __threadfence();
+                st[tile] = kIncFlag | (pre + total);
+                prefixS = (uint32_t)pre;
             }
-            warpSums[lane] = wi - w;  // exclusive warp offsets
         }
-        __syncthreads();
-        uint32_t run = carryS + warpSums[wid] + incl - local;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (i0 + q < C) {
-                cellStart[i0 + q] = run;
-                count[i0 + q] = 0u;
-            }
-            run += v[q];
-        }
-        __syncthreads();
-        if (tid == 1023) carryS = run;
-        __syncthreads();
     }
-    if (tid == 0) cellStart[C] = carryS;
+    __syncthreads();
+    uint32_t run = prefixS + warpSums[wid] + incl - local;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (i0 + q < C) {
+            binStart[i0 + q] = run;
+            count[i0 + q] = 0u;
+        }
+        run += v[q];
+    }
+    if ((C - 1) / 4 == tile * 1024 + tid) binStart[C] = run;  // owner of element C-1
 }
 
 __global__ void k_scatter(int n, const uint32_t* __restrict__ cell, const uint32_t* __restrict__ rank,
-                          const uint32_t* __restrict__ cellStart, const float2* __restrict__ posW,
+                          const uint32_t* __restrict__ binStart, const float2* __restrict__ posW,
                           const float2* __restrict__ velW, const float2* __restrict__ auxW,
                           const uint32_t* __restrict__ idW, float2* __restrict__ posS, float2* __restrict__ velS,
                           float2* __restrict__ auxS, uint32_t* __restrict__ idS) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t dst = cellStart[cell[i]] + rank[i];
+        const uint32_t dst = binStart[cell[i]] + rank[i];
         posS[dst] = posW[i];
         velS[dst] = velW[i];
         auxS[dst] = auxW[i];
@@ -242,7 +288,9 @@ __device__ __forceinline__ bool lp1(const Lines& L, int T, int no, float r, floa
         const float den = fmaf(njx, Dx, njy * Dy);
         const float num = sj - si * fmaf(njx, nix, njy * niy);
         if (fabsf(den) <= kEps) {
-            fl |= FL_G2;
+            // parallel: fail if pointing away, else skip; an eps-hit matters only if the
+            // exact crossing t = num/den could fall inside the chord (reading Q9)
+            if (fabsf(num) <= 2e-5f * r + 1e-6f) fl |= FL_G2;
             if (num > 0.0f) return false;
             continue;
         }
@@ -309,9 +357,10 @@ __device__ __forceinline__ void lp3(const Lines& L, const Lines& P, int T, int n
             for (int j = 0; j < i; ++j) {
                 const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
                 const float det = fmaf(nix, njy, -niy * njx);
-                if (fabsf(det) <= kEps) {
-                    fl |= FL_G2;
-                    if (fmaf(nix, njx, niy * njy) > 0.0f) continue;  // same direction
+                if (fabsf(det) <= kEps && fmaf(nix, njx, niy * njy) > 0.0f) {
+                    // same direction: skipped; matters only if the lines nearly coincide
+                    if (fabsf(sj - si) <= 2e-5f * r + 1e-6f) fl |= FL_G2;
+                    continue;
                 }
                 if (CNT) ++w.proj;
                 const float dx = njx - nix, dy = njy - niy;
@@ -341,7 +390,7 @@ struct StepArgs {
     const float2* __restrict__ velS;
     const float2* __restrict__ auxS;  // prefVel, or goal when m.goals
     const uint32_t* __restrict__ idS;
-    const uint32_t* __restrict__ cellStart;
+    const uint32_t* __restrict__ binStart;
     // outputs of a real step (work buffers, next step's binning)
     float2* posW;
     float2* velW;
@@ -441,42 +490,24 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
         const float2 aux = a.auxS[i];
         const uint32_t idi = a.idS[i];
         const int cx = cell_coord(pi.x, a.g.ox, a.g.cs, a.g.nx);
-        const int cy = cell_coord(pi.y, a.g.oy, a.g.cs, a.g.ny);
+        const int lgS = a.g.lgS;
+        const int nyS = a.g.ny << lgS;
+        const int cy = subrow_coord(pi.y, a.g) >> lgS;
 
         // ---- 2. k nearest within r_obs over the 3x3 bins -------------
-        // Five contiguous runs of the cell-sorted arrays: own cell first (tightest
-        // neighbours), then the rest of the own column, then the two side columns.
-        int rb[5], re[5];
-        {
-            const int ny = a.g.ny;
-            const int r0 = max(cy - 1, 0), r1 = min(cy + 1, ny - 1);
-            const int c = cx * ny + cy;
-            const int s0 = (int)a.cellStart[cx * ny + r0], s1 = (int)a.cellStart[c];
-            const int s2 = (int)a.cellStart[c + 1], s3 = (int)a.cellStart[cx * ny + r1 + 1];
-            rb[0] = s1; re[0] = s2;
-            rb[1] = s0; re[1] = s1;
-            rb[2] = s2; re[2] = s3;
-            if (cx > 0) {
-                rb[3] = (int)a.cellStart[(cx - 1) * ny + r0];
-                re[3] = (int)a.cellStart[(cx - 1) * ny + r1 + 1];
-            } else {
-                rb[3] = re[3] = 0;
-            }
-            if (cx + 1 < a.g.nx) {
-                rb[4] = (int)a.cellStart[(cx + 1) * ny + r0];
-                re[4] = (int)a.cellStart[(cx + 1) * ny + r1 + 1];
-            } else {
-                rb[4] = re[4] = 0;
-            }
-        }
+        // Each column of the stencil is one contiguous run of the sorted arrays, ordered by
+        // sub-row.  A radius guess rg from the local density restricts every run to the
+        // sub-rows within rg of the agent and skips a side column farther than rg; the
+        // result is exact by the check below (else one full 3x3 rescan).
         int cnt = 0;
         if (k > 0) {
+            const int rlo = max(cy - 1, 0) << lgS;              // first sub-row of the 3 rows
+            const int rhi = (min(cy + 1, a.g.ny - 1) + 1) << lgS; // one past the last
+            const int c0 = max(cx - 1, 0), c1 = min(cx + 1, a.g.nx - 1);
             int ncand = 0;
-#pragma unroll
-            for (int r = 0; r < 5; ++r) ncand += re[r] - rb[r];
-            // Radius guess from the 3x3 density: r^2 = 2.2 k / (pi rho), rho = ncand / (9 cs^2)
-            // (about 22 expected hits for k = 10).  Exactness does not depend on it: a too
-            // small guess that yields < k neighbours triggers a full-radius rescan.
+            for (int col = c0; col <= c1; ++col)
+                ncand += (int)a.binStart[col * nyS + rhi] - (int)a.binStart[col * nyS + rlo];
+            // r^2 = 2.2 k / (pi rho), rho = ncand / (9 cs^2): ~22 expected hits for k = 10
             float thr = a.m.nd2Fup;
             bool guessed = false;
             if (ncand > 4 * k) {
@@ -488,16 +519,40 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
             }
             for (int pass = 0; pass < 2; ++pass) {
                 const float thrPass = thr;
+                // sub-row window and side columns for this pass
+                int lo = rlo, hi = rhi - 1, cl = c0, cr = c1;
+                if (guessed) {
+                    const float rg = sqrtf(thr) * (1.0f + 1e-6f) + 1e-6f;
+                    const float h = a.g.cs / (float)(1 << lgS);
+                    const float ty = (pi.y - a.g.oy) / h;
+                    // one sub-row of margin each side absorbs the fp32 error of ty
+                    lo = max(lo, (int)floorf(fmaxf(ty - rg / h, -2.0f)) - 1);
+                    hi = min(hi, (int)floorf(fminf(ty + rg / h, (float)nyS + 2.0f)) + 1);
+                    const double xl = (double)a.g.ox + (double)cx * (double)a.g.cs;  // cell's left edge
+                    if ((double)pi.x - xl > (double)rg) cl = cx;                       // left column beyond rg
+                    if (xl + (double)a.g.cs - (double)pi.x > (double)rg) cr = cx;     // right column beyond rg
+                }
                 int nb = 0;
-#pragma unroll
-                for (int r = 0; r < 5; ++r) {
-                    for (int j = rb[r]; j < re[r]; ++j) {
-                        const float2 pj = a.posS[j];
-                        const float dx = pj.x - pi.x, dy = pj.y - pi.y;
-                        const float d2 = fmaf(dx, dx, dy * dy);
-                        if (d2 <= thr && j != i) {
-                            Bf[nb * T] = (uint32_t)j;
-                            if (++nb == capB) {  // buffer full: merge, tighten the bound
+                for (int q = 0; q < 3; ++q) {
+                    const int col = (q == 0) ? cx : (q == 1 ? cx - 1 : cx + 1);  // own column first
+                    if (col < cl || col > cr) continue;
+                    const int b = (int)a.binStart[col * nyS + lo];
+                    const int e = (int)a.binStart[col * nyS + hi + 1];
+                    if (CNT) w.cand += (uint32_t)(e - b);
+                    int j = b;
+                    for (; j + 1 < e; j += 2) {  // 2-way unrolled: two loads in flight
+                        const float2 p0 = a.posS[j];
+                        const float2 p1 = a.posS[j + 1];
+                        const float dx0 = p0.x - pi.x, dy0 = p0.y - pi.y;
+                        const float dx1 = p1.x - pi.x, dy1 = p1.y - pi.y;
+                        const float d20 = fmaf(dx0, dx0, dy0 * dy0);
+                        const float d21 = fmaf(dx1, dx1, dy1 * dy1);
+                        const bool a0 = d20 <= thr && j != i;
+                        const bool a1 = d21 <= thr && j + 1 != i;
+                        if (a0 | a1) {
+                            if (a0) Bf[nb++ * T] = (uint32_t)j;
+                            if (a1) Bf[nb++ * T] = (uint32_t)(j + 1);
+                            if (nb >= capB - 1) {  // buffer (nearly) full: merge, tighten
                                 cnt = merge_candidates(L0, L1, L2, cnt, k, Bf, nb, pi, a.m.nd2D, a.posS, a.idS);
                                 nb = 0;
                                 if (cnt == k) {
@@ -508,20 +563,33 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
                             }
                         }
                     }
+                    if (j < e) {
+                        const float2 p0 = a.posS[j];
+                        const float dx0 = p0.x - pi.x, dy0 = p0.y - pi.y;
+                        if (fmaf(dx0, dx0, dy0 * dy0) <= thr && j != i) Bf[nb++ * T] = (uint32_t)j;
+                        if (nb >= capB - 1) {
+                            cnt = merge_candidates(L0, L1, L2, cnt, k, Bf, nb, pi, a.m.nd2D, a.posS, a.idS);
+                            nb = 0;
+                            if (cnt == k) {
+                                const double lk = __hiloint2double((int)L1[(k - 1) * T], (int)L0[(k - 1) * T]);
+                                thr = fminf(thr, __fmul_ru(__double2float_ru(lk), 1.0f + 0x1p-20f));
+                            }
+                        }
+                    }
                 }
                 cnt = merge_candidates(L0, L1, L2, cnt, k, Bf, nb, pi, a.m.nd2D, a.posS, a.idS);
                 if (!guessed) break;
-                // Exact only if every candidate rejected by the guessed radius is strictly
-                // beyond the k-th key: rejected => key > thrPass (1 - 2^-22).
+                // Exact only if every candidate not kept -- rejected by the guessed radius
+                // (key > thrPass (1 - 2^-22)) or pruned geometrically (distance > rg) -- is
+                // strictly beyond the k-th key.
                 if (cnt == k) {
                     const double lk = __hiloint2double((int)L1[(k - 1) * T], (int)L0[(k - 1) * T]);
                     if (lk < (double)thrPass * (1.0 - 0x1p-20)) break;
                 }
-                cnt = 0;  // rescan at the full radius
+                cnt = 0;  // rescan the full 3x3 stencil at the full radius
                 thr = a.m.nd2Fup;
                 guessed = false;
             }
-            if (CNT) w.cand += (uint32_t)ncand;
         }
 
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
@@ -573,7 +641,7 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
                 for (int q = cnt; q < k; ++q) a.dbgNbr[(size_t)idi * k + q] = -1;
         } else {
             const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
-            const uint32_t c = cell_id(pn.x, pn.y, a.g);
+            const uint32_t c = bin_id(pn.x, pn.y, a.g);
             a.posW[i] = pn;
             a.velW[i] = make_float2(vx, vy);
             a.auxW[i] = aux;
@@ -597,16 +665,18 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
         }
     }
     if (!DRY) {
-        const int cInf = __syncthreads_count(fl & FL_INFEASIBLE);
-        const int cDeg = __syncthreads_count(fl & (FL_G1 | FL_G2));
-        const int cG1 = __syncthreads_count(fl & FL_G1);
-        const int cG2 = __syncthreads_count(fl & FL_G2);
-        const int cG3 = __syncthreads_count(fl & FL_G3);
-        // collision pairs: warp-reduce then one atomic per warp
+        // per-warp counts (ballot + popc), one relaxed atomic per warp and counter; no
+        // block barrier, so fast warps never wait for a slow LP in the same block
+        const int lane = tid & 31;
+        const int cInf = __popc(__ballot_sync(0xffffffffu, fl & FL_INFEASIBLE));
+        const int cDeg = __popc(__ballot_sync(0xffffffffu, fl & (FL_G1 | FL_G2)));
+        const int cG1 = __popc(__ballot_sync(0xffffffffu, fl & FL_G1));
+        const int cG2 = __popc(__ballot_sync(0xffffffffu, fl & FL_G2));
+        const int cG3 = __popc(__ballot_sync(0xffffffffu, fl & FL_G3));
         int c = nColl;
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if ((tid & 31) == 0 && c) atomicAdd(&a.stats[ST_COLLISION], (unsigned long long)c);
-        if (tid == 0) {
+        if (lane == 0) {
+            if (c) atomicAdd(&a.stats[ST_COLLISION], (unsigned long long)c);
             if (cInf) atomicAdd(&a.stats[ST_INFEASIBLE], (unsigned long long)cInf);
             if (cDeg) atomicAdd(&a.stats[ST_DEGENERATE], (unsigned long long)cDeg);
             if (cG1) atomicAdd(&a.stats[ST_G1], (unsigned long long)cG1);
