@@ -23,6 +23,7 @@ namespace {
 constexpr int kSubRowsLog2 = 3;  // 8 sort sub-rows per cell
 
 int scan_tiles(int64_t C) { return (int)((C + kScanTile - 1) / kScanTile); }
+int lp3_blocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + kStepThreads - 1) / kStepThreads, 148 * 8)); }
 
 thread_local std::string g_last_error;
 
@@ -81,7 +82,10 @@ struct orca_ctx {
     float2 *posW = nullptr, *velW = nullptr, *auxW = nullptr;
     uint32_t *idW = nullptr, *cellW = nullptr, *rankW = nullptr;
     uint32_t *count = nullptr, *binStart = nullptr;
-    unsigned long long* scanStatus = nullptr;  // look-back status words + ticket (zeroed per scan)
+    unsigned long long* scanStatus = nullptr;  // look-back status words + ticket + LP3 queue count
+    int4* qEntry = nullptr;                    // LP3 queue (capacity cap)
+    float4* qLines = nullptr;                  // cap x k lines
+    int lp3Smem = 0;
     unsigned long long* stats = nullptr;
     float* partial = nullptr;  // k_minmax partials
     float2* tmp2 = nullptr;    // id-ordered scratch (get_state / set_goals)
@@ -112,6 +116,10 @@ Model make_model(const orca_ctx* c) {
     float nd2f = (float)m.nd2D;
     if ((double)nd2f < m.nd2D) nd2f = std::nextafter(nd2f, INFINITY);
     m.nd2Fup = std::nextafter(nd2f * (1.0f + 0x1p-20f), INFINITY);
+    // fp32 d2 below nd2Lo proves kappa < nd^2 (relative error < 2^-22, margin 2^-20)
+    float nd2d = (float)m.nd2D;
+    if ((double)nd2d > m.nd2D) nd2d = std::nextafter(nd2d, 0.0f);
+    m.nd2Lo = std::nextafter(nd2d * (1.0f - 0x1p-20f), 0.0f);
     m.k = p.maxNeighbors;
     m.goals = c->goals ? 1 : 0;
     m.prefSpeed = c->prefSpeed;
@@ -136,6 +144,10 @@ StepArgs make_args(orca_ctx* c) {
     a.rankW = c->rankW;
     a.count = c->count;
     a.stats = c->stats;
+    a.qEntry = c->qEntry;
+    a.qLines = c->qLines;
+    a.qcap = (int)c->cap;
+    a.qCount = reinterpret_cast<unsigned int*>(c->scanStatus + scan_tiles(c->C) + 1);
     return a;
 }
 
@@ -148,6 +160,10 @@ orca_status ensure_capacity(orca_ctx* c, int64_t n, int64_t C) {
         for (auto pp : u4) dfree(*pp);
         for (auto pp : f2) CK(cudaMalloc(pp, cap * sizeof(float2)));
         for (auto pp : u4) CK(cudaMalloc(pp, cap * sizeof(uint32_t)));
+        dfree(c->qEntry);
+        dfree(c->qLines);
+        CK(cudaMalloc(&c->qEntry, cap * sizeof(int4)));
+        CK(cudaMalloc(&c->qLines, cap * std::max(1, c->p.maxNeighbors) * sizeof(float4)));
         c->cap = cap;
     }
     if (C > c->cellCap) {
@@ -156,7 +172,7 @@ orca_status ensure_capacity(orca_ctx* c, int64_t n, int64_t C) {
         dfree(c->scanStatus);
         CK(cudaMalloc(&c->count, (C + 4) * sizeof(uint32_t)));
         CK(cudaMalloc(&c->binStart, (C + 1) * sizeof(uint32_t)));
-        CK(cudaMalloc(&c->scanStatus, (scan_tiles(C) + 1) * sizeof(unsigned long long)));
+        CK(cudaMalloc(&c->scanStatus, (scan_tiles(C) + 2) * sizeof(unsigned long long)));
         c->cellCap = C;
     }
     return ORCA_OK;
@@ -165,7 +181,8 @@ orca_status ensure_capacity(orca_ctx* c, int64_t n, int64_t C) {
 // exclusive scan of the bin counts (memset of the look-back status + one launch)
 cudaError_t enqueue_scan(orca_ctx* c) {
     const int tiles = scan_tiles(c->C);
-    cudaError_t e = cudaMemsetAsync(c->scanStatus, 0, (tiles + 1) * sizeof(unsigned long long), c->stream);
+    // status words, tile ticket and the LP3 queue count (consumed by k_lp3 before this point)
+    cudaError_t e = cudaMemsetAsync(c->scanStatus, 0, (tiles + 2) * sizeof(unsigned long long), c->stream);
     if (e != cudaSuccess) return e;
     k_scan<<<tiles, 1024, 0, c->stream>>>(c->count, c->binStart, (int)c->C, c->scanStatus,
                                           reinterpret_cast<unsigned int*>(c->scanStatus + tiles));
@@ -185,6 +202,7 @@ cudaError_t enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
     if (n > 0) {
         const int blocks = (n + kStepThreads - 1) / kStepThreads;
         k_step<false><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
+        k_lp3<false><<<lp3_blocks(n), kStepThreads, c->lp3Smem, c->stream>>>(a);
     }
     if (ev) cudaEventRecord(ev[1], c->stream);
     enqueue_scan(c);
@@ -194,6 +212,19 @@ cudaError_t enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
                                                               c->auxW, c->idW, c->posS, c->velS, c->auxS, c->idS);
     if (ev) cudaEventRecord(ev[3], c->stream);
     return cudaGetLastError();
+}
+
+// The dry (debug) step: same kernels, outputs by id, state untouched; the LP3 queue
+// count is zeroed before and after so the next real step starts from an empty queue.
+cudaError_t dry_step(orca_ctx* c, StepArgs& a) {
+    const int n = (int)c->n;
+    cudaError_t e = cudaMemsetAsync(a.qCount, 0, sizeof(unsigned int), c->stream);
+    if (e != cudaSuccess) return e;
+    k_step<true><<<(n + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
+    k_lp3<true><<<lp3_blocks(n), kStepThreads, c->lp3Smem, c->stream>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(a.qCount, 0, sizeof(unsigned int), c->stream);
 }
 
 // Copy a float[2n] user array (host or device) into a device float2 buffer.
@@ -241,10 +272,15 @@ orca_status orca_create(const orca_params* params, int32_t device, orca_ctx** ou
     if (e == cudaSuccess) e = cudaMalloc(&c->partial, 1024 * 5 * sizeof(float));
     for (int q = 0; q < 9 && e == cudaSuccess; ++q) e = cudaEventCreate(&c->ev[q]);
     c->smemBytes = step_smem_per_thread(params->maxNeighbors) * kStepThreads;
+    c->lp3Smem = std::max(1, 6 * params->maxNeighbors) * 4 * kStepThreads;
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_lp3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
     if (e != cudaSuccess) {
         orca_destroy(c);
         return cuda_fail(e, "orca_create");
@@ -265,6 +301,8 @@ void orca_destroy(orca_ctx* c) {
     dfree(c->stats);
     dfree(c->partial);
     dfree(c->scanStatus);
+    dfree(c->qEntry);
+    dfree(c->qLines);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -326,6 +364,10 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
         g.nx = (int)tx + 2;
         g.ny = (int)ty + 2;
     }
+    g.csD = (double)cs;
+    g.invCs = 1.0 / (double)cs;
+    g.csSub = (double)cs / (double)(1 << g.lgS);
+    g.invCsSub = (double)(1 << g.lgS) / (double)cs;
     c->g = g;
     c->C = ((int64_t)g.nx * g.ny) << g.lgS;
     st = ensure_capacity(c, n, c->C);
@@ -523,8 +565,7 @@ orca_status orca_debug_step(orca_ctx* c, float* vnew, uint8_t* flags, int32_t* n
         a.dbgFlags = dF;
         a.dbgNbr = dN;
         a.dbgCnt = dC;
-        k_step<true><<<(n + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
-        e = cudaGetLastError();
+        e = dry_step(c, a);
     }
     if (e == cudaSuccess && vnew) e = cudaMemcpyAsync(vnew, dV, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->stream);
     if (e == cudaSuccess && flags) e = cudaMemcpyAsync(flags, dF, (size_t)n, cudaMemcpyDefault, c->stream);
@@ -553,8 +594,7 @@ orca_status orca_debug_work(orca_ctx* c, int64_t out[5]) {
     if (e == cudaSuccess) {
         StepArgs a = make_args(c);
         a.work = dW;
-        k_step<true><<<(n + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
-        e = cudaGetLastError();
+        e = dry_step(c, a);
     }
     Work h{};
     if (e == cudaSuccess) e = cudaMemcpyAsync(&h, dW, sizeof(Work), cudaMemcpyDeviceToHost, c->stream);

@@ -50,6 +50,8 @@ struct Grid {
     float ox, oy, cs;  // origin, cell size (fp32 values; widened exactly to fp64)
     int nx, ny;        // dims (cells of size cs = r_obs)
     int lgS;           // each cell is split into 2^lgS sub-rows for the sort order
+    double csD, invCs;        // fl64(cs), fl64(1/cs)
+    double csSub, invCsSub;   // cs / 2^lgS (exact), 2^lgS / cs
 };
 
 struct Model {
@@ -59,35 +61,46 @@ struct Model {
     double R2D;                   // fl64(R)^2
     double nd2D;                  // fl64(nd)^2 (exact: nd is fp32)
     float nd2Fup;                 // fp32 prefilter bound, rounded up with margin
+    float nd2Lo;                  // below this fp32 d2 a candidate is surely inside r_obs
     int k;                        // maxNeighbors
     int goals;                    // 1: aux holds goals, pref = g min(1, s/|g|)
     float prefSpeed;
 };
 
 // ------------------------------------------------------------------ cell (reading Q11)
-__device__ __forceinline__ int cell_coord(float x, float o, float cs, int nc) {
-    double t = __ddiv_rn(__dsub_rn((double)x, (double)o), (double)cs);
-    double f = floor(t);
-    f = fmax(f, 0.0);
-    f = fmin(f, (double)(nc - 1));
-    return (int)f;
+// floor(d / cs) of d = fl64(x) - fl64(o) without a division: q = floor(d * inv) is off by
+// at most one, and the residual r = d - q*cs is computed exactly by one fma (q*cs has
+// <= 53 bits for |q| < 2^29 and |r| < 2 cs), so the corrected q is the exact rational
+// floor -- which equals the oracle's floor(fl64(d / cs)): fl64 rounding of d/cs can never
+// reach an integer from below for fp32 inputs.  Clamped to [0, nc-1].
+__device__ __forceinline__ int floor_div_clamped(double d, double cs, double inv, int nc) {
+    const double q0 = __dmul_rn(d, inv);
+    if (q0 < -2.0) return 0;
+    if (q0 > (double)nc + 2.0) return nc - 1;
+    double q = floor(q0);
+    const double r = fma(-q, cs, d);
+    if (r < 0.0) q -= 1.0;
+    else if (r >= cs) q += 1.0;
+    q = fmax(q, 0.0);
+    q = fmin(q, (double)(nc - 1));
+    return (int)q;
 }
 
-// Sub-row of y: floor(t * 2^lgS) with t the same fp64 quotient as cell_coord, clamped;
-// its >> lgS is exactly the clamped cell row (scaling by a power of two is exact).
+__device__ __forceinline__ int cell_coord(float x, float o, double cs, double inv, int nc) {
+    return floor_div_clamped(__dsub_rn((double)x, (double)o), cs, inv, nc);
+}
+
+// Sub-row of y: floor((y - oy) / (cs / 2^lgS)), clamped; cs / 2^lgS is exact, and the
+// sub-row >> lgS is exactly the clamped cell row.
 __device__ __forceinline__ int subrow_coord(float y, const Grid& g) {
-    const double t = __ddiv_rn(__dsub_rn((double)y, (double)g.oy), (double)g.cs);
-    double f = floor(t * (double)(1 << g.lgS));
-    f = fmax(f, 0.0);
-    f = fmin(f, (double)((g.ny << g.lgS) - 1));
-    return (int)f;
+    return floor_div_clamped(__dsub_rn((double)y, (double)g.oy), g.csSub, g.invCsSub, g.ny << g.lgS);
 }
 
 // Bin id of the sort order: column-major over (cx, sub-row), so a strip of columns is
 // one contiguous id range, a coarse cell is 2^lgS consecutive bins, and each column run
 // of the 3x3 stencil is ordered by y at sub-row granularity.
 __device__ __forceinline__ uint32_t bin_id(float x, float y, const Grid& g) {
-    const int cx = cell_coord(x, g.ox, g.cs, g.nx);
+    const int cx = cell_coord(x, g.ox, g.csD, g.invCs, g.nx);
     const int sy = subrow_coord(y, g);
     return (uint32_t)cx * (uint32_t)(g.ny << g.lgS) + (uint32_t)sy;
 }
@@ -406,25 +419,22 @@ struct StepArgs {
     int32_t* dbgNbr;
     int32_t* dbgCnt;
     Work* work;  // dry step only: instrumented work counts (nullable)
+    // LP3 queue: agents whose LP2 failed are finished by k_lp3 (compacted)
+    int4* qEntry;          // (i, cnt | f << 8 | flags << 16, vx bits, vy bits)
+    float4* qLines;        // line m of entry q at [m * qcap + q] = (nx, ny, s, 0)
+    unsigned int* qCount;  // zeroed before every step
+    int qcap;
 };
 
 constexpr int kStepThreads = 128;
 
 // Per-thread shared memory (32-bit words, one column per thread, stride kStepThreads):
-//   region L: 3k words -- the top-k list as (key.lo, key.hi, j) during selection, then
+//   region L: 3k words -- the top-k list as (fp32 d2, -, j) during selection, then
 //             overwritten in place by the half-planes (nx, ny, s) in the same slots;
 //   region B: max(k + 24, 3k) words -- candidate buffer during the scan, then the LP3
 //             projected lines (3k words).
 __host__ __device__ constexpr int step_buf_words(int k) { return (k + 24 > 3 * k) ? k + 24 : 3 * k; }
 __host__ __device__ constexpr int step_smem_per_thread(int k) { return 4 * (3 * k + step_buf_words(k)); }
-
-// Exact (kappa, id) order of candidate j against list slot key/j (ids loaded only on
-// an exact key tie).
-__device__ __forceinline__ bool cand_less(double ka, uint32_t ja, double kb, uint32_t jb,
-                                          const uint32_t* __restrict__ idS) {
-    if (ka != kb) return ka < kb;
-    return idS[ja] < idS[jb];
-}
 
 __device__ __forceinline__ double exact_key(float2 pj, float2 pi) {
     const double Dx = __dsub_rn((double)pj.x, (double)pi.x);
@@ -432,32 +442,51 @@ __device__ __forceinline__ double exact_key(float2 pj, float2 pi) {
     return __dadd_rn(__dmul_rn(Dx, Dx), __dmul_rn(Dy, Dy));
 }
 
-// Merge the nb buffered candidates into the sorted top-k list (exact keys, ties by id).
-// Returns the new list length; the list is (key.lo, key.hi, j) in L0/L1/L2.
-__device__ __forceinline__ int merge_candidates(uint32_t* L0, uint32_t* L1, uint32_t* L2, int cnt, int k,
-                                                const uint32_t* Bf, int nb, float2 pi, double nd2,
-                                                const float2* __restrict__ posS, const uint32_t* __restrict__ idS) {
+// fp32 d^2 = fma(dx, dx, dy*dy) has relative error < 2^-22 against the exact fp64 key
+// kappa (reading Q11), so fa < fb (1 - 2^-20) proves kappa_a < kappa_b.  Only near-ties
+// (and tiny values, where subnormals void the bound) fall back to the exact keys.
+constexpr float kSep = 1.0f - 0x1p-20f;
+
+// Exact (kappa, id) order of candidates ja (fp32 d2 fa) and jb (fb) around agent pi.
+__device__ __forceinline__ bool cand_less(float fa, uint32_t ja, float fb, uint32_t jb, float2 pi,
+                                          const float2* __restrict__ posS, const uint32_t* __restrict__ idS) {
+    if (fa < fb * kSep && fb > 1e-30f) return true;
+    if (fb < fa * kSep && fa > 1e-30f) return false;
+    const double ka = exact_key(posS[ja], pi), kb = exact_key(posS[jb], pi);
+    if (ka != kb) return ka < kb;
+    return idS[ja] < idS[jb];
+}
+
+// Strictly within r_obs (reading Q10): exact test only near the boundary.
+__device__ __forceinline__ bool in_radius(float f, uint32_t j, float2 pi, float nd2Lo, float nd2Hi, double nd2,
+                                          const float2* __restrict__ posS) {
+    if (f < nd2Lo) return true;
+    if (f > nd2Hi) return false;
+    return exact_key(posS[j], pi) < nd2;
+}
+
+// Merge the nb buffered candidates (j; fp32 d2 recomputed) into the sorted top-k list
+// (Lf = fp32 d2 bits, Lj = j).  Returns the new list length.
+__device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int cnt, int k, const uint32_t* Bf,
+                                                int nb, float2 pi, const Model& m, const float2* __restrict__ posS,
+                                                const uint32_t* __restrict__ idS) {
     constexpr int T = kStepThreads;
     for (int b = 0; b < nb; ++b) {
         const uint32_t j = Bf[b * T];
-        const double key = exact_key(posS[j], pi);
-        if (!(key < nd2)) continue;  // strictly within r_obs (reading Q10)
-        if (cnt == k) {
-            const double lk = __hiloint2double((int)L1[(k - 1) * T], (int)L0[(k - 1) * T]);
-            if (!cand_less(key, j, lk, L2[(k - 1) * T], idS)) continue;
-        }
+        const float2 pj = posS[j];
+        const float dx = pj.x - pi.x, dy = pj.y - pi.y;
+        const float f = fmaf(dx, dx, dy * dy);
+        if (!in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
+        if (cnt == k && !cand_less(f, j, __uint_as_float(Lf[(k - 1) * T]), Lj[(k - 1) * T], pi, posS, idS))
+            continue;
         int p = (cnt < k) ? cnt : k - 1;
-        while (p > 0) {
-            const double pk = __hiloint2double((int)L1[(p - 1) * T], (int)L0[(p - 1) * T]);
-            if (!cand_less(key, j, pk, L2[(p - 1) * T], idS)) break;
-            L0[p * T] = L0[(p - 1) * T];
-            L1[p * T] = L1[(p - 1) * T];
-            L2[p * T] = L2[(p - 1) * T];
+        while (p > 0 && cand_less(f, j, __uint_as_float(Lf[(p - 1) * T]), Lj[(p - 1) * T], pi, posS, idS)) {
+            Lf[p * T] = Lf[(p - 1) * T];
+            Lj[p * T] = Lj[(p - 1) * T];
             --p;
         }
-        L0[p * T] = (uint32_t)__double2loint(key);
-        L1[p * T] = (uint32_t)__double2hiint(key);
-        L2[p * T] = j;
+        Lf[p * T] = __float_as_uint(f);
+        Lj[p * T] = j;
         if (cnt < k) ++cnt;
     }
     return cnt;
@@ -484,12 +513,13 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
     const bool active = i < a.n;
     uint32_t fl = 0;
     int nColl = 0;
+    bool deferred = false;
     if (active) {
         const float2 pi = a.posS[i];
         const float2 vi = a.velS[i];
         const float2 aux = a.auxS[i];
         const uint32_t idi = a.idS[i];
-        const int cx = cell_coord(pi.x, a.g.ox, a.g.cs, a.g.nx);
+        const int cx = cell_coord(pi.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
         const int lgS = a.g.lgS;
         const int nyS = a.g.ny << lgS;
         const int cy = subrow_coord(pi.y, a.g) >> lgS;
@@ -553,13 +583,10 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
                             if (a0) Bf[nb++ * T] = (uint32_t)j;
                             if (a1) Bf[nb++ * T] = (uint32_t)(j + 1);
                             if (nb >= capB - 1) {  // buffer (nearly) full: merge, tighten
-                                cnt = merge_candidates(L0, L1, L2, cnt, k, Bf, nb, pi, a.m.nd2D, a.posS, a.idS);
+                                cnt = merge_candidates(L0, L2, cnt, k, Bf, nb, pi, a.m, a.posS, a.idS);
                                 nb = 0;
-                                if (cnt == k) {
-                                    const double lk = __hiloint2double((int)L1[(k - 1) * T], (int)L0[(k - 1) * T]);
-                                    // fp32 d2 has relative error < 2^-22: margin 2^-20, rounded up
-                                    thr = fminf(thr, __fmul_ru(__double2float_ru(lk), 1.0f + 0x1p-20f));
-                                }
+                                if (cnt == k)  // any key <= the k-th has fp32 d2 <= fk (1 + 2^-20)
+                                    thr = fminf(thr, __fmul_ru(__uint_as_float(L0[(k - 1) * T]), 1.0f + 0x1p-20f));
                             }
                         }
                     }
@@ -568,24 +595,19 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
                         const float dx0 = p0.x - pi.x, dy0 = p0.y - pi.y;
                         if (fmaf(dx0, dx0, dy0 * dy0) <= thr && j != i) Bf[nb++ * T] = (uint32_t)j;
                         if (nb >= capB - 1) {
-                            cnt = merge_candidates(L0, L1, L2, cnt, k, Bf, nb, pi, a.m.nd2D, a.posS, a.idS);
+                            cnt = merge_candidates(L0, L2, cnt, k, Bf, nb, pi, a.m, a.posS, a.idS);
                             nb = 0;
-                            if (cnt == k) {
-                                const double lk = __hiloint2double((int)L1[(k - 1) * T], (int)L0[(k - 1) * T]);
-                                thr = fminf(thr, __fmul_ru(__double2float_ru(lk), 1.0f + 0x1p-20f));
-                            }
+                            if (cnt == k) thr = fminf(thr, __fmul_ru(__uint_as_float(L0[(k - 1) * T]), 1.0f + 0x1p-20f));
                         }
                     }
                 }
-                cnt = merge_candidates(L0, L1, L2, cnt, k, Bf, nb, pi, a.m.nd2D, a.posS, a.idS);
+                cnt = merge_candidates(L0, L2, cnt, k, Bf, nb, pi, a.m, a.posS, a.idS);
                 if (!guessed) break;
                 // Exact only if every candidate not kept -- rejected by the guessed radius
                 // (key > thrPass (1 - 2^-22)) or pruned geometrically (distance > rg) -- is
                 // strictly beyond the k-th key.
-                if (cnt == k) {
-                    const double lk = __hiloint2double((int)L1[(k - 1) * T], (int)L0[(k - 1) * T]);
-                    if (lk < (double)thrPass * (1.0 - 0x1p-20)) break;
-                }
+                // kappa_k <= fk (1 + 2^-22) < thrPass (1 - 2^-22) < any rejected kappa
+                if (cnt == k && (double)__uint_as_float(L0[(k - 1) * T]) < (double)thrPass * (1.0 - 0x1p-20)) break;
                 cnt = 0;  // rescan the full 3x3 stencil at the full radius
                 thr = a.m.nd2Fup;
                 guessed = false;
@@ -625,15 +647,29 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
         if (CNT) w.lines += (uint32_t)cnt;
         const int f = lp2<CNT>(L, T, cnt, a.m.maxSpeed, px, py, false, vx, vy, fl, w);
         if (f < cnt) {
+            // infeasible: queue the agent with its half-planes and LP2 point; k_lp3
+            // runs the least-penetration LP on a compacted set of agents (full warps)
             fl |= FL_INFEASIBLE;
-            lp3<CNT>(L, P, T, cnt, f, a.m.maxSpeed, vx, vy, fl, w);
-            float dl = 0.0f;
-            for (int q = 0; q < cnt; ++q) dl = fmaxf(dl, L.s[q * T] - fmaf(L.nx[q * T], vx, L.ny[q * T] * vy));
-            if (dl > 0.0f && dl < 1e-6f) fl |= FL_G3;
+            deferred = true;
+            const unsigned mask = __activemask();
+            const int lane = tid & 31;
+            const int leader = __ffs(mask) - 1;
+            unsigned base = 0;
+            if (lane == leader) base = atomicAdd(a.qCount, (unsigned)__popc(mask));
+            base = __shfl_sync(mask, base, leader);
+            const int q = (int)base + __popc(mask & ((1u << lane) - 1u));
+            a.qEntry[q] = make_int4(i, cnt | (f << 8) | ((int)fl << 16), __float_as_int(vx), __float_as_int(vy));
+            for (int m = 0; m < cnt; ++m)
+                a.qLines[(size_t)m * a.qcap + q] = make_float4(L.nx[m * T], L.ny[m * T], L.s[m * T], 0.0f);
+            if (DRY && a.dbgCnt) a.dbgCnt[idi] = cnt;
+            if (DRY && a.dbgNbr)
+                for (int q2 = cnt; q2 < k; ++q2) a.dbgNbr[(size_t)idi * k + q2] = -1;
         }
 
         // ---- 5. integrate (explicit Euler) + next step's binning ----------------------
-        if (DRY) {
+        if (deferred) {
+            // finished by k_lp3
+        } else if (DRY) {
             if (a.dbgV) a.dbgV[idi] = make_float2(vx, vy);
             if (a.dbgFlags) a.dbgFlags[idi] = (uint8_t)fl;
             if (a.dbgCnt) a.dbgCnt[idi] = cnt;
@@ -668,6 +704,7 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
         // per-warp counts (ballot + popc), one relaxed atomic per warp and counter; no
         // block barrier, so fast warps never wait for a slow LP in the same block
         const int lane = tid & 31;
+        if (deferred) fl = 0;  // counted by k_lp3 with its final flags
         const int cInf = __popc(__ballot_sync(0xffffffffu, fl & FL_INFEASIBLE));
         const int cDeg = __popc(__ballot_sync(0xffffffffu, fl & (FL_G1 | FL_G2)));
         const int cG1 = __popc(__ballot_sync(0xffffffffu, fl & FL_G1));
@@ -682,6 +719,90 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
             if (cG1) atomicAdd(&a.stats[ST_G1], (unsigned long long)cG1);
             if (cG2) atomicAdd(&a.stats[ST_G2], (unsigned long long)cG2);
             if (cG3) atomicAdd(&a.stats[ST_G3], (unsigned long long)cG3);
+        }
+    }
+}
+
+// ------------------------------------------------------------ LP3 on the queue
+// One thread per queued (infeasible) agent, grid-stride over the device-side queue
+// count; same smem column layout as k_step (lines, then projected lines).
+template <bool DRY>
+__global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
+    constexpr bool CNT = DRY;
+    WorkT w{0, 0, 0, 0, 0};
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int T = kStepThreads;
+    const int tid = threadIdx.x;
+    const int k = a.m.k;
+    float* base = reinterpret_cast<float*>(smem) + tid;
+    const Lines L{base, base + k * T, base + 2 * k * T};
+    const Lines P{base + 3 * k * T, base + 4 * k * T, base + 5 * k * T};
+    const int nq = (int)*a.qCount;
+    int cInf = 0, cDeg = 0, cG1 = 0, cG2 = 0, cG3 = 0;
+    for (int q = blockIdx.x * T + tid; q < nq; q += gridDim.x * T) {
+        const int4 e = a.qEntry[q];
+        const int i = e.x;
+        const int cnt = e.y & 0xff, f = (e.y >> 8) & 0xff;
+        uint32_t fl = (uint32_t)(e.y >> 16);
+        float vx = __int_as_float(e.z), vy = __int_as_float(e.w);
+        for (int m = 0; m < cnt; ++m) {
+            const float4 l = a.qLines[(size_t)m * a.qcap + q];
+            L.nx[m * T] = l.x;
+            L.ny[m * T] = l.y;
+            L.s[m * T] = l.z;
+        }
+        lp3<CNT>(L, P, T, cnt, f, a.m.maxSpeed, vx, vy, fl, w);
+        float dl = 0.0f;
+        for (int m = 0; m < cnt; ++m) dl = fmaxf(dl, L.s[m * T] - fmaf(L.nx[m * T], vx, L.ny[m * T] * vy));
+        if (dl > 0.0f && dl < 1e-6f) fl |= FL_G3;
+        const float2 pi = a.posS[i];
+        const uint32_t idi = a.idS[i];
+        if (DRY) {
+            if (a.dbgV) a.dbgV[idi] = make_float2(vx, vy);
+            if (a.dbgFlags) a.dbgFlags[idi] = (uint8_t)fl;
+        } else {
+            const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
+            const uint32_t c = bin_id(pn.x, pn.y, a.g);
+            a.posW[i] = pn;
+            a.velW[i] = make_float2(vx, vy);
+            a.auxW[i] = a.auxS[i];
+            a.idW[i] = idi;
+            a.cellW[i] = c;
+            a.rankW[i] = atomicAdd(&a.count[c], 1u);
+        }
+        cInf += 1;
+        cDeg += (fl & (FL_G1 | FL_G2)) != 0;
+        cG1 += (fl & FL_G1) != 0;
+        cG2 += (fl & FL_G2) != 0;
+        cG3 += (fl & FL_G3) != 0;
+    }
+    const int lane = tid & 31;
+    if (DRY) {
+        if (a.work) {
+            unsigned long long c[2] = {w.checks, w.lp1};
+            unsigned long long pj = w.proj;
+            for (int o = 16; o > 0; o >>= 1) {
+                c[0] += __shfl_xor_sync(0xffffffffu, c[0], o);
+                c[1] += __shfl_xor_sync(0xffffffffu, c[1], o);
+                pj += __shfl_xor_sync(0xffffffffu, pj, o);
+            }
+            if (lane == 0) {
+                atomicAdd(&a.work->checks, c[0]);
+                atomicAdd(&a.work->lp1, c[1]);
+                atomicAdd(&a.work->proj, pj);
+            }
+        }
+    } else {
+        int c[5] = {cInf, cDeg, cG1, cG2, cG3};
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+            for (int o = 16; o > 0; o >>= 1) c[r] += __shfl_xor_sync(0xffffffffu, c[r], o);
+        if (lane == 0) {
+            if (c[0]) atomicAdd(&a.stats[ST_INFEASIBLE], (unsigned long long)c[0]);
+            if (c[1]) atomicAdd(&a.stats[ST_DEGENERATE], (unsigned long long)c[1]);
+            if (c[2]) atomicAdd(&a.stats[ST_G1], (unsigned long long)c[2]);
+            if (c[3]) atomicAdd(&a.stats[ST_G2], (unsigned long long)c[3]);
+            if (c[4]) atomicAdd(&a.stats[ST_G3], (unsigned long long)c[4]);
         }
     }
 }
@@ -702,8 +823,8 @@ __global__ void k_cells(int n, const uint32_t* __restrict__ idS, const float2* _
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const float2 p = posS[i];
         const uint32_t id = idS[i];
-        cxOut[id] = cell_coord(p.x, g.ox, g.cs, g.nx);
-        cyOut[id] = cell_coord(p.y, g.oy, g.cs, g.ny);
+        cxOut[id] = cell_coord(p.x, g.ox, g.csD, g.invCs, g.nx);
+        cyOut[id] = cell_coord(p.y, g.oy, g.csD, g.invCs, g.ny);
     }
 }
 
