@@ -80,6 +80,7 @@ struct orca_ctx {
     float2 *posS = nullptr, *velS = nullptr, *auxS = nullptr;
     uint32_t* idS = nullptr;
     float2 *posW = nullptr, *velW = nullptr, *auxW = nullptr;
+    float *rk2S = nullptr, *rk2W = nullptr;  // previous k-th neighbour d2 (search bound)
     uint32_t *idW = nullptr, *cellW = nullptr, *rankW = nullptr;
     uint32_t *count = nullptr, *binStart = nullptr;
     unsigned long long* scanStatus = nullptr;  // look-back status words + ticket + LP3 queue count
@@ -134,6 +135,8 @@ StepArgs make_args(orca_ctx* c) {
     a.posS = c->posS;
     a.velS = c->velS;
     a.auxS = c->auxS;
+    a.rk2S = c->rk2S;
+    a.rk2W = c->rk2W;
     a.idS = c->idS;
     a.binStart = c->binStart;
     a.posW = c->posW;
@@ -162,6 +165,10 @@ orca_status ensure_capacity(orca_ctx* c, int64_t n, int64_t C) {
         for (auto pp : u4) CK(cudaMalloc(pp, cap * sizeof(uint32_t)));
         dfree(c->qEntry);
         dfree(c->qLines);
+        dfree(c->rk2S);
+        dfree(c->rk2W);
+        CK(cudaMalloc(&c->rk2S, cap * sizeof(float)));
+        CK(cudaMalloc(&c->rk2W, cap * sizeof(float)));
         CK(cudaMalloc(&c->qEntry, cap * sizeof(int4)));
         CK(cudaMalloc(&c->qLines, cap * std::max(1, c->p.maxNeighbors) * sizeof(float4)));
         c->cap = cap;
@@ -209,7 +216,8 @@ cudaError_t enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
     if (ev) cudaEventRecord(ev[2], c->stream);
     if (n > 0)
         k_scatter<<<grid_blocks(n, 256), 256, 0, c->stream>>>(n, c->cellW, c->rankW, c->binStart, c->posW, c->velW,
-                                                              c->auxW, c->idW, c->posS, c->velS, c->auxS, c->idS);
+                                                              c->auxW, c->idW, c->posS, c->velS, c->auxS, c->idS,
+                                                              c->rk2W, c->rk2S);
     if (ev) cudaEventRecord(ev[3], c->stream);
     return cudaGetLastError();
 }
@@ -303,6 +311,8 @@ void orca_destroy(orca_ctx* c) {
     dfree(c->scanStatus);
     dfree(c->qEntry);
     dfree(c->qLines);
+    dfree(c->rk2S);
+    dfree(c->rk2W);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -376,14 +386,14 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     // ids, initial binning, scan, scatter -> rest state
     CK(cudaMemsetAsync(c->count, 0, c->C * sizeof(uint32_t), c->stream));
     if (n > 0) {
-        k_iota<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->idW);
+        k_iota<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->idW, c->rk2W);
         k_hash<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->posW, c->g, c->cellW, c->rankW, c->count);
     }
     CK(enqueue_scan(c));
     if (n > 0)
         k_scatter<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->cellW, c->rankW, c->binStart, c->posW,
                                                               c->velW, c->auxW, c->idW, c->posS, c->velS, c->auxS,
-                                                              c->idS);
+                                                              c->idS, c->rk2W, c->rk2S);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     c->ready = true;

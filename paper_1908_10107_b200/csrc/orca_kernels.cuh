@@ -202,12 +202,14 @@ __global__ void k_scatter(int n, const uint32_t* __restrict__ cell, const uint32
                           const uint32_t* __restrict__ binStart, const float2* __restrict__ posW,
                           const float2* __restrict__ velW, const float2* __restrict__ auxW,
                           const uint32_t* __restrict__ idW, float2* __restrict__ posS, float2* __restrict__ velS,
-                          float2* __restrict__ auxS, uint32_t* __restrict__ idS) {
+                          float2* __restrict__ auxS, uint32_t* __restrict__ idS, const float* __restrict__ rk2W,
+                          float* __restrict__ rk2S) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t dst = binStart[cell[i]] + rank[i];
         posS[dst] = posW[i];
         velS[dst] = velW[i];
         auxS[dst] = auxW[i];
+        rk2S[dst] = rk2W[i];
         idS[dst] = idW[i];
     }
 }
@@ -402,12 +404,14 @@ struct StepArgs {
     const float2* __restrict__ posS;
     const float2* __restrict__ velS;
     const float2* __restrict__ auxS;  // prefVel, or goal when m.goals
+    const float* __restrict__ rk2S;   // previous step's fp32 d2 of the k-th neighbour (+inf: none)
     const uint32_t* __restrict__ idS;
     const uint32_t* __restrict__ binStart;
     // outputs of a real step (work buffers, next step's binning)
     float2* posW;
     float2* velW;
     float2* auxW;
+    float* rk2W;
     uint32_t* idW;
     uint32_t* cellW;
     uint32_t* rankW;
@@ -431,9 +435,8 @@ constexpr int kStepThreads = 128;
 // Per-thread shared memory (32-bit words, one column per thread, stride kStepThreads):
 //   region L: 3k words -- the top-k list as (fp32 d2, -, j) during selection, then
 //             overwritten in place by the half-planes (nx, ny, s) in the same slots;
-//   region B: max(k + 24, 3k) words -- candidate buffer during the scan, then the LP3
-//             projected lines (3k words).
-__host__ __device__ constexpr int step_buf_words(int k) { return (k + 24 > 3 * k) ? k + 24 : 3 * k; }
+//   region B: k + 8 words -- candidate buffer during the scan (merged when full).
+__host__ __device__ constexpr int step_buf_words(int k) { return k + 8; }
 __host__ __device__ constexpr int step_smem_per_thread(int k) { return 4 * (3 * k + step_buf_words(k)); }
 
 __device__ __forceinline__ double exact_key(float2 pj, float2 pi) {
@@ -493,7 +496,7 @@ __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int 
 }
 
 template <bool DRY>
-__global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
+__global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
     constexpr bool CNT = DRY;  // only the debug variant counts work
     WorkT w{0, 0, 0, 0, 0};
     extern __shared__ __align__(16) unsigned char smem[];
@@ -506,8 +509,6 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
     uint32_t* L2 = L1 + k * T;
     uint32_t* Bf = L2 + k * T;
     const Lines L{reinterpret_cast<float*>(L0), reinterpret_cast<float*>(L1), reinterpret_cast<float*>(L2)};
-    const Lines P{reinterpret_cast<float*>(Bf), reinterpret_cast<float*>(Bf) + k * T,
-                  reinterpret_cast<float*>(Bf) + 2 * k * T};
 
     const int i = blockIdx.x * T + tid;
     const bool active = i < a.n;
@@ -526,10 +527,13 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
 
         // ---- 2. k nearest within r_obs over the 3x3 bins -------------
         // Each column of the stencil is one contiguous run of the sorted arrays, ordered by
-        // sub-row.  A radius guess rg from the local density restricts every run to the
-        // sub-rows within rg of the agent and skips a side column farther than rg; the
-        // result is exact by the check below (else one full 3x3 rescan).
+        // sub-row.  A search radius rg restricts every run to the sub-rows within rg of the
+        // agent and skips a side column farther than rg; the result is exact by the check
+        // below (else one full 3x3 rescan).  rg comes from the previous step's k-th
+        // neighbour distance plus 2 maxSpeed dt (those k agents cannot have moved farther
+        // apart), or, without history, from the local density.
         int cnt = 0;
+        float fk = INFINITY;
         if (k > 0) {
             const int rlo = max(cy - 1, 0) << lgS;              // first sub-row of the 3 rows
             const int rhi = (min(cy + 1, a.g.ny - 1) + 1) << lgS; // one past the last
@@ -537,10 +541,19 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
             int ncand = 0;
             for (int col = c0; col <= c1; ++col)
                 ncand += (int)a.binStart[col * nyS + rhi] - (int)a.binStart[col * nyS + rlo];
-            // r^2 = 2.2 k / (pi rho), rho = ncand / (9 cs^2): ~22 expected hits for k = 10
             float thr = a.m.nd2Fup;
             bool guessed = false;
-            if (ncand > 4 * k) {
+            const float rk2p = a.rk2S[i];
+            if (rk2p < a.m.nd2Fup) {
+                const float marg = 2.0002f * a.m.maxSpeed * a.m.dt + 4e-7f * (fabsf(pi.x) + fabsf(pi.y)) + 1e-5f;
+                const float r = sqrtf(rk2p) * (1.0f + 1e-5f) + marg;
+                const float b = r * r * (1.0f + 1e-3f);
+                if (b < thr) {
+                    thr = b;
+                    guessed = true;
+                }
+            } else if (ncand > 4 * k) {
+                // r^2 = 2.2 k / (pi rho), rho = ncand / (9 cs^2): ~22 expected hits for k = 10
                 const float g = 2.2f * (float)k * 9.0f * a.g.cs * a.g.cs / (3.14159265f * (float)ncand);
                 if (g < thr) {
                     thr = g;
@@ -553,11 +566,12 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
                 int lo = rlo, hi = rhi - 1, cl = c0, cr = c1;
                 if (guessed) {
                     const float rg = sqrtf(thr) * (1.0f + 1e-6f) + 1e-6f;
-                    const float h = a.g.cs / (float)(1 << lgS);
-                    const float ty = (pi.y - a.g.oy) / h;
-                    // one sub-row of margin each side absorbs the fp32 error of ty
-                    lo = max(lo, (int)floorf(fmaxf(ty - rg / h, -2.0f)) - 1);
-                    hi = min(hi, (int)floorf(fminf(ty + rg / h, (float)nyS + 2.0f)) + 1);
+                    // sub-rows s with [oy + s h, oy + (s+1) h) within rg of y (h = cs/2^lgS):
+                    // ty in fp64 is accurate to ~1e-12 sub-rows, covered by the 1e-6 margin
+                    const double ty = __dmul_rn(__dsub_rn((double)pi.y, (double)a.g.oy), a.g.invCsSub);
+                    const double rs = (double)rg * a.g.invCsSub + 1e-6;
+                    lo = max(lo, (int)fmax(floor(ty - rs), -2.0));
+                    hi = min(hi, (int)fmin(floor(ty + rs), (double)nyS + 2.0));
                     const double xl = (double)a.g.ox + (double)cx * (double)a.g.cs;  // cell's left edge
                     if ((double)pi.x - xl > (double)rg) cl = cx;                       // left column beyond rg
                     if (xl + (double)a.g.cs - (double)pi.x > (double)rg) cr = cx;     // right column beyond rg
@@ -612,7 +626,9 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
                 thr = a.m.nd2Fup;
                 guessed = false;
             }
+            if (cnt == k) fk = __uint_as_float(L0[(k - 1) * T]);
         }
+        if (!DRY) a.rk2W[i] = fk;  // next step's search bound
 
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
         // (half-plane q overwrites list slot q in place: j is read before the write)
@@ -834,8 +850,12 @@ __global__ void k_gather_by_id(int n, const uint32_t* __restrict__ idS, const fl
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[idS[i]];
 }
 
-__global__ void k_iota(int n, uint32_t* __restrict__ id) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) id[i] = (uint32_t)i;
+// ids = array index; no search-bound history yet
+__global__ void k_iota(int n, uint32_t* __restrict__ id, float* __restrict__ rk2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        id[i] = (uint32_t)i;
+        rk2[i] = INFINITY;
+    }
 }
 
 // Block-partial min/max of the positions and a non-finite count over all input arrays.

@@ -29,7 +29,7 @@ if [[ $WHAT == all || $WHAT == ncu ]]; then
   echo "ncu full exit $?"
 fi
 if [[ $WHAT == ncufull || $WHAT == quick ]]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step -s 8 -c 1 -o $OUT/prof_kstep_$TAG \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_step|k_lp3" -s 16 -c 2 -o $OUT/prof_kstep_$TAG \
       python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_full_$TAG.txt 2>&1
   echo "ncu full exit $?"
   timeout 600 ncu --set full --clock-control none -k regex:"k_scatter|k_scan" -s 4 -c 2 -o $OUT/prof_bin_$TAG \
