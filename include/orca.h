@@ -173,8 +173,28 @@ orca_status orca_create_dist(const orca_params *params, int32_t device, int32_t 
                              int32_t world, const void *nccl_id128, orca_ctx **out);
 
 /* Local agents of this rank: ids int32[n_local] (nullable), pos/vel float[2 n_local]
- * (nullable); n_local from orca_get_count.  Synchronises. */
+ * (nullable), in the context's sorted order; n_local from orca_get_count.  Synchronises.
+ * Errors: NOT_READY, CAPACITY (a strip buffer overflowed; re-partition with set_agents). */
 orca_status orca_get_local_state(orca_ctx *ctx, int32_t *ids, float *pos, float *vel);
+
+/* In-process strip decomposition for testing on ONE GPU: `nstrips` strips held by one
+ * context, exchanging halos and migrants by device copies instead of NCCL (the same
+ * kernels and exchange buffers as orca_create_dist).  Results are bit-identical to
+ * orca_create (same ordered neighbour lists, global-id ties).  Errors: INVALID_ARGUMENT
+ * (nstrips outside [1, 64], maxSpeed * timeStep >= neighborDist), CUDA. */
+orca_status orca_create_strips(const orca_params *params, int32_t device, int32_t nstrips,
+                               orca_ctx **out);
+
+/* Strip partition (host only, no GPU): split columns [0, nx) into `world` contiguous
+ * strips of >= 1 column with near-equal agent counts.  colCount int64[nx] (agents per
+ * column), bounds int32[world + 1] out (strip s = [bounds[s], bounds[s+1])).
+ * Errors: INVALID_ARGUMENT (world < 1, world > nx, NULL, negative count). */
+orca_status orca_partition_columns(const int64_t *colCount, int32_t nx, int32_t world,
+                                   int32_t *bounds);
+
+/* Owned column ranges of the strips held by this context: bounds int32[2 * strips held]
+ * = (c0, c1) pairs.  Errors: NOT_READY. */
+orca_status orca_get_strips(orca_ctx *ctx, int32_t *bounds);
 
 #ifdef __cplusplus
 }

@@ -1,9 +1,14 @@
 // orca.cu -- host runtime + C ABI of liborca (include/orca.h).
 //
-// Owns device buffers, the context stream and the CUDA graph of n step bodies.  Every
-// arithmetic step of the ORCA update runs in the kernels of orca_kernels.cuh; this file
-// only validates arguments, allocates, copies and launches.
+// Owns device buffers, the context stream, the CUDA graph of n step bodies and the
+// strip decomposition.  Every arithmetic step of the ORCA update runs in
+// the kernels of orca_kernels.cuh; this file validates arguments, allocates, copies,
+// launches and moves exchange buffers (NCCL send/recv between ranks, or device copies
+// between the strips of an in-process "loopback" group used to test the decomposition on
+// one GPU).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -23,7 +28,12 @@ namespace {
 constexpr int kSubRowsLog2 = 3;  // 8 sort sub-rows per cell
 
 int scan_tiles(int64_t C) { return (int)((C + kScanTile - 1) / kScanTile); }
-int lp3_blocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + kStepThreads - 1) / kStepThreads, 148 * 8)); }
+int cap_blocks(int64_t n, int threads) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 148 * 32));
+}
+int lp3_blocks(int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + kStepThreads - 1) / kStepThreads, 148 * 8));
+}
 
 thread_local std::string g_last_error;
 
@@ -33,15 +43,21 @@ orca_status fail(orca_status s, const std::string& msg) {
 }
 
 orca_status cuda_fail(cudaError_t e, const char* what) {
-    cudaGetLastError();  // clear sticky-free errors
+    cudaGetLastError();
     return fail(e == cudaErrorMemoryAllocation ? ORCA_ERR_OUT_OF_MEMORY : ORCA_ERR_CUDA,
                 std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define CK(expr)                                      \
-    do {                                              \
-        cudaError_t _e = (expr);                      \
+#define CK(expr)                                            \
+    do {                                                    \
+        cudaError_t _e = (expr);                            \
         if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+    } while (0)
+
+#define CKS(expr)                     \
+    do {                              \
+        orca_status _s = (expr);      \
+        if (_s != ORCA_OK) return _s; \
     } while (0)
 
 bool finite_params(const orca_params* p) {
@@ -57,10 +73,126 @@ void dfree(T*& p) {
     p = nullptr;
 }
 
-int grid_blocks(int64_t n, int threads) {
-    int64_t b = (n + threads - 1) / threads;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
+// ---------------------------------------------------------------- NCCL (dlopen'ed)
+// liborca does not link NCCL: it binds the libnccl.so.2 already loaded by the process
+// (torch's) or the system one, so single-GPU use never needs it.
+struct NcclApi {
+    bool tried = false, ok = false;
+    std::string err;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    const char* (*errStr)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (api.tried) return api;
+    api.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        api.err = std::string("dlopen libnccl.so.2: ") + dlerror();
+        return api;
+    }
+    bool ok = true;
+    auto sym = [&](const char* n) {
+        void* p = dlsym(h, n);
+        if (!p) ok = false;
+        return p;
+    };
+    api.getUniqueId = (decltype(api.getUniqueId))sym("ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))sym("ncclCommInitRank");
+    api.commDestroy = (decltype(api.commDestroy))sym("ncclCommDestroy");
+    api.send = (decltype(api.send))sym("ncclSend");
+    api.recv = (decltype(api.recv))sym("ncclRecv");
+    api.groupStart = (decltype(api.groupStart))sym("ncclGroupStart");
+    api.groupEnd = (decltype(api.groupEnd))sym("ncclGroupEnd");
+    api.errStr = (decltype(api.errStr))sym("ncclGetErrorString");
+    api.ok = ok;
+    if (!ok) api.err = "libnccl.so.2 lacks a required symbol";
+    return api;
 }
+
+orca_status nccl_fail(ncclResult_t r, const char* what) {
+    NcclApi& N = nccl();
+    return fail(ORCA_ERR_NCCL, std::string(what) + ": " + (N.errStr ? N.errStr(r) : "?"));
+}
+
+// ------------------------------------------------------------- exchange buffers
+struct ExAlloc {
+    void* base = nullptr;
+    size_t bytes = 0;
+    ExBuf b{};
+};
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+orca_status ex_alloc(ExAlloc& x, int capM, int capH) {
+    if (x.base && x.b.capM >= capM && x.b.capH >= capH) return ORCA_OK;
+    dfree(x.base);
+    size_t sz[9] = {16, (size_t)capM * 8, (size_t)capM * 8, (size_t)capM * 8, (size_t)capM * 4,
+                    (size_t)capM * 4, (size_t)capH * 8, (size_t)capH * 8, (size_t)capH * 4};
+    size_t off[9], o = 0;
+    for (int q = 0; q < 9; ++q) {
+        off[q] = o;
+        o = align16(o + sz[q]);
+    }
+    x.bytes = o;
+    CK(cudaMalloc(&x.base, x.bytes));
+    CK(cudaMemset(x.base, 0, x.bytes));
+    char* p = (char*)x.base;
+    x.b.hdr = (int*)(p + off[0]);
+    x.b.mpos = (float2*)(p + off[1]);
+    x.b.mvel = (float2*)(p + off[2]);
+    x.b.maux = (float2*)(p + off[3]);
+    x.b.mid = (uint32_t*)(p + off[4]);
+    x.b.mrk2 = (float*)(p + off[5]);
+    x.b.hpos = (float2*)(p + off[6]);
+    x.b.hvel = (float2*)(p + off[7]);
+    x.b.hid = (uint32_t*)(p + off[8]);
+    x.b.capM = capM;
+    x.b.capH = capH;
+    return ORCA_OK;
+}
+
+// --------------------------------------------------------------------- a strip
+struct Domain {
+    int strip = 0;  // strip index in [0, world)
+    Grid g{};
+    int64_t nbins = 0, binCap = 0;
+    int capW = 0;
+    float2 *posS = nullptr, *velS = nullptr, *auxS = nullptr, *posW = nullptr, *velW = nullptr, *auxW = nullptr;
+    float *rk2S = nullptr, *rk2W = nullptr;
+    uint32_t *idS = nullptr, *idW = nullptr, *cellW = nullptr, *rankW = nullptr;
+    uint32_t *count = nullptr, *binStart = nullptr;
+    unsigned long long* scanStatus = nullptr;  // look-back status + ticket + LP3 queue count
+    int4* qEntry = nullptr;
+    float4* qLines = nullptr;
+    int* ctr = nullptr;
+    unsigned long long* stats = nullptr;
+    ExAlloc sendL, sendR, recvL, recvR;
+
+    void release() {
+        float2** f2[] = {&posS, &velS, &auxS, &posW, &velW, &auxW};
+        uint32_t** u4[] = {&idS, &idW, &cellW, &rankW, &count, &binStart};
+        for (auto p : f2) dfree(*p);
+        for (auto p : u4) dfree(*p);
+        dfree(rk2S);
+        dfree(rk2W);
+        dfree(scanStatus);
+        dfree(qEntry);
+        dfree(qLines);
+        dfree(ctr);
+        dfree(stats);
+        for (ExAlloc* x : {&sendL, &sendR, &recvL, &recvR}) dfree(x->base);
+    }
+};
 
 }  // namespace
 
@@ -68,34 +200,25 @@ struct orca_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     orca_params p{};
-    int64_t n = 0;
-    int64_t cap = 0;     // agent capacity of the buffers
-    int64_t cellCap = 0; // cell capacity
-    bool ready = false;
-    bool goals = false;
+    bool ready = false, goals = false;
     float prefSpeed = 0.0f;
-    Grid g{};
-    int64_t C = 0;     // sort bins = cells x 2^lgS sub-rows
-    // sorted (rest) state and work buffers
-    float2 *posS = nullptr, *velS = nullptr, *auxS = nullptr;
-    uint32_t* idS = nullptr;
-    float2 *posW = nullptr, *velW = nullptr, *auxW = nullptr;
-    float *rk2S = nullptr, *rk2W = nullptr;  // previous k-th neighbour d2 (search bound)
-    uint32_t *idW = nullptr, *cellW = nullptr, *rankW = nullptr;
-    uint32_t *count = nullptr, *binStart = nullptr;
-    unsigned long long* scanStatus = nullptr;  // look-back status words + ticket + LP3 queue count
-    int4* qEntry = nullptr;                    // LP3 queue (capacity cap)
-    float4* qLines = nullptr;                  // cap x k lines
-    int lp3Smem = 0;
-    unsigned long long* stats = nullptr;
-    float* partial = nullptr;  // k_minmax partials
-    float2* tmp2 = nullptr;    // id-ordered scratch (get_state / set_goals)
-    float2* tmp2b = nullptr;
+    int world = 1;  // strips in the whole decomposition
+    int rank = 0;   // NCCL rank (= the strip held by this context)
+    bool loopback = false;
+    ncclComm_t comm = nullptr;
+    std::vector<Domain> doms;
+    Grid gg{};  // global grid
+    int64_t nGlobal = 0;
+    int64_t stageCap = 0;
+    float2* stage = nullptr;                  // global inputs (pos | vel | aux), 3 x nGlobal
+    float2 *outA = nullptr, *outB = nullptr;  // id-ordered outputs
+    float* partial = nullptr;
+    int32_t* colHist = nullptr;
+    int colCap = 0;
     int64_t host_steps = 0, host_updates = 0;
-    // graph cache: (step count, executable), a few entries
     std::vector<std::pair<int, cudaGraphExec_t>> graphs;
-    cudaEvent_t ev[9] = {};
-    int smemBytes = 0;
+    cudaEvent_t ev[8] = {};
+    int smemBytes = 0, lp3Smem = 0;
 };
 
 namespace {
@@ -127,73 +250,82 @@ Model make_model(const orca_ctx* c) {
     return m;
 }
 
-StepArgs make_args(orca_ctx* c) {
+StepArgs make_args(orca_ctx* c, Domain& d) {
     StepArgs a{};
-    a.n = (int)c->n;
-    a.g = c->g;
+    a.g = d.g;
     a.m = make_model(c);
-    a.posS = c->posS;
-    a.velS = c->velS;
-    a.auxS = c->auxS;
-    a.rk2S = c->rk2S;
-    a.rk2W = c->rk2W;
-    a.idS = c->idS;
-    a.binStart = c->binStart;
-    a.posW = c->posW;
-    a.velW = c->velW;
-    a.auxW = c->auxW;
-    a.idW = c->idW;
-    a.cellW = c->cellW;
-    a.rankW = c->rankW;
-    a.count = c->count;
-    a.stats = c->stats;
-    a.qEntry = c->qEntry;
-    a.qLines = c->qLines;
-    a.qcap = (int)c->cap;
-    a.qCount = reinterpret_cast<unsigned int*>(c->scanStatus + scan_tiles(c->C) + 1);
+    a.posS = d.posS;
+    a.velS = d.velS;
+    a.auxS = d.auxS;
+    a.rk2S = d.rk2S;
+    a.idS = d.idS;
+    a.binStart = d.binStart;
+    a.posW = d.posW;
+    a.velW = d.velW;
+    a.auxW = d.auxW;
+    a.rk2W = d.rk2W;
+    a.idW = d.idW;
+    a.cellW = d.cellW;
+    a.rankW = d.rankW;
+    a.count = d.count;
+    a.stats = d.stats;
+    a.ctr = d.ctr;
+    a.capW = d.capW;
+    a.sendL = d.sendL.b;
+    a.sendR = d.sendR.b;
+    a.qEntry = d.qEntry;
+    a.qLines = d.qLines;
+    a.qcap = d.capW;
+    a.qCount = reinterpret_cast<unsigned int*>(d.scanStatus + scan_tiles(d.nbins) + 1);
     return a;
 }
 
-orca_status ensure_capacity(orca_ctx* c, int64_t n, int64_t C) {
-    if (n > c->cap) {
-        const int64_t cap = std::max<int64_t>(n, 1);
-        float2** f2[] = {&c->posS, &c->velS, &c->auxS, &c->posW, &c->velW, &c->auxW, &c->tmp2, &c->tmp2b};
-        uint32_t** u4[] = {&c->idS, &c->idW, &c->cellW, &c->rankW};
-        for (auto pp : f2) dfree(*pp);
-        for (auto pp : u4) dfree(*pp);
-        for (auto pp : f2) CK(cudaMalloc(pp, cap * sizeof(float2)));
-        for (auto pp : u4) CK(cudaMalloc(pp, cap * sizeof(uint32_t)));
-        dfree(c->qEntry);
-        dfree(c->qLines);
-        dfree(c->rk2S);
-        dfree(c->rk2W);
-        CK(cudaMalloc(&c->rk2S, cap * sizeof(float)));
-        CK(cudaMalloc(&c->rk2W, cap * sizeof(float)));
-        CK(cudaMalloc(&c->qEntry, cap * sizeof(int4)));
-        CK(cudaMalloc(&c->qLines, cap * std::max(1, c->p.maxNeighbors) * sizeof(float4)));
-        c->cap = cap;
+orca_status dom_alloc(orca_ctx* c, Domain& d, int capW, int64_t nbins, int capM, int capH) {
+    if (capW > d.capW) {
+        float2** f2[] = {&d.posS, &d.velS, &d.auxS, &d.posW, &d.velW, &d.auxW};
+        uint32_t** u4[] = {&d.idS, &d.idW, &d.cellW, &d.rankW};
+        for (auto p : f2) {
+            dfree(*p);
+            CK(cudaMalloc(p, (size_t)capW * sizeof(float2)));
+        }
+        for (auto p : u4) {
+            dfree(*p);
+            CK(cudaMalloc(p, (size_t)capW * sizeof(uint32_t)));
+        }
+        dfree(d.rk2S);
+        dfree(d.rk2W);
+        dfree(d.qEntry);
+        dfree(d.qLines);
+        CK(cudaMalloc(&d.rk2S, (size_t)capW * sizeof(float)));
+        CK(cudaMalloc(&d.rk2W, (size_t)capW * sizeof(float)));
+        CK(cudaMalloc(&d.qEntry, (size_t)capW * sizeof(int4)));
+        CK(cudaMalloc(&d.qLines, (size_t)capW * std::max(1, c->p.maxNeighbors) * sizeof(float4)));
+        d.capW = capW;
     }
-    if (C > c->cellCap) {
-        dfree(c->count);
-        dfree(c->binStart);
-        dfree(c->scanStatus);
-        CK(cudaMalloc(&c->count, (C + 4) * sizeof(uint32_t)));
-        CK(cudaMalloc(&c->binStart, (C + 1) * sizeof(uint32_t)));
-        CK(cudaMalloc(&c->scanStatus, (scan_tiles(C) + 2) * sizeof(unsigned long long)));
-        c->cellCap = C;
+    if (nbins > d.binCap) {
+        dfree(d.count);
+        dfree(d.binStart);
+        dfree(d.scanStatus);
+        CK(cudaMalloc(&d.count, (nbins + 4) * sizeof(uint32_t)));
+        CK(cudaMalloc(&d.binStart, (nbins + 1) * sizeof(uint32_t)));
+        CK(cudaMalloc(&d.scanStatus, (scan_tiles(nbins) + 2) * sizeof(unsigned long long)));
+        d.binCap = nbins;
+    }
+    if (!d.ctr) {
+        CK(cudaMalloc(&d.ctr, CT_COUNT * sizeof(int)));
+        CK(cudaMemset(d.ctr, 0, CT_COUNT * sizeof(int)));
+        CK(cudaMalloc(&d.stats, ST_COUNT * sizeof(unsigned long long)));
+        CK(cudaMemset(d.stats, 0, ST_COUNT * sizeof(unsigned long long)));
+    }
+    if (d.g.hasL) {
+        CKS(ex_alloc(d.sendL, capM, capH));
+        CKS(ex_alloc(d.recvL, capM, capH));
+    }
+    if (d.g.hasR) {
+        CKS(ex_alloc(d.sendR, capM, capH));
+        CKS(ex_alloc(d.recvR, capM, capH));
     }
     return ORCA_OK;
-}
-
-// exclusive scan of the bin counts (memset of the look-back status + one launch)
-cudaError_t enqueue_scan(orca_ctx* c) {
-    const int tiles = scan_tiles(c->C);
-    // status words, tile ticket and the LP3 queue count (consumed by k_lp3 before this point)
-    cudaError_t e = cudaMemsetAsync(c->scanStatus, 0, (tiles + 2) * sizeof(unsigned long long), c->stream);
-    if (e != cudaSuccess) return e;
-    k_scan<<<tiles, 1024, 0, c->stream>>>(c->count, c->binStart, (int)c->C, c->scanStatus,
-                                          reinterpret_cast<unsigned int*>(c->scanStatus + tiles));
-    return cudaGetLastError();
 }
 
 void drop_graph(orca_ctx* c) {
@@ -201,44 +333,189 @@ void drop_graph(orca_ctx* c) {
     c->graphs.clear();
 }
 
-// one step body: fused step kernel -> scan -> scatter (rest state = sorted arrays)
-cudaError_t enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
-    const int n = (int)c->n;
-    StepArgs a = make_args(c);
-    if (ev) cudaEventRecord(ev[0], c->stream);
-    if (n > 0) {
-        const int blocks = (n + kStepThreads - 1) / kStepThreads;
-        k_step<false><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
-        k_lp3<false><<<lp3_blocks(n), kStepThreads, c->lp3Smem, c->stream>>>(a);
-    }
-    if (ev) cudaEventRecord(ev[1], c->stream);
-    enqueue_scan(c);
-    if (ev) cudaEventRecord(ev[2], c->stream);
-    if (n > 0)
-        k_scatter<<<grid_blocks(n, 256), 256, 0, c->stream>>>(n, c->cellW, c->rankW, c->binStart, c->posW, c->velW,
-                                                              c->auxW, c->idW, c->posS, c->velS, c->auxS, c->idS,
-                                                              c->rk2W, c->rk2S);
-    if (ev) cudaEventRecord(ev[3], c->stream);
+cudaError_t enqueue_scan(orca_ctx* c, Domain& d) {
+    const int tiles = scan_tiles(d.nbins);
+    // status words, tile ticket and the LP3 queue count (consumed by k_lp3 before this point)
+    cudaError_t e = cudaMemsetAsync(d.scanStatus, 0, (tiles + 2) * sizeof(unsigned long long), c->stream);
+    if (e != cudaSuccess) return e;
+    k_scan<<<tiles, 1024, 0, c->stream>>>(d.count, d.binStart, (int)d.nbins, d.scanStatus,
+                                          reinterpret_cast<unsigned int*>(d.scanStatus + tiles));
     return cudaGetLastError();
+}
+
+cudaError_t enqueue_scatter(orca_ctx* c, Domain& d) {
+    k_scatter<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.ctr, d.cellW, d.rankW, d.binStart, d.posW, d.velW,
+                                                              d.auxW, d.idW, d.rk2W, d.posS, d.velS, d.auxS, d.idS,
+                                                              d.rk2S, d.capW);
+    return cudaGetLastError();
+}
+
+// Neighbour exchange of one step: every strip sends its L/R buffers and receives its
+// neighbours'.  Loopback: device copies between the strips of this context.  NCCL: one
+// group of send/recv with ranks +-1.
+orca_status enqueue_exchange(orca_ctx* c) {
+    if (c->world == 1) return ORCA_OK;
+    if (c->loopback) {
+        const int P = (int)c->doms.size();
+        for (int s = 0; s < P; ++s) {
+            Domain& d = c->doms[s];
+            if (d.g.hasR)
+                CK(cudaMemcpyAsync(c->doms[s + 1].recvL.base, d.sendR.base, d.sendR.bytes, cudaMemcpyDeviceToDevice,
+                                   c->stream));
+            if (d.g.hasL)
+                CK(cudaMemcpyAsync(c->doms[s - 1].recvR.base, d.sendL.base, d.sendL.bytes, cudaMemcpyDeviceToDevice,
+                                   c->stream));
+        }
+        return ORCA_OK;
+    }
+    NcclApi& N = nccl();
+    Domain& d = c->doms[0];
+    ncclResult_t r = N.groupStart();
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+    if (d.g.hasL) {
+        r = N.send(d.sendL.base, d.sendL.bytes, ncclUint8, c->rank - 1, c->comm, c->stream);
+        if (r == ncclSuccess) r = N.recv(d.recvL.base, d.recvL.bytes, ncclUint8, c->rank - 1, c->comm, c->stream);
+    }
+    if (r == ncclSuccess && d.g.hasR) {
+        r = N.send(d.sendR.base, d.sendR.bytes, ncclUint8, c->rank + 1, c->comm, c->stream);
+        if (r == ncclSuccess) r = N.recv(d.recvR.base, d.recvR.bytes, ncclUint8, c->rank + 1, c->comm, c->stream);
+    }
+    ncclResult_t r2 = N.groupEnd();
+    if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
+    if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
+    return ORCA_OK;
+}
+
+// One step body for every strip: reset per-step counters -> k_step (query, half-planes,
+// LP2, integrate, route) -> k_lp3 (queued infeasible agents) -> exchange -> k_receive ->
+// scan -> scatter.  ev (nullable): events around the stages for orca_step_timed.
+orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
+    if (ev) CK(cudaEventRecord(ev[0], c->stream));
+    for (Domain& d : c->doms) {
+        CK(cudaMemsetAsync(d.ctr + CT_NOWN, 0, 2 * sizeof(int), c->stream));  // NOWN, EXTRA
+        if (d.g.hasL) CK(cudaMemsetAsync(d.sendL.b.hdr, 0, 16, c->stream));
+        if (d.g.hasR) CK(cudaMemsetAsync(d.sendR.b.hdr, 0, 16, c->stream));
+        StepArgs a = make_args(c, d);
+        k_step<false><<<(d.capW + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
+        k_lp3<false><<<lp3_blocks(d.capW), kStepThreads, c->lp3Smem, c->stream>>>(a);
+    }
+    CK(cudaGetLastError());
+    if (ev) CK(cudaEventRecord(ev[1], c->stream));
+    CKS(enqueue_exchange(c));
+    for (Domain& d : c->doms) {
+        if (d.g.hasL || d.g.hasR) {
+            StepArgs a = make_args(c, d);
+            const int capX = (d.g.hasL ? d.recvL.b.capM + d.recvL.b.capH : 0) +
+                             (d.g.hasR ? d.recvR.b.capM + d.recvR.b.capH : 0);
+            k_receive<<<cap_blocks(capX, 256), 256, 0, c->stream>>>(a, d.recvL.b, d.recvR.b);
+        }
+    }
+    CK(cudaGetLastError());
+    if (ev) CK(cudaEventRecord(ev[2], c->stream));
+    for (Domain& d : c->doms) CK(enqueue_scan(c, d));
+    if (ev) CK(cudaEventRecord(ev[3], c->stream));
+    for (Domain& d : c->doms) CK(enqueue_scatter(c, d));
+    if (ev) CK(cudaEventRecord(ev[4], c->stream));
+    return ORCA_OK;
 }
 
 // The dry (debug) step: same kernels, outputs by id, state untouched; the LP3 queue
 // count is zeroed before and after so the next real step starts from an empty queue.
-cudaError_t dry_step(orca_ctx* c, StepArgs& a) {
-    const int n = (int)c->n;
+cudaError_t dry_step(orca_ctx* c, Domain& d, StepArgs& a) {
     cudaError_t e = cudaMemsetAsync(a.qCount, 0, sizeof(unsigned int), c->stream);
     if (e != cudaSuccess) return e;
-    k_step<true><<<(n + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
-    k_lp3<true><<<lp3_blocks(n), kStepThreads, c->lp3Smem, c->stream>>>(a);
+    k_step<true><<<(d.capW + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
+    k_lp3<true><<<lp3_blocks(d.capW), kStepThreads, c->lp3Smem, c->stream>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return cudaMemsetAsync(a.qCount, 0, sizeof(unsigned int), c->stream);
+}
+
+orca_status check_overflow(orca_ctx* c) {
+    int any = 0;
+    for (Domain& d : c->doms) {
+        if (!d.ctr) continue;
+        int f = 0;
+        CK(cudaMemcpyAsync(&f, d.ctr + CT_OVF, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        any |= f;
+    }
+    if (any)
+        return fail(ORCA_ERR_CAPACITY, std::string("strip buffer overflow (") + ((any & OVF_WORK) ? "work " : "") +
+                                           ((any & OVF_MIG) ? "migrants " : "") + ((any & OVF_HALO) ? "halo" : "") +
+                                           "); call orca_set_agents again to re-partition");
+    return ORCA_OK;
+}
+
+// owned range [o0, o1) of a domain (host read; synchronises)
+orca_status owned_range_host(orca_ctx* c, Domain& d, int* o0, int* o1) {
+    const int64_t nyS = (int64_t)d.g.ny << d.g.lgS;
+    uint32_t v[2];
+    CK(cudaMemcpyAsync(&v[0], d.binStart + (d.g.c0 - d.g.e0) * nyS, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&v[1], d.binStart + (d.g.c1 - d.g.e0) * nyS, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *o0 = (int)v[0];
+    *o1 = (int)v[1];
+    return ORCA_OK;
+}
+
+orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, orca_ctx** cp) {
+    if (!params || !out) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (!finite_params(params)) return fail(ORCA_ERR_INVALID_ARGUMENT, "parameter out of range or not finite");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(ORCA_ERR_INVALID_ARGUMENT, "no such CUDA device");
+    CK(cudaSetDevice(device));
+    orca_ctx* c = new (std::nothrow) orca_ctx();
+    if (!c) return fail(ORCA_ERR_OUT_OF_MEMORY, "host allocation");
+    c->device = device;
+    c->p = *params;
+    *cp = c;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&c->partial, 1024 * 5 * sizeof(float));
+    for (int q = 0; q < 8 && e == cudaSuccess; ++q) e = cudaEventCreate(&c->ev[q]);
+    c->smemBytes = step_smem_per_thread(params->maxNeighbors) * kStepThreads;
+    c->lp3Smem = std::max(1, 6 * params->maxNeighbors) * 4 * kStepThreads;
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_lp3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
+    if (e != cudaSuccess) return cuda_fail(e, "orca_create");
+    return ORCA_OK;
 }
 
 // Copy a float[2n] user array (host or device) into a device float2 buffer.
 cudaError_t copy_in(orca_ctx* c, float2* dst, const float* src, int64_t n) {
     if (n == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, src, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->stream);
+}
+
+// min/max of the staged positions + finiteness of the three staged arrays
+orca_status stage_bounds(orca_ctx* c, const float2* a, const float2* b, const float2* q, int64_t n, float mn[2],
+                         float mx[2]) {
+    const int blocks = std::min(1024, cap_blocks(n, 256));
+    k_minmax<<<blocks, 256, 0, c->stream>>>((int)n, a, b, q, c->partial);
+    CK(cudaGetLastError());
+    std::vector<float> h((size_t)blocks * 5);
+    CK(cudaMemcpyAsync(h.data(), c->partial, h.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    mn[0] = mn[1] = INFINITY;
+    mx[0] = mx[1] = -INFINITY;
+    double bad = 0;
+    for (int k = 0; k < blocks; ++k) {
+        mn[0] = std::min(mn[0], h[k * 5 + 0]);
+        mn[1] = std::min(mn[1], h[k * 5 + 1]);
+        mx[0] = std::max(mx[0], h[k * 5 + 2]);
+        mx[1] = std::max(mx[1], h[k * 5 + 3]);
+        bad += h[k * 5 + 4];
+    }
+    if (bad > 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "NaN/Inf in the input arrays");
+    return ORCA_OK;
 }
 
 }  // namespace
@@ -262,37 +539,95 @@ const char* orca_status_string(orca_status s) {
 
 const char* orca_last_error(void) { return g_last_error.c_str(); }
 
-orca_status orca_create(const orca_params* params, int32_t device, orca_ctx** out) {
-    if (!params || !out) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
-    *out = nullptr;
-    if (!finite_params(params)) return fail(ORCA_ERR_INVALID_ARGUMENT, "parameter out of range or not finite");
-    int ndev = 0;
-    CK(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) return fail(ORCA_ERR_INVALID_ARGUMENT, "no such CUDA device");
-    CK(cudaSetDevice(device));
-    orca_ctx* c = new (std::nothrow) orca_ctx();
-    if (!c) return fail(ORCA_ERR_OUT_OF_MEMORY, "host allocation");
-    c->device = device;
-    c->p = *params;
-    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaMalloc(&c->stats, ST_COUNT * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemset(c->stats, 0, ST_COUNT * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMalloc(&c->partial, 1024 * 5 * sizeof(float));
-    for (int q = 0; q < 9 && e == cudaSuccess; ++q) e = cudaEventCreate(&c->ev[q]);
-    c->smemBytes = step_smem_per_thread(params->maxNeighbors) * kStepThreads;
-    c->lp3Smem = std::max(1, 6 * params->maxNeighbors) * 4 * kStepThreads;
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_lp3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
-    if (e != cudaSuccess) {
-        orca_destroy(c);
-        return cuda_fail(e, "orca_create");
+orca_status orca_partition_columns(const int64_t* colCount, int32_t nx, int32_t world, int32_t* bounds) {
+    if (!colCount || !bounds || nx < 1 || world < 1 || world > nx)
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "need 1 <= world <= nx and non-null arrays");
+    double total = 0.0;
+    for (int c = 0; c < nx; ++c) {
+        if (colCount[c] < 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "negative count");
+        total += (double)colCount[c];
     }
+    bounds[0] = 0;
+    double cum = 0.0;
+    int c = 0;
+    for (int s = 1; s < world; ++s) {
+        const double target = total * s / world;
+        // at least one column for this strip and for every remaining one
+        const int lo = bounds[s - 1] + 1, hi = nx - (world - s);
+        while (c < lo) cum += (double)colCount[c++];
+        while (c < hi && cum + 0.5 * (double)colCount[c] < target) cum += (double)colCount[c++];
+        bounds[s] = c;
+    }
+    bounds[world] = nx;
+    return ORCA_OK;
+}
+
+orca_status orca_create(const orca_params* params, int32_t device, orca_ctx** out) {
+    orca_ctx* c = nullptr;
+    orca_status s = ctx_init(params, device, out, &c);
+    if (s != ORCA_OK) {
+        orca_destroy(c);
+        return s;
+    }
+    c->doms.resize(1);
+    *out = c;
+    return ORCA_OK;
+}
+
+orca_status orca_create_strips(const orca_params* params, int32_t device, int32_t nstrips, orca_ctx** out) {
+    if (nstrips < 1 || nstrips > 64) return fail(ORCA_ERR_INVALID_ARGUMENT, "nstrips out of range");
+    if (params && nstrips > 1 && !(params->maxSpeed * params->timeStep < params->neighborDist))
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "strips need maxSpeed * timeStep < neighborDist");
+    orca_ctx* c = nullptr;
+    orca_status s = ctx_init(params, device, out, &c);
+    if (s != ORCA_OK) {
+        orca_destroy(c);
+        return s;
+    }
+    c->doms.resize(nstrips);
+    c->world = nstrips;
+    c->loopback = true;
+    *out = c;
+    return ORCA_OK;
+}
+
+orca_status orca_nccl_unique_id(void* id128) {
+    if (!id128) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
+    NcclApi& N = nccl();
+    if (!N.ok) return fail(ORCA_ERR_NCCL, N.err);
+    ncclUniqueId id;
+    ncclResult_t r = N.getUniqueId(&id);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    std::memcpy(id128, &id, sizeof(id));
+    return ORCA_OK;
+}
+
+orca_status orca_create_dist(const orca_params* params, int32_t device, int32_t rank, int32_t world,
+                             const void* nccl_id128, orca_ctx** out) {
+    if (world < 1 || rank < 0 || rank >= world) return fail(ORCA_ERR_INVALID_ARGUMENT, "bad rank/world");
+    if (world == 1) return orca_create(params, device, out);
+    if (!nccl_id128) return fail(ORCA_ERR_INVALID_ARGUMENT, "null NCCL id");
+    if (params && !(params->maxSpeed * params->timeStep < params->neighborDist))
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "strips need maxSpeed * timeStep < neighborDist");
+    NcclApi& N = nccl();
+    if (!N.ok) return fail(ORCA_ERR_NCCL, N.err);
+    orca_ctx* c = nullptr;
+    orca_status s = ctx_init(params, device, out, &c);
+    if (s != ORCA_OK) {
+        orca_destroy(c);
+        return s;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id128, sizeof(id));
+    ncclResult_t r = N.commInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        c->comm = nullptr;
+        orca_destroy(c);
+        return nccl_fail(r, "ncclCommInitRank");
+    }
+    c->world = world;
+    c->rank = rank;
+    c->doms.resize(1);
     *out = c;
     return ORCA_OK;
 }
@@ -302,60 +637,45 @@ void orca_destroy(orca_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     drop_graph(c);
-    float2** f2[] = {&c->posS, &c->velS, &c->auxS, &c->posW, &c->velW, &c->auxW, &c->tmp2, &c->tmp2b};
-    uint32_t** u4[] = {&c->idS, &c->idW, &c->cellW, &c->rankW, &c->count, &c->binStart};
-    for (auto pp : f2) dfree(*pp);
-    for (auto pp : u4) dfree(*pp);
-    dfree(c->stats);
+    for (Domain& d : c->doms) d.release();
+    dfree(c->stage);
+    dfree(c->outA);
+    dfree(c->outB);
     dfree(c->partial);
-    dfree(c->scanStatus);
-    dfree(c->qEntry);
-    dfree(c->qLines);
-    dfree(c->rk2S);
-    dfree(c->rk2W);
+    dfree(c->colHist);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
 
 orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const float* vel, const float* pref) {
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
-    if (n < 0 || n > (int64_t)1 << 30) return fail(ORCA_ERR_INVALID_ARGUMENT, "n out of range");
+    if (n < 0 || n > ((int64_t)1 << 30)) return fail(ORCA_ERR_INVALID_ARGUMENT, "n out of range");
     if (n > 0 && (!pos || !vel || !pref)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->ready = false;
     c->goals = false;
-    // stage the inputs in the work buffers (capacity first; grid sized after min/max)
-    orca_status st = ensure_capacity(c, n, 1);
-    if (st) return st;
-    CK(copy_in(c, c->posW, pos, n));
-    CK(copy_in(c, c->velW, vel, n));
-    CK(copy_in(c, c->auxW, pref, n));
-    // bounds + finiteness on the device (inputs may be device pointers)
-    float mn[2] = {0.0f, 0.0f}, mx[2] = {0.0f, 0.0f};
-    if (n > 0) {
-        const int blocks = std::min(1024, grid_blocks(n, 256));
-        k_minmax<<<blocks, 256, 0, c->stream>>>((int)n, c->posW, c->velW, c->auxW, c->partial);
-        CK(cudaGetLastError());
-        std::vector<float> h((size_t)blocks * 5);
-        CK(cudaMemcpyAsync(h.data(), c->partial, h.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        mn[0] = mn[1] = INFINITY;
-        mx[0] = mx[1] = -INFINITY;
-        double bad = 0;
-        for (int b = 0; b < blocks; ++b) {
-            mn[0] = std::min(mn[0], h[b * 5 + 0]);
-            mn[1] = std::min(mn[1], h[b * 5 + 1]);
-            mx[0] = std::max(mx[0], h[b * 5 + 2]);
-            mx[1] = std::max(mx[1], h[b * 5 + 3]);
-            bad += h[b * 5 + 4];
-        }
-        if (bad > 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "NaN/Inf in pos/vel/prefVel");
+    // stage the global inputs (every rank of a decomposition gets the same arrays)
+    if (n > c->stageCap) {
+        dfree(c->stage);
+        dfree(c->outA);
+        dfree(c->outB);
+        CK(cudaMalloc(&c->stage, (size_t)n * 3 * sizeof(float2)));
+        CK(cudaMalloc(&c->outA, (size_t)n * sizeof(float2)));
+        CK(cudaMalloc(&c->outB, (size_t)n * sizeof(float2)));
+        c->stageCap = n;
     }
-    // frozen grid (reading Q12)
+    float2 *sp = c->stage, *sv = c->stage + n, *sa = c->stage + 2 * n;
+    CK(copy_in(c, sp, pos, n));
+    CK(copy_in(c, sv, vel, n));
+    CK(copy_in(c, sa, pref, n));
+    float mn[2] = {0.0f, 0.0f}, mx[2] = {0.0f, 0.0f};
+    if (n > 0) CKS(stage_bounds(c, sp, sv, sa, n, mn, mx));
+    // frozen global grid (reading Q12)
     const float cs = c->p.neighborDist;
     Grid g{};
     g.cs = cs;
@@ -378,24 +698,63 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     g.invCs = 1.0 / (double)cs;
     g.csSub = (double)cs / (double)(1 << g.lgS);
     g.invCsSub = (double)(1 << g.lgS) / (double)cs;
-    c->g = g;
-    c->C = ((int64_t)g.nx * g.ny) << g.lgS;
-    st = ensure_capacity(c, n, c->C);
-    if (st) return st;
-    c->n = n;
-    // ids, initial binning, scan, scatter -> rest state
-    CK(cudaMemsetAsync(c->count, 0, c->C * sizeof(uint32_t), c->stream));
-    if (n > 0) {
-        k_iota<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->idW, c->rk2W);
-        k_hash<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->posW, c->g, c->cellW, c->rankW, c->count);
+    c->gg = g;
+    c->nGlobal = n;
+    if (c->world > g.nx) return fail(ORCA_ERR_CAPACITY, "more strips than grid columns");
+    // column histogram -> strips (every rank computes the same partition)
+    std::vector<int64_t> colCount(g.nx, 0);
+    if (c->world > 1 && n > 0) {
+        if (g.nx > c->colCap) {
+            dfree(c->colHist);
+            CK(cudaMalloc(&c->colHist, (size_t)g.nx * sizeof(int32_t)));
+            c->colCap = g.nx;
+        }
+        CK(cudaMemsetAsync(c->colHist, 0, (size_t)g.nx * sizeof(int32_t), c->stream));
+        k_colhist<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, sp, g, c->colHist);
+        CK(cudaGetLastError());
+        std::vector<int32_t> h(g.nx);
+        CK(cudaMemcpyAsync(h.data(), c->colHist, (size_t)g.nx * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int x = 0; x < g.nx; ++x) colCount[x] = h[x];
+    } else {
+        colCount[0] = n;
     }
-    CK(enqueue_scan(c));
-    if (n > 0)
-        k_scatter<<<grid_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->cellW, c->rankW, c->binStart, c->posW,
-                                                              c->velW, c->auxW, c->idW, c->posS, c->velS, c->auxS,
-                                                              c->idS, c->rk2W, c->rk2S);
-    CK(cudaGetLastError());
+    std::vector<int32_t> bounds(c->world + 1);
+    CKS(orca_partition_columns(colCount.data(), g.nx, c->world, bounds.data()));
+    const int first = c->loopback ? 0 : c->rank;
+    for (size_t q = 0; q < c->doms.size(); ++q) {
+        Domain& d = c->doms[q];
+        const int s = first + (int)q;
+        d.strip = s;
+        d.g = g;
+        d.g.c0 = bounds[s];
+        d.g.c1 = bounds[s + 1];
+        d.g.e0 = std::max(d.g.c0 - 1, 0);
+        d.g.e1 = std::min(d.g.c1 + 1, g.nx);
+        d.g.hasL = s > 0;
+        d.g.hasR = s < c->world - 1;
+        d.nbins = ((int64_t)(d.g.e1 - d.g.e0) * g.ny) << g.lgS;
+        int64_t sel = 0;
+        for (int x = d.g.e0; x < d.g.e1; ++x) sel += colCount[x];
+        const int64_t edge = std::max(colCount[d.g.c0], colCount[d.g.c1 - 1]);
+        // single strip: exact; strips: headroom for density drift between re-partitions
+        const int64_t capW = (c->world == 1) ? std::max<int64_t>(n, 1) : sel + sel / 2 + 4096;
+        if (capW > ((int64_t)1 << 30)) return fail(ORCA_ERR_CAPACITY, "strip too large");
+        const int capH = (int)std::min<int64_t>(edge + edge / 2 + 1024, (int64_t)1 << 28);
+        const int capM = std::max(1024, capH / 4);
+        CKS(dom_alloc(c, d, (int)capW, d.nbins, capM, capH));
+        CK(cudaMemsetAsync(d.ctr, 0, CT_COUNT * sizeof(int), c->stream));
+        CK(cudaMemsetAsync(d.count, 0, d.nbins * sizeof(uint32_t), c->stream));
+        if (n > 0)
+            k_select<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, sp, sv, sa, d.g, d.posW, d.velW, d.auxW,
+                                                                d.idW, d.rk2W, d.cellW, d.rankW, d.count, d.ctr,
+                                                                d.capW);
+        CK(cudaGetLastError());
+        CK(enqueue_scan(c, d));
+        CK(enqueue_scatter(c, d));
+    }
     CK(cudaStreamSynchronize(c->stream));
+    CKS(check_overflow(c));
     c->ready = true;
     return ORCA_OK;
 }
@@ -404,22 +763,19 @@ orca_status orca_set_goals(orca_ctx* c, const float* goal, float prefSpeed) {
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     if (!(prefSpeed >= 0.0f) || !std::isfinite(prefSpeed)) return fail(ORCA_ERR_INVALID_ARGUMENT, "prefSpeed");
-    if (c->n > 0 && !goal) return fail(ORCA_ERR_INVALID_ARGUMENT, "null goal");
+    if (c->nGlobal > 0 && !goal) return fail(ORCA_ERR_INVALID_ARGUMENT, "null goal");
     CK(cudaSetDevice(c->device));
-    const int n = (int)c->n;
+    const int64_t n = c->nGlobal;
     if (n > 0) {
-        // goals arrive in id order: check finiteness, then permute into sorted order
-        CK(copy_in(c, c->tmp2, goal, n));
-        const int blocks = std::min(1024, grid_blocks(n, 256));
-        k_minmax<<<blocks, 256, 0, c->stream>>>(n, c->tmp2, c->tmp2, c->tmp2, c->partial);
-        std::vector<float> h((size_t)blocks * 5);
-        CK(cudaMemcpyAsync(h.data(), c->partial, h.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        for (int b = 0; b < blocks; ++b)
-            if (h[b * 5 + 4] > 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "NaN/Inf in goal");
-        // gather by id into the sorted aux array
-        k_gather_by_id<<<grid_blocks(n, 256), 256, 0, c->stream>>>(n, c->idS, c->tmp2, c->auxS);
-        CK(cudaGetLastError());
+        // goals arrive in id order (global): check finiteness, gather into sorted order
+        CK(copy_in(c, c->outA, goal, n));
+        float mn[2], mx[2];
+        CKS(stage_bounds(c, c->outA, c->outA, c->outA, n, mn, mx));
+        for (Domain& d : c->doms) {
+            k_gather_by_id<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, (int)d.nbins, d.idS, c->outA,
+                                                                          d.auxS);
+            CK(cudaGetLastError());
+        }
     }
     drop_graph(c);
     c->goals = true;
@@ -449,12 +805,12 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
             }
             cudaGraph_t gr;
             CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-            cudaError_t e = cudaSuccess;
-            for (int q = 0; q < s && e == cudaSuccess; ++q) e = enqueue_step(c, nullptr);
+            orca_status st = ORCA_OK;
+            for (int q = 0; q < s && st == ORCA_OK; ++q) st = enqueue_step(c, nullptr);
             cudaError_t e2 = cudaStreamEndCapture(c->stream, &gr);
-            if (e != cudaSuccess) return cuda_fail(e, "capture");
+            if (st != ORCA_OK) return st;
             if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
-            e = cudaGraphInstantiate(&exec, gr, 0);
+            cudaError_t e = cudaGraphInstantiate(&exec, gr, 0);
             cudaGraphDestroy(gr);
             if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
             c->graphs.emplace_back(s, exec);
@@ -463,7 +819,7 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
         remaining -= s;
     }
     c->host_steps += n_steps;
-    c->host_updates += (int64_t)n_steps * c->n;
+    c->host_updates += (int64_t)n_steps * c->nGlobal;
     return ORCA_OK;
 }
 
@@ -474,45 +830,39 @@ orca_status orca_step_timed(orca_ctx* c, int32_t n_steps, double ms[4]) {
     CK(cudaSetDevice(c->device));
     for (int q = 0; q < 4; ++q) ms[q] = 0.0;
     for (int s = 0; s < n_steps; ++s) {
-        CK(enqueue_step(c, c->ev));
-        CK(cudaEventSynchronize(c->ev[3]));
+        CKS(enqueue_step(c, c->ev));
+        CK(cudaEventSynchronize(c->ev[4]));
         float t;
         CK(cudaEventElapsedTime(&t, c->ev[0], c->ev[1]));
-        ms[0] += t;
-        CK(cudaEventElapsedTime(&t, c->ev[1], c->ev[2]));
-        ms[1] += t;
+        ms[0] += t;  // k_step + k_lp3
         CK(cudaEventElapsedTime(&t, c->ev[2], c->ev[3]));
-        ms[2] += t;
+        ms[1] += t;  // scan
+        CK(cudaEventElapsedTime(&t, c->ev[3], c->ev[4]));
+        ms[2] += t;  // scatter
+        CK(cudaEventElapsedTime(&t, c->ev[1], c->ev[2]));
+        ms[3] += t;  // exchange + receive
     }
     c->host_steps += n_steps;
-    c->host_updates += (int64_t)n_steps * c->n;
+    c->host_updates += (int64_t)n_steps * c->nGlobal;
     return ORCA_OK;
 }
 
 orca_status orca_get_state(orca_ctx* c, float* pos, float* vel) {
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    if (c->world > 1 && !c->loopback)
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "multi-rank context: use orca_get_local_state");
     CK(cudaSetDevice(c->device));
-    const int n = (int)c->n;
+    CKS(check_overflow(c));
+    const int64_t n = c->nGlobal;
     if (n > 0 && (pos || vel)) {
-        k_unpermute<<<grid_blocks(n, 256), 256, 0, c->stream>>>(n, c->idS, c->posS, c->velS, c->tmp2, c->tmp2b);
+        for (Domain& d : c->doms)
+            k_unpermute<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.idS, d.posS, d.velS,
+                                                                       pos ? c->outA : nullptr,
+                                                                       vel ? c->outB : nullptr);
         CK(cudaGetLastError());
-        if (pos) CK(cudaMemcpyAsync(pos, c->tmp2, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->stream));
-        if (vel) CK(cudaMemcpyAsync(vel, c->tmp2b, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->stream));
-    }
-    CK(cudaStreamSynchronize(c->stream));
-    return ORCA_OK;
-}
-
-orca_status orca_get_local_state(orca_ctx* c, int32_t* ids, float* pos, float* vel) {
-    if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
-    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
-    CK(cudaSetDevice(c->device));
-    const size_t n = (size_t)c->n;
-    if (n > 0) {
-        if (ids) CK(cudaMemcpyAsync(ids, c->idS, n * sizeof(uint32_t), cudaMemcpyDefault, c->stream));
-        if (pos) CK(cudaMemcpyAsync(pos, c->posS, n * sizeof(float2), cudaMemcpyDefault, c->stream));
-        if (vel) CK(cudaMemcpyAsync(vel, c->velS, n * sizeof(float2), cudaMemcpyDefault, c->stream));
+        if (pos) CK(cudaMemcpyAsync(pos, c->outA, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->stream));
+        if (vel) CK(cudaMemcpyAsync(vel, c->outB, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
     return ORCA_OK;
@@ -520,7 +870,39 @@ orca_status orca_get_local_state(orca_ctx* c, int32_t* ids, float* pos, float* v
 
 orca_status orca_get_count(orca_ctx* c, int64_t* n) {
     if (!c || !n) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
-    *n = c->n;
+    if (!c->ready) {
+        *n = 0;
+        return ORCA_OK;
+    }
+    CK(cudaSetDevice(c->device));
+    int64_t t = 0;
+    for (Domain& d : c->doms) {
+        int o0, o1;
+        CKS(owned_range_host(c, d, &o0, &o1));
+        t += o1 - o0;
+    }
+    *n = t;
+    return ORCA_OK;
+}
+
+orca_status orca_get_local_state(orca_ctx* c, int32_t* ids, float* pos, float* vel) {
+    if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    CK(cudaSetDevice(c->device));
+    CKS(check_overflow(c));
+    size_t off = 0;
+    for (Domain& d : c->doms) {
+        int o0, o1;
+        CKS(owned_range_host(c, d, &o0, &o1));
+        const size_t m = (size_t)(o1 - o0);
+        if (m > 0) {
+            if (ids) CK(cudaMemcpyAsync(ids + off, d.idS + o0, m * 4, cudaMemcpyDefault, c->stream));
+            if (pos) CK(cudaMemcpyAsync(pos + 2 * off, d.posS + o0, m * 8, cudaMemcpyDefault, c->stream));
+            if (vel) CK(cudaMemcpyAsync(vel + 2 * off, d.velS + o0, m * 8, cudaMemcpyDefault, c->stream));
+        }
+        off += m;
+    }
+    CK(cudaStreamSynchronize(c->stream));
     return ORCA_OK;
 }
 
@@ -528,13 +910,23 @@ orca_status orca_get_grid(orca_ctx* c, double origin[2], float* cs, int32_t dims
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     if (origin) {
-        origin[0] = c->g.ox;
-        origin[1] = c->g.oy;
+        origin[0] = c->gg.ox;
+        origin[1] = c->gg.oy;
     }
-    if (cs) *cs = c->g.cs;
+    if (cs) *cs = c->gg.cs;
     if (dims) {
-        dims[0] = c->g.nx;
-        dims[1] = c->g.ny;
+        dims[0] = c->gg.nx;
+        dims[1] = c->gg.ny;
+    }
+    return ORCA_OK;
+}
+
+orca_status orca_get_strips(orca_ctx* c, int32_t* bounds) {
+    if (!c || !bounds) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    for (size_t q = 0; q < c->doms.size(); ++q) {
+        bounds[2 * q] = c->doms[q].g.c0;
+        bounds[2 * q + 1] = c->doms[q].g.c1;
     }
     return ORCA_OK;
 }
@@ -543,13 +935,14 @@ orca_status orca_debug_cells(orca_ctx* c, int32_t* cx, int32_t* cy) {
     if (!c || !cx || !cy) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
-    const int n = (int)c->n;
+    const int64_t n = c->nGlobal;
     if (n > 0) {
-        int32_t* d = reinterpret_cast<int32_t*>(c->tmp2);  // 2 x int32 per agent
-        k_cells<<<grid_blocks(n, 256), 256, 0, c->stream>>>(n, c->idS, c->posS, c->g, d, d + n);
+        int32_t* d0 = reinterpret_cast<int32_t*>(c->outA);  // 2 x int32 per agent
+        for (Domain& d : c->doms)
+            k_cells<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.idS, d.posS, d0, d0 + n);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(cx, d, (size_t)n * sizeof(int32_t), cudaMemcpyDefault, c->stream));
-        CK(cudaMemcpyAsync(cy, d + n, (size_t)n * sizeof(int32_t), cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(cx, d0, (size_t)n * sizeof(int32_t), cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(cy, d0 + n, (size_t)n * sizeof(int32_t), cudaMemcpyDefault, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
     return ORCA_OK;
@@ -559,7 +952,7 @@ orca_status orca_debug_step(orca_ctx* c, float* vnew, uint8_t* flags, int32_t* n
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
-    const int n = (int)c->n;
+    const int64_t n = c->nGlobal;
     if (n == 0) return ORCA_OK;
     const int k = c->p.maxNeighbors;
     float2* dV = nullptr;
@@ -569,13 +962,14 @@ orca_status orca_debug_step(orca_ctx* c, float* vnew, uint8_t* flags, int32_t* n
     cudaError_t e = cudaMalloc(&dF, (size_t)n);
     if (e == cudaSuccess) e = cudaMalloc(&dC, (size_t)n * sizeof(int32_t));
     if (e == cudaSuccess && k > 0) e = cudaMalloc(&dN, (size_t)n * k * sizeof(int32_t));
-    if (e == cudaSuccess) {
-        StepArgs a = make_args(c);
+    for (Domain& d : c->doms) {
+        if (e != cudaSuccess) break;
+        StepArgs a = make_args(c, d);
         a.dbgV = dV;
         a.dbgFlags = dF;
         a.dbgNbr = dN;
         a.dbgCnt = dC;
-        e = dry_step(c, a);
+        e = dry_step(c, d, a);
     }
     if (e == cudaSuccess && vnew) e = cudaMemcpyAsync(vnew, dV, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->stream);
     if (e == cudaSuccess && flags) e = cudaMemcpyAsync(flags, dF, (size_t)n, cudaMemcpyDefault, c->stream);
@@ -596,15 +990,15 @@ orca_status orca_debug_work(orca_ctx* c, int64_t out[5]) {
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
     for (int q = 0; q < 5; ++q) out[q] = 0;
-    const int n = (int)c->n;
-    if (n == 0) return ORCA_OK;
+    if (c->nGlobal == 0) return ORCA_OK;
     Work* dW = nullptr;
     CK(cudaMalloc(&dW, sizeof(Work)));
     cudaError_t e = cudaMemsetAsync(dW, 0, sizeof(Work), c->stream);
-    if (e == cudaSuccess) {
-        StepArgs a = make_args(c);
+    for (Domain& d : c->doms) {
+        if (e != cudaSuccess) break;
+        StepArgs a = make_args(c, d);
         a.work = dW;
-        e = dry_step(c, a);
+        e = dry_step(c, d, a);
     }
     Work h{};
     if (e == cudaSuccess) e = cudaMemcpyAsync(&h, dW, sizeof(Work), cudaMemcpyDeviceToHost, c->stream);
@@ -622,24 +1016,31 @@ orca_status orca_debug_work(orca_ctx* c, int64_t out[5]) {
 orca_status orca_get_stats(orca_ctx* c, orca_stats* out) {
     if (!c || !out) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
     CK(cudaSetDevice(c->device));
-    unsigned long long h[ST_COUNT];
-    CK(cudaMemcpyAsync(h, c->stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    unsigned long long t[ST_COUNT] = {};
+    for (Domain& d : c->doms) {
+        if (!d.stats) continue;
+        unsigned long long h[ST_COUNT];
+        CK(cudaMemcpyAsync(h, d.stats, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int q = 0; q < ST_COUNT; ++q) t[q] += h[q];
+    }
     out->steps = c->host_steps;
     out->agent_updates = c->host_updates;
-    out->infeasible = (int64_t)h[ST_INFEASIBLE];
-    out->degenerate = (int64_t)h[ST_DEGENERATE];
-    out->coincident = (int64_t)h[ST_G1];
-    out->eps_parallel = (int64_t)h[ST_G2];
-    out->marginal = (int64_t)h[ST_G3];
-    out->collision_pairs = (int64_t)h[ST_COLLISION];
+    out->infeasible = (int64_t)t[ST_INFEASIBLE];
+    out->degenerate = (int64_t)t[ST_DEGENERATE];
+    out->coincident = (int64_t)t[ST_G1];
+    out->eps_parallel = (int64_t)t[ST_G2];
+    out->marginal = (int64_t)t[ST_G3];
+    out->collision_pairs = (int64_t)t[ST_COLLISION];
+    if (c->ready) CKS(check_overflow(c));
     return ORCA_OK;
 }
 
 orca_status orca_reset_stats(orca_ctx* c) {
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
     CK(cudaSetDevice(c->device));
-    CK(cudaMemsetAsync(c->stats, 0, ST_COUNT * sizeof(unsigned long long), c->stream));
+    for (Domain& d : c->doms)
+        if (d.stats) CK(cudaMemsetAsync(d.stats, 0, ST_COUNT * sizeof(unsigned long long), c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->host_steps = 0;
     c->host_updates = 0;
@@ -652,16 +1053,4 @@ orca_status orca_get_stream(orca_ctx* c, void** stream) {
     return ORCA_OK;
 }
 
-// ---- multi-GPU --------------------------------------------------------
-orca_status orca_nccl_unique_id(void* id128) {
-    if (!id128) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
-    return fail(ORCA_ERR_NCCL, "multi-GPU strips not built yet");
-}
-
-orca_status orca_create_dist(const orca_params* params, int32_t device, int32_t rank, int32_t world,
-                             const void* nccl_id128, orca_ctx** out) {
-    if (world == 1 && rank == 0) return orca_create(params, device, out);
-    (void)nccl_id128;
-    return fail(ORCA_ERR_NCCL, "multi-GPU strips not built yet");
-}
 }  // extern "C"

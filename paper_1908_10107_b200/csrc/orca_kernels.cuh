@@ -1,7 +1,7 @@
 // orca_kernels.cuh -- sm_100a device code of the ORCA step (arXiv 1908.10107).
 //
 // Product path.  Shares no code with oracle/.  Every stage of the step runs here:
-//   k_hash      cell hash + histogram (atomic rank = in-cell slot)     FLAME bins
+//   k_select    pick a strip's agents (owned + ghost columns), hash + histogram
 //   k_scan      exclusive scan (decoupled look-back) of the per-bin counts -> binStart
 //   k_scatter   counting-sort permutation into cell-sorted SoA
 //   k_step      3x3 k-nearest query -> ORCA half-planes -> LP2/LP3 -> integrate -> next hash
@@ -52,6 +52,10 @@ struct Grid {
     int lgS;           // each cell is split into 2^lgS sub-rows for the sort order
     double csD, invCs;        // fl64(cs), fl64(1/cs)
     double csSub, invCsSub;   // cs / 2^lgS (exact), 2^lgS / cs
+    // strip of this domain: owned columns [c0, c1); the local bins cover
+    // columns [e0, e1) = owned plus one ghost column on each side that exists
+    int c0, c1, e0, e1;
+    int hasL, hasR;           // a neighbour strip exists on that side
 };
 
 struct Model {
@@ -96,23 +100,57 @@ __device__ __forceinline__ int subrow_coord(float y, const Grid& g) {
     return floor_div_clamped(__dsub_rn((double)y, (double)g.oy), g.csSub, g.invCsSub, g.ny << g.lgS);
 }
 
-// Bin id of the sort order: column-major over (cx, sub-row), so a strip of columns is
-// one contiguous id range, a coarse cell is 2^lgS consecutive bins, and each column run
-// of the 3x3 stencil is ordered by y at sub-row granularity.
-__device__ __forceinline__ uint32_t bin_id(float x, float y, const Grid& g) {
-    const int cx = cell_coord(x, g.ox, g.csD, g.invCs, g.nx);
-    const int sy = subrow_coord(y, g);
-    return (uint32_t)cx * (uint32_t)(g.ny << g.lgS) + (uint32_t)sy;
+// Local bin id of the sort order: column-major over (cx - e0, sub-row), so the owned
+// strip is one contiguous id range, a coarse cell is 2^lgS consecutive bins, and each
+// column run of the 3x3 stencil is ordered by y at sub-row granularity.
+__device__ __forceinline__ uint32_t bin_of(int cx, int sy, const Grid& g) {
+    return (uint32_t)(cx - g.e0) * (uint32_t)(g.ny << g.lgS) + (uint32_t)sy;
 }
 
+constexpr uint32_t kInvalid = 0xffffffffu;  // work entry that left the strip
+
+// per-domain device counters
+enum { CT_NOWN = 0, CT_EXTRA, CT_OVF, CT_COUNT };
+constexpr int OVF_WORK = 1, OVF_MIG = 2, OVF_HALO = 4;
+
+// One direction of the neighbour exchange (fixed capacity; one NCCL send per step):
+// hdr = {emigrants, halo agents}; emigrants carry the full state, halo agents only what a
+// ghost needs (position, velocity, id).
+struct ExBuf {
+    int* hdr;
+    float2 *mpos, *mvel, *maux;
+    uint32_t* mid;
+    float* mrk2;
+    float2 *hpos, *hvel;
+    uint32_t* hid;
+    int capM, capH;
+};
+
 // ------------------------------------------------------------------------- binning
-__global__ void k_hash(int n, const float2* __restrict__ pos, Grid g, uint32_t* __restrict__ cell,
-                       uint32_t* __restrict__ rank, uint32_t* __restrict__ count) {
+// Select the agents of a strip (columns [e0, e1)) from the global input arrays into the
+// work buffers: ids = input index, no search-bound history; bin + atomic rank.
+__global__ void k_select(int n, const float2* __restrict__ pos, const float2* __restrict__ vel,
+                         const float2* __restrict__ aux, Grid g, float2* __restrict__ posW, float2* __restrict__ velW,
+                         float2* __restrict__ auxW, uint32_t* __restrict__ idW, float* __restrict__ rk2W,
+                         uint32_t* __restrict__ cellW, uint32_t* __restrict__ rankW, uint32_t* __restrict__ count,
+                         int* __restrict__ ctr, int capW) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        float2 p = pos[i];
-        uint32_t c = bin_id(p.x, p.y, g);
-        cell[i] = c;
-        rank[i] = atomicAdd(&count[c], 1u);
+        const float2 p = pos[i];
+        const int cx = cell_coord(p.x, g.ox, g.csD, g.invCs, g.nx);
+        if (cx < g.e0 || cx >= g.e1) continue;
+        const int w = atomicAdd(&ctr[CT_EXTRA], 1);
+        if (w >= capW) {
+            atomicOr(&ctr[CT_OVF], OVF_WORK);
+            continue;
+        }
+        const uint32_t c = bin_of(cx, subrow_coord(p.y, g), g);
+        posW[w] = p;
+        velW[w] = vel[i];
+        auxW[w] = aux[i];
+        idW[w] = (uint32_t)i;
+        rk2W[w] = INFINITY;
+        cellW[w] = c;
+        rankW[w] = atomicAdd(&count[c], 1u);
     }
 }
 
@@ -198,19 +236,24 @@ __global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uin
     if ((C - 1) / 4 == tile * 1024 + tid) binStart[C] = run;  // owner of element C-1
 }
 
-__global__ void k_scatter(int n, const uint32_t* __restrict__ cell, const uint32_t* __restrict__ rank,
-                          const uint32_t* __restrict__ binStart, const float2* __restrict__ posW,
-                          const float2* __restrict__ velW, const float2* __restrict__ auxW,
-                          const uint32_t* __restrict__ idW, float2* __restrict__ posS, float2* __restrict__ velS,
-                          float2* __restrict__ auxS, uint32_t* __restrict__ idS, const float* __restrict__ rk2W,
-                          float* __restrict__ rk2S) {
+// Counting-sort scatter of the nOwn + extra work entries (invalid = emigrated) into the
+// sorted arrays (grid-stride over the device-side count).
+__global__ void k_scatter(const int* __restrict__ ctr, const uint32_t* __restrict__ cell,
+                          const uint32_t* __restrict__ rank, const uint32_t* __restrict__ binStart,
+                          const float2* __restrict__ posW, const float2* __restrict__ velW,
+                          const float2* __restrict__ auxW, const uint32_t* __restrict__ idW,
+                          const float* __restrict__ rk2W, float2* __restrict__ posS, float2* __restrict__ velS,
+                          float2* __restrict__ auxS, uint32_t* __restrict__ idS, float* __restrict__ rk2S, int capW) {
+    const int n = min(ctr[CT_NOWN] + ctr[CT_EXTRA], capW);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t dst = binStart[cell[i]] + rank[i];
+        const uint32_t c = cell[i];
+        if (c == kInvalid) continue;
+        const uint32_t dst = binStart[c] + rank[i];
         posS[dst] = posW[i];
         velS[dst] = velW[i];
         auxS[dst] = auxW[i];
-        rk2S[dst] = rk2W[i];
         idS[dst] = idW[i];
+        rk2S[dst] = rk2W[i];
     }
 }
 
@@ -397,7 +440,6 @@ __device__ __forceinline__ void lp3(const Lines& L, const Lines& P, int T, int n
 
 // --------------------------------------------------------------------- fused step
 struct StepArgs {
-    int n;
     Grid g;
     Model m;
     // cell-sorted (rest) state
@@ -417,6 +459,9 @@ struct StepArgs {
     uint32_t* rankW;
     uint32_t* count;
     unsigned long long* stats;
+    int* ctr;   // per-domain counters (CT_*)
+    int capW;   // work / sorted array capacity
+    ExBuf sendL, sendR;
     // outputs of a dry (debug) step, indexed by global id
     float2* dbgV;
     uint8_t* dbgFlags;
@@ -495,6 +540,74 @@ __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int 
     return cnt;
 }
 
+// ---------------------------------------------------------- integrate + route
+__device__ __forceinline__ void push_halo(const ExBuf& x, int* ctr, float2 p, float2 v, uint32_t id) {
+    const int s = atomicAdd(&x.hdr[1], 1);
+    if (s >= x.capH) {
+        atomicOr(&ctr[CT_OVF], OVF_HALO);
+        return;
+    }
+    x.hpos[s] = p;
+    x.hvel[s] = v;
+    x.hid[s] = id;
+}
+
+// Append one entry to the work buffers at nOwn + extra (ghosts, immigrants).
+__device__ __forceinline__ void append_work(const StepArgs& a, int nOwn, int cx, int sy, float2 p, float2 v, float2 aux,
+                                            uint32_t id, float rk2) {
+    const int e = nOwn + atomicAdd(&a.ctr[CT_EXTRA], 1);
+    if (e >= a.capW) {
+        atomicOr(&a.ctr[CT_OVF], OVF_WORK);
+        return;
+    }
+    const uint32_t c = bin_of(cx, sy, a.g);
+    a.posW[e] = p;
+    a.velW[e] = v;
+    a.auxW[e] = aux;
+    a.idW[e] = id;
+    a.rk2W[e] = rk2;
+    a.cellW[e] = c;
+    a.rankW[e] = atomicAdd(&a.count[c], 1u);
+}
+
+// Explicit Euler p' = p + dt v' and routing for the next step: the agent
+// stays in this strip (bin + rank at its work slot w; a halo copy to the neighbour if it
+// sits in an edge column), or emigrates (exchange buffer, plus a local ghost entry since
+// it now sits in this strip's ghost column).  Single-GPU: always stays.
+__device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn, float2 pi, float vx, float vy,
+                                             float2 aux, uint32_t id, float rk2) {
+    const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
+    const float2 vn = make_float2(vx, vy);
+    const int cx = cell_coord(pn.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
+    const int sy = subrow_coord(pn.y, a.g);
+    if (cx >= a.g.c0 && cx < a.g.c1) {
+        const uint32_t c = bin_of(cx, sy, a.g);
+        a.posW[w] = pn;
+        a.velW[w] = vn;
+        a.auxW[w] = aux;
+        a.idW[w] = id;
+        a.rk2W[w] = rk2;
+        a.cellW[w] = c;
+        a.rankW[w] = atomicAdd(&a.count[c], 1u);
+        if (cx == a.g.c0 && a.g.hasL) push_halo(a.sendL, a.ctr, pn, vn, id);
+        if (cx == a.g.c1 - 1 && a.g.hasR) push_halo(a.sendR, a.ctr, pn, vn, id);
+    } else {
+        a.cellW[w] = kInvalid;
+        const ExBuf& x = (cx < a.g.c0) ? a.sendL : a.sendR;
+        const int s = atomicAdd(&x.hdr[0], 1);
+        if (s >= x.capM) {
+            atomicOr(&a.ctr[CT_OVF], OVF_MIG);
+        } else {
+            x.mpos[s] = pn;
+            x.mvel[s] = vn;
+            x.maux[s] = aux;
+            x.mid[s] = id;
+            x.mrk2[s] = rk2;
+        }
+        append_work(a, nOwn, cx, sy, pn, vn, aux, id, INFINITY);
+    }
+}
+
 template <bool DRY>
 __global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
     constexpr bool CNT = DRY;  // only the debug variant counts work
@@ -510,8 +623,14 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
     uint32_t* Bf = L2 + k * T;
     const Lines L{reinterpret_cast<float*>(L0), reinterpret_cast<float*>(L1), reinterpret_cast<float*>(L2)};
 
-    const int i = blockIdx.x * T + tid;
-    const bool active = i < a.n;
+    // owned agents are the contiguous sorted range of columns [c0, c1)
+    const int nyS0 = a.g.ny << a.g.lgS;
+    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * nyS0];
+    const int o1 = (int)a.binStart[(a.g.c1 - a.g.e0) * nyS0];
+    const int ws = blockIdx.x * T + tid;  // work slot
+    const int i = o0 + ws;                // sorted index
+    const bool active = i < o1;
+    if (!DRY && blockIdx.x == 0 && tid == 0) a.ctr[CT_NOWN] = o1 - o0;
     uint32_t fl = 0;
     int nColl = 0;
     bool deferred = false;
@@ -540,7 +659,7 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
             const int c0 = max(cx - 1, 0), c1 = min(cx + 1, a.g.nx - 1);
             int ncand = 0;
             for (int col = c0; col <= c1; ++col)
-                ncand += (int)a.binStart[col * nyS + rhi] - (int)a.binStart[col * nyS + rlo];
+                ncand += (int)a.binStart[(col - a.g.e0) * nyS + rhi] - (int)a.binStart[(col - a.g.e0) * nyS + rlo];
             float thr = a.m.nd2Fup;
             bool guessed = false;
             const float rk2p = a.rk2S[i];
@@ -580,8 +699,8 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
                 for (int q = 0; q < 3; ++q) {
                     const int col = (q == 0) ? cx : (q == 1 ? cx - 1 : cx + 1);  // own column first
                     if (col < cl || col > cr) continue;
-                    const int b = (int)a.binStart[col * nyS + lo];
-                    const int e = (int)a.binStart[col * nyS + hi + 1];
+                    const int b = (int)a.binStart[(col - a.g.e0) * nyS + lo];
+                    const int e = (int)a.binStart[(col - a.g.e0) * nyS + hi + 1];
                     if (CNT) w.cand += (uint32_t)(e - b);
                     int j = b;
                     for (; j + 1 < e; j += 2) {  // 2-way unrolled: two loads in flight
@@ -628,7 +747,7 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
             }
             if (cnt == k) fk = __uint_as_float(L0[(k - 1) * T]);
         }
-        if (!DRY) a.rk2W[i] = fk;  // next step's search bound
+        if (!DRY) a.rk2W[ws] = fk;  // next step's search bound (read back by k_lp3 for queued agents)
 
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
         // (half-plane q overwrites list slot q in place: j is read before the write)
@@ -692,14 +811,7 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
             if (a.dbgNbr)
                 for (int q = cnt; q < k; ++q) a.dbgNbr[(size_t)idi * k + q] = -1;
         } else {
-            const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
-            const uint32_t c = bin_id(pn.x, pn.y, a.g);
-            a.posW[i] = pn;
-            a.velW[i] = make_float2(vx, vy);
-            a.auxW[i] = aux;
-            a.idW[i] = idi;
-            a.cellW[i] = c;
-            a.rankW[i] = atomicAdd(&a.count[c], 1u);
+            finish_agent(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk);
         }
     }
     if (DRY && a.work) {
@@ -754,6 +866,8 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
     const Lines L{base, base + k * T, base + 2 * k * T};
     const Lines P{base + 3 * k * T, base + 4 * k * T, base + 5 * k * T};
     const int nq = (int)*a.qCount;
+    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * (a.g.ny << a.g.lgS)];
+    const int nOwn = (int)a.binStart[(a.g.c1 - a.g.e0) * (a.g.ny << a.g.lgS)] - o0;
     int cInf = 0, cDeg = 0, cG1 = 0, cG2 = 0, cG3 = 0;
     for (int q = blockIdx.x * T + tid; q < nq; q += gridDim.x * T) {
         const int4 e = a.qEntry[q];
@@ -777,14 +891,7 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
             if (a.dbgV) a.dbgV[idi] = make_float2(vx, vy);
             if (a.dbgFlags) a.dbgFlags[idi] = (uint8_t)fl;
         } else {
-            const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
-            const uint32_t c = bin_id(pn.x, pn.y, a.g);
-            a.posW[i] = pn;
-            a.velW[i] = make_float2(vx, vy);
-            a.auxW[i] = a.auxS[i];
-            a.idW[i] = idi;
-            a.cellW[i] = c;
-            a.rankW[i] = atomicAdd(&a.count[c], 1u);
+            finish_agent(a, i - o0, nOwn, pi, vx, vy, a.auxS[i], idi, a.rk2W[i - o0]);
         }
         cInf += 1;
         cDeg += (fl & (FL_G1 | FL_G2)) != 0;
@@ -824,19 +931,29 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
 }
 
 // ------------------------------------------------------------------ state utilities
-__global__ void k_unpermute(int n, const uint32_t* __restrict__ idS, const float2* __restrict__ posS,
-                            const float2* __restrict__ velS, float2* __restrict__ posOut,
-                            float2* __restrict__ velOut) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+// owned sorted range [o0, o1) of a domain
+__device__ __forceinline__ int2 owned_range(const uint32_t* __restrict__ binStart, const Grid& g) {
+    const int nyS = g.ny << g.lgS;
+    return make_int2((int)binStart[(g.c0 - g.e0) * nyS], (int)binStart[(g.c1 - g.e0) * nyS]);
+}
+
+// owned agents -> id-ordered outputs (pos, vel; either nullable); optional local export
+// (ids / pos / vel in sorted order starting at 0)
+__global__ void k_unpermute(const uint32_t* __restrict__ binStart, Grid g, const uint32_t* __restrict__ idS,
+                            const float2* __restrict__ posS, const float2* __restrict__ velS,
+                            float2* __restrict__ posOut, float2* __restrict__ velOut) {
+    const int2 r = owned_range(binStart, g);
+    for (int i = r.x + blockIdx.x * blockDim.x + threadIdx.x; i < r.y; i += gridDim.x * blockDim.x) {
         const uint32_t id = idS[i];
         if (posOut) posOut[id] = posS[i];
         if (velOut) velOut[id] = velS[i];
     }
 }
 
-__global__ void k_cells(int n, const uint32_t* __restrict__ idS, const float2* __restrict__ posS, Grid g,
-                        int32_t* __restrict__ cxOut, int32_t* __restrict__ cyOut) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+__global__ void k_cells(const uint32_t* __restrict__ binStart, Grid g, const uint32_t* __restrict__ idS,
+                        const float2* __restrict__ posS, int32_t* __restrict__ cxOut, int32_t* __restrict__ cyOut) {
+    const int2 r = owned_range(binStart, g);
+    for (int i = r.x + blockIdx.x * blockDim.x + threadIdx.x; i < r.y; i += gridDim.x * blockDim.x) {
         const float2 p = posS[i];
         const uint32_t id = idS[i];
         cxOut[id] = cell_coord(p.x, g.ox, g.csD, g.invCs, g.nx);
@@ -844,18 +961,48 @@ __global__ void k_cells(int n, const uint32_t* __restrict__ idS, const float2* _
     }
 }
 
-// out[i] = in[idS[i]]: id-ordered array -> sorted order
-__global__ void k_gather_by_id(int n, const uint32_t* __restrict__ idS, const float2* __restrict__ in,
-                               float2* __restrict__ out) {
+// out[i] = in[idS[i]] over all sorted entries (owned + ghosts): id-ordered -> sorted
+__global__ void k_gather_by_id(const uint32_t* __restrict__ binStart, int nbins, const uint32_t* __restrict__ idS,
+                               const float2* __restrict__ in, float2* __restrict__ out) {
+    const int n = (int)binStart[nbins];
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[idS[i]];
 }
 
-// ids = array index; no search-bound history yet
-__global__ void k_iota(int n, uint32_t* __restrict__ id, float* __restrict__ rk2) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        id[i] = (uint32_t)i;
-        rk2[i] = INFINITY;
+// Received neighbour data -> work buffers: emigrants of the neighbour become owned agents,
+// halo agents become ghosts (their columns decide which; both are just appended).
+__global__ void k_receive(StepArgs a, ExBuf rL, ExBuf rR) {
+    const int nOwn = a.ctr[CT_NOWN];
+    const int mL = a.g.hasL ? min(rL.hdr[0], rL.capM) : 0, hL = a.g.hasL ? min(rL.hdr[1], rL.capH) : 0;
+    const int mR = a.g.hasR ? min(rR.hdr[0], rR.capM) : 0, hR = a.g.hasR ? min(rR.hdr[1], rR.capH) : 0;
+    const int tot = mL + hL + mR + hR;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+        int q = t;
+        const ExBuf* x = &rL;
+        bool mig = true;
+        if (q < mL) {
+        } else if ((q -= mL) < hL) {
+            mig = false;
+        } else if ((q -= hL) < mR) {
+            x = &rR;
+        } else {
+            q -= mR;
+            x = &rR;
+            mig = false;
+        }
+        const float2 p = mig ? x->mpos[q] : x->hpos[q];
+        const int cx = cell_coord(p.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
+        const int sy = subrow_coord(p.y, a.g);
+        if (mig)
+            append_work(a, nOwn, cx, sy, p, x->mvel[q], x->maux[q], x->mid[q], x->mrk2[q]);
+        else
+            append_work(a, nOwn, cx, sy, p, x->hvel[q], make_float2(0.0f, 0.0f), x->hid[q], INFINITY);
     }
+}
+
+// agents per grid column (strip partition at set_agents)
+__global__ void k_colhist(int n, const float2* __restrict__ pos, Grid g, int32_t* __restrict__ hist) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        atomicAdd(&hist[cell_coord(pos[i].x, g.ox, g.csD, g.invCs, g.nx)], 1);
 }
 
 // Block-partial min/max of the positions and a non-finite count over all input arrays.

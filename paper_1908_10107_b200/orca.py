@@ -25,6 +25,7 @@ EXPORTS = [
     "orca_get_count", "orca_get_grid", "orca_debug_cells", "orca_debug_step", "orca_get_stats",
     "orca_reset_stats", "orca_get_stream", "orca_step_timed", "orca_status_string", "orca_last_error",
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
+    "orca_create_strips", "orca_partition_columns", "orca_get_strips",
 ]
 
 
@@ -76,6 +77,9 @@ def _load():
         "orca_create_dist": [P(Params), i32, i32, i32, vp, P(vp)],
         "orca_get_local_state": [vp, vp, vp, vp],
         "orca_debug_work": [vp, P(i64)],
+        "orca_create_strips": [P(Params), i32, i32, P(vp)],
+        "orca_partition_columns": [P(i64), i32, i32, P(i32)],
+        "orca_get_strips": [vp, P(i32)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -127,6 +131,15 @@ def make_params(timeStep=0.25, neighborDist=15.0, maxNeighbors=10, timeHorizon=5
     return Params(timeStep, neighborDist, maxNeighbors, timeHorizon, radius, maxSpeed)
 
 
+def partition_columns(col_count, world: int):
+    """Strip bounds (int32[world+1]) for per-column agent counts (host only)."""
+    cc = np.ascontiguousarray(col_count, np.int64)
+    b = np.zeros(world + 1, np.int32)
+    _check(_lib.orca_partition_columns(cc.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(cc), world,
+                                       b.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+    return b
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(_lib.orca_nccl_unique_id(buf))
@@ -137,14 +150,17 @@ class Orca:
     """One liborca context (orca_create / orca_create_dist ... orca_destroy)."""
 
     def __init__(self, params: Params | dict | None = None, device: int = 0, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, strips: int = 0):
         if params is None:
             params = make_params()
         elif isinstance(params, dict):
             params = make_params(**params)
         self.params = params
         self._ctx = ctypes.c_void_p()
-        if world == 1:
+        self.strips = max(1, strips)
+        if strips:
+            _check(_lib.orca_create_strips(ctypes.byref(params), device, strips, ctypes.byref(self._ctx)))
+        elif world == 1:
             _check(_lib.orca_create(ctypes.byref(params), device, ctypes.byref(self._ctx)))
         else:
             idb = ctypes.create_string_buffer(nccl_id, 128)
@@ -200,6 +216,11 @@ class Orca:
         vel = np.empty((n, 2), np.float32)
         _check(_lib.orca_get_local_state(self._ctx, _ptr(ids), _ptr(pos), _ptr(vel)))
         return ids, pos, vel
+
+    def strip_bounds(self):
+        b = np.zeros(2 * self.strips, np.int32)
+        _check(_lib.orca_get_strips(self._ctx, b.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+        return b.reshape(-1, 2)
 
     def grid(self):
         o = (ctypes.c_double * 2)()
