@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--variant", type=int, default=1, help="0: thread per agent, 1: 8-lane group per agent")
     return ap.parse_args()
 
 
@@ -203,6 +204,7 @@ def run_ours(args):
     ctx.set_agents(w["pos"], w["vel"], w["pref"])
     if w.get("goals") is not None:
         ctx.set_goals(w["goals"], w["pref_speed"])
+    ctx.set_variant(args.variant)
     stream = torch.cuda.ExternalStream(ctx.stream())
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -258,6 +260,18 @@ def run_ours(args):
     stage /= args.steps
     work1 = ctx.work()
     work = {k: 0.5 * (work0[k] + work1[k]) for k in work0}
+    # kernel variant A/B (same results bit for bit): fused-step ms per step
+    variant_ms = {}
+    for v in (0, 1):
+        ctx.set_variant(v)
+        ctx.step(2)
+        acc = 0.0
+        for s in range(max(3, args.steps // 4)):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            acc += ctx.step_timed(1)[0]
+        variant_ms[str(v)] = acc / max(3, args.steps // 4)
+    ctx.set_variant(args.variant)
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -295,11 +309,12 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get(args.config, {}).get("k_step_dram_bytes")
         except Exception:
             traffic = None
-    roofline = {"bound": "alu", "kernel": "k_step", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
+    roofline = {"bound": "alu", "kernel": "k_step(+k_lp3)", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "peak_source": f"148 SMs x 128 FP32 lanes x sm_max_mhz ({pk_kind} MEASURED_PEAKS.json)",
                 "ops_per_launch": ops, "work_per_launch": work,
-                "stage_ms": {"k_step": stage[0], "k_scan": stage[1], "k_scatter": stage[2]}}
+                "stage_ms": {"k_step+k_lp3": stage[0], "k_scan": stage[1], "k_scatter": stage[2],
+                             "exchange": stage[3]}}
     # HBM view of the binning kernels (context)
     hbm_bytes_scatter = n_total / world * (4 + 4 + 4 + 3 * 8 + 4 + 3 * 8 + 4)
     hbm = {"kernel": "k_scatter", "achieved_gbs": hbm_bytes_scatter / (stage[2] / 1000.0) / 1e9 if stage[2] > 0 else None,
@@ -313,7 +328,8 @@ def run_ours(args):
                    "l2": "flushed between timed steps (512 MiB write); per-step CUDA events on the library stream",
                    "parallelism": f"strips{world}" if world > 1 else "single"},
         "ms_per_step_l2_resident": ms_res,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": (4 if world == 1 else 5) * args.steps,
+        "kernel_variant": args.variant, "k_step_ms_by_variant": variant_ms,
         "roofline": roofline, "hbm_context": hbm,
         "stats": st,
     }

@@ -20,6 +20,7 @@
 
 #include "../../include/orca.h"
 #include "orca_kernels.cuh"
+#include "orca_step_group.cuh"
 
 using namespace orca;
 
@@ -134,7 +135,7 @@ struct ExAlloc {
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 orca_status ex_alloc(ExAlloc& x, int capM, int capH) {
-    if (x.base && x.b.capM >= capM && x.b.capH >= capH) return ORCA_OK;
+    if (x.base && x.b.capM == capM && x.b.capH == capH) return ORCA_OK;  // layouts must match exactly
     dfree(x.base);
     size_t sz[9] = {16, (size_t)capM * 8, (size_t)capM * 8, (size_t)capM * 8, (size_t)capM * 4,
                     (size_t)capM * 4, (size_t)capH * 8, (size_t)capH * 8, (size_t)capH * 4};
@@ -218,7 +219,8 @@ struct orca_ctx {
     int64_t host_steps = 0, host_updates = 0;
     std::vector<std::pair<int, cudaGraphExec_t>> graphs;
     cudaEvent_t ev[8] = {};
-    int smemBytes = 0, lp3Smem = 0;
+    int smemBytes = 0, lp3Smem = 0, groupSmem = 0;
+    int variant = 1;  // 0: thread per agent (k_step), 1: 8-lane group per agent (k_step_group)
 };
 
 namespace {
@@ -333,6 +335,15 @@ void drop_graph(orca_ctx* c) {
     c->graphs.clear();
 }
 
+// fused step kernel of the selected variant (same results bit for bit)
+template <bool DRY>
+void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
+    if (c->variant == 1)
+        k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
+    else
+        k_step<DRY><<<(d.capW + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
+}
+
 cudaError_t enqueue_scan(orca_ctx* c, Domain& d) {
     const int tiles = scan_tiles(d.nbins);
     // status words, tile ticket and the LP3 queue count (consumed by k_lp3 before this point)
@@ -396,7 +407,7 @@ orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
         if (d.g.hasL) CK(cudaMemsetAsync(d.sendL.b.hdr, 0, 16, c->stream));
         if (d.g.hasR) CK(cudaMemsetAsync(d.sendR.b.hdr, 0, 16, c->stream));
         StepArgs a = make_args(c, d);
-        k_step<false><<<(d.capW + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
+        launch_step<false>(c, d, a);
         k_lp3<false><<<lp3_blocks(d.capW), kStepThreads, c->lp3Smem, c->stream>>>(a);
     }
     CK(cudaGetLastError());
@@ -424,7 +435,7 @@ orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
 cudaError_t dry_step(orca_ctx* c, Domain& d, StepArgs& a) {
     cudaError_t e = cudaMemsetAsync(a.qCount, 0, sizeof(unsigned int), c->stream);
     if (e != cudaSuccess) return e;
-    k_step<true><<<(d.capW + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
+    launch_step<true>(c, d, a);
     k_lp3<true><<<lp3_blocks(d.capW), kStepThreads, c->lp3Smem, c->stream>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -485,6 +496,11 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
         e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_lp3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
+    c->groupSmem = group_words(params->maxNeighbors) * 4 * kGroupAgents;
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_step_group<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->groupSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_step_group<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->groupSmem);
     if (e != cudaSuccess) return cuda_fail(e, "orca_create");
     return ORCA_OK;
 }
@@ -721,6 +737,13 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     }
     std::vector<int32_t> bounds(c->world + 1);
     CKS(orca_partition_columns(colCount.data(), g.nx, c->world, bounds.data()));
+    // exchange capacities are global (sender and receiver must agree on the layout):
+    // 1.5x the largest strip-edge column of the whole partition
+    int64_t edgeMax = 0;
+    for (int s = 0; s < c->world; ++s)
+        edgeMax = std::max(edgeMax, std::max(colCount[bounds[s]], colCount[bounds[s + 1] - 1]));
+    const int capH = (int)std::min<int64_t>(edgeMax + edgeMax / 2 + 1024, (int64_t)1 << 28);
+    const int capM = std::max(1024, capH / 4);
     const int first = c->loopback ? 0 : c->rank;
     for (size_t q = 0; q < c->doms.size(); ++q) {
         Domain& d = c->doms[q];
@@ -736,12 +759,9 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
         d.nbins = ((int64_t)(d.g.e1 - d.g.e0) * g.ny) << g.lgS;
         int64_t sel = 0;
         for (int x = d.g.e0; x < d.g.e1; ++x) sel += colCount[x];
-        const int64_t edge = std::max(colCount[d.g.c0], colCount[d.g.c1 - 1]);
         // single strip: exact; strips: headroom for density drift between re-partitions
         const int64_t capW = (c->world == 1) ? std::max<int64_t>(n, 1) : sel + sel / 2 + 4096;
         if (capW > ((int64_t)1 << 30)) return fail(ORCA_ERR_CAPACITY, "strip too large");
-        const int capH = (int)std::min<int64_t>(edge + edge / 2 + 1024, (int64_t)1 << 28);
-        const int capM = std::max(1024, capH / 4);
         CKS(dom_alloc(c, d, (int)capW, d.nbins, capM, capH));
         CK(cudaMemsetAsync(d.ctr, 0, CT_COUNT * sizeof(int), c->stream));
         CK(cudaMemsetAsync(d.count, 0, d.nbins * sizeof(uint32_t), c->stream));
@@ -1044,6 +1064,14 @@ orca_status orca_reset_stats(orca_ctx* c) {
     CK(cudaStreamSynchronize(c->stream));
     c->host_steps = 0;
     c->host_updates = 0;
+    return ORCA_OK;
+}
+
+orca_status orca_set_variant(orca_ctx* c, int32_t variant) {
+    if (!c || variant < 0 || variant > 1) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be 0 or 1");
+    CK(cudaStreamSynchronize(c->stream));
+    drop_graph(c);
+    c->variant = variant;
     return ORCA_OK;
 }
 

@@ -25,7 +25,7 @@ EXPORTS = [
     "orca_get_count", "orca_get_grid", "orca_debug_cells", "orca_debug_step", "orca_get_stats",
     "orca_reset_stats", "orca_get_stream", "orca_step_timed", "orca_status_string", "orca_last_error",
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
-    "orca_create_strips", "orca_partition_columns", "orca_get_strips",
+    "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
 ]
 
 
@@ -80,6 +80,7 @@ def _load():
         "orca_create_strips": [P(Params), i32, i32, P(vp)],
         "orca_partition_columns": [P(i64), i32, i32, P(i32)],
         "orca_get_strips": [vp, P(i32)],
+        "orca_set_variant": [vp, i32],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -259,6 +260,10 @@ class Orca:
 
     def reset_stats(self):
         _check(_lib.orca_reset_stats(self._ctx))
+
+    def set_variant(self, variant: int):
+        """0 = thread per agent, 1 = 8-lane group per agent (same results)."""
+        _check(_lib.orca_set_variant(self._ctx, variant))
 
     def stream(self) -> int:
         s = ctypes.c_void_p()
