@@ -220,7 +220,7 @@ struct orca_ctx {
     std::vector<std::pair<int, cudaGraphExec_t>> graphs;
     cudaEvent_t ev[8] = {};
     int smemBytes = 0, lp3Smem = 0, groupSmem = 0;
-    int variant = 1;  // 0: thread per agent (k_step), 1: 8-lane group per agent (k_step_group)
+    int variant = 0;  // 0: thread per agent (k_step), 1: 8-lane group per agent (k_step_group)
 };
 
 namespace {
@@ -335,13 +335,27 @@ void drop_graph(orca_ctx* c) {
     c->graphs.clear();
 }
 
+// thread-per-agent step: register top-k list of 10 or 16 slots when k fits, else the
+// shared-memory list (same results bit for bit)
+template <bool DRY>
+void launch_thread_step(orca_ctx* c, Domain& d, StepArgs& a) {
+    const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
+    const int k = c->p.maxNeighbors;
+    if (k >= 1 && k <= 10)
+        k_step<DRY, 10><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
+    else if (k >= 1 && k <= 16)
+        k_step<DRY, 16><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
+    else
+        k_step<DRY, 0><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
+}
+
 // fused step kernel of the selected variant (same results bit for bit)
 template <bool DRY>
 void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     if (c->variant == 1)
         k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
     else
-        k_step<DRY><<<(d.capW + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
+        launch_thread_step<DRY>(c, d, a);
 }
 
 cudaError_t enqueue_scan(orca_ctx* c, Domain& d) {
@@ -488,10 +502,11 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
     for (int q = 0; q < 8 && e == cudaSuccess; ++q) e = cudaEventCreate(&c->ev[q]);
     c->smemBytes = step_smem_per_thread(params->maxNeighbors) * kStepThreads;
     c->lp3Smem = std::max(1, 6 * params->maxNeighbors) * 4 * kStepThreads;
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
+    const void* steps[] = {(const void*)k_step<false, 10>, (const void*)k_step<true, 10>,
+                           (const void*)k_step<false, 16>, (const void*)k_step<true, 16>,
+                           (const void*)k_step<false, 0>, (const void*)k_step<true, 0>};
+    for (const void* f : steps)
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
     if (e == cudaSuccess)
