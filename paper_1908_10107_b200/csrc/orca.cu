@@ -335,27 +335,13 @@ void drop_graph(orca_ctx* c) {
     c->graphs.clear();
 }
 
-// thread-per-agent step: register top-k list of 10 or 16 slots when k fits, else the
-// shared-memory list (same results bit for bit)
-template <bool DRY>
-void launch_thread_step(orca_ctx* c, Domain& d, StepArgs& a) {
-    const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
-    const int k = c->p.maxNeighbors;
-    if (k >= 1 && k <= 10)
-        k_step<DRY, 10><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
-    else if (k >= 1 && k <= 16)
-        k_step<DRY, 16><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
-    else
-        k_step<DRY, 0><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
-}
-
 // fused step kernel of the selected variant (same results bit for bit)
 template <bool DRY>
 void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     if (c->variant == 1)
         k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
     else
-        launch_thread_step<DRY>(c, d, a);
+        k_step<DRY><<<(d.capW + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
 }
 
 cudaError_t enqueue_scan(orca_ctx* c, Domain& d) {
@@ -502,11 +488,10 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
     for (int q = 0; q < 8 && e == cudaSuccess; ++q) e = cudaEventCreate(&c->ev[q]);
     c->smemBytes = step_smem_per_thread(params->maxNeighbors) * kStepThreads;
     c->lp3Smem = std::max(1, 6 * params->maxNeighbors) * 4 * kStepThreads;
-    const void* steps[] = {(const void*)k_step<false, 10>, (const void*)k_step<true, 10>,
-                           (const void*)k_step<false, 16>, (const void*)k_step<true, 16>,
-                           (const void*)k_step<false, 0>, (const void*)k_step<true, 0>};
-    for (const void* f : steps)
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
     if (e == cudaSuccess)

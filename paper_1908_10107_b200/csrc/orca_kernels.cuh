@@ -478,11 +478,12 @@ struct StepArgs {
 constexpr int kStepThreads = 128;
 
 // Per-thread shared memory (32-bit words, one column per thread, stride kStepThreads):
-//   region L: 3k words -- the top-k list as (fp32 d2, -, j) during selection (generic
-//             path), then the half-planes (nx, ny, s) in the same slots;
-//   region B: 2 (k + 8) words -- candidate buffer (j, fp32 d2) during the scan.
+//   [0, k)            top-k list fp32 d2   -> half-plane nx
+//   [k, 2k)           top-k list j         -> half-plane ny (slot q read before written)
+//   [2k, 2k + B)      candidate buffer j   -> half-plane s in its first k words
+//   [2k + B, 2k + 2B) candidate buffer fp32 d2            (B = k + 8)
 __host__ __device__ constexpr int step_buf_words(int k) { return k + 8; }
-__host__ __device__ constexpr int step_smem_per_thread(int k) { return 4 * (3 * k + 2 * step_buf_words(k)); }
+__host__ __device__ constexpr int step_smem_per_thread(int k) { return 4 * (2 * k + 2 * step_buf_words(k)); }
 
 __device__ __forceinline__ double exact_key(float2 pj, float2 pi) {
     const double Dx = __dsub_rn((double)pj.x, (double)pi.x);
@@ -513,88 +514,15 @@ __device__ __forceinline__ bool in_radius(float f, uint32_t j, float2 pi, float 
     return exact_key(posS[j], pi) < nd2;
 }
 
-// Register-resident sorted list of the KR nearest candidates (padded with +inf).  Insertion
-// is a branch-free compare-and-shift over all KR slots, so a warp stays converged however
-// many candidates each thread merges; only an fp32 near-tie takes the exact branch.
-template <int KR>
-struct RegList {
-    float f[KR];
-    uint32_t j[KR];
-};
-
-template <int KR>
-__device__ __forceinline__ void reg_clear(RegList<KR>& L) {
-#pragma unroll
-    for (int p = 0; p < KR; ++p) {
-        L.f[p] = INFINITY;
-        L.j[p] = 0xffffffffu;
-    }
-}
-
-template <int KR>
-__device__ __forceinline__ void reg_insert(RegList<KR>& L, float f, uint32_t j, float2 pi,
-                                           const float2* __restrict__ posS, const uint32_t* __restrict__ idS) {
-    // before[p]: slot p stays in front of the candidate (a prefix, the list being sorted)
-    int pos = 0;
-#pragma unroll
-    for (int p = 0; p < KR; ++p) {
-        const float of = L.f[p];
-        bool before = (of < f * kSep) && f > 1e-30f;          // surely smaller
-        const bool after = (f < of * kSep) && of > 1e-30f;    // surely larger (also of = +inf)
-        if (!before && !after && of != INFINITY) before = cand_less(of, L.j[p], f, j, pi, posS, idS);
-        pos += before ? 1 : 0;
-    }
-#pragma unroll
-    for (int p = KR - 1; p >= 1; --p) {
-        if (p > pos) {
-            L.f[p] = L.f[p - 1];
-            L.j[p] = L.j[p - 1];
-        } else if (p == pos) {
-            L.f[p] = f;
-            L.j[p] = j;
-        }
-    }
-    if (pos == 0) {
-        L.f[0] = f;
-        L.j[0] = j;
-    }
-}
-
-// f of slot q (q < KR; dynamic index resolved by selects, no local memory)
-template <int KR>
-__device__ __forceinline__ float reg_f(const RegList<KR>& L, int q) {
-    float r = INFINITY;
-#pragma unroll
-    for (int p = 0; p < KR; ++p) r = (p == q) ? L.f[p] : r;
-    return r;
-}
-
-// Merge buffered (j, f) candidates into the register list (inside r_obs only).
-template <int KR>
-__device__ __forceinline__ void reg_merge(RegList<KR>& L, int& cnt, const uint32_t* Bj, const float* Bff, int nb,
-                                          float2 pi, const Model& m, const float2* __restrict__ posS,
-                                          const uint32_t* __restrict__ idS) {
-    constexpr int T = kStepThreads;
-    for (int b = 0; b < nb; ++b) {
-        const uint32_t j = Bj[b * T];
-        const float f = Bff[b * T];
-        if (!in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
-        reg_insert<KR>(L, f, j, pi, posS, idS);
-        cnt = min(cnt + 1, KR);
-    }
-}
-
-// Merge the nb buffered candidates (j; fp32 d2 recomputed) into the sorted top-k list
-// (Lf = fp32 d2 bits, Lj = j).  Returns the new list length.
+// Merge the nb buffered candidates (j, fp32 d2) into the sorted top-k list (Lf = fp32 d2
+// bits, Lj = j).  Returns the new list length.
 __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int cnt, int k, const uint32_t* Bf,
-                                                int nb, float2 pi, const Model& m, const float2* __restrict__ posS,
-                                                const uint32_t* __restrict__ idS) {
+                                                const float* Bff, int nb, float2 pi, const Model& m,
+                                                const float2* __restrict__ posS, const uint32_t* __restrict__ idS) {
     constexpr int T = kStepThreads;
     for (int b = 0; b < nb; ++b) {
         const uint32_t j = Bf[b * T];
-        const float2 pj = posS[j];
-        const float dx = pj.x - pi.x, dy = pj.y - pi.y;
-        const float f = fmaf(dx, dx, dy * dy);
+        const float f = Bff[b * T];
         if (!in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
         if (cnt == k && !cand_less(f, j, __uint_as_float(Lf[(k - 1) * T]), Lj[(k - 1) * T], pi, posS, idS))
             continue;
@@ -679,10 +607,8 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
     }
 }
 
-// KR > 0: the top-k list lives in registers (k <= KR, branch-free merges); KR = 0: the
-// generic shared-memory list (any k <= ORCA_MAX_K).
-template <bool DRY, int KR>
-__global__ void __launch_bounds__(kStepThreads, 6) k_step(StepArgs a) {
+template <bool DRY>
+__global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
     constexpr bool CNT = DRY;  // only the debug variant counts work
     WorkT w{0, 0, 0, 0, 0};
     extern __shared__ __align__(16) unsigned char smem[];
@@ -690,12 +616,11 @@ __global__ void __launch_bounds__(kStepThreads, 6) k_step(StepArgs a) {
     const int tid = threadIdx.x;
     const int k = a.m.k;
     const int capB = step_buf_words(k);
-    uint32_t* L0 = reinterpret_cast<uint32_t*>(smem) + tid;
-    uint32_t* L1 = L0 + k * T;
-    uint32_t* L2 = L1 + k * T;
-    uint32_t* Bf = L2 + k * T;
-    float* Bff = reinterpret_cast<float*>(Bf + capB * T);
-    const Lines L{reinterpret_cast<float*>(L0), reinterpret_cast<float*>(L1), reinterpret_cast<float*>(L2)};
+    uint32_t* L0 = reinterpret_cast<uint32_t*>(smem) + tid;  // list d2 / nx
+    uint32_t* L1 = L0 + k * T;                                  // list j  / ny
+    uint32_t* Bf = L1 + k * T;                                  // buffer j / s
+    float* Bff = reinterpret_cast<float*>(Bf + capB * T);       // buffer d2
+    const Lines L{reinterpret_cast<float*>(L0), reinterpret_cast<float*>(L1), reinterpret_cast<float*>(Bf)};
 
     // owned agents are the contiguous sorted range of columns [c0, c1)
     const int nyS0 = a.g.ny << a.g.lgS;
@@ -727,19 +652,6 @@ __global__ void __launch_bounds__(kStepThreads, 6) k_step(StepArgs a) {
         // apart), or, without history, from the local density.
         int cnt = 0;
         float fk = INFINITY;
-        RegList<(KR > 0 ? KR : 1)> R;
-        auto merge = [&](int nb) {
-            if constexpr (KR > 0)
-                reg_merge<KR>(R, cnt, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
-            else
-                cnt = merge_candidates(L0, L2, cnt, k, Bf, nb, pi, a.m, a.posS, a.idS);
-        };
-        auto kth = [&]() -> float {  // fp32 d2 of the current k-th (valid when cnt >= k)
-            if constexpr (KR > 0)
-                return reg_f<KR>(R, k - 1);
-            else
-                return __uint_as_float(L0[(k - 1) * T]);
-        };
         if (k > 0) {
             const int rlo = max(cy - 1, 0) << lgS;              // first sub-row of the 3 rows
             const int rhi = (min(cy + 1, a.g.ny - 1) + 1) << lgS; // one past the last
@@ -783,8 +695,6 @@ __global__ void __launch_bounds__(kStepThreads, 6) k_step(StepArgs a) {
                     if (xl + (double)a.g.cs - (double)pi.x > (double)rg) cr = cx;     // right column beyond rg
                 }
                 int nb = 0;
-                cnt = 0;
-                if constexpr (KR > 0) reg_clear<KR>(R);
                 for (int q = 0; q < 3; ++q) {
                     const int col = (q == 0) ? cx : (q == 1 ? cx - 1 : cx + 1);  // own column first
                     if (col < cl || col > cr) continue;
@@ -811,10 +721,10 @@ __global__ void __launch_bounds__(kStepThreads, 6) k_step(StepArgs a) {
                                 Bff[nb++ * T] = d21;
                             }
                             if (nb >= capB - 1) {  // buffer (nearly) full: merge, tighten
-                                merge(nb);
+                                cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
                                 nb = 0;
-                                if (cnt >= k)  // any key <= the k-th has fp32 d2 <= fk (1 + 2^-20)
-                                    thr = fminf(thr, __fmul_ru(kth(), 1.0f + 0x1p-20f));
+                                if (cnt == k)  // any key <= the k-th has fp32 d2 <= fk (1 + 2^-20)
+                                    thr = fminf(thr, __fmul_ru(__uint_as_float(L0[(k - 1) * T]), 1.0f + 0x1p-20f));
                             }
                         }
                     }
@@ -827,37 +737,31 @@ __global__ void __launch_bounds__(kStepThreads, 6) k_step(StepArgs a) {
                             Bff[nb++ * T] = d20;
                         }
                         if (nb >= capB - 1) {
-                            merge(nb);
+                            cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
                             nb = 0;
-                            if (cnt >= k) thr = fminf(thr, __fmul_ru(kth(), 1.0f + 0x1p-20f));
+                            if (cnt == k) thr = fminf(thr, __fmul_ru(__uint_as_float(L0[(k - 1) * T]), 1.0f + 0x1p-20f));
                         }
                     }
                 }
-                merge(nb);
+                cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
                 if (!guessed) break;
                 // Exact only if every candidate not kept -- rejected by the guessed radius
                 // (key > thrPass (1 - 2^-22)) or pruned geometrically (distance > rg) -- is
                 // strictly beyond the k-th key.
                 // kappa_k <= fk (1 + 2^-22) < thrPass (1 - 2^-22) < any rejected kappa
-                if (cnt >= k && (double)kth() < (double)thrPass * (1.0 - 0x1p-20)) break;
-                // rescan the full 3x3 stencil at the full radius
+                if (cnt == k && (double)__uint_as_float(L0[(k - 1) * T]) < (double)thrPass * (1.0 - 0x1p-20)) break;
+                cnt = 0;  // rescan the full 3x3 stencil at the full radius
                 thr = a.m.nd2Fup;
                 guessed = false;
             }
-            if (cnt >= k) fk = kth();
-            cnt = min(cnt, k);
-            if constexpr (KR > 0) {  // neighbour indices to the shared list slots
-#pragma unroll
-                for (int q = 0; q < KR; ++q)
-                    if (q < cnt) L2[q * T] = R.j[q];
-            }
+            if (cnt == k) fk = __uint_as_float(L0[(k - 1) * T]);
         }
         if (!DRY) a.rk2W[ws] = fk;  // next step's search bound (read back by k_lp3 for queued agents)
 
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
         // (half-plane q overwrites list slot q in place: j is read before the write)
         for (int q = 0; q < cnt; ++q) {
-            const uint32_t j = L2[q * T];
+            const uint32_t j = L1[q * T];
             const float2 pj = a.posS[j];
             const float2 vj = a.velS[j];
             const uint32_t idj = a.idS[j];
