@@ -514,6 +514,66 @@ __device__ __forceinline__ bool in_radius(float f, uint32_t j, float2 pi, float 
     return exact_key(posS[j], pi) < nd2;
 }
 
+// Sort <= 16 buffered candidates (j, fp32 d2) in registers with a bitonic network (80
+// compare-exchanges, identical for every thread, so a warp stays converged).  Comparisons
+// are fp32; a pair not separated by the 2^-20 margin (a possible exact-order disagreement)
+// makes the function return -1 and the caller redoes the selection with the exact
+// insertion merge -- if every comparison agrees with the exact (kappa, id) order, so does
+// the network's output.  Candidates outside r_obs sort last as +inf.  Writes the first
+// min(k, valid) to the list (Lf, Lj) and returns that count.
+__device__ __forceinline__ int network_select16(uint32_t* Lf, uint32_t* Lj, int k, const uint32_t* Bf,
+                                                const float* Bff, int nb, float2 pi, const Model& m,
+                                                const float2* __restrict__ posS) {
+    constexpr int T = kStepThreads;
+    float f[16];
+    uint32_t j[16];
+    int valid = 0;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        if (b < nb) {
+            j[b] = Bf[b * T];
+            f[b] = Bff[b * T];
+            if (!in_radius(f[b], j[b], pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) f[b] = INFINITY;
+        } else {
+            j[b] = 0xffffffffu;
+            f[b] = INFINITY;
+        }
+        valid += (f[b] != INFINITY) ? 1 : 0;
+    }
+    bool near = false;
+#pragma unroll
+    for (int size = 2; size <= 16; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+            for (int a = 0; a < 16; ++a) {
+                const int b = a ^ stride;
+                if (b > a) {
+                    const bool up = (a & size) == 0;
+                    const int x = up ? b : a, y = up ? a : b;  // swap iff x < y
+                    const float fx = f[x], fy = f[y];
+                    const bool sw = fx < fy;
+                    near |= fy != INFINITY && !(fx < fy * kSep && fy > 1e-30f) && !(fy < fx * kSep && fx > 1e-30f);
+                    f[x] = sw ? fy : fx;
+                    f[y] = sw ? fx : fy;
+                    const uint32_t jx = j[x], jy = j[y];
+                    j[x] = sw ? jy : jx;
+                    j[y] = sw ? jx : jy;
+                }
+            }
+        }
+    }
+    if (near) return -1;
+    const int cnt = min(valid, k);
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+        if (q < cnt) {
+            Lf[q * T] = __float_as_uint(f[q]);
+            Lj[q * T] = j[q];
+        }
+    return cnt;
+}
+
 // Merge the nb buffered candidates (j, fp32 d2) into the sorted top-k list (Lf = fp32 d2
 // bits, Lj = j).  Returns the new list length.
 __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int cnt, int k, const uint32_t* Bf,
@@ -607,8 +667,11 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
     }
 }
 
+#ifndef ORCA_STEP_MINBLOCKS
+#define ORCA_STEP_MINBLOCKS 8  // resident blocks per SM the register budget is sized for
+#endif
 template <bool DRY>
-__global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
+__global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(StepArgs a) {
     constexpr bool CNT = DRY;  // only the debug variant counts work
     WorkT w{0, 0, 0, 0, 0};
     extern __shared__ __align__(16) unsigned char smem[];
@@ -743,7 +806,10 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(StepArgs a) {
                         }
                     }
                 }
-                cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
+                // common case (no mid-scan merge, few candidates): converged sorting network
+                int sel = -1;
+                if (cnt == 0 && nb <= 16 && k <= 16) sel = network_select16(L0, L1, k, Bf, Bff, nb, pi, a.m, a.posS);
+                cnt = (sel >= 0) ? sel : merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
                 if (!guessed) break;
                 // Exact only if every candidate not kept -- rejected by the guessed radius
                 // (key > thrPass (1 - 2^-22)) or pruned geometrically (distance > rg) -- is
