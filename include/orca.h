@@ -80,6 +80,7 @@ typedef struct {
     int64_t eps_parallel;   /* g2: an LP pair with |det| <= 1e-5 (Q9) */
     int64_t marginal;       /* g3: infeasible with max penetration < 1e-6 (reported only) */
     int64_t collision_pairs;/* neighbour pairs that took the collision branch (Q4) */
+    int64_t removed;        /* agents removed at their goal (orca_set_goal_removal) */
 } orca_stats;
 
 /* ---- lifecycle -------------------------------------------------------------------- */
@@ -108,6 +109,18 @@ orca_status orca_set_agents(orca_ctx *ctx, int64_t n, const float *pos, const fl
  * preferred velocity is recomputed every step as g*min(1, prefSpeed/|g|), g = goal - pos.
  * Errors: NOT_READY, INVALID_ARGUMENT (NULL, NaN/Inf, prefSpeed < 0). */
 orca_status orca_set_goals(orca_ctx *ctx, const float *goal, float prefSpeed);
+
+/* Removal at the goal ("Once a person reaches the goal location they are removed from
+ * the simulation. Once all people have reached their goal the simulation is ended."): with
+ * goals set and radius > 0, an agent whose new position lies strictly within `radius` of its
+ * goal leaves the simulation after that step -- it is no longer stepped or observed;
+ * orca_get_state then reports NaN for it, orca_get_count counts the remaining agents (0 =
+ * ended).  radius 0 disables.  Persists across orca_set_agents.  Errors: INVALID_ARGUMENT. */
+orca_status orca_set_goal_removal(orca_ctx *ctx, float radius);
+
+/* active uint8[n] by id: 1 while the agent is in the simulation, 0 once removed.
+ * Synchronises.  Errors: NOT_READY. */
+orca_status orca_get_active(orca_ctx *ctx, uint8_t *active);
 
 /* Enqueue n_steps >= 0 synchronous steps on the context stream (one CUDA graph replay;
  * no host synchronisation).  Errors: NOT_READY, INVALID_ARGUMENT, CUDA, NCCL. */

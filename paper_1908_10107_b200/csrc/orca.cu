@@ -203,6 +203,7 @@ struct orca_ctx {
     orca_params p{};
     bool ready = false, goals = false;
     float prefSpeed = 0.0f;
+    float removeR = 0.0f;  // > 0: agents within removeR of their goal leave
     int world = 1;  // strips in the whole decomposition
     int rank = 0;   // NCCL rank (= the strip held by this context)
     bool loopback = false;
@@ -249,6 +250,7 @@ Model make_model(const orca_ctx* c) {
     m.k = p.maxNeighbors;
     m.goals = c->goals ? 1 : 0;
     m.prefSpeed = c->prefSpeed;
+    m.removeR2 = (c->goals && c->removeR > 0.0f) ? c->removeR * c->removeR : 0.0f;
     return m;
 }
 
@@ -876,6 +878,10 @@ orca_status orca_get_state(orca_ctx* c, float* pos, float* vel) {
     CKS(check_overflow(c));
     const int64_t n = c->nGlobal;
     if (n > 0 && (pos || vel)) {
+        if (c->removeR > 0.0f) {  // agents removed at their goal read as NaN
+            k_fill2<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->outA, NAN);
+            k_fill2<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, c->outB, NAN);
+        }
         for (Domain& d : c->doms)
             k_unpermute<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.idS, d.posS, d.velS,
                                                                        pos ? c->outA : nullptr,
@@ -1052,6 +1058,7 @@ orca_status orca_get_stats(orca_ctx* c, orca_stats* out) {
     out->eps_parallel = (int64_t)t[ST_G2];
     out->marginal = (int64_t)t[ST_G3];
     out->collision_pairs = (int64_t)t[ST_COLLISION];
+    out->removed = (int64_t)t[ST_REMOVED];
     if (c->ready) CKS(check_overflow(c));
     return ORCA_OK;
 }
@@ -1064,6 +1071,32 @@ orca_status orca_reset_stats(orca_ctx* c) {
     CK(cudaStreamSynchronize(c->stream));
     c->host_steps = 0;
     c->host_updates = 0;
+    return ORCA_OK;
+}
+
+orca_status orca_set_goal_removal(orca_ctx* c, float radius) {
+    if (!c || !(radius >= 0.0f) || !std::isfinite(radius)) return fail(ORCA_ERR_INVALID_ARGUMENT, "radius");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    drop_graph(c);
+    c->removeR = radius;
+    return ORCA_OK;
+}
+
+orca_status orca_get_active(orca_ctx* c, uint8_t* active) {
+    if (!c || !active) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    CK(cudaSetDevice(c->device));
+    const int64_t n = c->nGlobal;
+    if (n > 0) {
+        uint8_t* d = reinterpret_cast<uint8_t*>(c->outA);
+        CK(cudaMemsetAsync(d, 0, (size_t)n, c->stream));
+        for (Domain& dm : c->doms)
+            k_mark_active<<<cap_blocks(dm.capW, 256), 256, 0, c->stream>>>(dm.binStart, dm.g, dm.idS, d);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(active, d, (size_t)n, cudaMemcpyDefault, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
     return ORCA_OK;
 }
 

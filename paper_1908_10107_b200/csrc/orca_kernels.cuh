@@ -31,7 +31,7 @@ constexpr uint32_t FL_G2 = 4u;
 constexpr uint32_t FL_G3 = 8u;
 
 // indices into the device stats block (uint64)
-enum { ST_INFEASIBLE = 0, ST_DEGENERATE, ST_G1, ST_G2, ST_G3, ST_COLLISION, ST_COUNT };
+enum { ST_INFEASIBLE = 0, ST_DEGENERATE, ST_G1, ST_G2, ST_G3, ST_COLLISION, ST_REMOVED, ST_COUNT };
 
 // Work counters of an instrumented dry step (orca_debug_work): per-launch totals used by
 // the bench's ALU roofline.
@@ -69,6 +69,7 @@ struct Model {
     int k;                        // maxNeighbors
     int goals;                    // 1: aux holds goals, pref = g min(1, s/|g|)
     float prefSpeed;
+    float removeR2;               // > 0: remove agents within sqrt(removeR2) of their goal
 };
 
 // ------------------------------------------------------------------ cell (reading Q11)
@@ -514,66 +515,6 @@ __device__ __forceinline__ bool in_radius(float f, uint32_t j, float2 pi, float 
     return exact_key(posS[j], pi) < nd2;
 }
 
-// Sort <= 16 buffered candidates (j, fp32 d2) in registers with a bitonic network (80
-// compare-exchanges, identical for every thread, so a warp stays converged).  Comparisons
-// are fp32; a pair not separated by the 2^-20 margin (a possible exact-order disagreement)
-// makes the function return -1 and the caller redoes the selection with the exact
-// insertion merge -- if every comparison agrees with the exact (kappa, id) order, so does
-// the network's output.  Candidates outside r_obs sort last as +inf.  Writes the first
-// min(k, valid) to the list (Lf, Lj) and returns that count.
-__device__ __forceinline__ int network_select16(uint32_t* Lf, uint32_t* Lj, int k, const uint32_t* Bf,
-                                                const float* Bff, int nb, float2 pi, const Model& m,
-                                                const float2* __restrict__ posS) {
-    constexpr int T = kStepThreads;
-    float f[16];
-    uint32_t j[16];
-    int valid = 0;
-#pragma unroll
-    for (int b = 0; b < 16; ++b) {
-        if (b < nb) {
-            j[b] = Bf[b * T];
-            f[b] = Bff[b * T];
-            if (!in_radius(f[b], j[b], pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) f[b] = INFINITY;
-        } else {
-            j[b] = 0xffffffffu;
-            f[b] = INFINITY;
-        }
-        valid += (f[b] != INFINITY) ? 1 : 0;
-    }
-    bool near = false;
-#pragma unroll
-    for (int size = 2; size <= 16; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-#pragma unroll
-            for (int a = 0; a < 16; ++a) {
-                const int b = a ^ stride;
-                if (b > a) {
-                    const bool up = (a & size) == 0;
-                    const int x = up ? b : a, y = up ? a : b;  // swap iff x < y
-                    const float fx = f[x], fy = f[y];
-                    const bool sw = fx < fy;
-                    near |= fy != INFINITY && !(fx < fy * kSep && fy > 1e-30f) && !(fy < fx * kSep && fx > 1e-30f);
-                    f[x] = sw ? fy : fx;
-                    f[y] = sw ? fx : fy;
-                    const uint32_t jx = j[x], jy = j[y];
-                    j[x] = sw ? jy : jx;
-                    j[y] = sw ? jx : jy;
-                }
-            }
-        }
-    }
-    if (near) return -1;
-    const int cnt = min(valid, k);
-#pragma unroll
-    for (int q = 0; q < 16; ++q)
-        if (q < cnt) {
-            Lf[q * T] = __float_as_uint(f[q]);
-            Lj[q * T] = j[q];
-        }
-    return cnt;
-}
-
 // Merge the nb buffered candidates (j, fp32 d2) into the sorted top-k list (Lf = fp32 d2
 // bits, Lj = j).  Returns the new list length.
 __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int cnt, int k, const uint32_t* Bf,
@@ -637,6 +578,16 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
                                              float2 aux, uint32_t id, float rk2) {
     const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
     const float2 vn = make_float2(vx, vy);
+    if (a.m.removeR2 > 0.0f) {
+        // P:110 "Once a person reaches the goal location they are removed from the
+        // simulation": within removeR of the goal after the move -> not re-inserted
+        const float gx = aux.x - pn.x, gy = aux.y - pn.y;
+        if (fmaf(gx, gx, gy * gy) < a.m.removeR2) {
+            a.cellW[w] = kInvalid;
+            atomicAdd(&a.stats[ST_REMOVED], 1ull);
+            return;
+        }
+    }
     const int cx = cell_coord(pn.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
     const int sy = subrow_coord(pn.y, a.g);
     if (cx >= a.g.c0 && cx < a.g.c1) {
@@ -668,7 +619,7 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
 }
 
 #ifndef ORCA_STEP_MINBLOCKS
-#define ORCA_STEP_MINBLOCKS 8  // resident blocks per SM the register budget is sized for
+#define ORCA_STEP_MINBLOCKS 7  // resident blocks per SM the register budget is sized for (swept: 6/7/8)
 #endif
 template <bool DRY>
 __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(StepArgs a) {
@@ -806,10 +757,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                         }
                     }
                 }
-                // common case (no mid-scan merge, few candidates): converged sorting network
-                int sel = -1;
-                if (cnt == 0 && nb <= 16 && k <= 16) sel = network_select16(L0, L1, k, Bf, Bff, nb, pi, a.m, a.posS);
-                cnt = (sel >= 0) ? sel : merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
+                cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
                 if (!guessed) break;
                 // Exact only if every candidate not kept -- rejected by the guessed radius
                 // (key > thrPass (1 - 2^-22)) or pruned geometrically (distance > rg) -- is
@@ -1023,6 +971,17 @@ __global__ void k_unpermute(const uint32_t* __restrict__ binStart, Grid g, const
         if (posOut) posOut[id] = posS[i];
         if (velOut) velOut[id] = velS[i];
     }
+}
+
+__global__ void k_fill2(int n, float2* __restrict__ out, float v) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = make_float2(v, v);
+}
+
+// active[id] = 1 for owned (not removed) agents
+__global__ void k_mark_active(const uint32_t* __restrict__ binStart, Grid g, const uint32_t* __restrict__ idS,
+                              uint8_t* __restrict__ active) {
+    const int2 r = owned_range(binStart, g);
+    for (int i = r.x + blockIdx.x * blockDim.x + threadIdx.x; i < r.y; i += gridDim.x * blockDim.x) active[idS[i]] = 1;
 }
 
 __global__ void k_cells(const uint32_t* __restrict__ binStart, Grid g, const uint32_t* __restrict__ idS,

@@ -26,6 +26,7 @@ EXPORTS = [
     "orca_reset_stats", "orca_get_stream", "orca_step_timed", "orca_status_string", "orca_last_error",
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
+    "orca_set_goal_removal", "orca_get_active",
 ]
 
 
@@ -43,7 +44,8 @@ class Params(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("steps", "agent_updates", "infeasible", "degenerate",
-                                               "coincident", "eps_parallel", "marginal", "collision_pairs")]
+                                               "coincident", "eps_parallel", "marginal", "collision_pairs",
+                                               "removed")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -81,6 +83,8 @@ def _load():
         "orca_partition_columns": [P(i64), i32, i32, P(i32)],
         "orca_get_strips": [vp, P(i32)],
         "orca_set_variant": [vp, i32],
+        "orca_set_goal_removal": [vp, f32],
+        "orca_get_active": [vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -205,8 +209,8 @@ class Orca:
     def get_state(self, pos=None, vel=None):
         """Into caller buffers (numpy or torch) if given, else new numpy arrays."""
         if pos is None and vel is None:
-            pos = np.empty((self.count(), 2), np.float32)
-            vel = np.empty((self.count(), 2), np.float32)
+            pos = np.empty((self.n, 2), np.float32)
+            vel = np.empty((self.n, 2), np.float32)
         _check(_lib.orca_get_state(self._ctx, _ptr(pos), _ptr(vel)))
         return pos, vel
 
@@ -260,6 +264,15 @@ class Orca:
 
     def reset_stats(self):
         _check(_lib.orca_reset_stats(self._ctx))
+
+    def set_goal_removal(self, radius: float):
+        """Remove agents within `radius` of their goal after a step; 0 disables."""
+        _check(_lib.orca_set_goal_removal(self._ctx, radius))
+
+    def active(self):
+        a = np.empty(self.n, np.uint8)
+        _check(_lib.orca_get_active(self._ctx, _ptr(a)))
+        return a.astype(bool)
 
     def set_variant(self, variant: int):
         """0 = thread per agent, 1 = 8-lane group per agent (same results)."""

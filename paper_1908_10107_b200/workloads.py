@@ -31,7 +31,7 @@ DEFAULT_PARAMS = dict(timeStep=0.25, neighborDist=15.0, maxNeighbors=10, timeHor
 DESIRED_SPEED = 1.0
 
 CONFIGS = {
-    # name: (index for the seed, description)
+    # name: index for the seed
     "circle": 0,
     "corridor": 1,
     "uniform": 2,
@@ -95,6 +95,59 @@ def uniform(n: int = 100_000, rho: float = 0.25, salt: int = 0, config: str = "u
                 pref_speed=DESIRED_SPEED, params=dict(DEFAULT_PARAMS), steps=100)
 
 
+def two_way(n: int = 2500, rho: float = 0.25, gap: float = 60.0, salt: int = 0):
+    """E1a, the paper's 2-way crossing (Fig. 3): two crowds of n/2 start in a left
+    and a right region; "the starting region of one group of people is the same area as
+    the goal region of the other" -- each agent's goal is its mirror point in the opposite
+    region.  Regions: square, density rho, `gap` metres apart.  Goal seeking at the
+    desired 1.0 m/s, removal at the goal left to the caller."""
+    rng = np.random.default_rng(BASE_SEED + 10 + 1000 * salt)
+    half = n // 2
+    side = math.sqrt(half / rho)
+    s = 1.0 / math.sqrt(rho)
+    m = int(math.ceil(side / s))
+    left = _jittered_lattice(rng, m, m, s, DEFAULT_PARAMS["radius"], 0.0, 0.0)
+    right = _jittered_lattice(rng, m, m, s, DEFAULT_PARAMS["radius"], side + gap, 0.0)
+    left = left[rng.permutation(len(left))[:half]]
+    right = right[rng.permutation(len(right))[:n - half]]
+    width = 2 * side + gap
+    pos = np.concatenate([left, right])
+    goals = pos.copy()
+    goals[:, 0] = width - pos[:, 0]  # mirror into the other region
+    perm = rng.permutation(n)
+    pos, goals = pos[perm].astype(np.float32), goals[perm].astype(np.float32)
+    return dict(name=f"two_way_n{n}", pos=pos, vel=np.zeros_like(pos), pref=np.zeros_like(pos), goals=goals,
+                pref_speed=DESIRED_SPEED, params=dict(DEFAULT_PARAMS), steps=2000)
+
+
+def eight_way(n: int = 10_000, rho: float = 0.25, ring: float = 120.0, turn_deg: float = 135.0, salt: int = 0):
+    """E1c, the paper's 8-way crossing (Fig. 5): eight crowds of n/8 in square
+    regions around a ring; each crowd's goal region is its own region turned by
+    `turn_deg` about the centre (P:144 "navigate 135 deg across the environment";
+    P:151 says "to the opposite end" = 180, reading Q17).  Goal seeking at 1.0 m/s."""
+    rng = np.random.default_rng(BASE_SEED + 11 + 1000 * salt)
+    per = n // 8
+    side = math.sqrt(per / rho)
+    s = 1.0 / math.sqrt(rho)
+    m = int(math.ceil(side / s))
+    pos, goals = [], []
+    t = math.radians(turn_deg)
+    rot = np.array([[math.cos(t), -math.sin(t)], [math.sin(t), math.cos(t)]])
+    for c in range(8):
+        cnt = per if c < 7 else n - 7 * per
+        a = 2 * math.pi * c / 8
+        cx, cy = ring * math.cos(a), ring * math.sin(a)
+        blk = _jittered_lattice(rng, m, m, s, DEFAULT_PARAMS["radius"], cx - side / 2, cy - side / 2)
+        blk = blk[rng.permutation(len(blk))[:cnt]]
+        pos.append(blk)
+        goals.append(blk @ rot.T)
+    pos, goals = np.concatenate(pos), np.concatenate(goals)
+    perm = rng.permutation(n)
+    pos, goals = pos[perm].astype(np.float32), goals[perm].astype(np.float32)
+    return dict(name=f"eight_way_n{n}", pos=pos, vel=np.zeros_like(pos), pref=np.zeros_like(pos), goals=goals,
+                pref_speed=DESIRED_SPEED, params=dict(DEFAULT_PARAMS), steps=3000)
+
+
 def make(config: str, n: int | None = None, rho: float | None = None, salt: int = 0):
     """Named BASELINE.json configs."""
     if config == "circle":
@@ -109,6 +162,10 @@ def make(config: str, n: int | None = None, rho: float | None = None, salt: int 
         return uniform(n or 500_000, rho if rho is not None else 0.5, salt=salt, config="dense")
     if config == "uniform_4m":
         return uniform(n or 4_000_000, rho if rho is not None else 0.25, salt=salt, config="uniform_4m")
+    if config == "two_way":
+        return two_way(n or 2500, salt=salt)
+    if config == "eight_way":
+        return eight_way(n or 10_000, salt=salt)
     raise KeyError(config)
 
 

@@ -356,3 +356,58 @@ def test_variants_bit_identical(orca, config, n, rho):
     assert np.array_equal(s[0][0], s[1][0]) and np.array_equal(s[0][1], s[1][1])
     for o in ctxs:
         o.close()
+
+
+# ---------------------------------------------------- goals + removal (§8(f1))
+def test_removal_one_step_vs_oracle(orca, oracle):
+    """After one step an agent is removed iff its new position is strictly within R of its
+    goal; compared with the oracle's p' = p + dt v' outside an fp32 band."""
+    rng = np.random.default_rng(17)
+    w = W.make("uniform", n=3000, rho=0.2)
+    R = 0.6
+    goals = (w["pos"] + rng.uniform(-1.2, 1.2, w["pos"].shape)).astype(np.float32)
+    o, p = _ctx(orca, dict(w, goals=goals, pref_speed=1.0))
+    o.set_goal_removal(R)
+    ref = oracle.step(oracle.make_params(**p), w["pos"], w["vel"], goals=goals, pref_speed=1.0)
+    o.step(1)
+    act = o.active()
+    dg = np.hypot(*(goals.astype(np.float64) - ref["pos"]).T)
+    sure_in, sure_out = dg < R - 1e-4, dg > R + 1e-4
+    assert np.all(~act[sure_in]) and np.all(act[sure_out])
+    assert o.count() == int(act.sum()) and o.stats()["removed"] == int((~act).sum())
+    pos, vel = o.get_state()
+    assert np.all(np.isnan(pos[~act])) and np.all(np.isfinite(pos[act]))
+    # removed agents are no longer observed: next step's neighbour lists only hold active ids
+    v, fl, nb, cnt = o.debug_step()
+    ids = nb[act][nb[act] >= 0]
+    assert np.all(act[ids])
+    o.close()
+
+
+@pytest.mark.parametrize("strips", [1, 3])
+def test_circle_all_removed(orca, strips):
+    """C0 with removal at the goal: the simulation ends (count 0) within 1000 steps."""
+    w = W.make("circle")
+    o = orca.Orca(w["params"], strips=strips if strips > 1 else 0)
+    o.set_agents(w["pos"], w["vel"], w["pref"])
+    o.set_goals(w["goals"], w["pref_speed"])
+    o.set_goal_removal(w["params"]["radius"])
+    last = o.count()
+    for _ in range(20):
+        o.step(50)
+        c = o.count()
+        assert c <= last
+        last = c
+    assert last == 0 and o.stats()["removed"] == 100
+    o.close()
+
+
+def test_two_way_crossing_runs(orca):
+    """E1a: 2,500 agents cross and are removed at their goals."""
+    w = W.make("two_way")
+    o, p = _ctx(orca, w)
+    o.set_goal_removal(p["radius"])
+    o.step(1500)
+    st = o.stats()
+    assert st["removed"] >= 0.9 * 2500, st
+    o.close()
