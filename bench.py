@@ -262,7 +262,7 @@ def run_ours(args):
     work = {k: 0.5 * (work0[k] + work1[k]) for k in work0}
     # kernel variant A/B (same results bit for bit): fused-step ms per step
     variant_ms = {}
-    for v in (0, 1):
+    for v in (0, 1, 2):
         ctx.set_variant(v)
         ctx.step(2)
         acc = 0.0

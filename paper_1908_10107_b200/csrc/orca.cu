@@ -340,10 +340,16 @@ void drop_graph(orca_ctx* c) {
 // fused step kernel of the selected variant (same results bit for bit)
 template <bool DRY>
 void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
+    const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
+    const int k = c->p.maxNeighbors;
     if (c->variant == 1)
         k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
+    else if (c->variant == 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
+        k_step<DRY, 0><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
+    else if (k <= 10)  // register top-k list
+        k_step<DRY, 10><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
     else
-        k_step<DRY><<<(d.capW + kStepThreads - 1) / kStepThreads, kStepThreads, c->smemBytes, c->stream>>>(a);
+        k_step<DRY, 16><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
 }
 
 cudaError_t enqueue_scan(orca_ctx* c, Domain& d) {
@@ -490,10 +496,11 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
     for (int q = 0; q < 8 && e == cudaSuccess; ++q) e = cudaEventCreate(&c->ev[q]);
     c->smemBytes = step_smem_per_thread(params->maxNeighbors) * kStepThreads;
     c->lp3Smem = std::max(1, 6 * params->maxNeighbors) * 4 * kStepThreads;
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
+    const void* stepFns[] = {(const void*)k_step<false, 0>,  (const void*)k_step<true, 0>,
+                             (const void*)k_step<false, 10>, (const void*)k_step<true, 10>,
+                             (const void*)k_step<false, 16>, (const void*)k_step<true, 16>};
+    for (const void* f : stepFns)
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
     if (e == cudaSuccess)
@@ -964,6 +971,7 @@ orca_status orca_debug_cells(orca_ctx* c, int32_t* cx, int32_t* cy) {
     const int64_t n = c->nGlobal;
     if (n > 0) {
         int32_t* d0 = reinterpret_cast<int32_t*>(c->outA);  // 2 x int32 per agent
+        CK(cudaMemsetAsync(d0, 0xff, (size_t)n * 2 * sizeof(int32_t), c->stream));  // removed: -1
         for (Domain& d : c->doms)
             k_cells<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.idS, d.posS, d0, d0 + n);
         CK(cudaGetLastError());
@@ -988,6 +996,13 @@ orca_status orca_debug_step(orca_ctx* c, float* vnew, uint8_t* flags, int32_t* n
     cudaError_t e = cudaMalloc(&dF, (size_t)n);
     if (e == cudaSuccess) e = cudaMalloc(&dC, (size_t)n * sizeof(int32_t));
     if (e == cudaSuccess && k > 0) e = cudaMalloc(&dN, (size_t)n * k * sizeof(int32_t));
+    // agents no longer in the simulation (removed at their goal): NaN, flags 0, cnt -1
+    if (e == cudaSuccess) {
+        k_fill2<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, dV, NAN);
+        e = cudaMemsetAsync(dF, 0, (size_t)n, c->stream);
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(dC, 0xff, (size_t)n * sizeof(int32_t), c->stream);
+    if (e == cudaSuccess && k > 0) e = cudaMemsetAsync(dN, 0xff, (size_t)n * k * sizeof(int32_t), c->stream);
     for (Domain& d : c->doms) {
         if (e != cudaSuccess) break;
         StepArgs a = make_args(c, d);
@@ -1101,7 +1116,7 @@ orca_status orca_get_active(orca_ctx* c, uint8_t* active) {
 }
 
 orca_status orca_set_variant(orca_ctx* c, int32_t variant) {
-    if (!c || variant < 0 || variant > 1) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be 0 or 1");
+    if (!c || variant < 0 || variant > 2) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be 0, 1 or 2");
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->variant = variant;

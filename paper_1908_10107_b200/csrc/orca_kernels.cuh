@@ -515,6 +515,71 @@ __device__ __forceinline__ bool in_radius(float f, uint32_t j, float2 pi, float 
     return exact_key(posS[j], pi) < nd2;
 }
 
+// Register-resident sorted list of the KR nearest candidates (+inf padded).  Insertion
+// compares in fp32 only and is branch-free (a warp stays converged however many
+// candidates each thread merges); a comparison inside the 2^-20 margin (a possible
+// exact-order disagreement) raises `tie`, and the caller then redoes the agent's selection
+// on the exact shared-memory path.  Without a tie, every comparison agrees with the exact
+// (kappa, id) order, so the list is the exact one.
+template <int KR>
+struct RegList {
+    float f[KR];
+    uint32_t j[KR];
+};
+
+template <int KR>
+__device__ __forceinline__ void reg_clear(RegList<KR>& L) {
+#pragma unroll
+    for (int p = 0; p < KR; ++p) {
+        L.f[p] = INFINITY;
+        L.j[p] = 0u;
+    }
+}
+
+template <int KR>
+__device__ __forceinline__ void reg_insert(RegList<KR>& L, float f, uint32_t j, bool& tie) {
+    int pos = 0;
+    bool t = !(f > 1e-30f);  // subnormal range: the relative error bound does not hold
+#pragma unroll
+    for (int p = 0; p < KR; ++p) {
+        const float of = L.f[p];
+        const bool before = of < f * kSep;  // slot p surely nearer
+        const bool after = f < of * kSep;   // slot p surely farther (also of = +inf)
+        t |= !(before || after);
+        pos += before ? 1 : 0;
+    }
+    tie |= t;
+#pragma unroll
+    for (int p = KR - 1; p >= 0; --p) {
+        const float pf = (p > 0) ? L.f[p - 1] : f;
+        const uint32_t pj = (p > 0) ? L.j[p - 1] : j;
+        L.f[p] = (p > pos) ? pf : ((p == pos) ? f : L.f[p]);
+        L.j[p] = (p > pos) ? pj : ((p == pos) ? j : L.j[p]);
+    }
+}
+
+template <int KR>
+__device__ __forceinline__ float reg_f(const RegList<KR>& L, int q) {
+    float r = INFINITY;
+#pragma unroll
+    for (int p = 0; p < KR; ++p) r = (p == q) ? L.f[p] : r;
+    return r;
+}
+
+// buffered (j, fp32 d2) candidates into the register list (inside r_obs only)
+template <int KR>
+__device__ __forceinline__ void reg_merge(RegList<KR>& L, int& cnt, const uint32_t* Bj, const float* Bff, int nb,
+                                          float2 pi, const Model& m, const float2* __restrict__ posS, bool& tie) {
+    constexpr int T = kStepThreads;
+    for (int b = 0; b < nb; ++b) {
+        const uint32_t j = Bj[b * T];
+        const float f = Bff[b * T];
+        if (!in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
+        reg_insert<KR>(L, f, j, tie);
+        cnt = min(cnt + 1, KR);
+    }
+}
+
 // Merge the nb buffered candidates (j, fp32 d2) into the sorted top-k list (Lf = fp32 d2
 // bits, Lj = j).  Returns the new list length.
 __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int cnt, int k, const uint32_t* Bf,
@@ -621,7 +686,8 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
 #ifndef ORCA_STEP_MINBLOCKS
 #define ORCA_STEP_MINBLOCKS 7  // resident blocks per SM the register budget is sized for (swept: 6/7/8)
 #endif
-template <bool DRY>
+// KR > 0: the top-k selection runs in a register list (k <= KR); KR = 0: shared memory.
+template <bool DRY, int KR>
 __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(StepArgs a) {
     constexpr bool CNT = DRY;  // only the debug variant counts work
     WorkT w{0, 0, 0, 0, 0};
@@ -692,6 +758,25 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                     guessed = true;
                 }
             }
+            // mode 0: register list (KR > 0, fp32 compares); mode 1: exact shared-memory
+            // list -- taken only if mode 0 met an fp32 near-tie (or KR == 0)
+            RegList<(KR > 0 ? KR : 1)> R;
+            bool tie = false;
+            const float thr0 = thr;
+            const bool guessed0 = guessed;
+            int mode = (KR > 0) ? 0 : 1;
+            auto merge = [&](int nb) {
+                if (KR > 0 && mode == 0)
+                    reg_merge<(KR > 0 ? KR : 1)>(R, cnt, Bf, Bff, nb, pi, a.m, a.posS, tie);
+                else
+                    cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
+            };
+            auto kth = [&]() -> float {  // fp32 d2 of the k-th (valid when cnt >= k)
+                if (KR > 0 && mode == 0) return reg_f<(KR > 0 ? KR : 1)>(R, k - 1);
+                return __uint_as_float(L0[(k - 1) * T]);
+            };
+          for (;;) {  // modes
+            if (KR > 0 && mode == 0) reg_clear<(KR > 0 ? KR : 1)>(R);
             for (int pass = 0; pass < 2; ++pass) {
                 const float thrPass = thr;
                 // sub-row window and side columns for this pass
@@ -735,10 +820,10 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                                 Bff[nb++ * T] = d21;
                             }
                             if (nb >= capB - 1) {  // buffer (nearly) full: merge, tighten
-                                cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
+                                merge(nb);
                                 nb = 0;
-                                if (cnt == k)  // any key <= the k-th has fp32 d2 <= fk (1 + 2^-20)
-                                    thr = fminf(thr, __fmul_ru(__uint_as_float(L0[(k - 1) * T]), 1.0f + 0x1p-20f));
+                                if (cnt >= k)  // any key <= the k-th has fp32 d2 <= fk (1 + 2^-20)
+                                    thr = fminf(thr, __fmul_ru(kth(), 1.0f + 0x1p-20f));
                             }
                         }
                     }
@@ -751,24 +836,37 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                             Bff[nb++ * T] = d20;
                         }
                         if (nb >= capB - 1) {
-                            cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
+                            merge(nb);
                             nb = 0;
-                            if (cnt == k) thr = fminf(thr, __fmul_ru(__uint_as_float(L0[(k - 1) * T]), 1.0f + 0x1p-20f));
+                            if (cnt >= k) thr = fminf(thr, __fmul_ru(kth(), 1.0f + 0x1p-20f));
                         }
                     }
                 }
-                cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
+                merge(nb);
                 if (!guessed) break;
                 // Exact only if every candidate not kept -- rejected by the guessed radius
                 // (key > thrPass (1 - 2^-22)) or pruned geometrically (distance > rg) -- is
                 // strictly beyond the k-th key.
                 // kappa_k <= fk (1 + 2^-22) < thrPass (1 - 2^-22) < any rejected kappa
-                if (cnt == k && (double)__uint_as_float(L0[(k - 1) * T]) < (double)thrPass * (1.0 - 0x1p-20)) break;
+                if (cnt >= k && (double)kth() < (double)thrPass * (1.0 - 0x1p-20)) break;
                 cnt = 0;  // rescan the full 3x3 stencil at the full radius
+                if (KR > 0 && mode == 0) reg_clear<(KR > 0 ? KR : 1)>(R);
                 thr = a.m.nd2Fup;
                 guessed = false;
             }
-            if (cnt == k) fk = __uint_as_float(L0[(k - 1) * T]);
+            if (!(KR > 0 && mode == 0 && tie)) break;
+            mode = 1;  // fp32 near-tie: redo this agent's selection on the exact path
+            cnt = 0;
+            thr = thr0;
+            guessed = guessed0;
+          }
+            if (cnt >= k) fk = kth();
+            cnt = min(cnt, k);
+            if (KR > 0 && mode == 0) {  // neighbour indices into the shared list slots
+#pragma unroll
+                for (int q = 0; q < (KR > 0 ? KR : 1); ++q)
+                    if (q < cnt) L1[q * T] = R.j[q];
+            }
         }
         if (!DRY) a.rk2W[ws] = fk;  // next step's search bound (read back by k_lp3 for queued agents)
 

@@ -235,15 +235,17 @@ class Orca:
         return np.array([o[0], o[1]], np.float64), cs.value, np.array([d[0], d[1]], np.int32)
 
     def debug_cells(self):
-        n = self.count()
+        """(cx, cy) int32[n] by id (all ids of set_agents; removed agents are -1)."""
+        n = self.n
         cx = np.empty(n, np.int32)
         cy = np.empty(n, np.int32)
         _check(_lib.orca_debug_cells(self._ctx, _ptr(cx), _ptr(cy)))
         return cx, cy
 
     def debug_step(self):
-        """(vnew (n,2) f32, flags u8, nbr (n,k) int32, cnt int32) for the current state."""
-        n = self.count()
+        """(vnew (n,2) f32, flags u8, nbr (n,k) int32, cnt int32) by id for the current
+        state (removed agents: NaN velocity, cnt -1)."""
+        n = self.n
         k = self.params.maxNeighbors
         v = np.empty((n, 2), np.float32)
         fl = np.empty(n, np.uint8)

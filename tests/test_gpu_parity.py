@@ -338,22 +338,25 @@ def test_strips_goals_circle(orca):
 
 @pytest.mark.parametrize("config,n,rho", [("uniform", 20000, 0.25), ("dense", 20000, None), ("uniform", 5000, 0.02)])
 def test_variants_bit_identical(orca, config, n, rho):
-    """Thread-per-agent (0) and 8-lane-group-per-agent (1) kernels: same neighbours,
-    velocities and trajectories bit for bit (the group LP uses exact min/max reductions)."""
+    """Thread-per-agent with a register (0) or shared-memory (2) top-k list and the
+    8-lane-group-per-agent kernel (1): same neighbours, velocities and trajectories bit for
+    bit (exact comparators; the group LP uses exact min/max reductions)."""
     w = W.make(config, n=n, rho=rho) if rho else W.make(config, n=n)
     ctxs = []
-    for v in (0, 1):
+    for v in (0, 1, 2):
         o, p = _ctx(orca, w)
         o.set_variant(v)
         ctxs.append(o)
     r = [o.debug_step() for o in ctxs]
-    assert np.array_equal(r[0][2], r[1][2]) and np.array_equal(r[0][3], r[1][3])
-    assert np.array_equal(r[0][0], r[1][0])
-    assert np.array_equal(r[0][1] & 1, r[1][1] & 1)
+    for q in (1, 2):
+        assert np.array_equal(r[0][2], r[q][2]) and np.array_equal(r[0][3], r[q][3])
+        assert np.array_equal(r[0][0], r[q][0])
+        assert np.array_equal(r[0][1] & 1, r[q][1] & 1)
     for o in ctxs:
         o.step(25)
     s = [o.get_state() for o in ctxs]
-    assert np.array_equal(s[0][0], s[1][0]) and np.array_equal(s[0][1], s[1][1])
+    for q in (1, 2):
+        assert np.array_equal(s[0][0], s[q][0]) and np.array_equal(s[0][1], s[q][1])
     for o in ctxs:
         o.close()
 
