@@ -344,7 +344,7 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int k = c->p.maxNeighbors;
     if (c->variant == 1)
         k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
-    else if (c->variant == 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
+    else if (c->variant == 0 || k < 1 || k > 16)  // shared-memory top-k list (any k)
         k_step<DRY, 0><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
     else if (k <= 10)  // register top-k list
         k_step<DRY, 10><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);

@@ -483,7 +483,7 @@ constexpr int kStepThreads = 128;
 //   [k, 2k)           top-k list j         -> half-plane ny (slot q read before written)
 //   [2k, 2k + B)      candidate buffer j   -> half-plane s in its first k words
 //   [2k + B, 2k + 2B) candidate buffer fp32 d2            (B = k + 8)
-__host__ __device__ constexpr int step_buf_words(int k) { return k + 8; }
+__host__ __device__ constexpr int step_buf_words(int k) { return k + 14; }
 __host__ __device__ constexpr int step_smem_per_thread(int k) { return 4 * (2 * k + 2 * step_buf_words(k)); }
 
 __device__ __forceinline__ double exact_key(float2 pj, float2 pi) {
@@ -709,6 +709,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     const int ws = blockIdx.x * T + tid;  // work slot
     const int i = o0 + ws;                // sorted index
     const bool active = i < o1;
+    const unsigned activeMask = __ballot_sync(0xffffffffu, active);  // lanes that step an agent
     if (!DRY && blockIdx.x == 0 && tid == 0) a.ctr[CT_NOWN] = o1 - o0;
     uint32_t fl = 0;
     int nColl = 0;
@@ -842,6 +843,11 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                         }
                     }
                 }
+                // reconverge the warp after the data-dependent scan loops, so the final
+                // merge runs once for all lanes instead of once per divergent subset.  Only
+                // at the first pass of the first mode, which every active lane executes
+                // exactly once (rescans / exact redos are per-lane and rare).
+                if (pass == 0 && mode == ((KR > 0) ? 0 : 1)) __syncwarp(activeMask);
                 merge(nb);
                 if (!guessed) break;
                 // Exact only if every candidate not kept -- rejected by the guessed radius
