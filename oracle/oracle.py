@@ -44,6 +44,12 @@ class Params(ctypes.Structure):
     ]
 
 
+class Agents(ctypes.Structure):
+    """or_agents: optional per-agent float[n] arrays (NULL = global value)."""
+    _fields_ = [("radius", ctypes.POINTER(ctypes.c_float)), ("maxSpeed", ctypes.POINTER(ctypes.c_float)),
+                ("prefSpeed", ctypes.POINTER(ctypes.c_float))]
+
+
 class Line(ctypes.Structure):
     _fields_ = [("px", ctypes.c_double), ("py", ctypes.c_double),
                 ("dx", ctypes.c_double), ("dy", ctypes.c_double)]
@@ -75,15 +81,15 @@ def lib():
         L.or_neighbors.argtypes = [ctypes.c_int64, f32p, f32p, ctypes.c_float, i32p,
                                    ctypes.c_float, ctypes.c_int32, i32p, i32p]
         L.or_orca_line.argtypes = [f32p, f32p, f32p, f32p, ctypes.c_int64, ctypes.c_int64,
-                                   ctypes.c_float, ctypes.c_float, ctypes.c_float, P(Line)]
+                                   ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, P(Line)]
         L.or_lp2.argtypes = [P(Line), ctypes.c_int, ctypes.c_double, f64p, ctypes.c_int, f64p, u32p]
         L.or_lp3.argtypes = [P(Line), ctypes.c_int, ctypes.c_int, ctypes.c_double, f64p, u32p]
         L.or_lp3.restype = None
         L.or_penetration.argtypes = [P(Line), ctypes.c_int, f64p]
         L.or_penetration.restype = ctypes.c_double
-        L.or_step.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float,
+        L.or_step.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float, P(Agents),
                               f32p, i32p, ctypes.c_int64, i64p, f64p, f64p, u8p, f64p, i32p, i32p]
-        L.or_run.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float,
+        L.or_run.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float, P(Agents),
                              ctypes.c_int32]
         L.or_run.restype = ctypes.c_int64
         _lib = L
@@ -139,12 +145,12 @@ def neighbors(pos, origin, cs, dims, nd, k):
     return nbr[:, :k], cnt
 
 
-def orca_line(pi, vi, pj, vj, idi, idj, radius, tau, dt):
-    """Returns ((px, py, dx, dy), branch_mask)."""
+def orca_line(pi, vi, pj, vj, idi, idj, radius, tau, dt, rj=None):
+    """Returns ((px, py, dx, dy), branch_mask).  radius = r_i; rj = r_j (default r_i)."""
     out = Line()
     a = [_f32(x) for x in (pi, vi, pj, vj)]
-    br = lib().or_orca_line(*[_p(x, ctypes.c_float) for x in a], idi, idj, radius, tau, dt,
-                            ctypes.byref(out))
+    br = lib().or_orca_line(*[_p(x, ctypes.c_float) for x in a], idi, idj, radius,
+                            radius if rj is None else rj, tau, dt, ctypes.byref(out))
     return (out.px, out.py, out.dx, out.dy), br
 
 
@@ -191,11 +197,30 @@ def penetration(lines, v):
     return lib().or_penetration(arr, n, _p(vv, ctypes.c_double))
 
 
+def _agents(props):
+    """props: None or dict(radius=, maxSpeed=, prefSpeed=) of float[n] (any may be None)."""
+    if not props:
+        return None, []
+    keep = []
+    arrs = []
+    for key in ("radius", "maxSpeed", "prefSpeed"):
+        v = props.get(key)
+        if v is None:
+            arrs.append(None)
+        else:
+            a = np.ascontiguousarray(v, np.float32)
+            keep.append(a)
+            arrs.append(_p(a, ctypes.c_float))
+    return ctypes.byref(Agents(*arrs)), keep
+
+
 def step(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, origin=None, dims=None,
-         agents=None, want_nbrs=False):
+         agents=None, want_nbrs=False, props=None):
     """One synchronous step from the given fp32 state.  If origin/dims are None the grid is
-    derived from `pos` (as at set_agents).  Returns a dict of numpy arrays indexed like
-    `agents` (or by id)."""
+    derived from `pos` (as at set_agents).  props: optional per-agent radius / maxSpeed /
+    prefSpeed arrays.  Returns a dict of numpy arrays indexed like `agents` (or by
+    id)."""
+    agp, _keep = _agents(props)
     pos = _f32(pos).reshape(-1, 2)
     vel = _f32(vel).reshape(-1, 2)
     n = len(pos)
@@ -219,7 +244,7 @@ def step(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, origin
     nbr = np.full((m, max(k, 1)), -1, np.int32) if want_nbrs else None
     cnt = np.zeros(m, np.int32) if want_nbrs else None
     rc = lib().or_step(ctypes.byref(params), n, _p(pos, ctypes.c_float), _p(vel, ctypes.c_float),
-                       _p(pref, ctypes.c_float), _p(goals, ctypes.c_float), pref_speed,
+                       _p(pref, ctypes.c_float), _p(goals, ctypes.c_float), pref_speed, agp,
                        _p(origin, ctypes.c_float), _p(dims, ctypes.c_int32), m, _p(ag, ctypes.c_int64),
                        _p(vnew, ctypes.c_double), _p(pnew, ctypes.c_double), _p(flags, ctypes.c_uint8),
                        _p(delta, ctypes.c_double), _p(nbr, ctypes.c_int32), _p(cnt, ctypes.c_int32))
@@ -232,14 +257,15 @@ def step(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, origin
     return out
 
 
-def run(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, steps=1):
+def run(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, steps=1, props=None):
     """nsteps full steps on fp32 state; returns (pos, vel, infeasible_agent_steps)."""
+    agp, _keep = _agents(props)
     pos = _f32(pos).reshape(-1, 2).copy()
     vel = _f32(vel).reshape(-1, 2).copy()
     pref = None if pref is None else _f32(pref).reshape(-1, 2)
     goals = None if goals is None else _f32(goals).reshape(-1, 2)
     r = lib().or_run(ctypes.byref(params), len(pos), _p(pos, ctypes.c_float), _p(vel, ctypes.c_float),
-                     _p(pref, ctypes.c_float), _p(goals, ctypes.c_float), pref_speed, steps)
+                     _p(pref, ctypes.c_float), _p(goals, ctypes.c_float), pref_speed, agp, steps)
     if r < 0:
         raise ValueError("or_run failed")
     return pos, vel, int(r)

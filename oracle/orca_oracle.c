@@ -180,13 +180,13 @@ void or_neighbors(int64_t n, const float *pos, const float origin[2], float cs,
 /* ---------------------------------------------------------------------------------- */
 
 int or_orca_line(const float pi[2], const float vi[2], const float pj[2], const float vj[2],
-                 int64_t idi, int64_t idj, float radius, float tau, float dt, or_line *out) {
+                 int64_t idi, int64_t idj, float ri, float rj, float tau, float dt, or_line *out) {
     const double rpx = (double)pj[0] - (double)pi[0]; /* relative position p_b - p_a */
     const double rpy = (double)pj[1] - (double)pi[1];
     const double rvx = (double)vi[0] - (double)vj[0]; /* relative velocity v_a - v_b (Q3) */
     const double rvy = (double)vi[1] - (double)vj[1];
     const double d2 = rpx * rpx + rpy * rpy;
-    const double R = (double)radius + (double)radius; /* r_a + r_b (Fig. 1(a)) */
+    const double R = (double)ri + (double)rj; /* r_a + r_b (Fig. 1(a)) */
     const double R2 = R * R;
     double dirx, diry, ux, uy;
     int branch;
@@ -408,7 +408,8 @@ static int params_ok(const or_params *p) {
 /* preferred velocity toward the goal at walking speed ("The agent's velocity is in
  * the direction of the goal location, scaled to the walking speed"; reading Q16). */
 static void pref_of(const float *pos, const float *pref, const float *goals, float prefSpeed,
-                    int64_t i, double out[2]) {
+                    const or_agents *ag, int64_t i, double out[2]) {
+    if (ag && ag->prefSpeed) prefSpeed = ag->prefSpeed[i]; /* P:128 per-person desired speed */
     if (!goals) {
         out[0] = (double)pref[2 * i];
         out[1] = (double)pref[2 * i + 1];
@@ -423,7 +424,7 @@ static void pref_of(const float *pos, const float *pref, const float *goals, flo
 }
 
 int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, const float *pref,
-            const float *goals, float prefSpeed, const float origin[2], const int32_t dims[2],
+            const float *goals, float prefSpeed, const or_agents *ag, const float origin[2], const int32_t dims[2],
             int64_t m, const int64_t *agents, double *vnew, double *pnew, uint8_t *flags,
             double *delta, int32_t *nbr, int32_t *cnt) {
     if (!params_ok(p) || n < 0 || (n > 0 && (!pos || !vel || (!pref && !goals)))) return -1;
@@ -431,7 +432,6 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, c
     if (m < 0) return -1;
     const int32_t k = p->maxNeighbors;
     const double nd2 = (double)p->neighborDist * (double)p->neighborDist;
-    const double maxSpeed = (double)p->maxSpeed;
     bins_t b;
     if (bins_build(&b, n, pos, origin, p->neighborDist, dims) != 0) return -1;
     cand_t *cand = (cand_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(cand_t));
@@ -447,17 +447,21 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, c
         /* 1. observe: neighbours through the bins */
         const int32_t c = neighbors_of(&b, n, pos, i, nd2, k, cand, nb);
         uint32_t diag = 0;
+        /* per-person radius and maximum speed, else the global ones */
+        const float ri = (ag && ag->radius) ? ag->radius[i] : p->radius;
+        const double maxSpeed = (double)((ag && ag->maxSpeed) ? ag->maxSpeed[i] : p->maxSpeed);
         /* 2. one ORCA half-plane per neighbour, nearest first (Fig. 1) */
         for (int32_t a = 0; a < c; ++a) {
             const int64_t j = nb[a];
-            int br = or_orca_line(pos + 2 * i, vel + 2 * i, pos + 2 * j, vel + 2 * j, i, j, p->radius,
+            const float rj = (ag && ag->radius) ? ag->radius[j] : p->radius;
+            int br = or_orca_line(pos + 2 * i, vel + 2 * i, pos + 2 * j, vel + 2 * j, i, j, ri, rj,
                                   p->timeHorizon, p->timeStep, &L[a]);
             if (br & 16) diag |= OR_FLAG_G1_COINCIDENT;
         }
         /* 3. LP: closest permitted velocity to the preferred one, else least
          *    penetration */
         double pv[2], v[2];
-        pref_of(pos, pref, goals, prefSpeed, i, pv);
+        pref_of(pos, pref, goals, prefSpeed, ag, i, pv);
         int infeasible = solve_agent(L, c, maxSpeed, pv, v, &diag);
         double dl = or_penetration(L, c, v);
         if (infeasible) {
@@ -492,7 +496,7 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, c
 }
 
 int64_t or_run(const or_params *p, int64_t n, float *pos, float *vel, const float *pref,
-               const float *goals, float prefSpeed, int32_t nsteps) {
+               const float *goals, float prefSpeed, const or_agents *ag, int32_t nsteps) {
     if (!params_ok(p) || n < 0 || nsteps < 0) return -1;
     float origin[2];
     int32_t dims[2];
@@ -502,7 +506,7 @@ int64_t or_run(const or_params *p, int64_t n, float *pos, float *vel, const floa
     uint8_t *fl = (uint8_t *)malloc((size_t)(n > 0 ? n : 1));
     int64_t infeasible = 0;
     for (int32_t s = 0; s < nsteps; ++s) {
-        if (or_step(p, n, pos, vel, pref, goals, prefSpeed, origin, dims, 0, NULL, vn, pn, fl, NULL,
+        if (or_step(p, n, pos, vel, pref, goals, prefSpeed, ag, origin, dims, 0, NULL, vn, pn, fl, NULL,
                     NULL, NULL) != 0) {
             infeasible = -1;
             break;

@@ -45,6 +45,16 @@ typedef struct {
     float maxSpeed;       /* m/s          ("capped maximum speed") */
 } or_params;
 
+/* Optional per-agent properties (P:128 heterogeneous crowds: "radius 0.5 m, 0.75 m or 1 m
+ * ... desired speed of 1 m/s, 1.33 m/s or 2 m/s ... maximum speed ... 125% of the desired
+ * speed").  Each array is float[n] by id, or NULL for the global value of or_params
+ * (radius, maxSpeed) / the prefSpeed argument. */
+typedef struct {
+    const float *radius;
+    const float *maxSpeed;
+    const float *prefSpeed;
+} or_agents;
+
 /* Per-agent diagnostic flags written by or_step. */
 #define OR_FLAG_INFEASIBLE 0x01u /* LP2 failed, LP3 (least penetration) used */
 #define OR_FLAG_G1_COINCIDENT 0x02u /* collision branch with w == 0 (reading Q15) */
@@ -82,12 +92,12 @@ void or_neighbors(int64_t n, const float *pos, const float origin[2], float cs,
 
 /* ---- ORCA half-plane (Fig. 1(b)-(c)) ------------------------------------ */
 
-/* Line ORCA_{i|j} for agent i against neighbour j with combined radius R = 2r.
+/* Line ORCA_{i|j} for agent i against neighbour j with combined radius R = ri + rj.
  * Returns a bitmask: 1 = collision branch, 2 = cutoff branch, 4 = left leg, 8 = right
  * leg, 16 = degenerate (coincident with w == 0).  Pin: closed forms (head-on, crossing,
  * cutoff, collision), reciprocity, VO-boundary tightness, pairwise no-collision. */
 int or_orca_line(const float pi[2], const float vi[2], const float pj[2], const float vj[2],
-                 int64_t idi, int64_t idj, float radius, float tau, float dt, or_line *out);
+                 int64_t idi, int64_t idj, float ri, float rj, float tau, float dt, or_line *out);
 
 /* ---- LP (Seidel incremental) ------------------------------------ */
 
@@ -116,7 +126,8 @@ double or_penetration(const or_line *lines, int n, const double v[2]);
  *   vnew[2m], pnew[2m] (fp64), flags[m], delta[m] (max penetration at vnew),
  *   nbr[m*k] / cnt[m] (nullable).  Returns 0 or -1 on bad arguments. */
 int or_step(const or_params *p, int64_t n, const float *pos, const float *vel,
-            const float *pref, const float *goals, float prefSpeed, const float origin[2],
+            const float *pref, const float *goals, float prefSpeed, const or_agents *ag,
+            const float origin[2],
             const int32_t dims[2], int64_t m, const int64_t *agents, double *vnew,
             double *pnew, uint8_t *flags, double *delta, int32_t *nbr, int32_t *cnt);
 
@@ -125,7 +136,7 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel,
  * the initial positions (frozen, reading Q12).  Returns the number of infeasible
  * agent-steps, or -1 on bad arguments. */
 int64_t or_run(const or_params *p, int64_t n, float *pos, float *vel, const float *pref,
-               const float *goals, float prefSpeed, int32_t nsteps);
+               const float *goals, float prefSpeed, const or_agents *ag, int32_t nsteps);
 
 #ifdef __cplusplus
 }

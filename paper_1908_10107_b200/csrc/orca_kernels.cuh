@@ -796,6 +796,9 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 }
                 int nb = 0;
                 for (int q = 0; q < 3; ++q) {
+                    // reconverge between the column runs (first pass of the first mode:
+                    // every active lane comes here exactly three times)
+                    if (pass == 0 && mode == ((KR > 0) ? 0 : 1)) __syncwarp(activeMask);
                     const int col = (q == 0) ? cx : (q == 1 ? cx - 1 : cx + 1);  // own column first
                     if (col < cl || col > cr) continue;
                     const int b = (int)a.binStart[(col - a.g.e0) * nyS + lo];
@@ -876,6 +879,9 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         }
         if (!DRY) a.rk2W[ws] = fk;  // next step's search bound (read back by k_lp3 for queued agents)
 
+        // Reconvergence points: each phase below runs exactly once per active lane, so the
+        // warp re-forms here after the data-dependent selection (r01l).
+        __syncwarp(activeMask);
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
         // (half-plane q overwrites list slot q in place: j is read before the write)
         for (int q = 0; q < cnt; ++q) {
@@ -893,6 +899,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             L.s[q * T] = s;
         }
 
+        __syncwarp(activeMask);
         // ---- 4. LP2, LP3 on failure ------------------------------------------
         float px, py;
         if (a.m.goals) {  // toward the goal at walking speed (reading Q16)
@@ -928,6 +935,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 for (int q2 = cnt; q2 < k; ++q2) a.dbgNbr[(size_t)idi * k + q2] = -1;
         }
 
+        __syncwarp(activeMask);
         // ---- 5. integrate (explicit Euler) + next step's binning ----------------------
         if (deferred) {
             // finished by k_lp3

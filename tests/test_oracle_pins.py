@@ -432,3 +432,65 @@ def test_degenerate_rate_small(oracle):
     p = _params(oracle)
     r = oracle.step(p, w["pos"], w["vel"], pref=w["pref"])
     assert np.count_nonzero(r["flags"] & oracle.FLAG_DEGENERATE) <= 4
+
+
+# ------------------------------------------- heterogeneous agents (§8(f2))
+def test_head_on_unequal_radii_closed_form(oracle):
+    """The head-on closed form depends on R = r_a + r_b only (Fig. 1(a)): unequal radii give
+    the same v* as equal radii with the same sum."""
+    d, v, tau = 5.0, 1.0, 10.0
+    for ra, rb in [(0.5, 1.0), (0.75, 0.25), (1.0, 1.0)]:
+        R = ra + rb
+        la, _ = oracle.orca_line([-d, 0], [v, 0], [d, 0], [-v, 0], 0, 1, ra, tau, 0.25, rj=rb)
+        lb, _ = oracle.orca_line([d, 0], [-v, 0], [-d, 0], [v, 0], 1, 0, rb, tau, 0.25, rj=ra)
+        va, _, _ = oracle.solve([la], 5.0, [v, 0])
+        vb, _, _ = oracle.solve([lb], 5.0, [-v, 0])
+        exp = np.array([v * (1 - R * R / (4 * d * d)), -v * R * math.sqrt(4 * d * d - R * R) / (4 * d * d)])
+        assert np.allclose(va, exp, atol=1e-6) and np.allclose(vb, -exp, atol=1e-6)
+
+
+def test_unequal_radii_reciprocity_and_no_collision(oracle):
+    rng = np.random.default_rng(31)
+    viol = 0
+    for pi, vi, pj, vj in _random_pairs(rng, 2000):
+        ra, rb = rng.choice([0.5, 0.75, 1.0], 2)
+        rel_p = pj.astype(np.float64) - pi.astype(np.float64)
+        la, _ = oracle.orca_line(pi, vi, pj, vj, 0, 1, ra, 5.0, 0.25, rj=rb)
+        lb, _ = oracle.orca_line(pj, vj, pi, vi, 1, 0, rb, 5.0, 0.25, rj=ra)
+        ua = 2 * (np.array(la[:2]) - vi.astype(np.float64))
+        ub = 2 * (np.array(lb[:2]) - vj.astype(np.float64))
+        assert np.allclose(ua, -ub, atol=1e-12)
+        if np.hypot(*rel_p) <= ra + rb:
+            continue
+        va, _, _ = oracle.solve([la], 50.0, rng.uniform(-2, 2, 2))
+        vb, _, _ = oracle.solve([lb], 50.0, rng.uniform(-2, 2, 2))
+        dv = vb - va
+        dd = float(dv @ dv)
+        t = 0.0 if dd == 0 else min(max(-float(rel_p @ dv) / dd, 0.0), 5.0)
+        viol += np.hypot(*(rel_p + t * dv)) - (ra + rb) < -1e-9
+    assert viol == 0
+
+
+def test_heterogeneous_step_invariants(oracle):
+    """Per-agent maxSpeed caps every velocity; lines use r_i + r_j; per-agent desired speed
+    with goals (max = 125 % of desired)."""
+    w = W.make("uniform", n=2000, rho=0.15)
+    rng = np.random.default_rng(5)
+    radius = rng.choice([0.5, 0.75, 1.0], 2000).astype(np.float32)
+    desired = rng.choice([1.0, 1.33, 2.0], 2000).astype(np.float32)
+    props = dict(radius=radius, maxSpeed=(1.25 * desired).astype(np.float32), prefSpeed=desired)
+    goals = (w["pos"] + rng.uniform(-50, 50, w["pos"].shape)).astype(np.float32)
+    p = _params(oracle)
+    r = oracle.step(p, w["pos"], w["vel"], goals=goals, props=props, want_nbrs=True)
+    sp = np.hypot(*r["vel"].T)
+    assert np.all(sp <= props["maxSpeed"].astype(np.float64) + 1e-9)
+    for i in range(0, 2000, 13):
+        lines = [oracle.orca_line(w["pos"][i], w["vel"][i], w["pos"][j], w["vel"][j], i, j, radius[i],
+                                  p.timeHorizon, p.timeStep, rj=radius[j])[0] for j in r["nbr"][i][:r["cnt"][i]]]
+        pen = pins.penetration_np(lines, r["vel"][i]) if lines else 0.0
+        if not r["flags"][i] & oracle.FLAG_INFEASIBLE:
+            assert pen <= 1e-9
+            g = goals[i].astype(np.float64) - w["pos"][i]
+            pref = g * min(1.0, desired[i] / np.hypot(*g))
+            ref = pins.lp_vertex_enumeration(lines, float(props["maxSpeed"][i]), pref)
+            assert ref is not None and np.allclose(r["vel"][i], ref, atol=1e-9)
