@@ -137,10 +137,11 @@ size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 orca_status ex_alloc(ExAlloc& x, int capM, int capH) {
     if (x.base && x.b.capM == capM && x.b.capH == capH) return ORCA_OK;  // layouts must match exactly
     dfree(x.base);
-    size_t sz[9] = {16, (size_t)capM * 8, (size_t)capM * 8, (size_t)capM * 8, (size_t)capM * 4,
-                    (size_t)capM * 4, (size_t)capH * 8, (size_t)capH * 8, (size_t)capH * 4};
-    size_t off[9], o = 0;
-    for (int q = 0; q < 9; ++q) {
+    size_t sz[11] = {16, (size_t)capM * 8, (size_t)capM * 8, (size_t)capM * 8, (size_t)capM * 4,
+                     (size_t)capM * 4, (size_t)capH * 8, (size_t)capH * 8, (size_t)capH * 4,
+                     (size_t)capM * 16, (size_t)capH * 4};
+    size_t off[11], o = 0;
+    for (int q = 0; q < 11; ++q) {
         off[q] = o;
         o = align16(o + sz[q]);
     }
@@ -157,6 +158,8 @@ orca_status ex_alloc(ExAlloc& x, int capM, int capH) {
     x.b.hpos = (float2*)(p + off[6]);
     x.b.hvel = (float2*)(p + off[7]);
     x.b.hid = (uint32_t*)(p + off[8]);
+    x.b.mprop = (float4*)(p + off[9]);
+    x.b.hrad = (float*)(p + off[10]);
     x.b.capM = capM;
     x.b.capH = capH;
     return ORCA_OK;
@@ -170,6 +173,8 @@ struct Domain {
     int capW = 0;
     float2 *posS = nullptr, *velS = nullptr, *auxS = nullptr, *posW = nullptr, *velW = nullptr, *auxW = nullptr;
     float *rk2S = nullptr, *rk2W = nullptr;
+    float4 *propS = nullptr, *propW = nullptr;  // heterogeneous crowds only
+    int propCap = 0;
     uint32_t *idS = nullptr, *idW = nullptr, *cellW = nullptr, *rankW = nullptr;
     uint32_t *count = nullptr, *binStart = nullptr;
     unsigned long long* scanStatus = nullptr;  // look-back status + ticket + LP3 queue count
@@ -186,6 +191,8 @@ struct Domain {
         for (auto p : u4) dfree(*p);
         dfree(rk2S);
         dfree(rk2W);
+        dfree(propS);
+        dfree(propW);
         dfree(scanStatus);
         dfree(qEntry);
         dfree(qLines);
@@ -204,6 +211,10 @@ struct orca_ctx {
     bool ready = false, goals = false;
     float prefSpeed = 0.0f;
     float removeR = 0.0f;  // > 0: agents within removeR of their goal leave
+    bool het = false;      // per-agent radius / maxSpeed / prefSpeed set
+    float maxSpeedAll = 0.0f;
+    float4* props4 = nullptr;  // id-ordered staging of the per-agent properties
+    int64_t props4Cap = 0;
     int world = 1;  // strips in the whole decomposition
     int rank = 0;   // NCCL rank (= the strip held by this context)
     bool loopback = false;
@@ -251,6 +262,7 @@ Model make_model(const orca_ctx* c) {
     m.goals = c->goals ? 1 : 0;
     m.prefSpeed = c->prefSpeed;
     m.removeR2 = (c->goals && c->removeR > 0.0f) ? c->removeR * c->removeR : 0.0f;
+    m.maxSpeedAll = c->het ? std::max(c->maxSpeedAll, p.maxSpeed) : p.maxSpeed;
     return m;
 }
 
@@ -268,6 +280,8 @@ StepArgs make_args(orca_ctx* c, Domain& d) {
     a.velW = d.velW;
     a.auxW = d.auxW;
     a.rk2W = d.rk2W;
+    a.propS = c->het ? d.propS : nullptr;
+    a.propW = c->het ? d.propW : nullptr;
     a.idW = d.idW;
     a.cellW = d.cellW;
     a.rankW = d.rankW;
@@ -342,9 +356,9 @@ template <bool DRY>
 void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
     const int k = c->p.maxNeighbors;
-    if (c->variant == 1)
+    if (c->variant == 1 && !c->het)  // (the group kernel is homogeneous-only)
         k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
-    else if (c->variant == 0 || k < 1 || k > 16)  // shared-memory top-k list (any k)
+    else if (c->variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
         k_step<DRY, 0><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
     else if (k <= 10)  // register top-k list
         k_step<DRY, 10><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
@@ -365,7 +379,8 @@ cudaError_t enqueue_scan(orca_ctx* c, Domain& d) {
 cudaError_t enqueue_scatter(orca_ctx* c, Domain& d) {
     k_scatter<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.ctr, d.cellW, d.rankW, d.binStart, d.posW, d.velW,
                                                               d.auxW, d.idW, d.rk2W, d.posS, d.velS, d.auxS, d.idS,
-                                                              d.rk2S, d.capW);
+                                                              d.rk2S, d.capW, c->het ? d.propW : nullptr,
+                                                              c->het ? d.propS : nullptr);
     return cudaGetLastError();
 }
 
@@ -668,6 +683,7 @@ void orca_destroy(orca_ctx* c) {
     dfree(c->outB);
     dfree(c->partial);
     dfree(c->colHist);
+    dfree(c->props4);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
@@ -684,6 +700,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     drop_graph(c);
     c->ready = false;
     c->goals = false;
+    c->het = false;
     // stage the global inputs (every rank of a decomposition gets the same arrays)
     if (n > c->stageCap) {
         dfree(c->stage);
@@ -1086,6 +1103,68 @@ orca_status orca_reset_stats(orca_ctx* c) {
     CK(cudaStreamSynchronize(c->stream));
     c->host_steps = 0;
     c->host_updates = 0;
+    return ORCA_OK;
+}
+
+orca_status orca_set_agent_props(orca_ctx* c, const float* radius, const float* maxSpeed, const float* prefSpeed) {
+    if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    const int64_t n = c->nGlobal;
+    drop_graph(c);
+    if (!radius && !maxSpeed && !prefSpeed) {  // back to the global parameters
+        c->het = false;
+        return ORCA_OK;
+    }
+    if (n == 0) return ORCA_OK;
+    // stage the three arrays (NULL -> global value) as float4 by id in the input stage
+    float* st = reinterpret_cast<float*>(c->stage);  // >= 6n floats
+    const float* src[3] = {radius, maxSpeed, prefSpeed};
+    // prefSpeed -1: use the orca_set_goals speed
+    const float def[3] = {c->p.radius, c->p.maxSpeed, -1.0f};
+    for (int q = 0; q < 3; ++q) {
+        if (src[q])
+            CK(cudaMemcpyAsync(st + q * n, src[q], (size_t)n * sizeof(float), cudaMemcpyDefault, c->stream));
+        else
+            k_fill1<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, st + q * n, def[q]);
+    }
+    if (c->props4Cap < n) {
+        dfree(c->props4);
+        CK(cudaMalloc(&c->props4, (size_t)n * sizeof(float4)));
+        c->props4Cap = n;
+    }
+    float4* props = c->props4;
+    const int blocks = std::min(1024, cap_blocks(n, 256));
+    k_pack_props<<<blocks, 256, 0, c->stream>>>((int)n, st, props, c->partial);
+    CK(cudaGetLastError());
+    std::vector<float> h((size_t)blocks * 5);
+    CK(cudaMemcpyAsync(h.data(), c->partial, h.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float vmax = 0.0f;
+    double bad = 0.0;
+    for (int b = 0; b < blocks; ++b) {
+        vmax = std::max(vmax, h[b * 5 + 0]);
+        bad += h[b * 5 + 4];
+    }
+    if (bad > 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "radius must be > 0 and speeds >= 0, finite");
+    if (c->world > 1 && !(vmax * c->p.timeStep < c->p.neighborDist))
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "strips need maxSpeed * timeStep < neighborDist");
+    for (Domain& d : c->doms) {
+        if (d.propCap < d.capW) {
+            dfree(d.propS);
+            dfree(d.propW);
+            CK(cudaMalloc(&d.propS, (size_t)d.capW * sizeof(float4)));
+            CK(cudaMalloc(&d.propW, (size_t)d.capW * sizeof(float4)));
+            d.propCap = d.capW;
+        }
+        k_gather4_by_id<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, (int)d.nbins, d.idS, props,
+                                                                       d.propS);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->het = true;
+    c->maxSpeedAll = vmax;
     return ORCA_OK;
 }
 

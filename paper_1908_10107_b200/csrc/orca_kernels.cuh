@@ -70,6 +70,7 @@ struct Model {
     int goals;                    // 1: aux holds goals, pref = g min(1, s/|g|)
     float prefSpeed;
     float removeR2;               // > 0: remove agents within sqrt(removeR2) of their goal
+    float maxSpeedAll;            // largest maxSpeed of any agent (history search bound)
 };
 
 // ------------------------------------------------------------------ cell (reading Q11)
@@ -124,6 +125,8 @@ struct ExBuf {
     float* mrk2;
     float2 *hpos, *hvel;
     uint32_t* hid;
+    float4* mprop;  // heterogeneous crowds: emigrant (radius, maxSpeed, prefSpeed, 0)
+    float* hrad;    // heterogeneous crowds: halo agent radius
     int capM, capH;
 };
 
@@ -244,7 +247,8 @@ __global__ void k_scatter(const int* __restrict__ ctr, const uint32_t* __restric
                           const float2* __restrict__ posW, const float2* __restrict__ velW,
                           const float2* __restrict__ auxW, const uint32_t* __restrict__ idW,
                           const float* __restrict__ rk2W, float2* __restrict__ posS, float2* __restrict__ velS,
-                          float2* __restrict__ auxS, uint32_t* __restrict__ idS, float* __restrict__ rk2S, int capW) {
+                          float2* __restrict__ auxS, uint32_t* __restrict__ idS, float* __restrict__ rk2S, int capW,
+                          const float4* __restrict__ propW, float4* __restrict__ propS) {
     const int n = min(ctr[CT_NOWN] + ctr[CT_EXTRA], capW);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t c = cell[i];
@@ -255,6 +259,7 @@ __global__ void k_scatter(const int* __restrict__ ctr, const uint32_t* __restric
         auxS[dst] = auxW[i];
         idS[dst] = idW[i];
         rk2S[dst] = rk2W[i];
+        if (propW) propS[dst] = propW[i];
     }
 }
 
@@ -263,8 +268,8 @@ __global__ void k_scatter(const int* __restrict__ ctr, const uint32_t* __restric
 // oracle's expression trees; geometry in fp32 Hessian form.  Returns flag bits
 // (FL_G1) and sets *collision.
 __device__ __forceinline__ uint32_t orca_line(float xi, float yi, float vxi, float vyi, float xj, float yj,
-                                              float vxj, float vyj, uint32_t idi, uint32_t idj, const Model& m,
-                                              float& nx, float& ny, float& s, int& collision) {
+                                              float vxj, float vyj, uint32_t idi, uint32_t idj, float R, double R2D,
+                                              const Model& m, float& nx, float& ny, float& s, int& collision) {
     const double rpx = __dsub_rn((double)xj, (double)xi);
     const double rpy = __dsub_rn((double)yj, (double)yi);
     const double rvx = __dsub_rn((double)vxi, (double)vxj);
@@ -272,30 +277,30 @@ __device__ __forceinline__ uint32_t orca_line(float xi, float yi, float vxi, flo
     const double d2 = __dadd_rn(__dmul_rn(rpx, rpx), __dmul_rn(rpy, rpy));
     uint32_t fl = 0;
     collision = 0;
-    if (d2 > m.R2D) {
+    if (d2 > R2D) {
         const double wx = __dsub_rn(rvx, __dmul_rn(m.invTauD, rpx));
         const double wy = __dsub_rn(rvy, __dmul_rn(m.invTauD, rpy));
         const double wl2 = __dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy));
         const double dot1 = __dadd_rn(__dmul_rn(wx, rpx), __dmul_rn(wy, rpy));
-        if (dot1 < 0.0 && __dmul_rn(dot1, dot1) > __dmul_rn(m.R2D, wl2)) {
+        if (dot1 < 0.0 && __dmul_rn(dot1, dot1) > __dmul_rn(R2D, wl2)) {
             // cut-off circle: n = w/|w|, s = n.v_i + (R/tau - |w|)/2
             const float wl = sqrtf((float)wl2);
             const float inv = 1.0f / wl;
             nx = (float)wx * inv;
             ny = (float)wy * inv;
-            s = fmaf(nx, vxi, ny * vyi) + 0.5f * (m.R * m.invTauF - wl);
+            s = fmaf(nx, vxi, ny * vyi) + 0.5f * (R * m.invTauF - wl);
         } else {
             // legs: s = n.(v_i + v_j)/2 since n is orthogonal to the leg direction
-            const float leg = sqrtf((float)__dsub_rn(d2, m.R2D));
+            const float leg = sqrtf((float)__dsub_rn(d2, R2D));
             const float px = (float)rpx, py = (float)rpy;
             const float invd2 = 1.0f / (float)d2;
             const double detw = __dsub_rn(__dmul_rn(rpx, wy), __dmul_rn(rpy, wx));
             if (detw > 0.0) {  // left leg
-                nx = -(px * m.R + py * leg) * invd2;
-                ny = (px * leg - py * m.R) * invd2;
+                nx = -(px * R + py * leg) * invd2;
+                ny = (px * leg - py * R) * invd2;
             } else {  // right leg (ties -> right, reading Q5)
-                nx = (py * leg - px * m.R) * invd2;
-                ny = -(px * leg + py * m.R) * invd2;
+                nx = (py * leg - px * R) * invd2;
+                ny = -(px * leg + py * R) * invd2;
             }
             s = 0.5f * fmaf(nx, vxi + vxj, ny * (vyi + vyj));
         }
@@ -317,7 +322,7 @@ __device__ __forceinline__ uint32_t orca_line(float xi, float yi, float vxi, flo
             nx = (float)wx * inv;
             ny = (float)wy * inv;
         }
-        s = fmaf(nx, vxi, ny * vyi) + 0.5f * (m.R * m.invDtF - wl);
+        s = fmaf(nx, vxi, ny * vyi) + 0.5f * (R * m.invDtF - wl);
     }
     return fl;
 }
@@ -448,6 +453,8 @@ struct StepArgs {
     const float2* __restrict__ velS;
     const float2* __restrict__ auxS;  // prefVel, or goal when m.goals
     const float* __restrict__ rk2S;   // previous step's fp32 d2 of the k-th neighbour (+inf: none)
+    const float4* __restrict__ propS; // heterogeneous crowds: (radius, maxSpeed, prefSpeed, 0);
+                                      // nullptr = the global parameters
     const uint32_t* __restrict__ idS;
     const uint32_t* __restrict__ binStart;
     // outputs of a real step (work buffers, next step's binning)
@@ -455,6 +462,7 @@ struct StepArgs {
     float2* velW;
     float2* auxW;
     float* rk2W;
+    float4* propW;
     uint32_t* idW;
     uint32_t* cellW;
     uint32_t* rankW;
@@ -606,7 +614,7 @@ __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int 
 }
 
 // ---------------------------------------------------------- integrate + route
-__device__ __forceinline__ void push_halo(const ExBuf& x, int* ctr, float2 p, float2 v, uint32_t id) {
+__device__ __forceinline__ void push_halo(const ExBuf& x, int* ctr, float2 p, float2 v, uint32_t id, float r) {
     const int s = atomicAdd(&x.hdr[1], 1);
     if (s >= x.capH) {
         atomicOr(&ctr[CT_OVF], OVF_HALO);
@@ -615,11 +623,12 @@ __device__ __forceinline__ void push_halo(const ExBuf& x, int* ctr, float2 p, fl
     x.hpos[s] = p;
     x.hvel[s] = v;
     x.hid[s] = id;
+    x.hrad[s] = r;
 }
 
 // Append one entry to the work buffers at nOwn + extra (ghosts, immigrants).
 __device__ __forceinline__ void append_work(const StepArgs& a, int nOwn, int cx, int sy, float2 p, float2 v, float2 aux,
-                                            uint32_t id, float rk2) {
+                                            uint32_t id, float rk2, float4 pr) {
     const int e = nOwn + atomicAdd(&a.ctr[CT_EXTRA], 1);
     if (e >= a.capW) {
         atomicOr(&a.ctr[CT_OVF], OVF_WORK);
@@ -631,6 +640,7 @@ __device__ __forceinline__ void append_work(const StepArgs& a, int nOwn, int cx,
     a.auxW[e] = aux;
     a.idW[e] = id;
     a.rk2W[e] = rk2;
+    if (a.propW) a.propW[e] = pr;
     a.cellW[e] = c;
     a.rankW[e] = atomicAdd(&a.count[c], 1u);
 }
@@ -638,9 +648,10 @@ __device__ __forceinline__ void append_work(const StepArgs& a, int nOwn, int cx,
 // Explicit Euler p' = p + dt v' and routing for the next step: the agent
 // stays in this strip (bin + rank at its work slot w; a halo copy to the neighbour if it
 // sits in an edge column), or emigrates (exchange buffer, plus a local ghost entry since
-// it now sits in this strip's ghost column).  Single-GPU: always stays.
+// it now sits in this strip's ghost column).  Single-GPU: always stays.  pr: the agent's
+// (radius, maxSpeed, prefSpeed, 0) when heterogeneous.
 __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn, float2 pi, float vx, float vy,
-                                             float2 aux, uint32_t id, float rk2) {
+                                             float2 aux, uint32_t id, float rk2, float4 pr) {
     const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
     const float2 vn = make_float2(vx, vy);
     if (a.m.removeR2 > 0.0f) {
@@ -662,10 +673,11 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
         a.auxW[w] = aux;
         a.idW[w] = id;
         a.rk2W[w] = rk2;
+        if (a.propW) a.propW[w] = pr;
         a.cellW[w] = c;
         a.rankW[w] = atomicAdd(&a.count[c], 1u);
-        if (cx == a.g.c0 && a.g.hasL) push_halo(a.sendL, a.ctr, pn, vn, id);
-        if (cx == a.g.c1 - 1 && a.g.hasR) push_halo(a.sendR, a.ctr, pn, vn, id);
+        if (cx == a.g.c0 && a.g.hasL) push_halo(a.sendL, a.ctr, pn, vn, id, pr.x);
+        if (cx == a.g.c1 - 1 && a.g.hasR) push_halo(a.sendR, a.ctr, pn, vn, id, pr.x);
     } else {
         a.cellW[w] = kInvalid;
         const ExBuf& x = (cx < a.g.c0) ? a.sendL : a.sendR;
@@ -678,11 +690,20 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
             x.maux[s] = aux;
             x.mid[s] = id;
             x.mrk2[s] = rk2;
+            x.mprop[s] = pr;
         }
-        append_work(a, nOwn, cx, sy, pn, vn, aux, id, INFINITY);
+        append_work(a, nOwn, cx, sy, pn, vn, aux, id, INFINITY, pr);
     }
 }
 
+// warp reconvergence points in k_step: after the column scans (COLS) and
+// at the once-per-agent phase boundaries (PHASES); the one before the final merge is always on
+#ifndef ORCA_SYNC_COLS
+#define ORCA_SYNC_COLS 0
+#endif
+#ifndef ORCA_SYNC_PHASES
+#define ORCA_SYNC_PHASES 1
+#endif
 #ifndef ORCA_STEP_MINBLOCKS
 #define ORCA_STEP_MINBLOCKS 7  // resident blocks per SM the register budget is sized for (swept: 6/7/8)
 #endif
@@ -719,6 +740,11 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         const float2 vi = a.velS[i];
         const float2 aux = a.auxS[i];
         const uint32_t idi = a.idS[i];
+        // per-agent (radius, maxSpeed, prefSpeed) of heterogeneous crowds
+        const bool het = a.propS != nullptr;
+        const float4 pr = het ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
+        const float ri = pr.x, vmaxi = pr.y, vprefi = (pr.z >= 0.0f) ? pr.z : a.m.prefSpeed;
+        (void)ri;
         const int cx = cell_coord(pi.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
         const int lgS = a.g.lgS;
         const int nyS = a.g.ny << lgS;
@@ -744,7 +770,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             bool guessed = false;
             const float rk2p = a.rk2S[i];
             if (rk2p < a.m.nd2Fup) {
-                const float marg = 2.0002f * a.m.maxSpeed * a.m.dt + 4e-7f * (fabsf(pi.x) + fabsf(pi.y)) + 1e-5f;
+                const float marg = 2.0002f * a.m.maxSpeedAll * a.m.dt + 4e-7f * (fabsf(pi.x) + fabsf(pi.y)) + 1e-5f;
                 const float r = sqrtf(rk2p) * (1.0f + 1e-5f) + marg;
                 const float b = r * r * (1.0f + 1e-3f);
                 if (b < thr) {
@@ -798,7 +824,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 for (int q = 0; q < 3; ++q) {
                     // reconverge between the column runs (first pass of the first mode:
                     // every active lane comes here exactly three times)
-                    if (pass == 0 && mode == ((KR > 0) ? 0 : 1)) __syncwarp(activeMask);
+                    if (ORCA_SYNC_COLS && pass == 0 && mode == ((KR > 0) ? 0 : 1)) __syncwarp(activeMask);
                     const int col = (q == 0) ? cx : (q == 1 ? cx - 1 : cx + 1);  // own column first
                     if (col < cl || col > cr) continue;
                     const int b = (int)a.binStart[(col - a.g.e0) * nyS + lo];
@@ -881,7 +907,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
 
         // Reconvergence points: each phase below runs exactly once per active lane, so the
         // warp re-forms here after the data-dependent selection (r01l).
-        __syncwarp(activeMask);
+        if (ORCA_SYNC_PHASES) __syncwarp(activeMask);
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
         // (half-plane q overwrites list slot q in place: j is read before the write)
         for (int q = 0; q < cnt; ++q) {
@@ -892,20 +918,28 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             if (DRY && a.dbgNbr) a.dbgNbr[(size_t)idi * k + q] = (int32_t)idj;
             float nx, ny, s;
             int coll;
-            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, idj, a.m, nx, ny, s, coll);
+            // combined radius R = r_i + r_j (Fig. 1(a)); per agent when heterogeneous
+            float Rp = a.m.R;
+            double R2p = a.m.R2D;
+            if (het) {
+                const double Rd = (double)ri + (double)a.propS[j].x;
+                R2p = Rd * Rd;
+                Rp = (float)Rd;
+            }
+            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, idj, Rp, R2p, a.m, nx, ny, s, coll);
             nColl += coll;
             L.nx[q * T] = nx;
             L.ny[q * T] = ny;
             L.s[q * T] = s;
         }
 
-        __syncwarp(activeMask);
+        if (ORCA_SYNC_PHASES) __syncwarp(activeMask);
         // ---- 4. LP2, LP3 on failure ------------------------------------------
         float px, py;
         if (a.m.goals) {  // toward the goal at walking speed (reading Q16)
             const float gx = aux.x - pi.x, gy = aux.y - pi.y;
             const float gl = sqrtf(fmaf(gx, gx, gy * gy));
-            const float sc = (gl > a.m.prefSpeed) ? a.m.prefSpeed / gl : 1.0f;
+            const float sc = (gl > vprefi) ? vprefi / gl : 1.0f;
             px = gx * sc;
             py = gy * sc;
         } else {
@@ -914,7 +948,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         }
         float vx, vy;
         if (CNT) w.lines += (uint32_t)cnt;
-        const int f = lp2<CNT>(L, T, cnt, a.m.maxSpeed, px, py, false, vx, vy, fl, w);
+        const int f = lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
         if (f < cnt) {
             // infeasible: queue the agent with its half-planes and LP2 point; k_lp3
             // runs the least-penetration LP on a compacted set of agents (full warps)
@@ -935,7 +969,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 for (int q2 = cnt; q2 < k; ++q2) a.dbgNbr[(size_t)idi * k + q2] = -1;
         }
 
-        __syncwarp(activeMask);
+        if (ORCA_SYNC_PHASES) __syncwarp(activeMask);
         // ---- 5. integrate (explicit Euler) + next step's binning ----------------------
         if (deferred) {
             // finished by k_lp3
@@ -946,7 +980,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             if (a.dbgNbr)
                 for (int q = cnt; q < k; ++q) a.dbgNbr[(size_t)idi * k + q] = -1;
         } else {
-            finish_agent(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk);
+            finish_agent(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk, pr);
         }
     }
     if (DRY && a.work) {
@@ -1016,7 +1050,8 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
             L.ny[m * T] = l.y;
             L.s[m * T] = l.z;
         }
-        lp3<CNT>(L, P, T, cnt, f, a.m.maxSpeed, vx, vy, fl, w);
+        const float4 pr = a.propS ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
+        lp3<CNT>(L, P, T, cnt, f, pr.y, vx, vy, fl, w);
         float dl = 0.0f;
         for (int m = 0; m < cnt; ++m) dl = fmaxf(dl, L.s[m * T] - fmaf(L.nx[m * T], vx, L.ny[m * T] * vy));
         if (dl > 0.0f && dl < 1e-6f) fl |= FL_G3;
@@ -1026,7 +1061,7 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
             if (a.dbgV) a.dbgV[idi] = make_float2(vx, vy);
             if (a.dbgFlags) a.dbgFlags[idi] = (uint8_t)fl;
         } else {
-            finish_agent(a, i - o0, nOwn, pi, vx, vy, a.auxS[i], idi, a.rk2W[i - o0]);
+            finish_agent(a, i - o0, nOwn, pi, vx, vy, a.auxS[i], idi, a.rk2W[i - o0], pr);
         }
         cInf += 1;
         cDeg += (fl & (FL_G1 | FL_G2)) != 0;
@@ -1085,6 +1120,51 @@ __global__ void k_unpermute(const uint32_t* __restrict__ binStart, Grid g, const
     }
 }
 
+__global__ void k_fill1(int n, float* __restrict__ out, float v) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = v;
+}
+
+// st = radius[n] | maxSpeed[n] | prefSpeed[n] (prefSpeed -1 = the set_goals speed) ->
+// props[i] = (radius, maxSpeed, prefSpeed, 0); partial[b] = {max maxSpeed, -, -, -, invalid}
+__global__ void k_pack_props(int n, const float* __restrict__ st, float4* __restrict__ props,
+                             float* __restrict__ partial) {
+    float vmax = 0.0f;
+    int bad = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float r = st[i], vm = st[n + i], vp = st[2 * n + i];
+        bad += !(isfinite(r) && r > 0.0f && isfinite(vm) && vm >= 0.0f && isfinite(vp) && (vp >= 0.0f || vp == -1.0f));
+        vmax = fmaxf(vmax, vm);
+        props[i] = make_float4(r, vm, vp, 0.0f);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    __shared__ float s[32][2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        s[wid][0] = vmax;
+        s[wid][1] = (float)bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.0f, b = 0.0f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            m = fmaxf(m, s[w][0]);
+            b += s[w][1];
+        }
+        partial[blockIdx.x * 5 + 0] = m;
+        partial[blockIdx.x * 5 + 4] = b;
+    }
+}
+
+// out[i] = in[idS[i]] over all sorted entries (owned + ghosts)
+__global__ void k_gather4_by_id(const uint32_t* __restrict__ binStart, int nbins, const uint32_t* __restrict__ idS,
+                                const float4* __restrict__ in, float4* __restrict__ out) {
+    const int n = (int)binStart[nbins];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[idS[i]];
+}
+
 __global__ void k_fill2(int n, float2* __restrict__ out, float v) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = make_float2(v, v);
 }
@@ -1139,9 +1219,10 @@ __global__ void k_receive(StepArgs a, ExBuf rL, ExBuf rR) {
         const int cx = cell_coord(p.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
         const int sy = subrow_coord(p.y, a.g);
         if (mig)
-            append_work(a, nOwn, cx, sy, p, x->mvel[q], x->maux[q], x->mid[q], x->mrk2[q]);
+            append_work(a, nOwn, cx, sy, p, x->mvel[q], x->maux[q], x->mid[q], x->mrk2[q], x->mprop[q]);
         else
-            append_work(a, nOwn, cx, sy, p, x->hvel[q], make_float2(0.0f, 0.0f), x->hid[q], INFINITY);
+            append_work(a, nOwn, cx, sy, p, x->hvel[q], make_float2(0.0f, 0.0f), x->hid[q], INFINITY,
+                        make_float4(x->hrad[q], 0.0f, 0.0f, 0.0f));
     }
 }
 

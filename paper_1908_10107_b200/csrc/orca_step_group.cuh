@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
             bool guessed = false;
             const float rk2p = a.rk2S[i];
             if (rk2p < a.m.nd2Fup) {
-                const float marg = 2.0002f * a.m.maxSpeed * a.m.dt + 4e-7f * (fabsf(pi.x) + fabsf(pi.y)) + 1e-5f;
+                const float marg = 2.0002f * a.m.maxSpeedAll * a.m.dt + 4e-7f * (fabsf(pi.x) + fabsf(pi.y)) + 1e-5f;
                 const float r = sqrtf(rk2p) * (1.0f + 1e-5f) + marg;
                 const float b = r * r * (1.0f + 1e-3f);
                 if (b < thr) {
@@ -309,7 +309,8 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
             if (DRY && a.dbgNbr) a.dbgNbr[(size_t)idi * k + q] = (int32_t)idj;
             float nx, ny, s;
             int coll;
-            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, idj, a.m, nx, ny, s, coll);
+            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, idj, a.m.R, a.m.R2D, a.m, nx, ny,
+                            s, coll);  // homogeneous only (heterogeneous crowds run variant 0)
             nColl += coll;
             Lnx[q] = nx;
             Lny[q] = ny;
@@ -355,7 +356,8 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
             if (a.dbgNbr)
                 for (int q = cnt + G.gl; q < k; q += kG) a.dbgNbr[(size_t)idi * k + q] = -1;
         } else if (!deferred && G.gl == 0) {
-            finish_agent(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk);
+            finish_agent(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk,
+                         make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f));
         }
     }
     // ---- counters: one lane per agent counts ---------------------------------------------
