@@ -118,6 +118,17 @@ orca_status orca_set_goals(orca_ctx *ctx, const float *goal, float prefSpeed);
  * ended).  radius 0 disables.  Persists across orca_set_agents.  Errors: INVALID_ARGUMENT. */
 orca_status orca_set_goal_removal(orca_ctx *ctx, float radius);
 
+/* Heterogeneous crowds ("an equal chance of being of radius 0.5 m, 0.75 m or 1 m ...
+ * desired speed of 1 m/s, 1.33 m/s or 2 m/s. The maximum speed is adjusted to be 125% of
+ * the desired speed"): per-agent radius, maxSpeed and prefSpeed, float[n] by id, each
+ * nullable (NULL -> the global radius / maxSpeed / the orca_set_goals speed).  A pair uses
+ * R = r_i + r_j; agent i's LP uses its own maxSpeed; with goals its preferred speed is its
+ * own.  All three NULL returns to the global parameters.  Call after orca_set_agents (which
+ * clears them).  The cell size stays neighborDist.  Errors: NOT_READY, INVALID_ARGUMENT
+ * (radius <= 0, negative speed, NaN/Inf; on strips maxSpeed * timeStep >= neighborDist). */
+orca_status orca_set_agent_props(orca_ctx *ctx, const float *radius, const float *maxSpeed,
+                                 const float *prefSpeed);
+
 /* active uint8[n] by id: 1 while the agent is in the simulation, 0 once removed.
  * Synchronises.  Errors: NOT_READY. */
 orca_status orca_get_active(orca_ctx *ctx, uint8_t *active);

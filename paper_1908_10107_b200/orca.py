@@ -26,7 +26,7 @@ EXPORTS = [
     "orca_reset_stats", "orca_get_stream", "orca_step_timed", "orca_status_string", "orca_last_error",
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
-    "orca_set_goal_removal", "orca_get_active",
+    "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props",
 ]
 
 
@@ -85,6 +85,7 @@ def _load():
         "orca_set_variant": [vp, i32],
         "orca_set_goal_removal": [vp, f32],
         "orca_get_active": [vp, vp],
+        "orca_set_agent_props": [vp, vp, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -266,6 +267,12 @@ class Orca:
 
     def reset_stats(self):
         _check(_lib.orca_reset_stats(self._ctx))
+
+    def set_agent_props(self, radius=None, max_speed=None, pref_speed=None):
+        """Per-agent radius / maxSpeed / prefSpeed (float[n] by id, each optional)."""
+        arrs = [None if a is None else _as_f32(np.asarray(a) if not hasattr(a, "data_ptr") else a)
+                for a in (radius, max_speed, pref_speed)]
+        _check(_lib.orca_set_agent_props(self._ctx, *[_ptr(a) for a in arrs]))
 
     def set_goal_removal(self, radius: float):
         """Remove agents within `radius` of their goal after a step; 0 disables."""

@@ -414,3 +414,61 @@ def test_two_way_crossing_runs(orca):
     st = o.stats()
     assert st["removed"] >= 0.9 * 2500, st
     o.close()
+
+
+# ------------------------------------------ heterogeneous crowds (§8(f2))
+def _het_props(n, seed=5):
+    rng = np.random.default_rng(seed)
+    radius = rng.choice([0.5, 0.75, 1.0], n).astype(np.float32)
+    desired = rng.choice([1.0, 1.33, 2.0], n).astype(np.float32)
+    return dict(radius=radius, maxSpeed=(1.25 * desired).astype(np.float32), prefSpeed=desired)
+
+
+@pytest.mark.parametrize("goals", [False, True])
+def test_heterogeneous_step_parity(orca, oracle, goals):
+    """Per-agent radius (R = r_i + r_j), maxSpeed and desired speed vs the oracle."""
+    w = W.make("uniform", n=4000, rho=0.15)
+    props = _het_props(len(w["pos"]))
+    if goals:
+        rng = np.random.default_rng(8)
+        w = dict(w, goals=(w["pos"] + rng.uniform(-40, 40, w["pos"].shape)).astype(np.float32), pref_speed=1.0)
+    o, p = _ctx(orca, w)
+    o.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+    v, fl, nb, cnt = o.debug_step()
+    ref = oracle.step(oracle.make_params(**p), w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"),
+                      pref_speed=1.0, want_nbrs=True, props=props)
+    assert np.array_equal(nb, ref["nbr"]) and np.array_equal(cnt, ref["cnt"])
+    deg = (ref["flags"] & oracle.FLAG_DEGENERATE) != 0
+    err = np.abs(v.astype(np.float64) - ref["vel"]).max(axis=1)
+    assert np.all((err <= VTOL) | deg), err[~deg].max()
+    assert deg.sum() <= max(1, 0.001 * len(deg))
+    sp = np.hypot(*v.T.astype(np.float64))
+    assert np.all(sp <= props["maxSpeed"].astype(np.float64) * (1 + 1e-6) + 1e-7)
+    o.step(1)
+    _, vel1 = o.get_state()
+    assert np.array_equal(vel1, v)
+    o.close()
+
+
+def test_heterogeneous_strips_and_history(orca):
+    """Heterogeneous crowd through 3 strips (radii travel with migrants and halos) equals
+    one strip bit for bit, and its history-bound query equals a fresh context's."""
+    w = W.make("uniform", n=20000, rho=0.15)
+    props = _het_props(len(w["pos"]), seed=9)
+    a, p = _ctx(orca, w)
+    a.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+    b = orca.Orca(p, strips=3)
+    b.set_agents(w["pos"], w["vel"], w["pref"])
+    b.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+    a.step(30)
+    b.step(30)
+    pa, va = a.get_state()
+    pb, vb = b.get_state()
+    assert np.array_equal(pa, pb) and np.array_equal(va, vb)
+    c = orca.Orca(p)
+    c.set_agents(pa, va, w["pref"])
+    c.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+    r1, r2 = a.debug_step(), c.debug_step()
+    assert np.array_equal(r1[2], r2[2]) and np.array_equal(r1[0], r2[0])
+    for o in (a, b, c):
+        o.close()
