@@ -137,6 +137,14 @@ orca_status orca_get_active(orca_ctx *ctx, uint8_t *active);
  * no host synchronisation).  Errors: NOT_READY, INVALID_ARGUMENT, CUDA, NCCL. */
 orca_status orca_step(orca_ctx *ctx, int32_t n_steps);
 
+/* Trace dump ("saving the agent data for each simulation step to a binary file",
+ * P:177): run n_steps steps and write every step's positions (and velocities if vframes
+ * != NULL) in id order into frames[s][n][2] (float, caller-owned; pinned host memory
+ * lets the copy engine overlap frame s with step s+1 on a separate stream, double
+ * buffered).  Removed agents read NaN.  Synchronises at the end.
+ * Errors: INVALID_ARGUMENT (NULL frames, multi-rank context), NOT_READY, CUDA. */
+orca_status orca_step_trace(orca_ctx *ctx, int32_t n_steps, float *frames, float *vframes);
+
 /* Current positions / velocities in id order into caller buffers float[2n] (either may
  * be NULL).  Synchronises.  Errors: NOT_READY, CUDA. */
 orca_status orca_get_state(orca_ctx *ctx, float *pos, float *vel);

@@ -215,6 +215,11 @@ struct orca_ctx {
     float maxSpeedAll = 0.0f;
     float4* props4 = nullptr;  // id-ordered staging of the per-agent properties
     int64_t props4Cap = 0;
+    // orca_step_trace: copy stream + double-buffered id-ordered frames (pos, vel) x 2
+    cudaStream_t copyStream = nullptr;
+    cudaEvent_t frameReady[2] = {}, frameFree[2] = {};
+    float2* traceBuf[4] = {};
+    int64_t traceCap = 0;
     int world = 1;  // strips in the whole decomposition
     int rank = 0;   // NCCL rank (= the strip held by this context)
     bool loopback = false;
@@ -684,6 +689,15 @@ void orca_destroy(orca_ctx* c) {
     dfree(c->partial);
     dfree(c->colHist);
     dfree(c->props4);
+    for (auto& b : c->traceBuf) dfree(b);
+    for (int b = 0; b < 2; ++b) {
+        if (c->frameReady[b]) cudaEventDestroy(c->frameReady[b]);
+        if (c->frameFree[b]) cudaEventDestroy(c->frameFree[b]);
+    }
+    if (c->copyStream) {
+        cudaStreamSynchronize(c->copyStream);
+        cudaStreamDestroy(c->copyStream);
+    }
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
@@ -1165,6 +1179,51 @@ orca_status orca_set_agent_props(orca_ctx* c, const float* radius, const float* 
     CK(cudaStreamSynchronize(c->stream));
     c->het = true;
     c->maxSpeedAll = vmax;
+    return ORCA_OK;
+}
+
+orca_status orca_step_trace(orca_ctx* c, int32_t n_steps, float* frames, float* vframes) {
+    if (!c || !frames || n_steps < 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "null frames or n_steps < 0");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    if (c->world > 1 && !c->loopback)
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "multi-rank context: trace each rank with orca_get_local_state");
+    CK(cudaSetDevice(c->device));
+    const int64_t n = c->nGlobal;
+    if (n == 0 || n_steps == 0) return orca_step(c, n_steps);
+    if (!c->copyStream) {
+        CK(cudaStreamCreateWithFlags(&c->copyStream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaEventCreateWithFlags(&c->frameReady[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->frameFree[b], cudaEventDisableTiming));
+        }
+    }
+    if (c->traceCap < n) {
+        for (int b = 0; b < 4; ++b) dfree(c->traceBuf[b]);
+        for (int b = 0; b < 4; ++b) CK(cudaMalloc(&c->traceBuf[b], (size_t)n * sizeof(float2)));
+        c->traceCap = n;
+    }
+    const size_t fb = (size_t)n * sizeof(float2);
+    for (int s = 0; s < n_steps; ++s) {
+        const int b = s & 1;
+        CKS(orca_step(c, 1));
+        if (s >= 2) CK(cudaStreamWaitEvent(c->stream, c->frameFree[b], 0));  // frame buffer b copied out
+        float2* fp = c->traceBuf[2 * b];
+        float2* fv = vframes ? c->traceBuf[2 * b + 1] : nullptr;
+        if (c->removeR > 0.0f) {
+            k_fill2<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, fp, NAN);
+            if (fv) k_fill2<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, fv, NAN);
+        }
+        for (Domain& d : c->doms)
+            k_unpermute<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.idS, d.posS, d.velS, fp, fv);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(c->frameReady[b], c->stream));
+        CK(cudaStreamWaitEvent(c->copyStream, c->frameReady[b], 0));
+        CK(cudaMemcpyAsync(frames + (size_t)s * 2 * n, fp, fb, cudaMemcpyDefault, c->copyStream));
+        if (vframes) CK(cudaMemcpyAsync(vframes + (size_t)s * 2 * n, fv, fb, cudaMemcpyDefault, c->copyStream));
+        CK(cudaEventRecord(c->frameFree[b], c->copyStream));
+    }
+    CK(cudaStreamSynchronize(c->copyStream));
+    CK(cudaStreamSynchronize(c->stream));
     return ORCA_OK;
 }
 

@@ -26,7 +26,7 @@ EXPORTS = [
     "orca_reset_stats", "orca_get_stream", "orca_step_timed", "orca_status_string", "orca_last_error",
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
-    "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props",
+    "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
 ]
 
 
@@ -86,6 +86,7 @@ def _load():
         "orca_set_goal_removal": [vp, f32],
         "orca_get_active": [vp, vp],
         "orca_set_agent_props": [vp, vp, vp, vp],
+        "orca_step_trace": [vp, i32, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -196,6 +197,17 @@ class Orca:
 
     def step(self, n_steps: int = 1):
         _check(_lib.orca_step(self._ctx, n_steps))
+
+    def step_trace(self, n_steps: int, frames=None, vframes=None, with_vel: bool = False):
+        """Run n_steps and return per-step positions (n_steps, n, 2) (and velocities): the
+        paper's per-step dump for visualisation.  Pass pinned torch tensors to
+        overlap the copies with the simulation."""
+        if frames is None:
+            frames = np.empty((n_steps, self.n, 2), np.float32)
+            if with_vel:
+                vframes = np.empty((n_steps, self.n, 2), np.float32)
+        _check(_lib.orca_step_trace(self._ctx, n_steps, _ptr(frames), _ptr(vframes)))
+        return (frames, vframes) if vframes is not None else frames
 
     def step_timed(self, n_steps: int):
         ms = (ctypes.c_double * 4)()

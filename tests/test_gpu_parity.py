@@ -472,3 +472,27 @@ def test_heterogeneous_strips_and_history(orca):
     assert np.array_equal(r1[2], r2[2]) and np.array_equal(r1[0], r2[0])
     for o in (a, b, c):
         o.close()
+
+
+def test_step_trace_frames(orca):
+    """Trace dump: frames equal get_state after every step; removed agents
+    read NaN; pinned torch buffers work (copy engine overlapped)."""
+    import torch
+    w = W.make("circle")
+    a, p = _ctx(orca, w)
+    b, _ = _ctx(orca, w)
+    a.set_goal_removal(0.5)
+    b.set_goal_removal(0.5)
+    frames = a.step_trace(120)
+    for s in range(120):
+        b.step(1)
+        pb, _ = b.get_state()
+        assert np.array_equal(frames[s], pb, equal_nan=True), s
+    fr = torch.empty((30, 100, 2), dtype=torch.float32).pin_memory()
+    vf = torch.empty((30, 100, 2), dtype=torch.float32).pin_memory()
+    a.step_trace(30, fr, vf)
+    b.step(30)
+    pb, vb = b.get_state()
+    assert np.array_equal(fr[-1].numpy(), pb, equal_nan=True) and np.array_equal(vf[-1].numpy(), vb, equal_nan=True)
+    a.close()
+    b.close()
