@@ -32,9 +32,8 @@ int scan_tiles(int64_t C) { return (int)((C + kScanTile - 1) / kScanTile); }
 int cap_blocks(int64_t n, int threads) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 148 * 32));
 }
-int lp3_blocks(int64_t n) {
-    return (int)std::max<int64_t>(1, std::min<int64_t>((n + kStepThreads - 1) / kStepThreads, 148 * 8));
-}
+// k_lp3 takes one queue entry per thread (the queue holds at most capW agents)
+int lp3_blocks(int64_t n) { return (int)std::max<int64_t>(1, (n + kStepThreads - 1) / kStepThreads); }
 
 thread_local std::string g_last_error;
 

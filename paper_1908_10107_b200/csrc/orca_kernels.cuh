@@ -408,6 +408,45 @@ __device__ __forceinline__ int lp2(const Lines& L, int T, int n, float r, float 
     return n;
 }
 
+// Warp-synchronised LP2 / LP3: the same arithmetic as lp2 / lp3, but every
+// lane in `mask` runs the same number (kmax) of constraint iterations -- lines it does not
+// have are skipped -- with a reconvergence point after each, so the lanes that re-solve on
+// the same line i run that re-solve together (with equal trip counts i) instead of drifting
+// apart.  Each lane in `mask` must call it exactly once with the same kmax.
+#ifndef ORCA_SYNC_LP
+#define ORCA_SYNC_LP 1
+#endif
+template <bool CNT>
+__device__ __forceinline__ int lp2_sync(const Lines& L, int T, int n, int kmax, float r, float optx, float opty,
+                                        float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask) {
+    const float l2 = fmaf(optx, optx, opty * opty);
+    if (l2 > r * r) {
+        const float sc = r / sqrtf(l2);
+        vx = optx * sc;
+        vy = opty * sc;
+    } else {
+        vx = optx;
+        vy = opty;
+    }
+    int failed = n;
+    for (int i = 0; i < kmax; ++i) {
+        if (i < n && failed == n) {
+            if (CNT) ++w.checks;
+            const float pen = L.s[i * T] - fmaf(L.nx[i * T], vx, L.ny[i * T] * vy);
+            if (pen > 0.0f) {
+                const float tx = vx, ty = vy;
+                if (!lp1<CNT>(L, T, i, r, optx, opty, false, vx, vy, fl, w)) {
+                    vx = tx;
+                    vy = ty;
+                    failed = i;
+                }
+            }
+        }
+        __syncwarp(mask);
+    }
+    return failed;
+}
+
 // LP3: least penetration from the LP2 failure index.  The projected constraint
 // "penetration_j <= penetration_i" is the line (n_j - n_i).v >= s_j - s_i, normalised.
 template <bool CNT>
@@ -441,6 +480,44 @@ __device__ __forceinline__ void lp3(const Lines& L, const Lines& P, int T, int n
             }
             dist = si - fmaf(nix, vx, niy * vy);
         }
+    }
+}
+
+// lp3 with a uniform kmax-iteration outer loop and a reconvergence point per line (see
+// lp2_sync); the inner projected LP2 is per lane.
+template <bool CNT>
+__device__ __forceinline__ void lp3_sync(const Lines& L, const Lines& P, int T, int n, int begin, int kmax, float r,
+                                         float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask) {
+    float dist = 0.0f;
+    for (int i = 0; i < kmax; ++i) {
+        if (i >= begin && i < n) {
+            const float nix = L.nx[i * T], niy = L.ny[i * T], si = L.s[i * T];
+            if (si - fmaf(nix, vx, niy * vy) > dist) {
+                int m = 0;
+                for (int j = 0; j < i; ++j) {
+                    const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
+                    const float det = fmaf(nix, njy, -niy * njx);
+                    if (fabsf(det) <= kEps && fmaf(nix, njx, niy * njy) > 0.0f) {
+                        if (fabsf(sj - si) <= 2e-5f * r + 1e-6f) fl |= FL_G2;
+                        continue;
+                    }
+                    if (CNT) ++w.proj;
+                    const float dx = njx - nix, dy = njy - niy;
+                    const float il = 1.0f / sqrtf(fmaf(dx, dx, dy * dy));
+                    P.nx[m * T] = dx * il;
+                    P.ny[m * T] = dy * il;
+                    P.s[m * T] = (sj - si) * il;
+                    ++m;
+                }
+                const float tx = vx, ty = vy;
+                if (lp2<CNT>(P, T, m, r, nix, niy, true, vx, vy, fl, w) < m) {
+                    vx = tx;
+                    vy = ty;
+                }
+                dist = si - fmaf(nix, vx, niy * vy);
+            }
+        }
+        __syncwarp(mask);
     }
 }
 
@@ -948,7 +1025,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         }
         float vx, vy;
         if (CNT) w.lines += (uint32_t)cnt;
-        const int f = lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
+        const int f = ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
+                                   : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
         if (f < cnt) {
             // infeasible: queue the agent with its half-planes and LP2 point; k_lp3
             // runs the least-penetration LP on a compacted set of agents (full warps)
@@ -1038,7 +1116,11 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
     const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * (a.g.ny << a.g.lgS)];
     const int nOwn = (int)a.binStart[(a.g.c1 - a.g.e0) * (a.g.ny << a.g.lgS)] - o0;
     int cInf = 0, cDeg = 0, cG1 = 0, cG2 = 0, cG3 = 0;
-    for (int q = blockIdx.x * T + tid; q < nq; q += gridDim.x * T) {
+    // one queue entry per thread (capacity grid): lanes of a warp reconverge inside lp3_sync
+    const int q = blockIdx.x * T + tid;
+    const bool act = q < nq;
+    const unsigned qmask = __ballot_sync(0xffffffffu, act);
+    if (act) {
         const int4 e = a.qEntry[q];
         const int i = e.x;
         const int cnt = e.y & 0xff, f = (e.y >> 8) & 0xff;
@@ -1051,7 +1133,10 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
             L.s[m * T] = l.z;
         }
         const float4 pr = a.propS ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
-        lp3<CNT>(L, P, T, cnt, f, pr.y, vx, vy, fl, w);
+        if (ORCA_SYNC_LP)
+            lp3_sync<CNT>(L, P, T, cnt, f, k, pr.y, vx, vy, fl, w, qmask);
+        else
+            lp3<CNT>(L, P, T, cnt, f, pr.y, vx, vy, fl, w);
         float dl = 0.0f;
         for (int m = 0; m < cnt; ++m) dl = fmaxf(dl, L.s[m * T] - fmaf(L.nx[m * T], vx, L.ny[m * T] * vy));
         if (dl > 0.0f && dl < 1e-6f) fl |= FL_G3;
