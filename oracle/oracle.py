@@ -50,6 +50,11 @@ class Agents(ctypes.Structure):
                 ("prefSpeed", ctypes.POINTER(ctypes.c_float))]
 
 
+class LpOrder(ctypes.Structure):
+    """or_lp_order: randomized = 0 nearest-first, 1 Fisher-Yates per (seed, step, id)."""
+    _fields_ = [("randomized", ctypes.c_int32), ("seed", ctypes.c_uint64), ("step", ctypes.c_int64)]
+
+
 class Line(ctypes.Structure):
     _fields_ = [("px", ctypes.c_double), ("py", ctypes.c_double),
                 ("dx", ctypes.c_double), ("dy", ctypes.c_double)]
@@ -88,9 +93,11 @@ def lib():
         L.or_penetration.argtypes = [P(Line), ctypes.c_int, f64p]
         L.or_penetration.restype = ctypes.c_double
         L.or_step.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float, P(Agents),
-                              f32p, i32p, ctypes.c_int64, i64p, f64p, f64p, u8p, f64p, i32p, i32p]
+                              P(LpOrder), f32p, i32p, ctypes.c_int64, i64p, f64p, f64p, u8p, f64p, i32p, i32p]
         L.or_run.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float, P(Agents),
-                             ctypes.c_int32]
+                             P(LpOrder), ctypes.c_int32]
+        L.or_lp_permutation.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, i32p]
+        L.or_lp_permutation.restype = None
         L.or_run.restype = ctypes.c_int64
         _lib = L
     return _lib
@@ -197,6 +204,17 @@ def penetration(lines, v):
     return lib().or_penetration(arr, n, _p(vv, ctypes.c_double))
 
 
+def lp_permutation(seed, step, agent_id, c):
+    """The randomized LP order: idx[slot] = neighbour-order index processed at `slot`."""
+    idx = np.zeros(max(c, 1), np.int32)
+    lib().or_lp_permutation(seed, step, agent_id, c, _p(idx, ctypes.c_int32))
+    return idx[:c]
+
+
+def _order(lp_seed, lp_step):
+    return None if lp_seed is None else ctypes.byref(LpOrder(1, lp_seed, lp_step))
+
+
 def _agents(props):
     """props: None or dict(radius=, maxSpeed=, prefSpeed=) of float[n] (any may be None)."""
     if not props:
@@ -215,10 +233,11 @@ def _agents(props):
 
 
 def step(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, origin=None, dims=None,
-         agents=None, want_nbrs=False, props=None):
+         agents=None, want_nbrs=False, props=None, lp_seed=None, lp_step=0):
     """One synchronous step from the given fp32 state.  If origin/dims are None the grid is
     derived from `pos` (as at set_agents).  props: optional per-agent radius / maxSpeed /
-    prefSpeed arrays.  Returns a dict of numpy arrays indexed like `agents` (or by
+    prefSpeed arrays.  lp_seed: None = nearest-first LP order, else the randomized
+    order of (lp_seed, lp_step, id) (reading Q8).  Returns a dict of numpy arrays indexed like `agents` (or by
     id)."""
     agp, _keep = _agents(props)
     pos = _f32(pos).reshape(-1, 2)
@@ -245,7 +264,7 @@ def step(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, origin
     cnt = np.zeros(m, np.int32) if want_nbrs else None
     rc = lib().or_step(ctypes.byref(params), n, _p(pos, ctypes.c_float), _p(vel, ctypes.c_float),
                        _p(pref, ctypes.c_float), _p(goals, ctypes.c_float), pref_speed, agp,
-                       _p(origin, ctypes.c_float), _p(dims, ctypes.c_int32), m, _p(ag, ctypes.c_int64),
+                       _order(lp_seed, lp_step), _p(origin, ctypes.c_float), _p(dims, ctypes.c_int32), m, _p(ag, ctypes.c_int64),
                        _p(vnew, ctypes.c_double), _p(pnew, ctypes.c_double), _p(flags, ctypes.c_uint8),
                        _p(delta, ctypes.c_double), _p(nbr, ctypes.c_int32), _p(cnt, ctypes.c_int32))
     if rc != 0:
@@ -257,7 +276,8 @@ def step(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, origin
     return out
 
 
-def run(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, steps=1, props=None):
+def run(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, steps=1, props=None,
+        lp_seed=None, lp_step=0):
     """nsteps full steps on fp32 state; returns (pos, vel, infeasible_agent_steps)."""
     agp, _keep = _agents(props)
     pos = _f32(pos).reshape(-1, 2).copy()
@@ -265,7 +285,8 @@ def run(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, steps=1
     pref = None if pref is None else _f32(pref).reshape(-1, 2)
     goals = None if goals is None else _f32(goals).reshape(-1, 2)
     r = lib().or_run(ctypes.byref(params), len(pos), _p(pos, ctypes.c_float), _p(vel, ctypes.c_float),
-                     _p(pref, ctypes.c_float), _p(goals, ctypes.c_float), pref_speed, agp, steps)
+                     _p(pref, ctypes.c_float), _p(goals, ctypes.c_float), pref_speed, agp,
+                     _order(lp_seed, lp_step), steps)
     if r < 0:
         raise ValueError("or_run failed")
     return pos, vel, int(r)

@@ -423,8 +423,32 @@ static void pref_of(const float *pos, const float *pref, const float *goals, flo
     out[1] = gy * s;
 }
 
+/* splitmix64 finaliser: the counter-based generator of the randomized LP order; integer
+ * only, so the CUDA path reproduces it bit for bit from the same inputs (no shared code) */
+static uint64_t or_mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+
+void or_lp_permutation(uint64_t seed, int64_t step, int64_t id, int32_t c, int32_t *idx) {
+    const uint64_t key = or_mix64(seed ^ or_mix64(((uint64_t)step << 32) ^ (uint64_t)id));
+    for (int32_t a = 0; a < c; ++a) idx[a] = a;
+    for (int32_t a = c - 1; a >= 1; --a) {
+        const uint64_t h = or_mix64(key ^ ((uint64_t)a * 0x9e3779b97f4a7c15ULL));
+        const int32_t b = (int32_t)(h % (uint64_t)(a + 1));
+        const int32_t t = idx[a];
+        idx[a] = idx[b];
+        idx[b] = t;
+    }
+}
+
 int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, const float *pref,
-            const float *goals, float prefSpeed, const or_agents *ag, const float origin[2], const int32_t dims[2],
+            const float *goals, float prefSpeed, const or_agents *ag, const or_lp_order *order,
+            const float origin[2], const int32_t dims[2],
             int64_t m, const int64_t *agents, double *vnew, double *pnew, uint8_t *flags,
             double *delta, int32_t *nbr, int32_t *cnt) {
     if (!params_ok(p) || n < 0 || (n > 0 && (!pos || !vel || (!pref && !goals)))) return -1;
@@ -457,6 +481,16 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, c
             int br = or_orca_line(pos + 2 * i, vel + 2 * i, pos + 2 * j, vel + 2 * j, i, j, ri, rj,
                                   p->timeHorizon, p->timeStep, &L[a]);
             if (br & 16) diag |= OR_FLAG_G1_COINCIDENT;
+        }
+        /* optional randomized constraint order ("based on the randomized incremental
+         * linear program solver of Seidel"; reading Q8): Fisher-Yates keyed by the
+         * counter-based hash of (seed, step, id) */
+        if (order && order->randomized && c > 1) {
+            or_line tmp[32];
+            int32_t idx[32];
+            or_lp_permutation(order->seed, order->step, i, c, idx);
+            for (int32_t a = 0; a < c; ++a) tmp[a] = L[idx[a]];
+            for (int32_t a = 0; a < c; ++a) L[a] = tmp[a];
         }
         /* 3. LP: closest permitted velocity to the preferred one, else least
          *    penetration */
@@ -496,7 +530,8 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, c
 }
 
 int64_t or_run(const or_params *p, int64_t n, float *pos, float *vel, const float *pref,
-               const float *goals, float prefSpeed, const or_agents *ag, int32_t nsteps) {
+               const float *goals, float prefSpeed, const or_agents *ag, const or_lp_order *order,
+               int32_t nsteps) {
     if (!params_ok(p) || n < 0 || nsteps < 0) return -1;
     float origin[2];
     int32_t dims[2];
@@ -506,7 +541,13 @@ int64_t or_run(const or_params *p, int64_t n, float *pos, float *vel, const floa
     uint8_t *fl = (uint8_t *)malloc((size_t)(n > 0 ? n : 1));
     int64_t infeasible = 0;
     for (int32_t s = 0; s < nsteps; ++s) {
-        if (or_step(p, n, pos, vel, pref, goals, prefSpeed, ag, origin, dims, 0, NULL, vn, pn, fl, NULL,
+        or_lp_order ord;
+        if (order) {
+            ord = *order;
+            ord.step = order->step + s;
+        }
+        if (or_step(p, n, pos, vel, pref, goals, prefSpeed, ag, order ? &ord : NULL, origin, dims, 0, NULL, vn, pn,
+                    fl, NULL,
                     NULL, NULL) != 0) {
             infeasible = -1;
             break;

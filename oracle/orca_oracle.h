@@ -55,6 +55,19 @@ typedef struct {
     const float *prefSpeed;
 } or_agents;
 
+/* Optional constraint order of the LP (reading Q8): randomized = 0 -> nearest first (the
+ * neighbour order); 1 -> a Fisher-Yates shuffle per agent and step keyed by the
+ * counter-based hash of (seed, step, agent id) ("randomized incremental").  `step`
+ * counts steps since the state was loaded. */
+typedef struct {
+    int32_t randomized;
+    uint64_t seed;
+    int64_t step;
+} or_lp_order;
+
+/* The shuffle: idx[slot] = neighbour-order index of the line processed at `slot`. */
+void or_lp_permutation(uint64_t seed, int64_t step, int64_t id, int32_t c, int32_t *idx);
+
 /* Per-agent diagnostic flags written by or_step. */
 #define OR_FLAG_INFEASIBLE 0x01u /* LP2 failed, LP3 (least penetration) used */
 #define OR_FLAG_G1_COINCIDENT 0x02u /* collision branch with w == 0 (reading Q15) */
@@ -127,7 +140,7 @@ double or_penetration(const or_line *lines, int n, const double v[2]);
  *   nbr[m*k] / cnt[m] (nullable).  Returns 0 or -1 on bad arguments. */
 int or_step(const or_params *p, int64_t n, const float *pos, const float *vel,
             const float *pref, const float *goals, float prefSpeed, const or_agents *ag,
-            const float origin[2],
+            const or_lp_order *order, const float origin[2],
             const int32_t dims[2], int64_t m, const int64_t *agents, double *vnew,
             double *pnew, uint8_t *flags, double *delta, int32_t *nbr, int32_t *cnt);
 
@@ -136,7 +149,8 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel,
  * the initial positions (frozen, reading Q12).  Returns the number of infeasible
  * agent-steps, or -1 on bad arguments. */
 int64_t or_run(const or_params *p, int64_t n, float *pos, float *vel, const float *pref,
-               const float *goals, float prefSpeed, const or_agents *ag, int32_t nsteps);
+               const float *goals, float prefSpeed, const or_agents *ag, const or_lp_order *order,
+               int32_t nsteps);
 
 #ifdef __cplusplus
 }

@@ -494,3 +494,55 @@ def test_heterogeneous_step_invariants(oracle):
             pref = g * min(1.0, desired[i] / np.hypot(*g))
             ref = pins.lp_vertex_enumeration(lines, float(props["maxSpeed"][i]), pref)
             assert ref is not None and np.allclose(r["vel"][i], ref, atol=1e-9)
+
+
+# ------------------------------------------- randomized constraint order (§8(f3), reading Q8)
+def test_lp_permutation_is_a_uniform_permutation(oracle):
+    """P:82 "randomized incremental": every order is a permutation of the c lines, and the
+    Fisher-Yates shuffle of the counter-based hash is uniform (chi-square over the 6 orders
+    of 3 lines; every line equally likely at every slot for c = 10)."""
+    for c in (0, 1, 2, 5, 10, 32):
+        for key in range(50):
+            idx = oracle.lp_permutation(12345, key % 7, key * 977, c)
+            assert sorted(idx.tolist()) == list(range(c))
+    counts = {}
+    for agent in range(6000):
+        t = tuple(oracle.lp_permutation(7, 3, agent, 3).tolist())
+        counts[t] = counts.get(t, 0) + 1
+    assert len(counts) == 6
+    chi2 = sum((v - 1000.0) ** 2 / 1000.0 for v in counts.values())
+    assert chi2 < 20.5  # p = 0.001 at 5 dof
+    slot = np.zeros((10, 10))
+    for agent in range(5000):
+        for s, q in enumerate(oracle.lp_permutation(99, agent % 3, agent, 10)):
+            slot[s, q] += 1
+    assert np.all(np.abs(slot - 500.0) < 5 * math.sqrt(500 * 0.9))
+    # the order depends on every key component
+    base = oracle.lp_permutation(1, 2, 3, 16)
+    for args in [(2, 2, 3), (1, 3, 3), (1, 2, 4)]:
+        assert not np.array_equal(base, oracle.lp_permutation(*args, 16))
+
+
+def test_randomized_order_same_optimum(oracle):
+    """The LP optimum does not depend on the constraint order (a strictly convex
+    objective over a convex region has one minimiser; the 3-D fallback has one minimal
+    penetration): with the randomized order every feasible agent reaches the vertex-
+    enumeration optimum and every infeasible one the same delta as nearest-first."""
+    w = W.make("uniform", n=3000, rho=0.5)
+    p = _params(oracle)
+    a = oracle.step(p, w["pos"], w["vel"], pref=w["pref"], want_nbrs=True)
+    b = oracle.step(p, w["pos"], w["vel"], pref=w["pref"], want_nbrs=True, lp_seed=2024, lp_step=5)
+    assert np.array_equal(a["nbr"], b["nbr"])
+    inf = (a["flags"] & oracle.FLAG_INFEASIBLE) != 0
+    assert np.array_equal(inf, (b["flags"] & oracle.FLAG_INFEASIBLE) != 0)
+    assert np.count_nonzero(inf) > 10
+    feas = ~inf
+    assert np.allclose(a["vel"][feas], b["vel"][feas], atol=1e-9)
+    assert np.allclose(a["delta"][inf], b["delta"][inf], atol=1e-9)
+    deg = (a["flags"] | b["flags"]) & oracle.FLAG_DEGENERATE
+    same_v = np.all(np.isclose(a["vel"], b["vel"], atol=1e-9), axis=1)
+    assert np.all(same_v | (deg != 0) | inf)
+    # but the solver really saw another order: the processed sequence differs
+    moved = sum(not np.array_equal(oracle.lp_permutation(2024, 5, i, int(c)), np.arange(c))
+                for i, c in enumerate(b["cnt"]) if c > 1)
+    assert moved > 0.9 * np.count_nonzero(b["cnt"] > 1)
