@@ -233,9 +233,13 @@ struct orca_ctx {
     int32_t* colHist = nullptr;
     int colCap = 0;
     int64_t host_steps = 0, host_updates = 0;
+    int64_t steps_total = 0;  // steps since creation (never reset): the LP-order step index
     std::vector<std::pair<int, cudaGraphExec_t>> graphs;
     cudaEvent_t ev[8] = {};
     int smemBytes = 0, lp3Smem = 0, groupSmem = 0;
+    int lpRandom = 0;              // randomized LP constraint order (orca_set_lp_order)
+    unsigned long long lpSeed = 0;
+    int64_t lpStep0 = 0, lpMark = 0;  // step index t = lpStep0 + steps_total - lpMark
     int variant = 0;  // 0: thread per agent (k_step), 1: 8-lane group per agent (k_step_group)
 };
 
@@ -267,6 +271,8 @@ Model make_model(const orca_ctx* c) {
     m.prefSpeed = c->prefSpeed;
     m.removeR2 = (c->goals && c->removeR > 0.0f) ? c->removeR * c->removeR : 0.0f;
     m.maxSpeedAll = c->het ? std::max(c->maxSpeedAll, p.maxSpeed) : p.maxSpeed;
+    m.lpRandom = c->lpRandom;
+    m.lpSeed = c->lpSeed;
     return m;
 }
 
@@ -360,7 +366,7 @@ template <bool DRY>
 void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
     const int k = c->p.maxNeighbors;
-    if (c->variant == 1 && !c->het)  // (the group kernel is homogeneous-only)
+    if (c->variant == 1 && !c->het && !c->lpRandom)  // (group kernel: homogeneous, nearest-first)
         k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
     else if (c->variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
         k_step<DRY, 0><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
@@ -380,8 +386,8 @@ cudaError_t enqueue_scan(orca_ctx* c, Domain& d) {
     return cudaGetLastError();
 }
 
-cudaError_t enqueue_scatter(orca_ctx* c, Domain& d) {
-    k_scatter<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.ctr, d.cellW, d.rankW, d.binStart, d.posW, d.velW,
+cudaError_t enqueue_scatter(orca_ctx* c, Domain& d, int bump) {
+    k_scatter<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.ctr, bump, d.cellW, d.rankW, d.binStart, d.posW, d.velW,
                                                               d.auxW, d.idW, d.rk2W, d.posS, d.velS, d.auxS, d.idS,
                                                               d.rk2S, d.capW, c->het ? d.propW : nullptr,
                                                               c->het ? d.propS : nullptr);
@@ -452,7 +458,7 @@ orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
     if (ev) CK(cudaEventRecord(ev[2], c->stream));
     for (Domain& d : c->doms) CK(enqueue_scan(c, d));
     if (ev) CK(cudaEventRecord(ev[3], c->stream));
-    for (Domain& d : c->doms) CK(enqueue_scatter(c, d));
+    for (Domain& d : c->doms) CK(enqueue_scatter(c, d, 1));
     if (ev) CK(cudaEventRecord(ev[4], c->stream));
     return ORCA_OK;
 }
@@ -803,6 +809,10 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
         if (capW > ((int64_t)1 << 30)) return fail(ORCA_ERR_CAPACITY, "strip too large");
         CKS(dom_alloc(c, d, (int)capW, d.nbins, capM, capH));
         CK(cudaMemsetAsync(d.ctr, 0, CT_COUNT * sizeof(int), c->stream));
+        {
+            const int t = (int)(c->lpStep0 + c->steps_total - c->lpMark);  // LP-order step index
+            k_set_int<<<1, 1, 0, c->stream>>>(d.ctr + CT_STEP, t);
+        }
         CK(cudaMemsetAsync(d.count, 0, d.nbins * sizeof(uint32_t), c->stream));
         if (n > 0)
             k_select<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, sp, sv, sa, d.g, d.posW, d.velW, d.auxW,
@@ -810,7 +820,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
                                                                 d.capW);
         CK(cudaGetLastError());
         CK(enqueue_scan(c, d));
-        CK(enqueue_scatter(c, d));
+        CK(enqueue_scatter(c, d, 0));
     }
     CK(cudaStreamSynchronize(c->stream));
     CKS(check_overflow(c));
@@ -878,6 +888,7 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
         remaining -= s;
     }
     c->host_steps += n_steps;
+    c->steps_total += n_steps;
     c->host_updates += (int64_t)n_steps * c->nGlobal;
     return ORCA_OK;
 }
@@ -902,6 +913,7 @@ orca_status orca_step_timed(orca_ctx* c, int32_t n_steps, double ms[4]) {
         ms[3] += t;  // exchange + receive
     }
     c->host_steps += n_steps;
+    c->steps_total += n_steps;
     c->host_updates += (int64_t)n_steps * c->nGlobal;
     return ORCA_OK;
 }
@@ -1232,6 +1244,33 @@ orca_status orca_set_goal_removal(orca_ctx* c, float radius) {
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->removeR = radius;
+    return ORCA_OK;
+}
+
+// device step counters of every domain := the current LP-order step index
+cudaError_t write_lp_step(orca_ctx* c) {
+    const int t = (int)(c->lpStep0 + c->steps_total - c->lpMark);
+    for (Domain& d : c->doms) {
+        if (!d.ctr) continue;
+        k_set_int<<<1, 1, 0, c->stream>>>(d.ctr + CT_STEP, t);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaStreamSynchronize(c->stream);
+}
+
+orca_status orca_set_lp_order(orca_ctx* c, int32_t randomized, uint64_t seed, int64_t first_step) {
+    if (!c || (randomized != 0 && randomized != 1)) return fail(ORCA_ERR_INVALID_ARGUMENT, "randomized must be 0 or 1");
+    if (first_step < 0 || first_step >= ((int64_t)1 << 31) - ((int64_t)1 << 24))
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "first_step out of range");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    drop_graph(c);
+    c->lpRandom = randomized;
+    c->lpSeed = seed;
+    c->lpStep0 = first_step;
+    c->lpMark = c->steps_total;
+    CK(write_lp_step(c));
     return ORCA_OK;
 }
 

@@ -71,6 +71,8 @@ struct Model {
     float prefSpeed;
     float removeR2;               // > 0: remove agents within sqrt(removeR2) of their goal
     float maxSpeedAll;            // largest maxSpeed of any agent (history search bound)
+    int lpRandom;                 // 1: randomized LP constraint order (reading Q8)
+    unsigned long long lpSeed;
 };
 
 // ------------------------------------------------------------------ cell (reading Q11)
@@ -112,7 +114,7 @@ __device__ __forceinline__ uint32_t bin_of(int cx, int sy, const Grid& g) {
 constexpr uint32_t kInvalid = 0xffffffffu;  // work entry that left the strip
 
 // per-domain device counters
-enum { CT_NOWN = 0, CT_EXTRA, CT_OVF, CT_COUNT };
+enum { CT_NOWN = 0, CT_EXTRA, CT_OVF, CT_STEP, CT_COUNT };  // CT_STEP: steps since set_agents
 constexpr int OVF_WORK = 1, OVF_MIG = 2, OVF_HALO = 4;
 
 // One direction of the neighbour exchange (fixed capacity; one NCCL send per step):
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uin
 
 // Counting-sort scatter of the nOwn + extra work entries (invalid = emigrated) into the
 // sorted arrays (grid-stride over the device-side count).
-__global__ void k_scatter(const int* __restrict__ ctr, const uint32_t* __restrict__ cell,
+__global__ void k_scatter(int* __restrict__ ctr, int bump, const uint32_t* __restrict__ cell,
                           const uint32_t* __restrict__ rank, const uint32_t* __restrict__ binStart,
                           const float2* __restrict__ posW, const float2* __restrict__ velW,
                           const float2* __restrict__ auxW, const uint32_t* __restrict__ idW,
@@ -250,6 +252,7 @@ __global__ void k_scatter(const int* __restrict__ ctr, const uint32_t* __restric
                           float2* __restrict__ auxS, uint32_t* __restrict__ idS, float* __restrict__ rk2S, int capW,
                           const float4* __restrict__ propW, float4* __restrict__ propS) {
     const int n = min(ctr[CT_NOWN] + ctr[CT_EXTRA], capW);
+    if (bump && blockIdx.x == 0 && threadIdx.x == 0) ctr[CT_STEP] += 1;  // the step is complete
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t c = cell[i];
         if (c == kInvalid) continue;
@@ -260,6 +263,34 @@ __global__ void k_scatter(const int* __restrict__ ctr, const uint32_t* __restric
         idS[dst] = idW[i];
         rk2S[dst] = rk2W[i];
         if (propW) propS[dst] = propW[i];
+    }
+}
+
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
+// --------------------------------------------- randomized constraint order (Q8)
+// splitmix64 finaliser; integer only, so the permutation is the oracle's bit for bit.
+__device__ __forceinline__ unsigned long long lp_mix64(unsigned long long x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+
+// Fisher-Yates over the c entries x[0], x[T], ... keyed by (seed, step, id): applying the
+// swaps of the shuffle of the identity to the list yields x'[s] = x[idx[s]].
+__device__ __forceinline__ void lp_shuffle(uint32_t* x, int T, int c, unsigned long long seed, int step,
+                                           uint32_t id) {
+    const unsigned long long key =
+        lp_mix64(seed ^ lp_mix64(((unsigned long long)(long long)step << 32) ^ (unsigned long long)id));
+    for (int a = c - 1; a >= 1; --a) {
+        const unsigned long long h = lp_mix64(key ^ ((unsigned long long)a * 0x9e3779b97f4a7c15ULL));
+        const int b = (int)(h % (unsigned long long)(a + 1));
+        const uint32_t t = x[a * T];
+        x[a * T] = x[b * T];
+        x[b * T] = t;
     }
 }
 
@@ -986,13 +1017,16 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         // warp re-forms here after the data-dependent selection (r01l).
         if (ORCA_SYNC_PHASES) __syncwarp(activeMask);
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
+        if (DRY && a.dbgNbr)  // neighbours in (distance, id) order
+            for (int q = 0; q < cnt; ++q) a.dbgNbr[(size_t)idi * k + q] = (int32_t)a.idS[L1[q * T]];
+        // optional randomized LP order (P:82 Seidel, reading Q8): permute the list first
+        if (a.m.lpRandom && cnt > 1) lp_shuffle(L1, T, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
         // (half-plane q overwrites list slot q in place: j is read before the write)
         for (int q = 0; q < cnt; ++q) {
             const uint32_t j = L1[q * T];
             const float2 pj = a.posS[j];
             const float2 vj = a.velS[j];
             const uint32_t idj = a.idS[j];
-            if (DRY && a.dbgNbr) a.dbgNbr[(size_t)idi * k + q] = (int32_t)idj;
             float nx, ny, s;
             int coll;
             // combined radius R = r_i + r_j (Fig. 1(a)); per agent when heterogeneous

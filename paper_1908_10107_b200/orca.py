@@ -27,6 +27,7 @@ EXPORTS = [
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
+    "orca_set_lp_order",
 ]
 
 
@@ -87,6 +88,7 @@ def _load():
         "orca_get_active": [vp, vp],
         "orca_set_agent_props": [vp, vp, vp, vp],
         "orca_step_trace": [vp, i32, vp, vp],
+        "orca_set_lp_order": [vp, i32, ctypes.c_uint64, i64],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -289,6 +291,12 @@ class Orca:
     def set_goal_removal(self, radius: float):
         """Remove agents within `radius` of their goal after a step; 0 disables."""
         _check(_lib.orca_set_goal_removal(self._ctx, radius))
+
+    def set_lp_order(self, randomized: bool, seed: int = 0, first_step: int = 0):
+        """LP constraint order (reading Q8): False = nearest first; True = the
+        counter-based Fisher-Yates order of (seed, t, id), t = first_step for the next step
+        and +1 per step (the oracle's lp_seed / lp_step)."""
+        _check(_lib.orca_set_lp_order(self._ctx, 1 if randomized else 0, seed, first_step))
 
     def active(self):
         a = np.empty(self.n, np.uint8)

@@ -48,10 +48,13 @@ def _oracle_params(oracle, p):
     return oracle.make_params(**p)
 
 
-def compare_step(orca, oracle, w, agents=None, max_deg=None, **over):
+def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, **over):
     """One step from the state in w on both sides; returns a report dict and asserts the
-    bar.  agents: optional sample of ids for large inputs (oracle computes one by one)."""
+    bar.  agents: optional sample of ids for large inputs (oracle computes one by one).
+    lp: optional (seed, step) of the randomized LP order (reading Q8)."""
     o, p = _ctx(orca, w, **over)
+    if lp is not None:
+        o.set_lp_order(True, lp[0], lp[1])
     op = _oracle_params(oracle, p)
     origin, cs, dims = o.grid()
     oorigin, odims = oracle.grid_derive(w["pos"], op.neighborDist)
@@ -63,7 +66,8 @@ def compare_step(orca, oracle, w, agents=None, max_deg=None, **over):
     # one step (dry) on the GPU
     v, fl, nb, cnt = o.debug_step()
     ref = oracle.step(op, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"),
-                      pref_speed=w.get("pref_speed", 1.0), agents=agents, want_nbrs=True)
+                      pref_speed=w.get("pref_speed", 1.0), agents=agents, want_nbrs=True,
+                      lp_seed=None if lp is None else lp[0], lp_step=0 if lp is None else lp[1])
     ids = np.arange(len(w["pos"])) if agents is None else np.asarray(agents)
     # neighbours (bit-exact)
     assert np.array_equal(cnt[ids], ref["cnt"])
@@ -496,3 +500,75 @@ def test_step_trace_frames(orca):
     assert np.array_equal(fr[-1].numpy(), pb, equal_nan=True) and np.array_equal(vf[-1].numpy(), vb, equal_nan=True)
     a.close()
     b.close()
+
+
+# ------------------------------------- randomized LP constraint order (§8(f3), Q8)
+@pytest.mark.parametrize("config,n,rho,lp", [("uniform", 3000, 0.5, (2024, 0)), ("dense", 4000, None, (7, 123456)),
+                                             ("uniform", 2500, 0.1, (2 ** 64 - 1, 99))])
+def test_randomized_order_parity(orca, oracle, config, n, rho, lp):
+    """The same counter-based Fisher-Yates order on both sides: velocities within the bar,
+    including the infeasible agents whose least-penetration answer may depend on order."""
+    w = W.make(config, n=n, rho=rho) if rho else W.make(config, n=n)
+    r = compare_step(orca, oracle, w, lp=lp)
+    assert r["n_inf"] > 0
+
+
+def test_randomized_order_circle_crush(orca, oracle):
+    """The circle's central crush (order-sensitive infeasible LPs) with a randomized order."""
+    w = W.make("circle")
+    op = oracle.make_params(**w["params"])
+    pos, vel, _ = oracle.run(op, w["pos"], w["vel"], goals=w["goals"], pref_speed=1.0, steps=300,
+                             lp_seed=5, lp_step=0)
+    compare_step(orca, oracle, dict(w, pos=pos, vel=vel), lp=(5, 300))
+
+
+def test_randomized_order_resume_and_strips(orca):
+    """t advances by one per step and survives set_agents (checkpoint/resume reproduces the
+    uninterrupted run bit for bit); strips and the register-list variant agree bit for bit;
+    nearest-first and randomized runs share every feasible velocity."""
+    w = W.make("uniform", n=20000, rho=0.4)
+    a, p = _ctx(orca, w)
+    a.set_lp_order(True, 11, 40)
+    a.step(6)
+    b, _ = _ctx(orca, w)  # resumed: 2 steps, reload the state, 4 more
+    b.set_lp_order(True, 11, 40)
+    b.step(2)
+    pos2, vel2 = b.get_state()
+    b.set_agents(pos2, vel2, w["pref"])
+    b.step(4)
+    c = orca.Orca(p)  # fresh context from the step-2 checkpoint at t = 42
+    c.set_agents(pos2, vel2, w["pref"])
+    c.set_lp_order(True, 11, 42)
+    c.step(4)
+    d = orca.Orca(p, strips=3)
+    d.set_agents(w["pos"], w["vel"], w["pref"])
+    d.set_lp_order(True, 11, 40)
+    d.step(6)
+    e, _ = _ctx(orca, w)
+    e.set_variant(2)
+    e.set_lp_order(True, 11, 40)
+    e.step(6)
+    ref = a.get_state()
+    for o in (b, c, d, e):
+        s = o.get_state()
+        assert np.array_equal(ref[0], s[0]) and np.array_equal(ref[1], s[1])
+    # a different t changes the order: some infeasible agent moves differently, while the
+    # feasible ones (unique optimum) are unchanged
+    f, _ = _ctx(orca, w)
+    g, _ = _ctx(orca, w)
+    f.set_lp_order(True, 11, 0)
+    g.set_lp_order(True, 11, 1)
+    vf, ff, _, _ = f.debug_step()
+    vg, fg, _, _ = g.debug_step()
+    h, _ = _ctx(orca, w)
+    vh, fh, _, _ = h.debug_step()
+    feas = ((ff | fg | fh) & 0x7) == 0  # feasible, no g1/g2 event on any side
+    assert np.array_equal(ff & 1, fh & 1) and np.array_equal(ff & 1, fg & 1)
+    assert np.max(np.abs(vf[feas] - vh[feas])) < VTOL
+    assert np.max(np.abs(vf[feas] - vg[feas])) < VTOL
+    with pytest.raises(Exception):
+        a.set_lp_order(True, 1, -1)
+    with pytest.raises(Exception):
+        a.set_lp_order(True, 1, 2 ** 31)
+    for o in (a, b, c, d, e, f, g, h):
+        o.close()
