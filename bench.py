@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--variant", type=int, default=0, help="0: thread per agent, 1: 8-lane group per agent")
+    ap.add_argument("--variant", type=int, default=0, help="0: thread per agent, 1: 8-lane group per agent, 2: register top-k, 3: work-unit LP2")
     return ap.parse_args()
 
 
@@ -262,7 +262,7 @@ def run_ours(args):
     work = {k: 0.5 * (work0[k] + work1[k]) for k in work0}
     # kernel variant A/B (same results bit for bit): fused-step ms per step
     variant_ms = {}
-    for v in (0, 1, 2):
+    for v in (0, 1, 2, 3):
         ctx.set_variant(v)
         ctx.step(2)
         acc = 0.0

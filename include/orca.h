@@ -193,7 +193,9 @@ orca_status orca_reset_stats(orca_ctx *ctx);
 /* Kernel variant of the fused step (all compute the same result bit for bit; the default
  * is chosen by measurement): 0 = one thread per agent with a shared-memory
  * top-k list (default), 1 = an 8-lane group per agent, 2 = one thread per agent with a
- * register top-k list (k <= 16; else shared memory).  Errors: INVALID_ARGUMENT. */
+ * register top-k list (k <= 16; else shared memory), 3 = variant 0 with the paper's
+ * work-unit LP2 (lanes that need no re-solve evaluate the constraints of lanes
+ * that do).  Errors: INVALID_ARGUMENT. */
 orca_status orca_set_variant(orca_ctx *ctx, int32_t variant);
 
 /* The context's cudaStream_t (as void*), e.g. for CUDA-event timing by the caller. */

@@ -368,6 +368,8 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int k = c->p.maxNeighbors;
     if (c->variant == 1 && !c->het && !c->lpRandom)  // (group kernel: homogeneous, nearest-first)
         k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
+    else if (c->variant == 3)  // work-unit LP2 (P:84-89 ablation)
+        k_step<DRY, 0, true><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
     else if (c->variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
         k_step<DRY, 0><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
     else if (k <= 10)  // register top-k list
@@ -523,7 +525,8 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
     c->lp3Smem = std::max(1, 6 * params->maxNeighbors) * 4 * kStepThreads;
     const void* stepFns[] = {(const void*)k_step<false, 0>,  (const void*)k_step<true, 0>,
                              (const void*)k_step<false, 10>, (const void*)k_step<true, 10>,
-                             (const void*)k_step<false, 16>, (const void*)k_step<true, 16>};
+                             (const void*)k_step<false, 16>, (const void*)k_step<true, 16>,
+                             (const void*)k_step<false, 0, true>, (const void*)k_step<true, 0, true>};
     for (const void* f : stepFns)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
     if (e == cudaSuccess)
@@ -1292,7 +1295,7 @@ orca_status orca_get_active(orca_ctx* c, uint8_t* active) {
 }
 
 orca_status orca_set_variant(orca_ctx* c, int32_t variant) {
-    if (!c || variant < 0 || variant > 2) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be 0, 1 or 2");
+    if (!c || variant < 0 || variant > 3) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be 0, 1, 2 or 3");
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->variant = variant;

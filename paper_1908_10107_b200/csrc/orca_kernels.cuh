@@ -478,6 +478,135 @@ __device__ __forceinline__ int lp2_sync(const Lines& L, int T, int n, int kmax, 
     return failed;
 }
 
+// Work-unit LP2 (§8(f3)): "subdivide the calculation into work units ... If the
+// thread does not need to compute a new velocity, then it can aid in another problem's
+// calculation."  Same constraint loop as lp2_sync; at line i the lanes whose current point
+// violates it (a warp-uniform ballot V) need the LP1 re-solve against lines 0..i-1.  One
+// work unit = one (problem, line j) pair: a segment of S = 2^ceil(log2 i) lanes takes one
+// problem, lane j of the segment evaluates line j of that problem (read from the owner's
+// shared-memory column), and a segmented inclusive max/min scan rebuilds the chord interval
+// [tL, tR] of every prefix -- the serial loop's state after line j -- so the first failing
+// line, the g2 flags up to it and the final interval equal the serial lp1's bit for bit
+// (max/min are exact).  32/S problems per round; with more than `maxRounds` rounds the warp
+// keeps the serial per-lane re-solve for that line.  Requires the lanes of `mask` to be
+// lanes 0..popc(mask)-1 (k_step's active lanes are a prefix of the warp).
+#ifndef ORCA_WU_ROUNDS
+#define ORCA_WU_ROUNDS 2
+#endif
+template <bool CNT>
+__device__ __forceinline__ int lp2_wu(const Lines& L, int T, int n, int kmax, float r, float optx, float opty,
+                                      float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask) {
+    const float l2 = fmaf(optx, optx, opty * opty);
+    if (l2 > r * r) {
+        const float sc = r / sqrtf(l2);
+        vx = optx * sc;
+        vy = opty * sc;
+    } else {
+        vx = optx;
+        vy = opty;
+    }
+    const int lane = threadIdx.x & 31;
+    const int A = __popc(mask);  // participating lanes 0..A-1
+    int failed = n;
+    for (int i = 0; i < kmax; ++i) {
+        bool need = false;
+        if (i < n && failed == n) {
+            if (CNT) ++w.checks;
+            need = L.s[i * T] - fmaf(L.nx[i * T], vx, L.ny[i * T] * vy) > 0.0f;
+        }
+        const unsigned V = __ballot_sync(mask, need);
+        if (V == 0u) continue;
+        const int S = (i <= 1) ? 1 : (1 << (32 - __clz(i - 1)));  // segment width >= i
+        const int P = A / S;                                       // problems per round
+        const int nV = __popc(V);
+        if (i == 0 || P == 0 || nV > P * ORCA_WU_ROUNDS) {
+            // serial per-lane re-solve (no lines to check, or too many problems)
+            if (need) {
+                const float tx = vx, ty = vy;
+                if (!lp1<CNT>(L, T, i, r, optx, opty, false, vx, vy, fl, w)) {
+                    vx = tx;
+                    vy = ty;
+                    failed = i;
+                }
+            }
+            __syncwarp(mask);
+            continue;
+        }
+        const int myRank = __popc(V & ((1u << lane) - 1u));  // owners: rank among V
+        __shared__ unsigned char wuOwner[1024];                // problem rank -> owner lane
+        const int wb = threadIdx.x & ~31;
+        if (need) wuOwner[wb + myRank] = (unsigned char)lane;
+        __syncwarp(mask);
+        const int seg = lane / S, j = lane - seg * S;
+        const unsigned segBits = (S == 32) ? 0xffffffffu : ((1u << S) - 1u);
+        for (int base = 0; base < nV; base += P) {
+            const int p = base + seg;
+            const bool valid = (seg < P) && (p < nV);
+            const int o = valid ? (int)wuOwner[wb + p] : lane;  // owner lane of problem p
+            const int d = o - lane;                              // column offset to the owner
+            const float ro = __shfl_sync(mask, r, o);
+            const float nix = L.nx[i * T + d], niy = L.ny[i * T + d], si = L.s[i * T + d];
+            const float sq = sqrtf(fmaxf((ro - si) * (ro + si), 0.0f));
+            float tL = -sq, tR = sq;
+            bool parF = false, g2 = false;
+            if (valid && j < i) {
+                const float Dx = niy, Dy = -nix;
+                const float njx = L.nx[j * T + d], njy = L.ny[j * T + d], sj = L.s[j * T + d];
+                const float den = fmaf(njx, Dx, njy * Dy);
+                const float num = sj - si * fmaf(njx, nix, njy * niy);
+                if (fabsf(den) <= kEps) {
+                    g2 = fabsf(num) <= 2e-5f * ro + 1e-6f;
+                    parF = num > 0.0f;
+                } else {
+                    const float t = num / den;
+                    if (den > 0.0f)
+                        tL = fmaxf(tL, t);
+                    else
+                        tR = fminf(tR, t);
+                }
+            }
+            // segmented inclusive scan: (tL, tR) of lane j = the serial state after line j
+            for (int q = 1; q < S; q <<= 1) {
+                const float uL = __shfl_up_sync(mask, tL, q, S);
+                const float uR = __shfl_up_sync(mask, tR, q, S);
+                if (j >= q) {
+                    tL = fmaxf(tL, uL);
+                    tR = fminf(tR, uR);
+                }
+            }
+            const bool fail = valid && j < i && (parF || tL > tR);
+            const unsigned Bf = (__ballot_sync(mask, fail) >> (seg * S)) & segBits;
+            const int f = Bf ? __ffs(Bf) - 1 : i;  // first failing line (i: none)
+            const unsigned Bg = (__ballot_sync(mask, g2 && j <= f) >> (seg * S)) & segBits;
+            const int code = (f >= i ? 1 : 0) | (Bg ? 2 : 0) | ((f < i ? f + 1 : i) << 2);
+            // lane i-1 of the owner's segment holds the whole interval: deliver it
+            const bool mine = need && myRank >= base && myRank < base + P;
+            const int src = mine ? (myRank - base) * S + i - 1 : lane;
+            const float rL = __shfl_sync(mask, tL, src), rR = __shfl_sync(mask, tR, src);
+            const int rc = __shfl_sync(mask, code, src);
+            if (mine) {
+                const float oix = L.nx[i * T], oiy = L.ny[i * T], osi = L.s[i * T];
+                if ((r - osi) * (r + osi) < 0.0f) {
+                    failed = i;  // empty chord: the serial lp1 fails before any line
+                } else {
+                    if (CNT) w.lp1 += (uint32_t)(rc >> 2);
+                    if (rc & 2) fl |= FL_G2;
+                    if (rc & 1) {
+                        const float Dx = oiy, Dy = -oix;
+                        const float od = fmaf(optx, Dx, opty * Dy);
+                        const float t = fminf(fmaxf(od, rL), rR);
+                        vx = fmaf(t, Dx, osi * oix);
+                        vy = fmaf(t, Dy, osi * oiy);
+                    } else {
+                        failed = i;
+                    }
+                }
+            }
+        }
+    }
+    return failed;
+}
+
 // LP3: least penetration from the LP2 failure index.  The projected constraint
 // "penetration_j <= penetration_i" is the line (n_j - n_i).v >= s_j - s_i, normalised.
 template <bool CNT>
@@ -816,7 +945,8 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
 #define ORCA_STEP_MINBLOCKS 7  // resident blocks per SM the register budget is sized for (swept: 6/7/8)
 #endif
 // KR > 0: the top-k selection runs in a register list (k <= KR); KR = 0: shared memory.
-template <bool DRY, int KR>
+// WU: LP2 with the paper's work units (lp2_wu) instead of per-lane re-solves.
+template <bool DRY, int KR, bool WU = false>
 __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(StepArgs a) {
     constexpr bool CNT = DRY;  // only the debug variant counts work
     WorkT w{0, 0, 0, 0, 0};
@@ -1059,8 +1189,9 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         }
         float vx, vy;
         if (CNT) w.lines += (uint32_t)cnt;
-        const int f = ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
-                                   : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
+        const int f = WU ? lp2_wu<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
+                         : ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
+                                        : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
         if (f < cnt) {
             // infeasible: queue the agent with its half-planes and LP2 point; k_lp3
             // runs the least-penetration LP on a compacted set of agents (full warps)

@@ -48,11 +48,13 @@ def _oracle_params(oracle, p):
     return oracle.make_params(**p)
 
 
-def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, **over):
+def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, variant=None, **over):
     """One step from the state in w on both sides; returns a report dict and asserts the
     bar.  agents: optional sample of ids for large inputs (oracle computes one by one).
     lp: optional (seed, step) of the randomized LP order (reading Q8)."""
     o, p = _ctx(orca, w, **over)
+    if variant is not None:
+        o.set_variant(variant)
     if lp is not None:
         o.set_lp_order(True, lp[0], lp[1])
     op = _oracle_params(oracle, p)
@@ -342,24 +344,27 @@ def test_strips_goals_circle(orca):
 
 @pytest.mark.parametrize("config,n,rho", [("uniform", 20000, 0.25), ("dense", 20000, None), ("uniform", 5000, 0.02)])
 def test_variants_bit_identical(orca, config, n, rho):
-    """Thread-per-agent with a register (0) or shared-memory (2) top-k list and the
-    8-lane-group-per-agent kernel (1): same neighbours, velocities and trajectories bit for
-    bit (exact comparators; the group LP uses exact min/max reductions)."""
+    """Thread-per-agent with a shared-memory (0) or register (2) top-k list, the
+    8-lane-group-per-agent kernel (1) and the work-unit LP2 (3): same neighbours, velocities
+    and trajectories bit for bit (exact comparators; the group and work-unit LPs use exact
+    min/max reductions).  The work-unit LP also reproduces every flag and work counter."""
     w = W.make(config, n=n, rho=rho) if rho else W.make(config, n=n)
     ctxs = []
-    for v in (0, 1, 2):
+    for v in (0, 1, 2, 3):
         o, p = _ctx(orca, w)
         o.set_variant(v)
         ctxs.append(o)
     r = [o.debug_step() for o in ctxs]
-    for q in (1, 2):
+    for q in (1, 2, 3):
         assert np.array_equal(r[0][2], r[q][2]) and np.array_equal(r[0][3], r[q][3])
         assert np.array_equal(r[0][0], r[q][0])
         assert np.array_equal(r[0][1] & 1, r[q][1] & 1)
+    assert np.array_equal(r[0][1], r[3][1])
+    assert ctxs[0].work() == ctxs[3].work()
     for o in ctxs:
         o.step(25)
     s = [o.get_state() for o in ctxs]
-    for q in (1, 2):
+    for q in (1, 2, 3):
         assert np.array_equal(s[0][0], s[q][0]) and np.array_equal(s[0][1], s[q][1])
     for o in ctxs:
         o.close()
@@ -572,3 +577,36 @@ def test_randomized_order_resume_and_strips(orca):
         a.set_lp_order(True, 1, 2 ** 31)
     for o in (a, b, c, d, e, f, g, h):
         o.close()
+
+
+# ------------------------------------------------ work-unit LP2 (§8(f3))
+@pytest.mark.parametrize("case", ["dense", "circle_crush", "k32"])
+def test_work_unit_lp_parity(orca, oracle, case):
+    """Variant 3 (idle lanes evaluate other lanes' LP1 constraints) against the oracle on the
+    LP-heaviest inputs: the dense crowd, the circle's central crush and k = 32 (segments of
+    32 lanes, one problem per round)."""
+    if case == "dense":
+        compare_step(orca, oracle, W.make("dense", n=4000), variant=3)
+    elif case == "k32":
+        compare_step(orca, oracle, W.make("uniform", n=3000, rho=0.5), variant=3, maxNeighbors=32)
+    else:
+        w = W.make("circle")
+        op = oracle.make_params(**w["params"])
+        pos, vel, _ = oracle.run(op, w["pos"], w["vel"], goals=w["goals"], pref_speed=1.0, steps=300)
+        compare_step(orca, oracle, dict(w, pos=pos, vel=vel), variant=3)
+
+
+def test_work_unit_lp_bit_identical_k_sweep(orca):
+    """Bit-identity of variant 3 with variant 0 (velocities, flags, work counters) over k,
+    including k not a power of two and a ragged last warp."""
+    w = W.make("uniform", n=4099, rho=0.6)
+    for k in (1, 2, 3, 5, 9, 16, 17, 31, 32):
+        a, _ = _ctx(orca, w, maxNeighbors=k)
+        b, _ = _ctx(orca, w, maxNeighbors=k)
+        b.set_variant(3)
+        ra, rb = a.debug_step(), b.debug_step()
+        for x, y in zip(ra, rb):
+            assert np.array_equal(x, y), k
+        assert a.work() == b.work(), k
+        a.close()
+        b.close()
