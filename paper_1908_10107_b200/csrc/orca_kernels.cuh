@@ -728,8 +728,16 @@ constexpr int kStepThreads = 128;
 //   [k, 2k)           top-k list j         -> half-plane ny (slot q read before written)
 //   [2k, 2k + B)      candidate buffer j   -> half-plane s in its first k words
 //   [2k + B, 2k + 2B) candidate buffer fp32 d2            (B = k + 8)
-__host__ __device__ constexpr int step_buf_words(int k) { return k + 14; }
-__host__ __device__ constexpr int step_smem_per_thread(int k) { return 4 * (2 * k + 2 * step_buf_words(k)); }
+#ifndef ORCA_BUF_EXTRA
+#define ORCA_BUF_EXTRA 14  // candidate buffer = k + this many entries
+#endif
+__host__ __device__ constexpr int step_buf_words(int k) { return k + ORCA_BUF_EXTRA; }
+#ifndef ORCA_BUF1
+#define ORCA_BUF1 1  // 1: the buffer keeps j only; the merge recomputes the fp32 d2 (r01o: -8 %)
+#endif
+__host__ __device__ constexpr int step_smem_per_thread(int k) {
+    return 4 * (2 * k + (ORCA_BUF1 ? 1 : 2) * step_buf_words(k));
+}
 
 __device__ __forceinline__ double exact_key(float2 pj, float2 pi) {
     const double Dx = __dsub_rn((double)pj.x, (double)pi.x);
@@ -811,6 +819,18 @@ __device__ __forceinline__ float reg_f(const RegList<KR>& L, int q) {
     return r;
 }
 
+// fp32 d2 of buffered candidate b: stored, or (ORCA_BUF1) recomputed with the scan's
+// expression -- the same bits
+__device__ __forceinline__ float buf_d2(const float* Bff, int b, uint32_t j, float2 pi,
+                                        const float2* __restrict__ posS) {
+    if (ORCA_BUF1) {
+        const float2 p = posS[j];
+        const float dx = p.x - pi.x, dy = p.y - pi.y;
+        return fmaf(dx, dx, dy * dy);
+    }
+    return Bff[b * kStepThreads];
+}
+
 // buffered (j, fp32 d2) candidates into the register list (inside r_obs only)
 template <int KR>
 __device__ __forceinline__ void reg_merge(RegList<KR>& L, int& cnt, const uint32_t* Bj, const float* Bff, int nb,
@@ -818,7 +838,7 @@ __device__ __forceinline__ void reg_merge(RegList<KR>& L, int& cnt, const uint32
     constexpr int T = kStepThreads;
     for (int b = 0; b < nb; ++b) {
         const uint32_t j = Bj[b * T];
-        const float f = Bff[b * T];
+        const float f = buf_d2(Bff, b, j, pi, posS);
         if (!in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
         reg_insert<KR>(L, f, j, tie);
         cnt = min(cnt + 1, KR);
@@ -833,7 +853,7 @@ __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int 
     constexpr int T = kStepThreads;
     for (int b = 0; b < nb; ++b) {
         const uint32_t j = Bf[b * T];
-        const float f = Bff[b * T];
+        const float f = buf_d2(Bff, b, j, pi, posS);
         if (!in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
         if (cnt == k && !cand_less(f, j, __uint_as_float(Lf[(k - 1) * T]), Lj[(k - 1) * T], pi, posS, idS))
             continue;
@@ -942,7 +962,7 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
 #define ORCA_SYNC_PHASES 0  // swept: 1M 0.495 ms (0) vs 0.529 ms (1)
 #endif
 #ifndef ORCA_STEP_MINBLOCKS
-#define ORCA_STEP_MINBLOCKS 7  // resident blocks per SM the register budget is sized for (swept: 6/7/8)
+#define ORCA_STEP_MINBLOCKS 8  // resident blocks per SM the register budget is sized for (swept r01o)
 #endif
 // KR > 0: the top-k selection runs in a register list (k <= KR); KR = 0: shared memory.
 // WU: LP2 with the paper's work units (lp2_wu) instead of per-lane re-solves.
@@ -1081,11 +1101,13 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                         if (a0 | a1) {
                             if (a0) {
                                 Bf[nb * T] = (uint32_t)j;
-                                Bff[nb++ * T] = d20;
+                                if (!ORCA_BUF1) Bff[nb * T] = d20;
+                                ++nb;
                             }
                             if (a1) {
                                 Bf[nb * T] = (uint32_t)(j + 1);
-                                Bff[nb++ * T] = d21;
+                                if (!ORCA_BUF1) Bff[nb * T] = d21;
+                                ++nb;
                             }
                             if (nb >= capB - 1) {  // buffer (nearly) full: merge, tighten
                                 merge(nb);
@@ -1101,7 +1123,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                         const float d20 = fmaf(dx0, dx0, dy0 * dy0);
                         if (d20 <= thr && j != i) {
                             Bf[nb * T] = (uint32_t)j;
-                            Bff[nb++ * T] = d20;
+                            if (!ORCA_BUF1) Bff[nb * T] = d20;
+                            ++nb;
                         }
                         if (nb >= capB - 1) {
                             merge(nb);
