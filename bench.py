@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--lp3-lanes", type=int, default=1, help="lanes per infeasible agent in the LP3 kernel")
     ap.add_argument("--variant", type=int, default=0, help="0: thread per agent, 1: 8-lane group per agent, 2: register top-k, 3: work-unit LP2")
     return ap.parse_args()
 
@@ -205,6 +206,7 @@ def run_ours(args):
     if w.get("goals") is not None:
         ctx.set_goals(w["goals"], w["pref_speed"])
     ctx.set_variant(args.variant)
+    ctx.set_lp3_lanes(args.lp3_lanes)
     stream = torch.cuda.ExternalStream(ctx.stream())
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -272,6 +274,18 @@ def run_ours(args):
             acc += ctx.step_timed(1)[0]
         variant_ms[str(v)] = acc / max(3, args.steps // 4)
     ctx.set_variant(args.variant)
+    # LP3 kernel lanes per infeasible agent A/B (same results bit for bit)
+    lp3_ms = {}
+    for lanes in (1, 4, 8, 16):
+        ctx.set_lp3_lanes(lanes)
+        ctx.step(2)
+        acc = 0.0
+        for s in range(max(3, args.steps // 4)):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            acc += ctx.step_timed(1)[0]
+        lp3_ms[str(lanes)] = acc / max(3, args.steps // 4)
+    ctx.set_lp3_lanes(args.lp3_lanes)
 
     # ---- e2e through the public API with pinned host buffers: every step uploads the
     # state (orca_set_agents: H2D, grid, partition, binning), steps once and reads the
@@ -350,6 +364,7 @@ def run_ours(args):
         "ms_per_step_l2_resident": ms_res,
         "gpu_launches": (4 if world == 1 else 5) * args.steps,
         "kernel_variant": args.variant, "k_step_ms_by_variant": variant_ms,
+        "lp3_lanes": args.lp3_lanes, "k_step_ms_by_lp3_lanes": lp3_ms,
         "roofline": roofline, "hbm_context": hbm,
         "stats": st,
     }

@@ -21,6 +21,7 @@
 #include "../../include/orca.h"
 #include "orca_kernels.cuh"
 #include "orca_step_group.cuh"
+#include "orca_lp3_group.cuh"
 
 using namespace orca;
 
@@ -240,7 +241,8 @@ struct orca_ctx {
     int lpRandom = 0;              // randomized LP constraint order (orca_set_lp_order)
     unsigned long long lpSeed = 0;
     int64_t lpStep0 = 0, lpMark = 0;  // step index t = lpStep0 + steps_total - lpMark
-    int variant = 0;  // 0: thread per agent (k_step), 1: 8-lane group per agent (k_step_group)
+    int variant = 0;
+    int lp3Lanes = ORCA_LP3_GROUP;  // lanes per queued agent in the LP3 kernel (1 = thread)  // 0: thread per agent (k_step), 1: 8-lane group per agent (k_step_group)
 };
 
 namespace {
@@ -361,6 +363,26 @@ void drop_graph(orca_ctx* c) {
     c->graphs.clear();
 }
 
+// LP3 on the queue (same results bit for bit): a GW-lane group per agent on a persistent
+// grid (ORCA_LP3_GROUP > 1), else one thread per agent on a capacity grid
+template <bool DRY, int GW>
+void launch_lp3_grp(orca_ctx* c, Domain& d, StepArgs& a) {
+    constexpr int ppb = kStepThreads / GW;
+    const int blocks = (int)std::min<int64_t>((d.capW + ppb - 1) / ppb, 148 * 16);
+    k_lp3_grp<DRY, GW><<<std::max(blocks, 1), kStepThreads, lp3_grp_words(c->p.maxNeighbors) * 4 * ppb, c->stream>>>(
+        a);
+}
+
+template <bool DRY>
+void launch_lp3(orca_ctx* c, Domain& d, StepArgs& a) {
+    switch (c->lp3Lanes) {
+        case 4: launch_lp3_grp<DRY, 4>(c, d, a); break;
+        case 8: launch_lp3_grp<DRY, 8>(c, d, a); break;
+        case 16: launch_lp3_grp<DRY, 16>(c, d, a); break;
+        default: k_lp3<DRY><<<lp3_blocks(d.capW), kStepThreads, c->lp3Smem, c->stream>>>(a);
+    }
+}
+
 // fused step kernel of the selected variant (same results bit for bit)
 template <bool DRY>
 void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
@@ -443,7 +465,7 @@ orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
         if (d.g.hasR) CK(cudaMemsetAsync(d.sendR.b.hdr, 0, 16, c->stream));
         StepArgs a = make_args(c, d);
         launch_step<false>(c, d, a);
-        k_lp3<false><<<lp3_blocks(d.capW), kStepThreads, c->lp3Smem, c->stream>>>(a);
+        launch_lp3<false>(c, d, a);
     }
     CK(cudaGetLastError());
     if (ev) CK(cudaEventRecord(ev[1], c->stream));
@@ -471,7 +493,7 @@ cudaError_t dry_step(orca_ctx* c, Domain& d, StepArgs& a) {
     cudaError_t e = cudaMemsetAsync(a.qCount, 0, sizeof(unsigned int), c->stream);
     if (e != cudaSuccess) return e;
     launch_step<true>(c, d, a);
-    k_lp3<true><<<lp3_blocks(d.capW), kStepThreads, c->lp3Smem, c->stream>>>(a);
+    launch_lp3<true>(c, d, a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return cudaMemsetAsync(a.qCount, 0, sizeof(unsigned int), c->stream);
@@ -1260,6 +1282,16 @@ cudaError_t write_lp_step(orca_ctx* c) {
         if (e != cudaSuccess) return e;
     }
     return cudaStreamSynchronize(c->stream);
+}
+
+orca_status orca_set_lp3_lanes(orca_ctx* c, int32_t lanes) {
+    if (!c || (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16))
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "lanes must be 1, 4, 8 or 16");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    drop_graph(c);
+    c->lp3Lanes = lanes;
+    return ORCA_OK;
 }
 
 orca_status orca_set_lp_order(orca_ctx* c, int32_t randomized, uint64_t seed, int64_t first_step) {

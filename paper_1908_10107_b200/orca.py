@@ -27,7 +27,7 @@ EXPORTS = [
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
-    "orca_set_lp_order",
+    "orca_set_lp_order", "orca_set_lp3_lanes",
 ]
 
 
@@ -89,6 +89,7 @@ def _load():
         "orca_set_agent_props": [vp, vp, vp, vp],
         "orca_step_trace": [vp, i32, vp, vp],
         "orca_set_lp_order": [vp, i32, ctypes.c_uint64, i64],
+        "orca_set_lp3_lanes": [vp, i32],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -291,6 +292,10 @@ class Orca:
     def set_goal_removal(self, radius: float):
         """Remove agents within `radius` of their goal after a step; 0 disables."""
         _check(_lib.orca_set_goal_removal(self._ctx, radius))
+
+    def set_lp3_lanes(self, lanes: int):
+        """Lanes per infeasible agent in the LP3 kernel: 1 (thread), 4, 8 or 16; same results."""
+        _check(_lib.orca_set_lp3_lanes(self._ctx, lanes))
 
     def set_lp_order(self, randomized: bool, seed: int = 0, first_step: int = 0):
         """LP constraint order (reading Q8): False = nearest first; True = the

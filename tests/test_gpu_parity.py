@@ -48,13 +48,15 @@ def _oracle_params(oracle, p):
     return oracle.make_params(**p)
 
 
-def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, variant=None, **over):
+def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, variant=None, lp3_lanes=None, **over):
     """One step from the state in w on both sides; returns a report dict and asserts the
     bar.  agents: optional sample of ids for large inputs (oracle computes one by one).
     lp: optional (seed, step) of the randomized LP order (reading Q8)."""
     o, p = _ctx(orca, w, **over)
     if variant is not None:
         o.set_variant(variant)
+    if lp3_lanes is not None:
+        o.set_lp3_lanes(lp3_lanes)
     if lp is not None:
         o.set_lp_order(True, lp[0], lp[1])
     op = _oracle_params(oracle, p)
@@ -610,3 +612,42 @@ def test_work_unit_lp_bit_identical_k_sweep(orca):
         assert a.work() == b.work(), k
         a.close()
         b.close()
+
+
+# ------------------------------------------------ group LP3 kernel
+@pytest.mark.parametrize("config,n,k", [("dense", 20000, 10), ("uniform", 6000, 32), ("uniform", 3001, 3)])
+def test_lp3_lanes_bit_identical(orca, config, n, k):
+    """The least-penetration kernel with 1 (thread), 4, 8 or 16 lanes per agent: the same
+    velocities, flags, work counters, trajectories and statistics bit for bit (k = 32 runs
+    LP1/projection chunks beyond one group width)."""
+    w = W.make(config, n=n) if config == "dense" else W.make(config, n=n, rho=0.6)
+    ctxs = []
+    for lanes in (1, 4, 8, 16):
+        o, _ = _ctx(orca, w, maxNeighbors=k)
+        o.set_lp3_lanes(lanes)
+        ctxs.append(o)
+    r = [o.debug_step() for o in ctxs]
+    assert np.count_nonzero(r[0][1] & 1) > 0
+    wk = [o.work() for o in ctxs]
+    for q in (1, 2, 3):
+        for x, y in zip(r[0], r[q]):
+            assert np.array_equal(x, y), q
+        assert wk[0] == wk[q], q
+    for o in ctxs:
+        o.step(20)
+    s = [o.get_state() for o in ctxs]
+    st = [o.stats() for o in ctxs]
+    for q in (1, 2, 3):
+        assert np.array_equal(s[0][0], s[q][0]) and np.array_equal(s[0][1], s[q][1]), q
+        assert st[0] == st[q], q
+    with pytest.raises(Exception):
+        ctxs[0].set_lp3_lanes(3)
+    for o in ctxs:
+        o.close()
+
+
+@pytest.mark.parametrize("lanes", [4, 16])
+def test_lp3_group_vs_oracle(orca, oracle, lanes):
+    """The group LP3 kernels against the oracle on the dense crowd (many infeasible LPs)."""
+    r = compare_step(orca, oracle, W.make("dense", n=4000), lp3_lanes=lanes)
+    assert r["n_inf"] > 0
