@@ -236,6 +236,7 @@ struct orca_ctx {
     int64_t host_steps = 0, host_updates = 0;
     int64_t steps_total = 0;  // steps since creation (never reset): the LP-order step index
     std::vector<std::pair<int, cudaGraphExec_t>> graphs;
+    std::vector<unsigned char> graphKey;  // graph_key() the cached graphs were captured with
     cudaEvent_t ev[8] = {};
     int smemBytes = 0, lp3Smem = 0, groupSmem = 0;
     int lpRandom = 0;              // randomized LP constraint order (orca_set_lp_order)
@@ -361,6 +362,32 @@ orca_status dom_alloc(orca_ctx* c, Domain& d, int capW, int64_t nbins, int capM,
 void drop_graph(orca_ctx* c) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.second);
     c->graphs.clear();
+    c->graphKey.clear();
+}
+
+// Everything a captured step body depends on: the kernel arguments of every strip (device
+// pointers, grid, model), launch sizes, the exchange buffers and the kernel selection.  A
+// cached graph is replayed only while this is unchanged, so orca_set_agents with the same
+// layout (e.g. reloading a checkpoint every step) keeps the graphs.
+std::vector<unsigned char> graph_key(orca_ctx* c) {
+    std::vector<unsigned char> k;
+    auto put = [&k](const void* p, size_t n) {
+        const unsigned char* b = static_cast<const unsigned char*>(p);
+        k.insert(k.end(), b, b + n);
+    };
+    const int hdr[6] = {c->variant, c->lp3Lanes, c->smemBytes, c->world, c->loopback ? 1 : 0, (int)c->doms.size()};
+    put(hdr, sizeof hdr);
+    for (Domain& d : c->doms) {
+        const StepArgs a = make_args(c, d);
+        put(&a, sizeof a);
+        put(&d.capW, sizeof d.capW);
+        put(&d.nbins, sizeof d.nbins);
+        for (const ExAlloc* x : {&d.sendL, &d.sendR, &d.recvL, &d.recvR}) {
+            put(&x->base, sizeof x->base);
+            put(&x->bytes, sizeof x->bytes);
+        }
+    }
+    return k;
 }
 
 // LP3 on the queue (same results bit for bit): a GW-lane group per agent on a persistent
@@ -741,7 +768,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     if (n > 0 && (!pos || !vel || !pref)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
-    drop_graph(c);
+    // cached step graphs stay: orca_step re-captures only if graph_key() changed
     c->ready = false;
     c->goals = false;
     c->het = false;
@@ -884,6 +911,13 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
     if (n_steps < 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "n_steps < 0");
     if (n_steps == 0) return ORCA_OK;
     CK(cudaSetDevice(c->device));
+    {
+        std::vector<unsigned char> key = graph_key(c);
+        if (key != c->graphKey) {
+            drop_graph(c);
+            c->graphKey = std::move(key);
+        }
+    }
     // one graph of up to kChunk step bodies, replayed
     const int kChunk = 64;
     int remaining = n_steps;

@@ -61,6 +61,7 @@ struct Grid {
 struct Model {
     float dt, maxSpeed, R;        // R = 2 r (combined radius, Fig. 1(a))
     float invTauF, invDtF;        // fp32 copies for the continuous geometry
+    float pad0;                   // explicit (no implicit padding: the host compares the bytes)
     double invTauD, invDtD;       // 1/fl64(tau), 1/fl64(dt) for the predicates
     double R2D;                   // fl64(R)^2
     double nd2D;                  // fl64(nd)^2 (exact: nd is fp32)
@@ -707,6 +708,7 @@ struct StepArgs {
     unsigned long long* stats;
     int* ctr;   // per-domain counters (CT_*)
     int capW;   // work / sorted array capacity
+    int pad0;   // explicit (no implicit padding: the host compares the bytes, graph_key)
     ExBuf sendL, sendR;
     // outputs of a dry (debug) step, indexed by global id
     float2* dbgV;
@@ -719,7 +721,9 @@ struct StepArgs {
     float4* qLines;        // line m of entry q at [m * qcap + q] = (nx, ny, s, 0)
     unsigned int* qCount;  // zeroed before every step
     int qcap;
+    int pad1;
 };
+static_assert(sizeof(Grid) == 80 && sizeof(Model) == 96 && sizeof(ExBuf) % 8 == 0, "padding-free layouts");
 
 constexpr int kStepThreads = 128;
 
@@ -961,6 +965,9 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
 #ifndef ORCA_SYNC_PHASES
 #define ORCA_SYNC_PHASES 0  // swept: 1M 0.495 ms (0) vs 0.529 ms (1)
 #endif
+#ifndef ORCA_COLD_LAMBDA
+#define ORCA_COLD_LAMBDA 1.6f  // no history: guessed radius holds ~this x k agents on average (r01q)
+#endif
 #ifndef ORCA_STEP_MINBLOCKS
 #define ORCA_STEP_MINBLOCKS 8  // resident blocks per SM the register budget is sized for (swept r01o)
 #endif
@@ -1037,7 +1044,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 }
             } else if (ncand > 4 * k) {
                 // r^2 = 2.2 k / (pi rho), rho = ncand / (9 cs^2): ~22 expected hits for k = 10
-                const float g = 2.2f * (float)k * 9.0f * a.g.cs * a.g.cs / (3.14159265f * (float)ncand);
+                const float g = ORCA_COLD_LAMBDA * (float)k * 9.0f * a.g.cs * a.g.cs / (3.14159265f * (float)ncand);
                 if (g < thr) {
                     thr = g;
                     guessed = true;
@@ -1062,7 +1069,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             };
           for (;;) {  // modes
             if (KR > 0 && mode == 0) reg_clear<(KR > 0 ? KR : 1)>(R);
-            for (int pass = 0; pass < 2; ++pass) {
+            for (int pass = 0; pass < 3; ++pass) {
                 const float thrPass = thr;
                 // sub-row window and side columns for this pass
                 int lo = rlo, hi = rhi - 1, cl = c0, cr = c1;
@@ -1145,10 +1152,18 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 // strictly beyond the k-th key.
                 // kappa_k <= fk (1 + 2^-22) < thrPass (1 - 2^-22) < any rejected kappa
                 if (cnt >= k && (double)kth() < (double)thrPass * (1.0 - 0x1p-20)) break;
-                cnt = 0;  // rescan the full 3x3 stencil at the full radius
+                // Too few within the guess (cnt < k): widen it once to ~1.5 k expected
+                // agents at the observed density, else rescan the full stencil at r_obs.
+                const float wid = (pass == 0 && cnt < k)
+                                      ? thrPass * 1.5f * (float)k / (float)max(cnt, 1) : INFINITY;
+                cnt = 0;
                 if (KR > 0 && mode == 0) reg_clear<(KR > 0 ? KR : 1)>(R);
-                thr = a.m.nd2Fup;
-                guessed = false;
+                if (wid < a.m.nd2Fup) {
+                    thr = wid;
+                } else {
+                    thr = a.m.nd2Fup;
+                    guessed = false;
+                }
             }
             if (!(KR > 0 && mode == 0 && tie)) break;
             mode = 1;  // fp32 near-tie: redo this agent's selection on the exact path

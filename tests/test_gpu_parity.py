@@ -651,3 +651,33 @@ def test_lp3_group_vs_oracle(orca, oracle, lanes):
     """The group LP3 kernels against the oracle on the dense crowd (many infeasible LPs)."""
     r = compare_step(orca, oracle, W.make("dense", n=4000), lp3_lanes=lanes)
     assert r["n_inf"] > 0
+
+
+def test_graph_cache_across_set_agents(orca):
+    """Cached step graphs survive orca_set_agents only while every captured argument is
+    unchanged (graph_key): reloading the same layout reuses them, a new grid or capacity
+    re-captures; either way the trajectory equals a fresh context's bit for bit."""
+    w1 = W.make("uniform", n=20000, rho=0.25)
+    w2 = W.make("uniform", n=30000, rho=0.4)
+    a, p = _ctx(orca, w1)
+    a.step(3)
+    a.set_agents(w2["pos"], w2["vel"], w2["pref"])  # other grid and capacity
+    a.step(3)
+    b = orca.Orca(p)
+    b.set_agents(w2["pos"], w2["vel"], w2["pref"])
+    b.step(3)
+    sa, sb = a.get_state(), b.get_state()
+    assert np.array_equal(sa[0], sb[0]) and np.array_equal(sa[1], sb[1])
+    for _ in range(3):  # the e2e pattern: reload the same state, step, read back
+        a.set_agents(w2["pos"], w2["vel"], w2["pref"])
+        a.step(3)
+        sa = a.get_state()
+        assert np.array_equal(sa[0], sb[0]) and np.array_equal(sa[1], sb[1])
+    a.set_agents(w1["pos"], w1["vel"], w1["pref"])  # smaller input into the larger buffers
+    a.step(3)
+    c, _ = _ctx(orca, w1)
+    c.step(3)
+    sa, sc = a.get_state(), c.get_state()
+    assert np.array_equal(sa[0], sc[0]) and np.array_equal(sa[1], sc[1])
+    for o in (a, b, c):
+        o.close()
