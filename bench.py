@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-suite", action="store_true", help="skip the other BASELINE workloads (N=1 only)")
     ap.add_argument("--lp3-lanes", type=int, default=1, help="lanes per infeasible agent in the LP3 kernel")
     ap.add_argument("--variant", type=int, default=0, help="0: thread per agent, 1: 8-lane group per agent, 2: register top-k, 3: work-unit LP2")
     return ap.parse_args()
@@ -175,6 +176,62 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "agent-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def suite(orca, torch, peak_tops):
+    """BASELINE.json's other workloads at N=1 (north star: "throughput on synthetic circle,
+    bidirectional-corridor and random-uniform crowds"): device time per frame of K graph-
+    replayed steps after W warm-up steps (small working sets: L2-resident), agent-updates/s,
+    and the step's ALU fraction (counted lane-ops of k_step+k_lp3 / whole-step time / peak).
+    Plus the launch-chain latency floor (a 1-agent context)."""
+    from paper_1908_10107_b200 import workloads as W
+    cases = [("circle_C0", W.make("circle"), 0, 1000), ("corridor_C1", W.make("corridor"), 0, 600)]
+    for rho in (0.01, 0.05, 0.1, 0.25, 0.5):
+        cases.append((f"uniform100k_rho{rho}", W.make("uniform", rho=rho), 10, 100))
+    cases.append(("dense_C3", W.make("dense"), 5, 40))
+    out = {}
+    for name, w, warm, steps in cases:
+        ctx = orca.Orca(w["params"])
+        ctx.set_agents(w["pos"], w["vel"], w["pref"])
+        if w.get("goals") is not None:
+            ctx.set_goals(w["goals"], w["pref_speed"])
+        if warm:
+            ctx.step(warm)
+        work = ctx.work()
+        stream = torch.cuda.ExternalStream(ctx.stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            ctx.step(steps)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        n = len(w["pos"])
+        ops = sum(OPS[k] * work[k] for k in OPS)
+        st = ctx.stats()
+        out[name] = {"n_agents": n, "steps": steps, "warmup": warm, "ms_per_frame": ms,
+                     "agent_updates_per_s": n / (ms / 1000.0),
+                     "alu_frac_of_step": ops / (ms / 1000.0) / (peak_tops * 1e12),
+                     "infeasible_per_step": st["infeasible"] / max(1, st["steps"]),
+                     "remaining": ctx.count() if w.get("goals") is not None else n}
+        ctx.close()
+    # latency floor: the same launch chain on one agent
+    ctx = orca.Orca(W.DEFAULT_PARAMS)
+    one = np.zeros((1, 2), np.float32)
+    ctx.set_agents(one, one, one)
+    ctx.step(10)
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        ctx.step(200)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    out["latency_floor_ms_per_step"] = e0.elapsed_time(e1) / 200
+    ctx.close()
+    return out
 
 
 def run_ours(args):
@@ -397,8 +454,11 @@ def run_ours(args):
             line["cpu_baseline"] = {"value": r, "unit": "agent-updates/s", "cores": 1, "kind": "oracle",
                                     "sample": f"{m} random agents of the initial {n_total}-agent state, one step, "
                                               f"single thread, {el:.1f} s"}
-        print(json.dumps(line), flush=True)
     ctx.close()
+    if rank == 0:
+        if world == 1 and not args.no_suite:
+            line["suite"] = suite(orca, torch, peak)
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -98,7 +98,9 @@ void orca_destroy(orca_ctx *ctx);
  * is the preferred velocity held constant over steps (reading Q16) unless orca_set_goals
  * is called afterwards.  Freezes the grid: origin = fl32(min - r_obs) per axis, dims =
  * floor((max - origin)/r_obs) + 2 (reading Q12); later positions outside are clamped to
- * edge cells.  Bins the agents.  Clears any goals.
+ * edge cells.  Bins the agents.  Clears any goals.  With the same n as the loaded state,
+ * each agent keeps its last k-th-neighbour distance as its first search radius (by id; a
+ * performance hint only -- the neighbour selection is exact for any radius).
  * Errors: INVALID_ARGUMENT (n < 0, NULL with n > 0, NaN/Inf), CAPACITY (grid larger than
  * 2^28 cells), OUT_OF_MEMORY, CUDA. */
 orca_status orca_set_agents(orca_ctx *ctx, int64_t n, const float *pos, const float *vel,

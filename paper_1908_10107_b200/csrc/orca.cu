@@ -768,6 +768,9 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     if (n > 0 && (!pos || !vel || !pref)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
+    // same agent count as the loaded state: keep each agent's last k-th neighbour distance
+    // as its first search radius (a hint; the selection is exact for any radius)
+    const bool keepHist = c->ready && c->nGlobal == n && n > 0;
     // cached step graphs stay: orca_step re-captures only if graph_key() changed
     c->ready = false;
     c->goals = false;
@@ -783,6 +786,14 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
         c->stageCap = n;
     }
     float2 *sp = c->stage, *sv = c->stage + n, *sa = c->stage + 2 * n;
+    float* hist = nullptr;
+    if (keepHist) {  // before any domain is re-allocated
+        hist = reinterpret_cast<float*>(c->outA);
+        k_fill1<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, hist, INFINITY);
+        for (Domain& d : c->doms)
+            k_hist_by_id<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.idS, d.rk2S, hist);
+        CK(cudaGetLastError());
+    }
     CK(copy_in(c, sp, pos, n));
     CK(copy_in(c, sv, vel, n));
     CK(copy_in(c, sa, pref, n));
@@ -869,7 +880,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
         if (n > 0)
             k_select<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, sp, sv, sa, d.g, d.posW, d.velW, d.auxW,
                                                                 d.idW, d.rk2W, d.cellW, d.rankW, d.count, d.ctr,
-                                                                d.capW);
+                                                                d.capW, hist);
         CK(cudaGetLastError());
         CK(enqueue_scan(c, d));
         CK(enqueue_scatter(c, d, 0));

@@ -140,7 +140,7 @@ __global__ void k_select(int n, const float2* __restrict__ pos, const float2* __
                          const float2* __restrict__ aux, Grid g, float2* __restrict__ posW, float2* __restrict__ velW,
                          float2* __restrict__ auxW, uint32_t* __restrict__ idW, float* __restrict__ rk2W,
                          uint32_t* __restrict__ cellW, uint32_t* __restrict__ rankW, uint32_t* __restrict__ count,
-                         int* __restrict__ ctr, int capW) {
+                         int* __restrict__ ctr, int capW, const float* __restrict__ hist) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const float2 p = pos[i];
         const int cx = cell_coord(p.x, g.ox, g.csD, g.invCs, g.nx);
@@ -155,10 +155,20 @@ __global__ void k_select(int n, const float2* __restrict__ pos, const float2* __
         velW[w] = vel[i];
         auxW[w] = aux[i];
         idW[w] = (uint32_t)i;
-        rk2W[w] = INFINITY;
+        rk2W[w] = hist ? hist[i] : INFINITY;  // search-radius hint only (results are exact either way)
         cellW[w] = c;
         rankW[w] = atomicAdd(&count[c], 1u);
     }
+}
+
+// Previous k-th neighbour distances of the owned agents by id (out is +inf-filled): the
+// first search radius of the next orca_set_agents with the same agent count.
+__global__ void k_hist_by_id(const uint32_t* __restrict__ binStart, Grid g, const uint32_t* __restrict__ idS,
+                             const float* __restrict__ rk2S, float* __restrict__ out) {
+    const int nyS = g.ny << g.lgS;
+    const int o0 = (int)binStart[(g.c0 - g.e0) * nyS], o1 = (int)binStart[(g.c1 - g.e0) * nyS];
+    for (int i = o0 + blockIdx.x * blockDim.x + threadIdx.x; i < o1; i += gridDim.x * blockDim.x)
+        out[idS[i]] = rk2S[i];
 }
 
 // Single-pass exclusive scan (decoupled look-back) over C bin counts: tiles of 4096

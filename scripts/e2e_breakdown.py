@@ -11,6 +11,7 @@ from paper_1908_10107_b200 import orca as O  # noqa: E402
 from paper_1908_10107_b200 import workloads as W  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "uniform_1m"
+warm = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # reload the state after `warm` steps
 w = W.make(cfg)
 n = len(w["pos"])
 ctx = O.Orca(w["params"])
@@ -19,7 +20,10 @@ hv = torch.from_numpy(w["vel"]).pin_memory()
 hq = torch.from_numpy(w["pref"]).pin_memory()
 op = torch.empty((n, 2), dtype=torch.float32).pin_memory()
 ov = torch.empty((n, 2), dtype=torch.float32).pin_memory()
-dp = torch.from_numpy(w["pos"]).cuda()
+if warm:
+    ctx.set_agents(hp, hv, hq)
+    ctx.step(warm)
+    ctx.get_state(hp, hv)
 for _ in range(3):
     ctx.set_agents(hp, hv, hq)
     ctx.step(1)
@@ -52,7 +56,7 @@ for _ in range(R):
     h[: n * 4].copy_(x[: n * 4], non_blocking=True)
 torch.cuda.synchronize()
 d2h = (time.perf_counter() - t0) / R
-print(cfg, {k: round(1000 * v / R, 4) for k, v in T.items()},
+print(cfg, "warm", warm, {k: round(1000 * v / R, 4) for k, v in T.items()},
       f"raw H2D {n*24/1e6:.0f} MB {1000*h2d:.3f} ms ({n*24/h2d/1e9:.1f} GB/s), "
       f"raw D2H {n*16/1e6:.0f} MB {1000*d2h:.3f} ms ({n*16/d2h/1e9:.1f} GB/s)")
 # step(1) + sync without reloading (history radius valid, graph cached)

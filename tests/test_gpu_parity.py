@@ -679,5 +679,16 @@ def test_graph_cache_across_set_agents(orca):
     c.step(3)
     sa, sc = a.get_state(), c.get_state()
     assert np.array_equal(sa[0], sc[0]) and np.array_equal(sa[1], sc[1])
-    for o in (a, b, c):
+    # same n, unrelated state: the kept search-radius hints are wrong, the result is exact
+    w3 = W.make("uniform", n=20000, rho=0.6, salt=3)
+    a.set_agents(w3["pos"], w3["vel"], w3["pref"])
+    va, fa, na, ca = a.debug_step()
+    a.step(3)
+    d, _ = _ctx(orca, w3)
+    vd, fd, nd, cd = d.debug_step()
+    d.step(3)
+    assert np.array_equal(na, nd) and np.array_equal(ca, cd) and np.array_equal(va, vd)
+    sa, sd = a.get_state(), d.get_state()
+    assert np.array_equal(sa[0], sd[0]) and np.array_equal(sa[1], sd[1])
+    for o in (a, b, c, d):
         o.close()
