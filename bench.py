@@ -413,15 +413,19 @@ def run_ours(args):
     t_step = stage[0] / 1000.0
     achieved = ops / t_step / 1e12
     peak = SMS * FP32_LANES_PER_SM * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    traffic = None
+    traffic, ncu = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get("k_step_dram_bytes")
+            ent = json.load(open(tpath)).get(args.config, {})
+            traffic = ent.get("k_step_dram_bytes")
+            keep = ("issue_slots_busy_pct", "avg_active_threads_per_warp", "achieved_occupancy_pct",
+                    "fma_pipe_active_pct", "alu_pipe_active_pct", "fp64_pipe_active_pct", "report")
+            ncu = {k: v for k, v in ent.get("k_step_ncu", {}).items() if k in keep} or None
         except Exception:
-            traffic = None
+            traffic, ncu = None, None
     roofline = {"bound": "alu", "kernel": "k_step(+k_lp3)", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
-                "frac": achieved / peak, "traffic": traffic,
+                "frac": achieved / peak, "traffic": traffic, "ncu": ncu,
                 "peak_source": f"148 SMs x 128 FP32 lanes x sm_max_mhz ({pk_kind} MEASURED_PEAKS.json)",
                 "ops_per_launch": ops, "work_per_launch": work,
                 "stage_ms": {"k_step+k_lp3": stage[0], "k_scan": stage[1], "k_scatter": stage[2],
