@@ -291,11 +291,14 @@ def run_ours(args):
                 ctx.step(1)
                 evs[s][1].record(stream)
         barrier()
-    ms = float(sum(a.elapsed_time(b) for a, b in evs))
+    per = [a.elapsed_time(b) for a, b in evs]
+    ms = float(sum(per))
+    per_step_stats = [float(np.median(per)), float(np.min(per)), float(np.max(per))]
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms] + per_step_stats, dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(t[0].item())
+        per_step_stats = [float(x) for x in t[1:].tolist()]
     st = ctx.stats()
     ms_per_step = ms / args.steps
     value = n_total * args.steps / (ms / 1000.0)
@@ -443,6 +446,7 @@ def run_ours(args):
                    "l2": "flushed between timed steps (512 MiB write); per-step CUDA events on the library stream",
                    "parallelism": f"strips{world}" if world > 1 else "single"},
         "ms_per_step_l2_resident": ms_res,
+        "ms_per_step_median_min_max": per_step_stats,
         "gpu_launches": (4 if world == 1 else 5) * args.steps,
         "kernel_variant": args.variant, "k_step_ms_by_variant": variant_ms,
         "lp3_lanes": args.lp3_lanes, "k_step_ms_by_lp3_lanes": lp3_ms,

@@ -33,8 +33,15 @@ int scan_tiles(int64_t C) { return (int)((C + kScanTile - 1) / kScanTile); }
 int cap_blocks(int64_t n, int threads) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 148 * 32));
 }
-// k_lp3 takes one queue entry per thread (the queue holds at most capW agents)
-int lp3_blocks(int64_t n) { return (int)std::max<int64_t>(1, (n + kStepThreads - 1) / kStepThreads); }
+// k_lp3 takes one queue entry per thread (the queue holds at most capW agents), grid-stride
+// beyond ORCA_LP3_WAVES waves of resident blocks
+#ifndef ORCA_LP3_WAVES
+#define ORCA_LP3_WAVES 4
+#endif
+int lp3_blocks(int64_t n) {
+    const int64_t need = (n + kStepThreads - 1) / kStepThreads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)148 * 7 * ORCA_LP3_WAVES));
+}
 
 thread_local std::string g_last_error;
 
