@@ -81,6 +81,7 @@ typedef struct {
     int64_t marginal;       /* g3: infeasible with max penetration < 1e-6 (reported only) */
     int64_t collision_pairs;/* neighbour pairs that took the collision branch (Q4) */
     int64_t removed;        /* agents removed at their goal (orca_set_goal_removal) */
+    int64_t rebalances;     /* strip re-partitions since creation (orca_rebalance; automatic) */
 } orca_stats;
 
 /* ---- lifecycle -------------------------------------------------------------------- */
@@ -254,6 +255,15 @@ orca_status orca_partition_columns(const int64_t *colCount, int32_t nx, int32_t 
 
 /* Owned column ranges of the strips held by this context: bounds int32[2 * strips held]
  * = (c0, c1) pairs.  Errors: NOT_READY. */
+/* Re-partition the strips from the current state (agent-count quantiles of the columns
+ * on the frozen grid) and re-size their buffers.  Done automatically before every chunk of
+ * up to 64 steps when a strip could outgrow its capacities within the chunk (a crowd
+ * converging into one strip); every rank of a multi-GPU context must call it together
+ * (it all-gathers the state over NCCL).  Results are unchanged (bit-identical to one
+ * strip); goals, per-agent properties, removals and counters carry over.  Single-strip
+ * contexts: no-op.  Synchronises.  Errors: NOT_READY, CUDA, NCCL, CAPACITY. */
+orca_status orca_rebalance(orca_ctx *ctx);
+
 orca_status orca_get_strips(orca_ctx *ctx, int32_t *bounds);
 
 #ifdef __cplusplus

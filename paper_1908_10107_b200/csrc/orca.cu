@@ -94,6 +94,9 @@ struct NcclApi {
     ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*groupStart)() = nullptr;
     ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*errStr)(ncclResult_t) = nullptr;
 };
 
@@ -121,6 +124,8 @@ NcclApi& nccl() {
     api.recv = (decltype(api.recv))sym("ncclRecv");
     api.groupStart = (decltype(api.groupStart))sym("ncclGroupStart");
     api.groupEnd = (decltype(api.groupEnd))sym("ncclGroupEnd");
+    api.allReduce = (decltype(api.allReduce))sym("ncclAllReduce");
+    api.allGather = (decltype(api.allGather))sym("ncclAllGather");
     api.errStr = (decltype(api.errStr))sym("ncclGetErrorString");
     api.ok = ok;
     if (!ok) api.err = "libnccl.so.2 lacks a required symbol";
@@ -250,7 +255,15 @@ struct orca_ctx {
     unsigned long long lpSeed = 0;
     int64_t lpStep0 = 0, lpMark = 0;  // step index t = lpStep0 + steps_total - lpMark
     int variant = 0;
-    int lp3Lanes = ORCA_LP3_GROUP;  // lanes per queued agent in the LP3 kernel (1 = thread)  // 0: thread per agent (k_step), 1: 8-lane group per agent (k_step_group)
+    int lp3Lanes = ORCA_LP3_GROUP;  // lanes per queued agent in the LP3 kernel (1 = thread)
+    // strip rebalance: by-id active flags, all-gather records, fill reports
+    uint8_t* activeBuf = nullptr;
+    int64_t activeCap = 0;
+    float4* gatherBuf = nullptr;
+    size_t gatherCap = 0;  // float4 entries
+    int* report = nullptr;
+    int reportCap = 0;
+    int64_t rebalances = 0;
 };
 
 namespace {
@@ -627,6 +640,196 @@ orca_status stage_bounds(orca_ctx* c, const float2* a, const float2* b, const fl
     return ORCA_OK;
 }
 
+// Strips from the global by-id arrays (every rank holds the same arrays): column histogram
+// of the active agents -> partition -> per-strip capacities, selection, scan, scatter.
+// The grid (c->gg) is frozen; hist (nullable) seeds the per-agent search radius; active
+// (nullable) excludes agents removed at their goal.  Used by orca_set_agents and by the
+// strip rebalance.
+orca_status build_domains(orca_ctx* c, int64_t n, const float2* sp, const float2* sv, const float2* sa,
+                          const float* hist, const uint8_t* active) {
+    const Grid& g = c->gg;
+    if (c->world > g.nx) return fail(ORCA_ERR_CAPACITY, "more strips than grid columns");
+    // column histogram -> strips (every rank computes the same partition)
+    std::vector<int64_t> colCount(g.nx, 0);
+    if (c->world > 1 && n > 0) {
+        if (g.nx > c->colCap) {
+            dfree(c->colHist);
+            CK(cudaMalloc(&c->colHist, (size_t)g.nx * sizeof(int32_t)));
+            c->colCap = g.nx;
+        }
+        CK(cudaMemsetAsync(c->colHist, 0, (size_t)g.nx * sizeof(int32_t), c->stream));
+        k_colhist<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, sp, g, c->colHist, active);
+        CK(cudaGetLastError());
+        std::vector<int32_t> h(g.nx);
+        CK(cudaMemcpyAsync(h.data(), c->colHist, (size_t)g.nx * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int x = 0; x < g.nx; ++x) colCount[x] = h[x];
+    } else {
+        colCount[0] = n;
+    }
+    std::vector<int32_t> bounds(c->world + 1);
+    CKS(orca_partition_columns(colCount.data(), g.nx, c->world, bounds.data()));
+    // exchange capacities are global (sender and receiver must agree on the layout):
+    // 1.5x the largest strip-edge column of the whole partition
+    int64_t edgeMax = 0;
+    for (int s = 0; s < c->world; ++s)
+        edgeMax = std::max(edgeMax, std::max(colCount[bounds[s]], colCount[bounds[s + 1] - 1]));
+    const int capH = (int)std::min<int64_t>(edgeMax + edgeMax / 2 + 1024, (int64_t)1 << 28);
+    const int capM = std::max(1024, capH / 4);
+    const int first = c->loopback ? 0 : c->rank;
+    for (size_t q = 0; q < c->doms.size(); ++q) {
+        Domain& d = c->doms[q];
+        const int s = first + (int)q;
+        d.strip = s;
+        d.g = g;
+        d.g.c0 = bounds[s];
+        d.g.c1 = bounds[s + 1];
+        d.g.e0 = std::max(d.g.c0 - 1, 0);
+        d.g.e1 = std::min(d.g.c1 + 1, g.nx);
+        d.g.hasL = s > 0;
+        d.g.hasR = s < c->world - 1;
+        d.nbins = ((int64_t)(d.g.e1 - d.g.e0) * g.ny) << g.lgS;
+        int64_t sel = 0;
+        for (int x = d.g.e0; x < d.g.e1; ++x) sel += colCount[x];
+        // single strip: exact; strips: headroom for density drift between re-partitions
+        const int64_t capW = (c->world == 1) ? std::max<int64_t>(n, 1) : sel + sel / 2 + 4096;
+        if (capW > ((int64_t)1 << 30)) return fail(ORCA_ERR_CAPACITY, "strip too large");
+        CKS(dom_alloc(c, d, (int)capW, d.nbins, capM, capH));
+        CK(cudaMemsetAsync(d.ctr, 0, CT_COUNT * sizeof(int), c->stream));
+        {
+            const int t = (int)(c->lpStep0 + c->steps_total - c->lpMark);  // LP-order step index
+            k_set_int<<<1, 1, 0, c->stream>>>(d.ctr + CT_STEP, t);
+        }
+        CK(cudaMemsetAsync(d.count, 0, d.nbins * sizeof(uint32_t), c->stream));
+        if (n > 0)
+            k_select<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, sp, sv, sa, d.g, d.posW, d.velW, d.auxW,
+                                                                d.idW, d.rk2W, d.cellW, d.rankW, d.count, d.ctr,
+                                                                d.capW, hist, active);
+        CK(cudaGetLastError());
+        CK(enqueue_scan(c, d));
+        CK(enqueue_scatter(c, d, 0));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    CKS(check_overflow(c));
+    c->ready = true;
+    return ORCA_OK;
+}
+
+// Per-agent properties (heterogeneous crowds) from the by-id copy into every strip's
+// sorted order, after the strips were (re)built.
+orca_status refresh_props(orca_ctx* c) {
+    if (!c->het || !c->props4) return ORCA_OK;
+    for (Domain& d : c->doms) {
+        if (d.propCap < d.capW) {
+            dfree(d.propS);
+            dfree(d.propW);
+            CK(cudaMalloc(&d.propS, (size_t)d.capW * sizeof(float4)));
+            CK(cudaMalloc(&d.propW, (size_t)d.capW * sizeof(float4)));
+            d.propCap = d.capW;
+        }
+        k_gather4_by_id<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, (int)d.nbins, d.idS, c->props4,
+                                                                       d.propS);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return ORCA_OK;
+}
+
+// Re-partition the strips from the current state: every strip's owned agents
+// go back to by-id arrays (all-gathered between ranks), then build_domains re-runs the
+// partition on the frozen grid.  Goals / preferred velocities (aux), per-agent properties,
+// removals, search-radius history, counters and the LP-order step index carry over; the
+// step results do not depend on the partition (bit-identical to one strip).
+orca_status rebalance(orca_ctx* c) {
+    const int64_t n = c->nGlobal;
+    if (n == 0) return ORCA_OK;
+    if (c->activeCap < n) {
+        dfree(c->activeBuf);
+        CK(cudaMalloc(&c->activeBuf, (size_t)n));
+        c->activeCap = n;
+    }
+    float2 *sp = c->stage, *sv = c->stage + n, *sa = c->stage + 2 * n;
+    float* hist = reinterpret_cast<float*>(c->outA);
+    CK(cudaMemsetAsync(c->activeBuf, 0, (size_t)n, c->stream));
+    k_fill1<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, hist, INFINITY);
+    if (c->loopback || c->world == 1) {
+        for (Domain& d : c->doms)
+            k_gather_state<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.idS, d.posS, d.velS,
+                                                                          d.auxS, d.rk2S, sp, sv, sa, hist,
+                                                                          c->activeBuf);
+        CK(cudaGetLastError());
+    } else {
+        NcclApi& N = nccl();
+        Domain& d = c->doms[0];
+        // records per rank = the largest owned count (all-gather needs equal sizes)
+        k_fill_report<<<1, 32, 0, c->stream>>>(d.binStart, d.g, c->report);
+        ncclResult_t r = N.allReduce(c->report, c->report + 3, 1, ncclInt32, ncclMax, c->comm, c->stream);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+        int cap = 0;
+        CK(cudaMemcpyAsync(&cap, c->report + 3, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        cap = std::max(cap, 1);
+        const size_t need = (size_t)2 * cap * (c->world + 1);
+        if (c->gatherCap < need) {
+            dfree(c->gatherBuf);
+            CK(cudaMalloc(&c->gatherBuf, need * sizeof(float4)));
+            c->gatherCap = need;
+        }
+        float4* mine = c->gatherBuf;
+        float4* all = c->gatherBuf + (size_t)2 * cap;
+        k_pack_owned<<<cap_blocks(cap, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.idS, d.posS, d.velS, d.auxS,
+                                                                  d.rk2S, mine, cap);
+        r = N.allGather(mine, all, (size_t)8 * cap, ncclFloat32, c->comm, c->stream);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+        k_unpack_gathered<<<cap_blocks((int64_t)cap * c->world, 256), 256, 0, c->stream>>>(
+            all, cap * c->world, sp, sv, sa, hist, c->activeBuf);
+        CK(cudaGetLastError());
+    }
+    c->ready = false;
+    CKS(build_domains(c, n, sp, sv, sa, hist, c->activeBuf));
+    CKS(refresh_props(c));
+    c->rebalances += 1;
+    return ORCA_OK;
+}
+
+// Before a chunk of up to 64 steps: rebalance if a strip could outgrow its capacities
+// within the chunk.  Agents move at most 64 maxSpeed dt < 1.5 columns in a chunk, so a
+// strip gains at most ~1.5 edge columns' worth of agents, and an edge column stays within
+// its halo buffer while it is below 70 % of it.  One small read-back per chunk (strips only).
+orca_status maybe_rebalance(orca_ctx* c) {
+    if (c->world == 1 || c->nGlobal == 0) return ORCA_OK;
+    const int nd = (int)c->doms.size();
+    if (c->reportCap < 3 * nd + 4) {
+        dfree(c->report);
+        CK(cudaMalloc(&c->report, (size_t)(3 * nd + 4) * sizeof(int)));
+        c->reportCap = 3 * nd + 4;
+    }
+    int* rep = c->report + 4;  // [0, 4) is scratch for the rebalance all-reduce
+    for (int q = 0; q < nd; ++q) k_fill_report<<<1, 32, 0, c->stream>>>(c->doms[q].binStart, c->doms[q].g, rep + 3 * q);
+    CK(cudaGetLastError());
+    std::vector<int> h(3 * nd);
+    CK(cudaMemcpyAsync(h.data(), rep, h.size() * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    int need = 0;
+    for (int q = 0; q < nd; ++q) {
+        const Domain& d = c->doms[q];
+        const int owned = h[3 * q], colL = h[3 * q + 1], colR = h[3 * q + 2];
+        const int capH = d.g.hasL ? d.sendL.b.capH : (d.g.hasR ? d.sendR.b.capH : INT32_MAX);
+        if ((int64_t)owned + (3 * ((int64_t)colL + colR)) / 2 > (int64_t)d.capW) need = 1;
+        if (d.g.hasL && (int64_t)colL * 10 > (int64_t)capH * 7) need = 1;
+        if (d.g.hasR && (int64_t)colR * 10 > (int64_t)capH * 7) need = 1;
+    }
+    if (!c->loopback) {  // every rank must take the same decision
+        NcclApi& N = nccl();
+        CK(cudaMemcpyAsync(c->report, &need, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        ncclResult_t r = N.allReduce(c->report, c->report, 1, ncclInt32, ncclMax, c->comm, c->stream);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+        CK(cudaMemcpyAsync(&need, c->report, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    return need ? rebalance(c) : ORCA_OK;
+}
+
 }  // namespace
 
 // =============================================================================== ABI
@@ -753,6 +956,9 @@ void orca_destroy(orca_ctx* c) {
     dfree(c->partial);
     dfree(c->colHist);
     dfree(c->props4);
+    dfree(c->activeBuf);
+    dfree(c->gatherBuf);
+    dfree(c->report);
     for (auto& b : c->traceBuf) dfree(b);
     for (int b = 0; b < 2; ++b) {
         if (c->frameReady[b]) cudaEventDestroy(c->frameReady[b]);
@@ -831,71 +1037,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     g.invCsSub = (double)(1 << g.lgS) / (double)cs;
     c->gg = g;
     c->nGlobal = n;
-    if (c->world > g.nx) return fail(ORCA_ERR_CAPACITY, "more strips than grid columns");
-    // column histogram -> strips (every rank computes the same partition)
-    std::vector<int64_t> colCount(g.nx, 0);
-    if (c->world > 1 && n > 0) {
-        if (g.nx > c->colCap) {
-            dfree(c->colHist);
-            CK(cudaMalloc(&c->colHist, (size_t)g.nx * sizeof(int32_t)));
-            c->colCap = g.nx;
-        }
-        CK(cudaMemsetAsync(c->colHist, 0, (size_t)g.nx * sizeof(int32_t), c->stream));
-        k_colhist<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, sp, g, c->colHist);
-        CK(cudaGetLastError());
-        std::vector<int32_t> h(g.nx);
-        CK(cudaMemcpyAsync(h.data(), c->colHist, (size_t)g.nx * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        for (int x = 0; x < g.nx; ++x) colCount[x] = h[x];
-    } else {
-        colCount[0] = n;
-    }
-    std::vector<int32_t> bounds(c->world + 1);
-    CKS(orca_partition_columns(colCount.data(), g.nx, c->world, bounds.data()));
-    // exchange capacities are global (sender and receiver must agree on the layout):
-    // 1.5x the largest strip-edge column of the whole partition
-    int64_t edgeMax = 0;
-    for (int s = 0; s < c->world; ++s)
-        edgeMax = std::max(edgeMax, std::max(colCount[bounds[s]], colCount[bounds[s + 1] - 1]));
-    const int capH = (int)std::min<int64_t>(edgeMax + edgeMax / 2 + 1024, (int64_t)1 << 28);
-    const int capM = std::max(1024, capH / 4);
-    const int first = c->loopback ? 0 : c->rank;
-    for (size_t q = 0; q < c->doms.size(); ++q) {
-        Domain& d = c->doms[q];
-        const int s = first + (int)q;
-        d.strip = s;
-        d.g = g;
-        d.g.c0 = bounds[s];
-        d.g.c1 = bounds[s + 1];
-        d.g.e0 = std::max(d.g.c0 - 1, 0);
-        d.g.e1 = std::min(d.g.c1 + 1, g.nx);
-        d.g.hasL = s > 0;
-        d.g.hasR = s < c->world - 1;
-        d.nbins = ((int64_t)(d.g.e1 - d.g.e0) * g.ny) << g.lgS;
-        int64_t sel = 0;
-        for (int x = d.g.e0; x < d.g.e1; ++x) sel += colCount[x];
-        // single strip: exact; strips: headroom for density drift between re-partitions
-        const int64_t capW = (c->world == 1) ? std::max<int64_t>(n, 1) : sel + sel / 2 + 4096;
-        if (capW > ((int64_t)1 << 30)) return fail(ORCA_ERR_CAPACITY, "strip too large");
-        CKS(dom_alloc(c, d, (int)capW, d.nbins, capM, capH));
-        CK(cudaMemsetAsync(d.ctr, 0, CT_COUNT * sizeof(int), c->stream));
-        {
-            const int t = (int)(c->lpStep0 + c->steps_total - c->lpMark);  // LP-order step index
-            k_set_int<<<1, 1, 0, c->stream>>>(d.ctr + CT_STEP, t);
-        }
-        CK(cudaMemsetAsync(d.count, 0, d.nbins * sizeof(uint32_t), c->stream));
-        if (n > 0)
-            k_select<<<cap_blocks(n, 256), 256, 0, c->stream>>>((int)n, sp, sv, sa, d.g, d.posW, d.velW, d.auxW,
-                                                                d.idW, d.rk2W, d.cellW, d.rankW, d.count, d.ctr,
-                                                                d.capW, hist);
-        CK(cudaGetLastError());
-        CK(enqueue_scan(c, d));
-        CK(enqueue_scatter(c, d, 0));
-    }
-    CK(cudaStreamSynchronize(c->stream));
-    CKS(check_overflow(c));
-    c->ready = true;
-    return ORCA_OK;
+    return build_domains(c, n, sp, sv, sa, hist, nullptr);
 }
 
 orca_status orca_set_goals(orca_ctx* c, const float* goal, float prefSpeed) {
@@ -929,18 +1071,19 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
     if (n_steps < 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "n_steps < 0");
     if (n_steps == 0) return ORCA_OK;
     CK(cudaSetDevice(c->device));
-    {
-        std::vector<unsigned char> key = graph_key(c);
-        if (key != c->graphKey) {
-            drop_graph(c);
-            c->graphKey = std::move(key);
-        }
-    }
     // one graph of up to kChunk step bodies, replayed
     const int kChunk = 64;
     int remaining = n_steps;
     while (remaining > 0) {
         const int s = std::min(remaining, kChunk);
+        CKS(maybe_rebalance(c));  // strips only: capacities for the next chunk
+        {
+            std::vector<unsigned char> key = graph_key(c);
+            if (key != c->graphKey) {
+                drop_graph(c);
+                c->graphKey = std::move(key);
+            }
+        }
         cudaGraphExec_t exec = nullptr;
         for (auto& g : c->graphs)
             if (g.first == s) exec = g.second;
@@ -977,6 +1120,7 @@ orca_status orca_step_timed(orca_ctx* c, int32_t n_steps, double ms[4]) {
     CK(cudaSetDevice(c->device));
     for (int q = 0; q < 4; ++q) ms[q] = 0.0;
     for (int s = 0; s < n_steps; ++s) {
+        if (s % 64 == 0) CKS(maybe_rebalance(c));
         CKS(enqueue_step(c, c->ev));
         CK(cudaEventSynchronize(c->ev[4]));
         float t;
@@ -1193,6 +1337,7 @@ orca_status orca_get_stats(orca_ctx* c, orca_stats* out) {
     out->marginal = (int64_t)t[ST_G3];
     out->collision_pairs = (int64_t)t[ST_COLLISION];
     out->removed = (int64_t)t[ST_REMOVED];
+    out->rebalances = c->rebalances;
     if (c->ready) CKS(check_overflow(c));
     return ORCA_OK;
 }
@@ -1334,6 +1479,21 @@ cudaError_t write_lp_step(orca_ctx* c) {
         if (e != cudaSuccess) return e;
     }
     return cudaStreamSynchronize(c->stream);
+}
+
+orca_status orca_rebalance(orca_ctx* c) {
+    if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    if (c->world == 1) return ORCA_OK;
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    CKS(check_overflow(c));
+    if (c->reportCap < 3 * (int)c->doms.size() + 4) {
+        dfree(c->report);
+        CK(cudaMalloc(&c->report, (size_t)(3 * c->doms.size() + 4) * sizeof(int)));
+        c->reportCap = 3 * (int)c->doms.size() + 4;
+    }
+    return rebalance(c);
 }
 
 orca_status orca_set_lp3_lanes(orca_ctx* c, int32_t lanes) {

@@ -140,8 +140,10 @@ __global__ void k_select(int n, const float2* __restrict__ pos, const float2* __
                          const float2* __restrict__ aux, Grid g, float2* __restrict__ posW, float2* __restrict__ velW,
                          float2* __restrict__ auxW, uint32_t* __restrict__ idW, float* __restrict__ rk2W,
                          uint32_t* __restrict__ cellW, uint32_t* __restrict__ rankW, uint32_t* __restrict__ count,
-                         int* __restrict__ ctr, int capW, const float* __restrict__ hist) {
+                         int* __restrict__ ctr, int capW, const float* __restrict__ hist,
+                         const uint8_t* __restrict__ active) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (active && !active[i]) continue;  // removed at its goal
         const float2 p = pos[i];
         const int cx = cell_coord(p.x, g.ox, g.csD, g.invCs, g.nx);
         if (cx < g.e0 || cx >= g.e1) continue;
@@ -169,6 +171,72 @@ __global__ void k_hist_by_id(const uint32_t* __restrict__ binStart, Grid g, cons
     const int o0 = (int)binStart[(g.c0 - g.e0) * nyS], o1 = (int)binStart[(g.c1 - g.e0) * nyS];
     for (int i = o0 + blockIdx.x * blockDim.x + threadIdx.x; i < o1; i += gridDim.x * blockDim.x)
         out[idS[i]] = rk2S[i];
+}
+
+// ---- strip rebalance: the owned agents of every strip back to by-id arrays
+// Owned agents -> by-id global arrays (pos, vel, aux, search-radius history) + active flag.
+__global__ void k_gather_state(const uint32_t* __restrict__ binStart, Grid g, const uint32_t* __restrict__ idS,
+                               const float2* __restrict__ posS, const float2* __restrict__ velS,
+                               const float2* __restrict__ auxS, const float* __restrict__ rk2S,
+                               float2* __restrict__ pos, float2* __restrict__ vel, float2* __restrict__ aux,
+                               float* __restrict__ rk2, uint8_t* __restrict__ active) {
+    const int nyS = g.ny << g.lgS;
+    const int o0 = (int)binStart[(g.c0 - g.e0) * nyS], o1 = (int)binStart[(g.c1 - g.e0) * nyS];
+    for (int i = o0 + blockIdx.x * blockDim.x + threadIdx.x; i < o1; i += gridDim.x * blockDim.x) {
+        const uint32_t id = idS[i];
+        pos[id] = posS[i];
+        vel[id] = velS[i];
+        aux[id] = auxS[i];
+        rk2[id] = rk2S[i];
+        active[id] = 1;
+    }
+}
+
+// Owned agents -> fixed-size records for the all-gather between ranks: record q =
+// (id bits, rk2, pos.x, pos.y), (vel.x, vel.y, aux.x, aux.y); unused records have id ~0.
+__global__ void k_pack_owned(const uint32_t* __restrict__ binStart, Grid g, const uint32_t* __restrict__ idS,
+                             const float2* __restrict__ posS, const float2* __restrict__ velS,
+                             const float2* __restrict__ auxS, const float* __restrict__ rk2S,
+                             float4* __restrict__ out, int cap) {
+    const int nyS = g.ny << g.lgS;
+    const int o0 = (int)binStart[(g.c0 - g.e0) * nyS], o1 = (int)binStart[(g.c1 - g.e0) * nyS];
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < cap; q += gridDim.x * blockDim.x) {
+        const int i = o0 + q;
+        if (i < o1) {
+            const float2 p = posS[i], v = velS[i], x = auxS[i];
+            out[2 * q] = make_float4(__uint_as_float(idS[i]), rk2S[i], p.x, p.y);
+            out[2 * q + 1] = make_float4(v.x, v.y, x.x, x.y);
+        } else {
+            out[2 * q] = make_float4(__uint_as_float(0xffffffffu), 0.0f, 0.0f, 0.0f);
+        }
+    }
+}
+
+__global__ void k_unpack_gathered(const float4* __restrict__ in, int total, float2* __restrict__ pos,
+                                  float2* __restrict__ vel, float2* __restrict__ aux, float* __restrict__ rk2,
+                                  uint8_t* __restrict__ active) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
+        const float4 a = in[2 * q];
+        const uint32_t id = __float_as_uint(a.x);
+        if (id == 0xffffffffu) continue;
+        const float4 b = in[2 * q + 1];
+        pos[id] = make_float2(a.z, a.w);
+        vel[id] = make_float2(b.x, b.y);
+        aux[id] = make_float2(b.z, b.w);
+        rk2[id] = a.y;
+        active[id] = 1;
+    }
+}
+
+// Fill report of a strip: owned agents and the populations of its two edge columns.
+__global__ void k_fill_report(const uint32_t* __restrict__ binStart, Grid g, int* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    const int nyS = g.ny << g.lgS;
+    const int b0 = (int)binStart[(g.c0 - g.e0) * nyS], b1 = (int)binStart[(g.c0 - g.e0 + 1) * nyS];
+    const int b2 = (int)binStart[(g.c1 - 1 - g.e0) * nyS], b3 = (int)binStart[(g.c1 - g.e0) * nyS];
+    out[0] = b3 - b0;
+    out[1] = b1 - b0;
+    out[2] = b3 - b2;
 }
 
 // Single-pass exclusive scan (decoupled look-back) over C bin counts: tiles of 4096
@@ -1538,9 +1606,10 @@ __global__ void k_receive(StepArgs a, ExBuf rL, ExBuf rR) {
 }
 
 // agents per grid column (strip partition at set_agents)
-__global__ void k_colhist(int n, const float2* __restrict__ pos, Grid g, int32_t* __restrict__ hist) {
+__global__ void k_colhist(int n, const float2* __restrict__ pos, Grid g, int32_t* __restrict__ hist,
+                          const uint8_t* __restrict__ active) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        atomicAdd(&hist[cell_coord(pos[i].x, g.ox, g.csD, g.invCs, g.nx)], 1);
+        if (!active || active[i]) atomicAdd(&hist[cell_coord(pos[i].x, g.ox, g.csD, g.invCs, g.nx)], 1);
 }
 
 // Block-partial min/max of the positions and a non-finite count over all input arrays.

@@ -27,7 +27,7 @@ EXPORTS = [
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
-    "orca_set_lp_order", "orca_set_lp3_lanes",
+    "orca_set_lp_order", "orca_set_lp3_lanes", "orca_rebalance",
 ]
 
 
@@ -46,7 +46,7 @@ class Params(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("steps", "agent_updates", "infeasible", "degenerate",
                                                "coincident", "eps_parallel", "marginal", "collision_pairs",
-                                               "removed")]
+                                               "removed", "rebalances")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -90,6 +90,7 @@ def _load():
         "orca_step_trace": [vp, i32, vp, vp],
         "orca_set_lp_order": [vp, i32, ctypes.c_uint64, i64],
         "orca_set_lp3_lanes": [vp, i32],
+        "orca_rebalance": [vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -292,6 +293,11 @@ class Orca:
     def set_goal_removal(self, radius: float):
         """Remove agents within `radius` of their goal after a step; 0 disables."""
         _check(_lib.orca_set_goal_removal(self._ctx, radius))
+
+    def rebalance(self):
+        """Re-partition the strips from the current state (automatic when a strip nears its
+        capacities; every rank must call it together)."""
+        _check(_lib.orca_rebalance(self._ctx))
 
     def set_lp3_lanes(self, lanes: int):
         """Lanes per infeasible agent in the LP3 kernel: 1 (thread), 4, 8 or 16; same results."""

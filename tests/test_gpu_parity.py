@@ -692,3 +692,62 @@ def test_graph_cache_across_set_agents(orca):
     assert np.array_equal(sa[0], sd[0]) and np.array_equal(sa[1], sd[1])
     for o in (a, b, c, d):
         o.close()
+
+
+# ------------------------------------------------ strip rebalance
+def test_strips_rebalance_carries_state(orca):
+    """orca_rebalance mid-run (heterogeneous agents, goals, removal at the goal, randomized LP
+    order): the strips are re-partitioned and the trajectory stays bit-identical to one strip."""
+    w = W.make("uniform", n=30000, rho=0.3)
+    n = len(w["pos"])
+    rng = np.random.default_rng(11)
+    goals = (w["pos"] + rng.uniform(-60, 60, w["pos"].shape)).astype(np.float32)
+    props = _het_props(n, seed=9)
+    ctxs = []
+    for strips in (0, 4):
+        o = orca.Orca(w["params"], strips=strips)
+        o.set_agents(w["pos"], w["vel"], w["pref"])
+        o.set_goals(goals, 1.0)
+        o.set_goal_removal(2.0)
+        o.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+        o.set_lp_order(True, 5, 0)
+        ctxs.append(o)
+    a, b = ctxs
+    for o in ctxs:
+        o.step(20)
+    b.rebalance()
+    assert b.stats()["rebalances"] >= 1
+    for o in ctxs:
+        o.step(30)
+    sa, sb = a.get_state(), b.get_state()
+    assert np.array_equal(sa[0], sb[0], equal_nan=True) and np.array_equal(sa[1], sb[1], equal_nan=True)
+    assert np.array_equal(a.active(), b.active()) and a.count() == b.count() < n
+    ta, tb = a.stats(), b.stats()
+    for key in ("infeasible", "degenerate", "collision_pairs", "removed"):
+        assert ta[key] == tb[key], key
+    for o in ctxs:
+        o.close()
+
+
+def test_strips_rebalance_convergent_crowd(orca):
+    """A crowd converging on one point piles into the middle strips: the automatic rebalance
+    re-partitions before any strip outgrows its buffers, and the run stays bit-identical to
+    one strip (no overflow error)."""
+    w = W.make("uniform", n=20000, rho=0.25)
+    centre = w["pos"].mean(axis=0)
+    goals = np.repeat(centre[None].astype(np.float32), len(w["pos"]), axis=0)
+    a = orca.Orca(w["params"])
+    b = orca.Orca(w["params"], strips=5)
+    for o in (a, b):
+        o.set_agents(w["pos"], w["vel"], w["pref"])
+        o.set_goals(goals, 1.0)
+    for _ in range(12):
+        a.step(64)
+        b.step(64)
+    sa, sb = a.get_state(), b.get_state()
+    assert np.array_equal(sa[0], sb[0]) and np.array_equal(sa[1], sb[1])
+    assert b.stats()["rebalances"] >= 1
+    # the crowd really converged: most agents within 80 m of the centre
+    assert np.mean(np.hypot(*(sa[0] - centre).T) < 80.0) > 0.8
+    for o in (a, b):
+        o.close()
