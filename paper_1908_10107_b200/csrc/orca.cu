@@ -104,8 +104,11 @@ NcclApi& nccl() {
     static NcclApi api;
     if (api.tried) return api;
     api.tried = true;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // ORCA_NCCL_LIB: an alternative implementation of the same API (the tests' host-staged
+    // stand-in, tests/fake_nccl, lets several processes share one GPU)
+    const char* alt = getenv("ORCA_NCCL_LIB");
+    void* h = (alt && *alt) ? dlopen(alt, RTLD_NOW | RTLD_LOCAL) : dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h && !(alt && *alt)) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) {
         api.err = std::string("dlopen libnccl.so.2: ") + dlerror();
