@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-suite", action="store_true", help="skip the other BASELINE workloads (N=1 only)")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="test only: all ranks on GPU 0 (gloo for torch, ORCA_NCCL_LIB=tests/fake_nccl for liborca)")
     ap.add_argument("--lp3-lanes", type=int, default=1, help="lanes per infeasible agent in the LP3 kernel")
     ap.add_argument("--variant", type=int, default=0, help="0: thread per agent, 1: 8-lane group per agent, 2: register top-k, 3: work-unit LP2")
     return ap.parse_args()
@@ -240,9 +242,14 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     assert world == args.gpus or world == 1, "launch N>1 with torchrun"
+    if args.shared_gpu:  # test mode: every rank on GPU 0, liborca's NCCL from ORCA_NCCL_LIB
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1908_10107_b200 import build as B
     if rank == 0:
         B.build()

@@ -88,3 +88,24 @@ def test_multirank_strips_bit_identical(orca, tmp_path, world, scenario):
         assert tot[k] == rs[k], k
     assert len(set(rebal)) == 1 and rebal[0] >= 1  # every rank rebalanced together
     ref.close()
+
+
+@pytest.mark.gpu
+def test_bench_multirank_shared_gpu(orca, tmp_path):
+    """bench.py's N>1 path (torchrun, per-rank strips, max-over-ranks timing, e2e gather) on
+    one GPU through the fake NCCL: one valid JSON line from rank 0."""
+    import json
+    lib = _build_fake()
+    env = dict(os.environ, ORCA_NCCL_LIB=lib)
+    root = os.path.dirname(HERE)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(29600 + secrets.randbelow(300)), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "4", "--warmup", "3", "--config", "uniform", "--e2e-steps", "2",
+           "--shared-gpu"]
+    r = subprocess.run(cmd, env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "strips2"
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["roofline"]["frac"] > 0
