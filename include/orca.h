@@ -264,6 +264,15 @@ orca_status orca_partition_columns(const int64_t *colCount, int32_t nx, int32_t 
  * contexts: no-op.  Synchronises.  Errors: NOT_READY, CUDA, NCCL, CAPACITY. */
 orca_status orca_rebalance(orca_ctx *ctx);
 
+/* Transport of the per-step strip exchange: 0 (default) = peer memory -- a
+ * k_push kernel stores exactly the used halo/migration records into the neighbour's receive
+ * buffer (cudaIpc mapping over NVLink between ranks; the neighbour strip's buffer in
+ * loopback) and raises an arrival flag the neighbour's k_receive waits on (bounded: a
+ * missing neighbour step is an error, never a hang); 1 = NCCL send/recv of the whole
+ * buffers (loopback: device copies), the baseline.  Multi-rank contexts: every rank must
+ * call it together.  Synchronises.  Errors: INVALID_ARGUMENT, CUDA, NCCL. */
+orca_status orca_set_transport(orca_ctx *ctx, int32_t mode);
+
 orca_status orca_get_strips(orca_ctx *ctx, int32_t *bounds);
 
 #ifdef __cplusplus

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 #include <new>
 #include <string>
 #include <vector>
@@ -38,6 +39,8 @@ int cap_blocks(int64_t n, int threads) {
 #ifndef ORCA_LP3_WAVES
 #define ORCA_LP3_WAVES 4
 #endif
+constexpr int kPushBlocks = 64;  // k_push grid (last-block completion)
+
 int lp3_blocks(int64_t n) {
     const int64_t need = (n + kStepThreads - 1) / kStepThreads;
     return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)148 * 7 * ORCA_LP3_WAVES));
@@ -198,8 +201,25 @@ struct Domain {
     int* ctr = nullptr;
     unsigned long long* stats = nullptr;
     ExAlloc sendL, sendR, recvL, recvR;
+    // peer-memory transport: receive buffers of odd steps, the neighbours' receive buffers
+    // as seen from here ([parity]), cudaIpc mappings to close, k_push completion counters
+    ExAlloc recvL1, recvR1;
+    ExBuf peerL[2] = {}, peerR[2] = {};
+    void* ipcOpen[4] = {};
+    unsigned int* pushDone = nullptr;
+
+    void close_ipc() {
+        for (void*& p : ipcOpen)
+            if (p) {
+                cudaIpcCloseMemHandle(p);
+                p = nullptr;
+            }
+    }
 
     void release() {
+        close_ipc();
+        dfree(pushDone);
+        for (ExAlloc* x : {&recvL1, &recvR1}) dfree(x->base);
         float2** f2[] = {&posS, &velS, &auxS, &posW, &velW, &auxW};
         uint32_t** u4[] = {&idS, &idW, &cellW, &rankW, &count, &binStart};
         for (auto p : f2) dfree(*p);
@@ -267,6 +287,8 @@ struct orca_ctx {
     int* report = nullptr;
     int reportCap = 0;
     int64_t rebalances = 0;
+    int transport = 0;  // 0: peer memory (k_push / cudaIpc), 1: NCCL send/recv (loopback: copies)
+    unsigned char* ipcStage = nullptr;  // device staging of the cudaIpc handles for the all-gather
 };
 
 namespace {
@@ -374,11 +396,20 @@ orca_status dom_alloc(orca_ctx* c, Domain& d, int capW, int64_t nbins, int capM,
     if (d.g.hasL) {
         CKS(ex_alloc(d.sendL, capM, capH));
         CKS(ex_alloc(d.recvL, capM, capH));
+        CKS(ex_alloc(d.recvL1, capM, capH));
     }
     if (d.g.hasR) {
         CKS(ex_alloc(d.sendR, capM, capH));
         CKS(ex_alloc(d.recvR, capM, capH));
+        CKS(ex_alloc(d.recvR1, capM, capH));
     }
+    if (!d.pushDone) {
+        CK(cudaMalloc(&d.pushDone, 2 * sizeof(unsigned int)));
+        CK(cudaMemset(d.pushDone, 0, 2 * sizeof(unsigned int)));
+    }
+    // arrival flags restart with the exchange sequence number (CT_XSTEP = 0)
+    for (ExAlloc* x : {&d.recvL, &d.recvL1, &d.recvR, &d.recvR1})
+        if (x->base) CK(cudaMemsetAsync(x->b.hdr, 0, 16, c->stream));
     return ORCA_OK;
 }
 
@@ -398,17 +429,20 @@ std::vector<unsigned char> graph_key(orca_ctx* c) {
         const unsigned char* b = static_cast<const unsigned char*>(p);
         k.insert(k.end(), b, b + n);
     };
-    const int hdr[6] = {c->variant, c->lp3Lanes, c->smemBytes, c->world, c->loopback ? 1 : 0, (int)c->doms.size()};
+    const int hdr[7] = {c->variant, c->lp3Lanes, c->smemBytes, c->world, c->loopback ? 1 : 0, (int)c->doms.size(),
+                        c->transport};
     put(hdr, sizeof hdr);
     for (Domain& d : c->doms) {
         const StepArgs a = make_args(c, d);
         put(&a, sizeof a);
         put(&d.capW, sizeof d.capW);
         put(&d.nbins, sizeof d.nbins);
-        for (const ExAlloc* x : {&d.sendL, &d.sendR, &d.recvL, &d.recvR}) {
+        for (const ExAlloc* x : {&d.sendL, &d.sendR, &d.recvL, &d.recvR, &d.recvL1, &d.recvR1}) {
             put(&x->base, sizeof x->base);
             put(&x->bytes, sizeof x->bytes);
         }
+        put(d.peerL, sizeof d.peerL);
+        put(d.peerR, sizeof d.peerR);
     }
     return k;
 }
@@ -473,6 +507,16 @@ cudaError_t enqueue_scatter(orca_ctx* c, Domain& d, int bump) {
 // group of send/recv with ranks +-1.
 orca_status enqueue_exchange(orca_ctx* c) {
     if (c->world == 1) return ORCA_OK;
+    if (c->transport == 0) {  // peer memory: exact-size remote stores + arrival flags
+        for (Domain& d : c->doms) {
+            if (d.g.hasL)
+                k_push<<<kPushBlocks, 256, 0, c->stream>>>(d.sendL.b, d.peerL[0], d.peerL[1], d.ctr, d.pushDone);
+            if (d.g.hasR)
+                k_push<<<kPushBlocks, 256, 0, c->stream>>>(d.sendR.b, d.peerR[0], d.peerR[1], d.ctr, d.pushDone + 1);
+        }
+        CK(cudaGetLastError());
+        return ORCA_OK;
+    }
     if (c->loopback) {
         const int P = (int)c->doms.size();
         for (int s = 0; s < P; ++s) {
@@ -525,7 +569,8 @@ orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
             StepArgs a = make_args(c, d);
             const int capX = (d.g.hasL ? d.recvL.b.capM + d.recvL.b.capH : 0) +
                              (d.g.hasR ? d.recvR.b.capM + d.recvR.b.capH : 0);
-            k_receive<<<cap_blocks(capX, 256), 256, 0, c->stream>>>(a, d.recvL.b, d.recvR.b);
+            k_receive<<<cap_blocks(capX, 256), 256, 0, c->stream>>>(a, d.recvL.b, d.recvL1.b, d.recvR.b,
+                                                                    d.recvR1.b, c->transport == 0 ? 1 : 0);
         }
     }
     CK(cudaGetLastError());
@@ -558,6 +603,9 @@ orca_status check_overflow(orca_ctx* c) {
         CK(cudaStreamSynchronize(c->stream));
         any |= f;
     }
+    if (any & OVF_TIMEOUT)
+        return fail(ORCA_ERR_INTERNAL, "strip exchange timed out waiting for a neighbour's step (every rank must "
+                                       "call orca_step with the same counts)");
     if (any)
         return fail(ORCA_ERR_CAPACITY, std::string("strip buffer overflow (") + ((any & OVF_WORK) ? "work " : "") +
                                            ((any & OVF_MIG) ? "migrants " : "") + ((any & OVF_HALO) ? "halo" : "") +
@@ -643,6 +691,85 @@ orca_status stage_bounds(orca_ctx* c, const float2* a, const float2* b, const fl
     return ORCA_OK;
 }
 
+// ExBuf of a neighbour's receive buffer mapped at `base`: same layout as the local
+// template (exchange capacities are global, so every strip's buffers share one layout).
+ExBuf rebase(const ExAlloc& tmpl, void* base) {
+    ExBuf b = tmpl.b;
+    const char* t = static_cast<const char*>(tmpl.base);
+    char* n = static_cast<char*>(base);
+    auto mv = [&](auto*& p) {
+        using P = std::remove_reference_t<decltype(p)>;
+        p = reinterpret_cast<P>(n + (reinterpret_cast<const char*>(p) - t));
+    };
+    mv(b.hdr);
+    mv(b.mpos);
+    mv(b.mvel);
+    mv(b.maux);
+    mv(b.mid);
+    mv(b.mrk2);
+    mv(b.hpos);
+    mv(b.hvel);
+    mv(b.hid);
+    mv(b.mprop);
+    mv(b.hrad);
+    return b;
+}
+
+// Peer-memory transport: where every strip's k_push writes.  Loopback: the
+// neighbour strip's receive buffers.  Ranks: cudaIpc handles of every rank's four receive
+// buffers are all-gathered over NCCL (a collective: all ranks call it together, after their
+// arrival flags were reset), and the neighbours' buffers are mapped (NVLink peer access).
+orca_status setup_peers(orca_ctx* c) {
+    if (c->world == 1 || c->transport != 0) return ORCA_OK;
+    if (c->loopback) {
+        const int P = (int)c->doms.size();
+        for (int s = 0; s < P; ++s) {
+            Domain& d = c->doms[s];
+            if (d.g.hasL) {
+                d.peerL[0] = c->doms[s - 1].recvR.b;
+                d.peerL[1] = c->doms[s - 1].recvR1.b;
+            }
+            if (d.g.hasR) {
+                d.peerR[0] = c->doms[s + 1].recvL.b;
+                d.peerR[1] = c->doms[s + 1].recvL1.b;
+            }
+        }
+        return ORCA_OK;
+    }
+    Domain& d = c->doms[0];
+    struct Handles {
+        cudaIpcMemHandle_t h[4];  // recvL (even, odd), recvR (even, odd)
+    };
+    Handles mine;
+    std::memset(&mine, 0, sizeof mine);
+    const ExAlloc* xs[4] = {&d.recvL, &d.recvL1, &d.recvR, &d.recvR1};
+    for (int q = 0; q < 4; ++q)
+        if (xs[q]->base) CK(cudaIpcGetMemHandle(&mine.h[q], xs[q]->base));
+    const size_t hb = sizeof(Handles);
+    if (!c->ipcStage) CK(cudaMalloc(&c->ipcStage, hb * (c->world + 1)));
+    CK(cudaMemcpyAsync(c->ipcStage, &mine, hb, cudaMemcpyHostToDevice, c->stream));
+    NcclApi& N = nccl();
+    ncclResult_t r = N.allGather(c->ipcStage, c->ipcStage + hb, hb, ncclUint8, c->comm, c->stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather (cudaIpc handles)");
+    std::vector<Handles> all(c->world);
+    CK(cudaMemcpyAsync(all.data(), c->ipcStage + hb, hb * c->world, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    d.close_ipc();
+    std::memset(d.peerL, 0, sizeof d.peerL);
+    std::memset(d.peerR, 0, sizeof d.peerR);
+    for (int p = 0; p < 2; ++p) {
+        if (d.g.hasL) {  // the left neighbour's right-side receive buffers
+            CK(cudaIpcOpenMemHandle(&d.ipcOpen[p], all[c->rank - 1].h[2 + p], cudaIpcMemLazyEnablePeerAccess));
+            d.peerL[p] = rebase(d.recvL, d.ipcOpen[p]);
+        }
+        if (d.g.hasR) {  // the right neighbour's left-side receive buffers
+            CK(cudaIpcOpenMemHandle(&d.ipcOpen[2 + p], all[c->rank + 1].h[p], cudaIpcMemLazyEnablePeerAccess));
+            d.peerR[p] = rebase(d.recvR, d.ipcOpen[2 + p]);
+        }
+    }
+    return ORCA_OK;
+}
+
 // Strips from the global by-id arrays (every rank holds the same arrays): column histogram
 // of the active agents -> partition -> per-strip capacities, selection, scan, scatter.
 // The grid (c->gg) is frozen; hist (nullable) seeds the per-agent search radius; active
@@ -714,6 +841,7 @@ orca_status build_domains(orca_ctx* c, int64_t n, const float2* sp, const float2
     }
     CK(cudaStreamSynchronize(c->stream));
     CKS(check_overflow(c));
+    CKS(setup_peers(c));
     c->ready = true;
     return ORCA_OK;
 }
@@ -961,6 +1089,7 @@ void orca_destroy(orca_ctx* c) {
     dfree(c->props4);
     dfree(c->activeBuf);
     dfree(c->gatherBuf);
+    dfree(c->ipcStage);
     dfree(c->report);
     for (auto& b : c->traceBuf) dfree(b);
     for (int b = 0; b < 2; ++b) {
@@ -1482,6 +1611,25 @@ cudaError_t write_lp_step(orca_ctx* c) {
         if (e != cudaSuccess) return e;
     }
     return cudaStreamSynchronize(c->stream);
+}
+
+orca_status orca_set_transport(orca_ctx* c, int32_t mode) {
+    if (!c || (mode != 0 && mode != 1)) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    if (mode == c->transport) return ORCA_OK;
+    c->transport = mode;
+    if (c->ready && c->world > 1) {
+        // a new exchange sequence on every strip: counters and arrival flags from zero
+        for (Domain& d : c->doms) {
+            k_set_int<<<1, 1, 0, c->stream>>>(d.ctr + CT_XSTEP, 0);
+            for (ExAlloc* x : {&d.recvL, &d.recvL1, &d.recvR, &d.recvR1})
+                if (x->base) CK(cudaMemsetAsync(x->b.hdr, 0, 16, c->stream));
+        }
+        CK(cudaStreamSynchronize(c->stream));
+        CKS(setup_peers(c));
+    }
+    return ORCA_OK;
 }
 
 orca_status orca_rebalance(orca_ctx* c) {

@@ -115,8 +115,10 @@ __device__ __forceinline__ uint32_t bin_of(int cx, int sy, const Grid& g) {
 constexpr uint32_t kInvalid = 0xffffffffu;  // work entry that left the strip
 
 // per-domain device counters
-enum { CT_NOWN = 0, CT_EXTRA, CT_OVF, CT_STEP, CT_COUNT };  // CT_STEP: steps since set_agents
-constexpr int OVF_WORK = 1, OVF_MIG = 2, OVF_HALO = 4;
+// CT_STEP: the LP-order step index; CT_XSTEP: steps since the strips were built (the
+// exchange sequence number, equal on every rank)
+enum { CT_NOWN = 0, CT_EXTRA, CT_OVF, CT_STEP, CT_XSTEP, CT_COUNT };
+constexpr int OVF_WORK = 1, OVF_MIG = 2, OVF_HALO = 4, OVF_TIMEOUT = 8;
 
 // One direction of the neighbour exchange (fixed capacity; one NCCL send per step):
 // hdr = {emigrants, halo agents}; emigrants carry the full state, halo agents only what a
@@ -331,7 +333,10 @@ __global__ void k_scatter(int* __restrict__ ctr, int bump, const uint32_t* __res
                           float2* __restrict__ auxS, uint32_t* __restrict__ idS, float* __restrict__ rk2S, int capW,
                           const float4* __restrict__ propW, float4* __restrict__ propS) {
     const int n = min(ctr[CT_NOWN] + ctr[CT_EXTRA], capW);
-    if (bump && blockIdx.x == 0 && threadIdx.x == 0) ctr[CT_STEP] += 1;  // the step is complete
+    if (bump && blockIdx.x == 0 && threadIdx.x == 0) {  // the step is complete
+        ctr[CT_STEP] += 1;
+        ctr[CT_XSTEP] += 1;
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t c = cell[i];
         if (c == kInvalid) continue;
@@ -1575,7 +1580,78 @@ __global__ void k_gather_by_id(const uint32_t* __restrict__ binStart, int nbins,
 
 // Received neighbour data -> work buffers: emigrants of the neighbour become owned agents,
 // halo agents become ghosts (their columns decide which; both are just appended).
-__global__ void k_receive(StepArgs a, ExBuf rL, ExBuf rR) {
+// Peer-memory exchange: copy the used records of a local send buffer into
+// the neighbour's receive buffer of this step's parity -- remote stores over NVLink (a
+// cudaIpc mapping between ranks; the neighbour strip's own buffer in loopback) -- and, once
+// every block's stores are fenced system-wide, publish the counts and the arrival flag
+// hdr[3] = step + 1.  Receive buffers alternate by step parity, so a fast sender never
+// overwrites what a slow receiver is still reading (it has waited for that receiver's next
+// step in between).
+__global__ void k_push(ExBuf s, ExBuf d0, ExBuf d1, const int* __restrict__ ctr, unsigned int* __restrict__ done) {
+    const int t = ctr[CT_XSTEP];
+    const ExBuf& d = (t & 1) ? d1 : d0;
+    const int nM = min(s.hdr[0], s.capM), nH = min(s.hdr[1], s.capH);
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nM + nH; q += gridDim.x * blockDim.x) {
+        if (q < nM) {
+            d.mpos[q] = s.mpos[q];
+            d.mvel[q] = s.mvel[q];
+            d.maux[q] = s.maux[q];
+            d.mid[q] = s.mid[q];
+            d.mrk2[q] = s.mrk2[q];
+            d.mprop[q] = s.mprop[q];
+        } else {
+            const int h = q - nM;
+            d.hpos[h] = s.hpos[h];
+            d.hvel[h] = s.hvel[h];
+            d.hid[h] = s.hid[h];
+            d.hrad[h] = s.hrad[h];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(done, 1u) == gridDim.x - 1) {  // last block: every record is out
+            volatile int* h = d.hdr;
+            h[0] = s.hdr[0];
+            h[1] = s.hdr[1];
+            __threadfence_system();
+            h[3] = t + 1;
+            *done = 0u;
+        }
+    }
+}
+
+// Wait (bounded) until the neighbour's records of this step have arrived (flag hdr[3]).
+__device__ __forceinline__ void wait_arrival(const ExBuf& b, int want, int* ctr) {
+    volatile const int* f = b.hdr + 3;
+    long long spins = 0;
+    while (*f < want) {
+        __nanosleep(200);
+        if (++spins > 50000000ll) {  // ~10 s: a missing neighbour step -> error, never a hang
+            atomicOr(&ctr[CT_OVF], OVF_TIMEOUT);
+            break;
+        }
+    }
+}
+
+// Append the received emigrants (owned) and halo agents (ghosts) to the work arrays.  wait:
+// peer-memory transport (buffers of this step's parity, arrival flags); else the buffers
+// were filled in stream order (NCCL / loopback copies) and rL0 / rR0 are used.
+__global__ void k_receive(StepArgs a, ExBuf rL0, ExBuf rL1, ExBuf rR0, ExBuf rR1, int wait) {
+    const int xt = a.ctr[CT_XSTEP];
+    const ExBuf rL = (wait && (xt & 1)) ? rL1 : rL0;
+    const ExBuf rR = (wait && (xt & 1)) ? rR1 : rR0;
+    if (wait) {
+        __shared__ int ok;
+        if (threadIdx.x == 0) {
+            if (a.g.hasL) wait_arrival(rL, xt + 1, a.ctr);
+            if (a.g.hasR) wait_arrival(rR, xt + 1, a.ctr);
+            __threadfence_system();
+            ok = 1;
+        }
+        __syncthreads();
+        (void)ok;
+    }
     const int nOwn = a.ctr[CT_NOWN];
     const int mL = a.g.hasL ? min(rL.hdr[0], rL.capM) : 0, hL = a.g.hasL ? min(rL.hdr[1], rL.capH) : 0;
     const int mR = a.g.hasR ? min(rR.hdr[0], rR.capM) : 0, hR = a.g.hasR ? min(rR.hdr[1], rR.capH) : 0;

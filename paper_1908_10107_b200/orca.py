@@ -27,7 +27,7 @@ EXPORTS = [
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
-    "orca_set_lp_order", "orca_set_lp3_lanes", "orca_rebalance",
+    "orca_set_lp_order", "orca_set_lp3_lanes", "orca_rebalance", "orca_set_transport",
 ]
 
 
@@ -91,6 +91,7 @@ def _load():
         "orca_set_lp_order": [vp, i32, ctypes.c_uint64, i64],
         "orca_set_lp3_lanes": [vp, i32],
         "orca_rebalance": [vp],
+        "orca_set_transport": [vp, i32],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -293,6 +294,11 @@ class Orca:
     def set_goal_removal(self, radius: float):
         """Remove agents within `radius` of their goal after a step; 0 disables."""
         _check(_lib.orca_set_goal_removal(self._ctx, radius))
+
+    def set_transport(self, mode: int):
+        """Strip exchange: 0 = peer memory (k_push + arrival flags, default), 1 = NCCL
+        send/recv (loopback: device copies); every rank must call it together."""
+        _check(_lib.orca_set_transport(self._ctx, mode))
 
     def rebalance(self):
         """Re-partition the strips from the current state (automatic when a strip nears its

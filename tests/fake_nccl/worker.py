@@ -16,6 +16,7 @@ rank, world, uid, out, scenario = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3
 nid = uid.encode().ljust(128, b"\0")
 w, run = S.SCENARIOS[scenario]()
 ctx = O.Orca(w["params"], device=0, rank=rank, world=world, nccl_id=nid)
+ctx.set_transport(int(os.environ.get("ORCA_TEST_TRANSPORT", "0")))
 run(ctx, w)
 ids, pos, vel = ctx.get_local_state()
 st = ctx.stats()

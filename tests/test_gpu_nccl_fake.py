@@ -41,11 +41,14 @@ def orca():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,scenario", [(2, "uniform"), (3, "uniform"), (4, "convergent")])
-def test_multirank_strips_bit_identical(orca, tmp_path, world, scenario):
+@pytest.mark.parametrize("world,scenario,transport", [(2, "uniform", 0), (3, "uniform", 0), (4, "convergent", 0),
+                                                      (3, "uniform", 1), (4, "convergent", 1)])
+def test_multirank_strips_bit_identical(orca, tmp_path, world, scenario, transport):
+    """transport 0: peer memory (k_push into cudaIpc-mapped receive buffers + arrival flags);
+    1: ncclSend/ncclRecv of the whole buffers (through the stand-in)."""
     lib = _build_fake()
     uid = "/orca_fake_" + secrets.token_hex(8)
-    env = dict(os.environ, ORCA_NCCL_LIB=lib)
+    env = dict(os.environ, ORCA_NCCL_LIB=lib, ORCA_TEST_TRANSPORT=str(transport))
     procs, outs = [], []
     for r in range(world):
         out = str(tmp_path / f"rank{r}.npz")

@@ -751,3 +751,27 @@ def test_strips_rebalance_convergent_crowd(orca):
     assert np.mean(np.hypot(*(sa[0] - centre).T) < 80.0) > 0.8
     for o in (a, b):
         o.close()
+
+
+def test_strips_transports_bit_identical(orca):
+    """Loopback strips with the peer-memory exchange (k_push + arrival flags, default) and with
+    whole-buffer device copies: identical trajectories, also across a switch mid-run."""
+    w = W.make("uniform", n=30000, rho=0.35)
+    a = orca.Orca(w["params"], strips=4)
+    b = orca.Orca(w["params"], strips=4)
+    b.set_transport(1)
+    for o in (a, b):
+        o.set_agents(w["pos"], w["vel"], w["pref"])
+        o.step(40)
+    a.set_transport(1)
+    b.set_transport(0)
+    for o in (a, b):
+        o.step(30)
+    sa, sb = a.get_state(), b.get_state()
+    assert np.array_equal(sa[0], sb[0]) and np.array_equal(sa[1], sb[1])
+    c, _ = _ctx(orca, w)
+    c.step(70)
+    sc = c.get_state()
+    assert np.array_equal(sa[0], sc[0]) and np.array_equal(sa[1], sc[1])
+    for o in (a, b, c):
+        o.close()
