@@ -451,7 +451,8 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": w["name"], "n_agents": n_total, "rho": rho, **w["params"],
                    "l2": "flushed between timed steps (512 MiB write); per-step CUDA events on the library stream",
-                   "parallelism": f"strips{world}" if world > 1 else "single"},
+                   "parallelism": f"strips{world}" if world > 1 else "single",
+                   "exchange": ("peer-memory" if ctx.transport() == 0 else "nccl") if world > 1 else None},
         "ms_per_step_l2_resident": ms_res,
         "ms_per_step_median_min_max": per_step_stats,
         "gpu_launches": (4 if world == 1 else 5) * args.steps,

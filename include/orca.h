@@ -273,6 +273,10 @@ orca_status orca_rebalance(orca_ctx *ctx);
  * call it together.  Synchronises.  Errors: INVALID_ARGUMENT, CUDA, NCCL. */
 orca_status orca_set_transport(orca_ctx *ctx, int32_t mode);
 
+/* The transport in use (0 / 1 as above).  A multi-rank context falls back from 0 to 1 on
+ * every rank when some pair of neighbouring GPUs cannot map each other's memory. */
+orca_status orca_get_transport(orca_ctx *ctx, int32_t *mode);
+
 orca_status orca_get_strips(orca_ctx *ctx, int32_t *bounds);
 
 #ifdef __cplusplus

@@ -757,15 +757,34 @@ orca_status setup_peers(orca_ctx* c) {
     d.close_ipc();
     std::memset(d.peerL, 0, sizeof d.peerL);
     std::memset(d.peerR, 0, sizeof d.peerR);
-    for (int p = 0; p < 2; ++p) {
+    int ok = 1;
+    for (int p = 0; p < 2 && ok; ++p) {
         if (d.g.hasL) {  // the left neighbour's right-side receive buffers
-            CK(cudaIpcOpenMemHandle(&d.ipcOpen[p], all[c->rank - 1].h[2 + p], cudaIpcMemLazyEnablePeerAccess));
-            d.peerL[p] = rebase(d.recvL, d.ipcOpen[p]);
+            if (cudaIpcOpenMemHandle(&d.ipcOpen[p], all[c->rank - 1].h[2 + p], cudaIpcMemLazyEnablePeerAccess) ==
+                cudaSuccess)
+                d.peerL[p] = rebase(d.recvL, d.ipcOpen[p]);
+            else
+                ok = 0;
         }
-        if (d.g.hasR) {  // the right neighbour's left-side receive buffers
-            CK(cudaIpcOpenMemHandle(&d.ipcOpen[2 + p], all[c->rank + 1].h[p], cudaIpcMemLazyEnablePeerAccess));
-            d.peerR[p] = rebase(d.recvR, d.ipcOpen[2 + p]);
+        if (ok && d.g.hasR) {  // the right neighbour's left-side receive buffers
+            if (cudaIpcOpenMemHandle(&d.ipcOpen[2 + p], all[c->rank + 1].h[p], cudaIpcMemLazyEnablePeerAccess) ==
+                cudaSuccess)
+                d.peerR[p] = rebase(d.recvR, d.ipcOpen[2 + p]);
+            else
+                ok = 0;
         }
+    }
+    // no peer mapping between some pair of GPUs: every rank falls back to NCCL together
+    cudaGetLastError();
+    int* flag = reinterpret_cast<int*>(c->ipcStage);
+    CK(cudaMemcpyAsync(flag, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    r = N.allReduce(flag, flag, 1, ncclInt32, ncclMin, c->comm, c->stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce (peer mapping)");
+    CK(cudaMemcpyAsync(&ok, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (!ok) {
+        d.close_ipc();
+        c->transport = 1;
     }
     return ORCA_OK;
 }
@@ -1629,6 +1648,12 @@ orca_status orca_set_transport(orca_ctx* c, int32_t mode) {
         CK(cudaStreamSynchronize(c->stream));
         CKS(setup_peers(c));
     }
+    return ORCA_OK;
+}
+
+orca_status orca_get_transport(orca_ctx* c, int32_t* mode) {
+    if (!c || !mode) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
+    *mode = c->transport;
     return ORCA_OK;
 }
 

@@ -28,6 +28,7 @@ EXPORTS = [
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
     "orca_set_lp_order", "orca_set_lp3_lanes", "orca_rebalance", "orca_set_transport",
+    "orca_get_transport",
 ]
 
 
@@ -92,6 +93,7 @@ def _load():
         "orca_set_lp3_lanes": [vp, i32],
         "orca_rebalance": [vp],
         "orca_set_transport": [vp, i32],
+        "orca_get_transport": [vp, P(i32)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -299,6 +301,11 @@ class Orca:
         """Strip exchange: 0 = peer memory (k_push + arrival flags, default), 1 = NCCL
         send/recv (loopback: device copies); every rank must call it together."""
         _check(_lib.orca_set_transport(self._ctx, mode))
+
+    def transport(self) -> int:
+        m = ctypes.c_int32()
+        _check(_lib.orca_get_transport(self._ctx, ctypes.byref(m)))
+        return m.value
 
     def rebalance(self):
         """Re-partition the strips from the current state (automatic when a strip nears its

@@ -111,4 +111,5 @@ def test_bench_multirank_shared_gpu(orca, tmp_path):
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "strips2"
+    assert d["config"]["exchange"] == "peer-memory"
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["roofline"]["frac"] > 0
