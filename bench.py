@@ -455,7 +455,10 @@ def run_ours(args):
                    "exchange": ("peer-memory" if ctx.transport() == 0 else "nccl") if world > 1 else None},
         "ms_per_step_l2_resident": ms_res,
         "ms_per_step_median_min_max": per_step_stats,
-        "gpu_launches": (4 if world == 1 else 5) * args.steps,
+        # per step: k_step, k_lp3, k_scan, k_scatter (+ strips: k_receive and one k_push per
+        # neighbour with the peer-memory exchange)
+        "gpu_launches": (4 if world == 1 else
+                         5 + ((2 if 0 < rank < world - 1 else 1) if ctx.transport() == 0 else 0)) * args.steps,
         "kernel_variant": args.variant, "k_step_ms_by_variant": variant_ms,
         "lp3_lanes": args.lp3_lanes, "k_step_ms_by_lp3_lanes": lp3_ms,
         "roofline": roofline, "hbm_context": hbm,
