@@ -407,8 +407,8 @@ orca_status dom_alloc(orca_ctx* c, Domain& d, int capW, int64_t nbins, int capM,
         CK(cudaMalloc(&d.pushDone, 2 * sizeof(unsigned int)));
         CK(cudaMemset(d.pushDone, 0, 2 * sizeof(unsigned int)));
     }
-    // arrival flags restart with the exchange sequence number (CT_XSTEP = 0)
-    for (ExAlloc* x : {&d.recvL, &d.recvL1, &d.recvR, &d.recvR1})
+    // arrival flags restart with the exchange sequence number (CT_XSTEP = 0); send buffers empty
+    for (ExAlloc* x : {&d.recvL, &d.recvL1, &d.recvR, &d.recvR1, &d.sendL, &d.sendR})
         if (x->base) CK(cudaMemsetAsync(x->b.hdr, 0, 16, c->stream));
     return ORCA_OK;
 }
@@ -484,11 +484,14 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
         k_step<DRY, 16><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
 }
 
-cudaError_t enqueue_scan(orca_ctx* c, Domain& d) {
+// zero: clear the status words, tile ticket and LP3 queue count first (at set-up); in the
+// step body the previous step's k_scatter has already cleared them
+cudaError_t enqueue_scan(orca_ctx* c, Domain& d, bool zero) {
     const int tiles = scan_tiles(d.nbins);
-    // status words, tile ticket and the LP3 queue count (consumed by k_lp3 before this point)
-    cudaError_t e = cudaMemsetAsync(d.scanStatus, 0, (tiles + 2) * sizeof(unsigned long long), c->stream);
-    if (e != cudaSuccess) return e;
+    if (zero) {
+        cudaError_t e = cudaMemsetAsync(d.scanStatus, 0, (tiles + 2) * sizeof(unsigned long long), c->stream);
+        if (e != cudaSuccess) return e;
+    }
     k_scan<<<tiles, 1024, 0, c->stream>>>(d.count, d.binStart, (int)d.nbins, d.scanStatus,
                                           reinterpret_cast<unsigned int*>(d.scanStatus + tiles));
     return cudaGetLastError();
@@ -498,7 +501,8 @@ cudaError_t enqueue_scatter(orca_ctx* c, Domain& d, int bump) {
     k_scatter<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.ctr, bump, d.cellW, d.rankW, d.binStart, d.posW, d.velW,
                                                               d.auxW, d.idW, d.rk2W, d.posS, d.velS, d.auxS, d.idS,
                                                               d.rk2S, d.capW, c->het ? d.propW : nullptr,
-                                                              c->het ? d.propS : nullptr);
+                                                              c->het ? d.propS : nullptr, d.scanStatus,
+                                                              scan_tiles(d.nbins) + 2);
     return cudaGetLastError();
 }
 
@@ -554,9 +558,10 @@ orca_status enqueue_exchange(orca_ctx* c) {
 orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
     if (ev) CK(cudaEventRecord(ev[0], c->stream));
     for (Domain& d : c->doms) {
-        CK(cudaMemsetAsync(d.ctr + CT_NOWN, 0, 2 * sizeof(int), c->stream));  // NOWN, EXTRA
-        if (d.g.hasL) CK(cudaMemsetAsync(d.sendL.b.hdr, 0, 16, c->stream));
-        if (d.g.hasR) CK(cudaMemsetAsync(d.sendR.b.hdr, 0, 16, c->stream));
+        if (c->transport != 0) {  // (the peer-memory k_push empties the send buffers itself)
+            if (d.g.hasL) CK(cudaMemsetAsync(d.sendL.b.hdr, 0, 16, c->stream));
+            if (d.g.hasR) CK(cudaMemsetAsync(d.sendR.b.hdr, 0, 16, c->stream));
+        }
         StepArgs a = make_args(c, d);
         launch_step<false>(c, d, a);
         launch_lp3<false>(c, d, a);
@@ -575,7 +580,7 @@ orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
     }
     CK(cudaGetLastError());
     if (ev) CK(cudaEventRecord(ev[2], c->stream));
-    for (Domain& d : c->doms) CK(enqueue_scan(c, d));
+    for (Domain& d : c->doms) CK(enqueue_scan(c, d, false));
     if (ev) CK(cudaEventRecord(ev[3], c->stream));
     for (Domain& d : c->doms) CK(enqueue_scatter(c, d, 1));
     if (ev) CK(cudaEventRecord(ev[4], c->stream));
@@ -855,7 +860,7 @@ orca_status build_domains(orca_ctx* c, int64_t n, const float2* sp, const float2
                                                                 d.idW, d.rk2W, d.cellW, d.rankW, d.count, d.ctr,
                                                                 d.capW, hist, active);
         CK(cudaGetLastError());
-        CK(enqueue_scan(c, d));
+        CK(enqueue_scan(c, d, true));
         CK(enqueue_scatter(c, d, 0));
     }
     CK(cudaStreamSynchronize(c->stream));
@@ -1642,7 +1647,7 @@ orca_status orca_set_transport(orca_ctx* c, int32_t mode) {
         // a new exchange sequence on every strip: counters and arrival flags from zero
         for (Domain& d : c->doms) {
             k_set_int<<<1, 1, 0, c->stream>>>(d.ctr + CT_XSTEP, 0);
-            for (ExAlloc* x : {&d.recvL, &d.recvL1, &d.recvR, &d.recvR1})
+            for (ExAlloc* x : {&d.recvL, &d.recvL1, &d.recvR, &d.recvR1, &d.sendL, &d.sendR})
                 if (x->base) CK(cudaMemsetAsync(x->b.hdr, 0, 16, c->stream));
         }
         CK(cudaStreamSynchronize(c->stream));

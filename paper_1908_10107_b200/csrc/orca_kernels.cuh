@@ -331,7 +331,12 @@ __global__ void k_scatter(int* __restrict__ ctr, int bump, const uint32_t* __res
                           const float2* __restrict__ auxW, const uint32_t* __restrict__ idW,
                           const float* __restrict__ rk2W, float2* __restrict__ posS, float2* __restrict__ velS,
                           float2* __restrict__ auxS, uint32_t* __restrict__ idS, float* __restrict__ rk2S, int capW,
-                          const float4* __restrict__ propW, float4* __restrict__ propS) {
+                          const float4* __restrict__ propW, float4* __restrict__ propS,
+                          unsigned long long* __restrict__ scanStatus, int nStatus) {
+    // the scan is done: clear its status words, tile ticket and the LP3 queue count for the
+    // next step (saves a memset node per step)
+    if (blockIdx.x == 0)
+        for (int q = threadIdx.x; q < nStatus; q += blockDim.x) scanStatus[q] = 0ull;
     const int n = min(ctr[CT_NOWN] + ctr[CT_EXTRA], capW);
     if (bump && blockIdx.x == 0 && threadIdx.x == 0) {  // the step is complete
         ctr[CT_STEP] += 1;
@@ -1088,7 +1093,10 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     const int i = o0 + ws;                // sorted index
     const bool active = i < o1;
     const unsigned activeMask = __ballot_sync(0xffffffffu, active);  // lanes that step an agent
-    if (!DRY && blockIdx.x == 0 && tid == 0) a.ctr[CT_NOWN] = o1 - o0;
+    if (!DRY && blockIdx.x == 0 && tid == 0) {  // per-step counters (k_receive appends after CT_NOWN)
+        a.ctr[CT_NOWN] = o1 - o0;
+        a.ctr[CT_EXTRA] = 0;
+    }
     uint32_t fl = 0;
     int nColl = 0;
     bool deferred = false;
@@ -1617,6 +1625,8 @@ __global__ void k_push(ExBuf s, ExBuf d0, ExBuf d1, const int* __restrict__ ctr,
             __threadfence_system();
             h[3] = t + 1;
             *done = 0u;
+            s.hdr[0] = 0;  // the local send buffer is empty again for the next step
+            s.hdr[1] = 0;
         }
     }
 }

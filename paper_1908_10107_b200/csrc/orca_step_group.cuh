@@ -191,7 +191,10 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
     const int ws = blockIdx.x * kGroupAgents + ag;
     const int i = o0 + ws;
     const bool active = i < o1;  // group-uniform
-    if (!DRY && blockIdx.x == 0 && tid == 0) a.ctr[CT_NOWN] = o1 - o0;
+    if (!DRY && blockIdx.x == 0 && tid == 0) {
+        a.ctr[CT_NOWN] = o1 - o0;
+        a.ctr[CT_EXTRA] = 0;
+    }
     uint32_t fl = 0;
     int nColl = 0;
     bool deferred = false;
