@@ -285,25 +285,37 @@ __global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uin
         }
         warpSums[lane] = wi - w;  // exclusive warp offsets
         const uint32_t total = __shfl_sync(0xffffffffu, wi, 31);
-        if (lane == 0) {
-            // publish the aggregate, look back for the inclusive prefix of earlier tiles
-            volatile unsigned long long* st = status;
-            if (tile == 0) {
+        // publish the aggregate, then a warp-parallel look-back: lane l reads the status of
+        // tile t - l; the nearest inclusive prefix ends the walk, else 32 aggregates are
+        // summed and the window moves 32 tiles back
+        volatile unsigned long long* st = status;
+        if (tile == 0) {
+            if (lane == 0) {
                 st[0] = kIncFlag | total;
                 prefixS = 0;
-            } else {
-                st[tile] = kAggFlag | total;
-                unsigned long long pre = 0;
-                int t = tile - 1;
-                while (true) {
-                    unsigned long long x;
+            }
+        } else {
+            if (lane == 0) st[tile] = kAggFlag | total;
+            unsigned long long pre = 0;
+            int t = tile - 1;
+            while (true) {
+                const int idx = t - lane;
+                unsigned long long x = kIncFlag;  // before tile 0: an inclusive zero
+                if (idx >= 0) {
                     do {
-                        x = st[t];
+                        x = st[idx];
                     } while ((x >> 62) == 0);
-                    pre += x & kValMask;
-                    if ((x >> 62) == 2) break;
-                    --t;
                 }
+                const unsigned inc = __ballot_sync(0xffffffffu, (x >> 62) == 2);
+                const int first = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive (or the window)
+                unsigned long long v = (lane <= first) ? (x & kValMask) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                pre += v;
+                if (inc) break;
+                t -= 32;
+            }
+            if (lane == 0) {
                 __threadfence();
                 st[tile] = kIncFlag | (pre + total);
                 prefixS = (uint32_t)pre;
