@@ -775,3 +775,27 @@ def test_strips_transports_bit_identical(orca):
     assert np.array_equal(sa[0], sc[0]) and np.array_equal(sa[1], sc[1])
     for o in (a, b, c):
         o.close()
+
+
+@pytest.mark.parametrize("offset", [(-3.0e4, 1.7e4), (6.5e4, -6.5e4)])
+def test_far_from_origin(orca, oracle, offset):
+    """A crowd tens of km from the origin (fp32 ulp of the coordinates ~ 4-8 mm, negative and
+    positive): cells and neighbour lists stay bit-exact, velocities within the bar."""
+    w = W.make("uniform", n=3000, rho=0.4)
+    pos = (w["pos"].astype(np.float64) + np.array(offset)).astype(np.float32)
+    compare_step(orca, oracle, dict(w, pos=pos))
+
+
+def test_grid_capacity_and_recovery(orca):
+    """A domain too large for the sort bins (two agents 10^7 m apart -> > 2^28 bins) is refused
+    with ORCA_ERR_CAPACITY; the context stays usable with a valid crowd afterwards."""
+    o = orca.Orca(W.DEFAULT_PARAMS)
+    far = np.array([[0.0, 0.0], [1.0e7, 1.0e7]], np.float32)
+    with pytest.raises(orca.OrcaError) as e:
+        o.set_agents(far, np.zeros_like(far), np.zeros_like(far))
+    assert e.value.status == 6
+    w = W.make("uniform", n=500, rho=0.2)
+    o.set_agents(w["pos"], w["vel"], w["pref"])
+    o.step(3)
+    assert o.count() == 500
+    o.close()
