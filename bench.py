@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-suite", action="store_true", help="skip the other BASELINE workloads (N=1 only)")
+    ap.add_argument("--no-multicore", action="store_true", help="skip the all-cores oracle baseline")
     ap.add_argument("--shared-gpu", action="store_true",
                     help="test only: all ranks on GPU 0 (gloo for torch, ORCA_NCCL_LIB=tests/fake_nccl for liborca)")
     ap.add_argument("--lp3-lanes", type=int, default=1, help="lanes per infeasible agent in the LP3 kernel")
@@ -150,6 +151,42 @@ def oracle_rate(w, seconds, rng_seed=0):
     return m / el, m, el
 
 
+_MC = {}
+
+
+def _mc_worker(chunk):
+    from oracle import oracle as O
+    w = _MC["w"]
+    p = O.make_params(**w["params"])
+    O.step(p, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"), pref_speed=w.get("pref_speed", 1.0),
+           agents=chunk)
+    return len(chunk)
+
+
+def oracle_rate_multicore(w, seconds, rate1):
+    """The same oracle on all host cores: P forked processes step disjoint parts of one agent
+    sample of the same state (each builds the bins of the full state, as a real multi-core
+    run would); wall-clock of the whole pool.  Returns (agents/s, sample, elapsed, P)."""
+    import multiprocessing as mp
+    try:
+        procs = len(os.sched_getaffinity(0))
+    except AttributeError:
+        procs = os.cpu_count() or 1
+    n = len(w["pos"])
+    m = int(min(n, max(2000, rate1 * seconds * procs * 0.7)))
+    rng = np.random.default_rng(12345)
+    sample = np.sort(rng.choice(n, m, replace=False))
+    chunks = np.array_split(sample, procs * 2)
+    _MC["w"] = w
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_mc_worker, chunks[:procs])  # warm the workers (imports, library load)
+        t0 = time.perf_counter()
+        done = sum(pool.map(_mc_worker, chunks))
+        el = time.perf_counter() - t0
+    return done / el, done, el, procs
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -218,6 +255,26 @@ def suite(orca, torch, peak_tops):
                      "infeasible_per_step": st["infeasible"] / max(1, st["steps"]),
                      "remaining": ctx.count() if w.get("goals") is not None else n}
         ctx.close()
+    # per-step trace dump (f4): 100 steps of 100k agents with every frame copied to
+    # pinned host memory on the copy stream, against the same 100 steps without frames
+    w = W.make("uniform")
+    n = len(w["pos"])
+    ctx = orca.Orca(w["params"])
+    ctx.set_agents(w["pos"], w["vel"], w["pref"])
+    ctx.step(10)
+    frames = torch.empty((100, n, 2), dtype=torch.float32).pin_memory()
+    ctx.step_trace(5, frames[:5])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.step(100)
+    ctx.count()  # synchronises
+    plain = (time.perf_counter() - t0) * 10.0
+    t0 = time.perf_counter()
+    ctx.step_trace(100, frames)
+    traced = (time.perf_counter() - t0) * 10.0
+    out["trace_uniform100k"] = {"ms_per_step_plain_wall": plain, "ms_per_step_with_frames_wall": traced,
+                                "frame_bytes": n * 8}
+    ctx.close()
     # latency floor: the same launch chain on one agent
     ctx = orca.Orca(W.DEFAULT_PARAMS)
     one = np.zeros((1, 2), np.float32)
@@ -473,6 +530,12 @@ def run_ours(args):
             line["cpu_baseline"] = {"value": r, "unit": "agent-updates/s", "cores": 1, "kind": "oracle",
                                     "sample": f"{m} random agents of the initial {n_total}-agent state, one step, "
                                               f"single thread, {el:.1f} s"}
+            if not args.no_multicore:
+                rm, mm, elm, procs = oracle_rate_multicore(w, args.cpu_seconds / 2, r)
+                line["cpu_baseline_multicore"] = {
+                    "value": rm, "unit": "agent-updates/s", "cores": procs, "kind": "oracle x P processes",
+                    "sample": f"{mm} random agents of the initial {n_total}-agent state split over {procs} forked "
+                              f"processes (each bins the full state), one step, {elm:.1f} s wall"}
     ctx.close()
     if rank == 0:
         if world == 1 and not args.no_suite:

@@ -82,6 +82,8 @@ typedef struct {
     int64_t collision_pairs;/* neighbour pairs that took the collision branch (Q4) */
     int64_t removed;        /* agents removed at their goal (orca_set_goal_removal) */
     int64_t rebalances;     /* strip re-partitions since creation (orca_rebalance; automatic) */
+    int64_t regrids;        /* grid re-derivations since creation (an agent reached the outer
+                               cell ring; automatic, reading Q12) */
 } orca_stats;
 
 /* ---- lifecycle -------------------------------------------------------------------- */

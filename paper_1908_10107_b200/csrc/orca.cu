@@ -288,6 +288,11 @@ struct orca_ctx {
     int reportCap = 0;
     int64_t rebalances = 0;
     int transport = 0;  // 0: peer memory (k_push / cudaIpc), 1: NCCL send/recv (loopback: copies)
+    // set (host-mapped, no synchronisation) when an agent enters the grid's outer cell ring:
+    // the grid is re-derived before the next chunk of steps (reading Q12)
+    int* gridFlagHost = nullptr;
+    int* gridFlagDev = nullptr;
+    int64_t regrids = 0;
     unsigned char* ipcStage = nullptr;  // device staging of the cudaIpc handles for the all-gather
 };
 
@@ -352,6 +357,7 @@ StepArgs make_args(orca_ctx* c, Domain& d) {
     a.qEntry = d.qEntry;
     a.qLines = d.qLines;
     a.qcap = d.capW;
+    a.gridFlag = c->gridFlagDev;
     a.qCount = reinterpret_cast<unsigned int*>(d.scanStatus + scan_tiles(d.nbins) + 1);
     return a;
 }
@@ -645,6 +651,11 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
     *cp = c;
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&c->partial, 1024 * 5 * sizeof(float));
+    if (e == cudaSuccess) e = cudaHostAlloc(&c->gridFlagHost, sizeof(int), cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+        *c->gridFlagHost = 0;
+        e = cudaHostGetDevicePointer(&c->gridFlagDev, c->gridFlagHost, 0);
+    }
     for (int q = 0; q < 8 && e == cudaSuccess; ++q) e = cudaEventCreate(&c->ev[q]);
     c->smemBytes = step_smem_per_thread(params->maxNeighbors) * kStepThreads;
     c->lp3Smem = std::max(1, 6 * params->maxNeighbors) * 4 * kStepThreads;
@@ -675,9 +686,9 @@ cudaError_t copy_in(orca_ctx* c, float2* dst, const float* src, int64_t n) {
 
 // min/max of the staged positions + finiteness of the three staged arrays
 orca_status stage_bounds(orca_ctx* c, const float2* a, const float2* b, const float2* q, int64_t n, float mn[2],
-                         float mx[2]) {
+                         float mx[2], const uint8_t* active = nullptr) {
     const int blocks = std::min(1024, cap_blocks(n, 256));
-    k_minmax<<<blocks, 256, 0, c->stream>>>((int)n, a, b, q, c->partial);
+    k_minmax<<<blocks, 256, 0, c->stream>>>((int)n, a, b, q, c->partial, active);
     CK(cudaGetLastError());
     std::vector<float> h((size_t)blocks * 5);
     CK(cudaMemcpyAsync(h.data(), c->partial, h.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
@@ -693,6 +704,36 @@ orca_status stage_bounds(orca_ctx* c, const float2* a, const float2* b, const fl
         bad += h[k * 5 + 4];
     }
     if (bad > 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "NaN/Inf in the input arrays");
+    return ORCA_OK;
+}
+
+// The frozen grid of reading Q12 from the bounding box [mn, mx] of the agents: origin =
+// fl32(min - cs), dims = floor((max - origin) / cs) + 2 (one margin cell on each side).
+orca_status derive_grid(orca_ctx* c, int64_t n, const float mn[2], const float mx[2], int margin = 1) {
+    const float cs = c->p.neighborDist;
+    Grid g{};
+    g.cs = cs;
+    g.lgS = kSubRowsLog2;
+    if (n == 0) {
+        g.ox = g.oy = 0.0f;
+        g.nx = g.ny = 1;
+    } else {
+        const float mc = cs * (float)margin;
+        volatile float ox = mn[0] - mc, oy = mn[1] - mc;
+        g.ox = ox;
+        g.oy = oy;
+        const double tx = std::floor(((double)mx[0] - (double)g.ox) / (double)cs) + margin + 1;
+        const double ty = std::floor(((double)mx[1] - (double)g.oy) / (double)cs) + margin + 1;
+        if (tx > 1e9 || ty > 1e9 || tx * ty * (double)(1 << kSubRowsLog2) > (double)(1 << 28))
+            return fail(ORCA_ERR_CAPACITY, "grid would exceed 2^28 sort bins");
+        g.nx = (int)tx;
+        g.ny = (int)ty;
+    }
+    g.csD = (double)cs;
+    g.invCs = 1.0 / (double)cs;
+    g.csSub = (double)cs / (double)(1 << g.lgS);
+    g.invCsSub = (double)(1 << g.lgS) / (double)cs;
+    c->gg = g;
     return ORCA_OK;
 }
 
@@ -895,7 +936,7 @@ orca_status refresh_props(orca_ctx* c) {
 // partition on the frozen grid.  Goals / preferred velocities (aux), per-agent properties,
 // removals, search-radius history, counters and the LP-order step index carry over; the
 // step results do not depend on the partition (bit-identical to one strip).
-orca_status rebalance(orca_ctx* c) {
+orca_status rebalance(orca_ctx* c, bool regrid) {
     const int64_t n = c->nGlobal;
     if (n == 0) return ORCA_OK;
     if (c->activeCap < n) {
@@ -940,10 +981,23 @@ orca_status rebalance(orca_ctx* c) {
             all, cap * c->world, sp, sv, sa, hist, c->activeBuf);
         CK(cudaGetLastError());
     }
+    if (regrid) {  // a new frozen grid around the agents still in the simulation
+        float mn[2], mx[2];
+        CKS(stage_bounds(c, sp, sv, sa, n, mn, mx, c->activeBuf));
+        if (!(mn[0] <= mx[0])) {  // nobody left: keep the grid
+            mn[0] = mx[0] = c->gg.ox + c->gg.cs;
+            mn[1] = mx[1] = c->gg.oy + c->gg.cs;
+        }
+        // margin: a 64-step chunk moves agents up to 64 maxSpeed dt before the next check
+        const float reach = 64.0f * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
+        CKS(derive_grid(c, n, mn, mx, 1 + (int)std::ceil(reach / c->p.neighborDist)));
+        c->regrids += 1;
+    } else {
+        c->rebalances += 1;
+    }
     c->ready = false;
     CKS(build_domains(c, n, sp, sv, sa, hist, c->activeBuf));
     CKS(refresh_props(c));
-    c->rebalances += 1;
     return ORCA_OK;
 }
 
@@ -952,7 +1006,14 @@ orca_status rebalance(orca_ctx* c) {
 // strip gains at most ~1.5 edge columns' worth of agents, and an edge column stays within
 // its halo buffer while it is below 70 % of it.  One small read-back per chunk (strips only).
 orca_status maybe_rebalance(orca_ctx* c) {
-    if (c->world == 1 || c->nGlobal == 0) return ORCA_OK;
+    if (c->nGlobal == 0) return ORCA_OK;
+    volatile int* outside = c->gridFlagHost;
+    if (c->world == 1) {  // no strips: only the grid check, without a synchronisation
+        if (!*outside) return ORCA_OK;
+        CK(cudaStreamSynchronize(c->stream));
+        *outside = 0;
+        return rebalance(c, true);
+    }
     const int nd = (int)c->doms.size();
     if (c->reportCap < 3 * nd + 4) {
         dfree(c->report);
@@ -974,7 +1035,8 @@ orca_status maybe_rebalance(orca_ctx* c) {
         if (d.g.hasL && (int64_t)colL * 10 > (int64_t)capH * 7) need = 1;
         if (d.g.hasR && (int64_t)colR * 10 > (int64_t)capH * 7) need = 1;
     }
-    if (!c->loopback) {  // every rank must take the same decision
+    if (*outside) need = 2;  // (read after the synchronisation: every earlier step is done)
+    if (!c->loopback) {  // every rank must take the same decision (2 = re-grid, 1 = re-partition)
         NcclApi& N = nccl();
         CK(cudaMemcpyAsync(c->report, &need, sizeof(int), cudaMemcpyHostToDevice, c->stream));
         ncclResult_t r = N.allReduce(c->report, c->report, 1, ncclInt32, ncclMax, c->comm, c->stream);
@@ -982,7 +1044,9 @@ orca_status maybe_rebalance(orca_ctx* c) {
         CK(cudaMemcpyAsync(&need, c->report, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
     }
-    return need ? rebalance(c) : ORCA_OK;
+    if (!need) return ORCA_OK;
+    *outside = 0;
+    return rebalance(c, need == 2);
 }
 
 }  // namespace
@@ -1111,6 +1175,7 @@ void orca_destroy(orca_ctx* c) {
     dfree(c->partial);
     dfree(c->colHist);
     dfree(c->props4);
+    if (c->gridFlagHost) cudaFreeHost(c->gridFlagHost);
     dfree(c->activeBuf);
     dfree(c->gatherBuf);
     dfree(c->ipcStage);
@@ -1137,6 +1202,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     if (n > 0 && (!pos || !vel || !pref)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
+    *c->gridFlagHost = 0;  // a new grid is derived below
     // same agent count as the loaded state: keep each agent's last k-th neighbour distance
     // as its first search radius (a hint; the selection is exact for any radius)
     const bool keepHist = c->ready && c->nGlobal == n && n > 0;
@@ -1169,29 +1235,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     float mn[2] = {0.0f, 0.0f}, mx[2] = {0.0f, 0.0f};
     if (n > 0) CKS(stage_bounds(c, sp, sv, sa, n, mn, mx));
     // frozen global grid (reading Q12)
-    const float cs = c->p.neighborDist;
-    Grid g{};
-    g.cs = cs;
-    g.lgS = kSubRowsLog2;
-    if (n == 0) {
-        g.ox = g.oy = 0.0f;
-        g.nx = g.ny = 1;
-    } else {
-        volatile float ox = mn[0] - cs, oy = mn[1] - cs;
-        g.ox = ox;
-        g.oy = oy;
-        const double tx = std::floor(((double)mx[0] - (double)g.ox) / (double)cs);
-        const double ty = std::floor(((double)mx[1] - (double)g.oy) / (double)cs);
-        if (tx + 2 > 1e9 || ty + 2 > 1e9 || (tx + 2) * (ty + 2) * (double)(1 << kSubRowsLog2) > (double)(1 << 28))
-            return fail(ORCA_ERR_CAPACITY, "grid would exceed 2^28 sort bins");
-        g.nx = (int)tx + 2;
-        g.ny = (int)ty + 2;
-    }
-    g.csD = (double)cs;
-    g.invCs = 1.0 / (double)cs;
-    g.csSub = (double)cs / (double)(1 << g.lgS);
-    g.invCsSub = (double)(1 << g.lgS) / (double)cs;
-    c->gg = g;
+    CKS(derive_grid(c, n, mn, mx));
     c->nGlobal = n;
     return build_domains(c, n, sp, sv, sa, hist, nullptr);
 }
@@ -1494,6 +1538,7 @@ orca_status orca_get_stats(orca_ctx* c, orca_stats* out) {
     out->collision_pairs = (int64_t)t[ST_COLLISION];
     out->removed = (int64_t)t[ST_REMOVED];
     out->rebalances = c->rebalances;
+    out->regrids = c->regrids;
     if (c->ready) CKS(check_overflow(c));
     return ORCA_OK;
 }
@@ -1674,7 +1719,7 @@ orca_status orca_rebalance(orca_ctx* c) {
         CK(cudaMalloc(&c->report, (size_t)(3 * c->doms.size() + 4) * sizeof(int)));
         c->reportCap = 3 * (int)c->doms.size() + 4;
     }
-    return rebalance(c);
+    return rebalance(c, false);
 }
 
 orca_status orca_set_lp3_lanes(orca_ctx* c, int32_t lanes) {

@@ -828,6 +828,7 @@ struct StepArgs {
     unsigned int* qCount;  // zeroed before every step
     int qcap;
     int pad1;
+    int* gridFlag;  // host-mapped: set when an agent enters the grid's outer cell ring
 };
 static_assert(sizeof(Grid) == 80 && sizeof(Model) == 96 && sizeof(ExBuf) % 8 == 0, "padding-free layouts");
 
@@ -1036,6 +1037,10 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
     }
     const int cx = cell_coord(pn.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
     const int sy = subrow_coord(pn.y, a.g);
+    if (a.gridFlag) {  // the outer ring: beyond it positions are clamped -> re-derive the grid
+        const int cyc = sy >> a.g.lgS;
+        if (cx == 0 || cx == a.g.nx - 1 || cyc == 0 || cyc == a.g.ny - 1) *a.gridFlag = 1;
+    }
     if (cx >= a.g.c0 && cx < a.g.c1) {
         const uint32_t c = bin_of(cx, sy, a.g);
         a.posW[w] = pn;
@@ -1713,10 +1718,12 @@ __global__ void k_colhist(int n, const float2* __restrict__ pos, Grid g, int32_t
 // Block-partial min/max of the positions and a non-finite count over all input arrays.
 // partial[b] = {minx, miny, maxx, maxy, nonfinite}
 __global__ void k_minmax(int n, const float2* __restrict__ pos, const float2* __restrict__ vel,
-                         const float2* __restrict__ aux, float* __restrict__ partial) {
+                         const float2* __restrict__ aux, float* __restrict__ partial,
+                         const uint8_t* __restrict__ active) {
     float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
     int bad = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (active && !active[i]) continue;  // removed at its goal
         const float2 p = pos[i];
         const float2 v = vel[i];
         const float2 q = aux[i];

@@ -47,7 +47,7 @@ class Params(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("steps", "agent_updates", "infeasible", "degenerate",
                                                "coincident", "eps_parallel", "marginal", "collision_pairs",
-                                               "removed", "rebalances")]
+                                               "removed", "rebalances", "regrids")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

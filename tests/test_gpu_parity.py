@@ -799,3 +799,39 @@ def test_grid_capacity_and_recovery(orca):
     o.step(3)
     assert o.count() == 500
     o.close()
+
+
+@pytest.mark.parametrize("strips", [0, 3])
+def test_expanding_crowd_regrids(orca, strips):
+    """An open crowd spreads beyond the grid frozen at set_agents: when an agent reaches the
+    outer cell ring the grid is re-derived (reading Q12), so the step stays fast, and the state
+    steps exactly like a fresh context loaded with it (same neighbour lists and velocities)."""
+    import time
+    w = W.make("uniform", n=20000, rho=0.25)
+    a = orca.Orca(w["params"], strips=strips)
+    a.set_agents(w["pos"], w["vel"], w["pref"])
+    a.step(64)
+    a.count()
+    t0 = time.perf_counter()
+    a.step(64)
+    a.count()
+    early = time.perf_counter() - t0
+    for _ in range(6):
+        a.step(64)
+    st = a.stats()
+    assert st["regrids"] >= 1
+    t0 = time.perf_counter()
+    a.step(64)
+    a.count()
+    late = time.perf_counter() - t0
+    assert late < 3.0 * early + 0.05, (early, late)
+    pos, vel = a.get_state()
+    origin, cs, dims = a.grid()
+    assert np.all(pos >= origin.astype(np.float32)) and np.all(pos < origin + cs * dims)  # nobody clamped
+    b = orca.Orca(w["params"])
+    b.set_agents(pos, vel, w["pref"])
+    va, fa, na, ca = a.debug_step()
+    vb, fb, nb, cb = b.debug_step()
+    assert np.array_equal(na, nb) and np.array_equal(ca, cb) and np.array_equal(va, vb)
+    a.close()
+    b.close()
