@@ -195,9 +195,10 @@ orca_status orca_debug_work(orca_ctx *ctx, int64_t out[5]);
 orca_status orca_get_stats(orca_ctx *ctx, orca_stats *out);
 orca_status orca_reset_stats(orca_ctx *ctx);
 
-/* Kernel variant of the fused step (all compute the same result bit for bit; the default
- * is chosen by measurement): 0 = one thread per agent with a shared-memory
- * top-k list (default), 1 = an 8-lane group per agent, 2 = one thread per agent with a
+/* Kernel variant of the fused step (all compute the same result bit for bit; chosen by
+ * measurement): -1 = automatic (default: 1 for strips of fewer than ~24k
+ * agents, where the step is latency bound, else 0), 0 = one thread per agent with a
+ * shared-memory top-k list, 1 = an 8-lane group per agent, 2 = one thread per agent with a
  * register top-k list (k <= 16; else shared memory), 3 = variant 0 with the paper's
  * work-unit LP2 (lanes that need no re-solve evaluate the constraints of lanes
  * that do).  Errors: INVALID_ARGUMENT. */

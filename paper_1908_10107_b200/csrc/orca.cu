@@ -189,6 +189,7 @@ struct Domain {
     Grid g{};
     int64_t nbins = 0, binCap = 0;
     int capW = 0;
+    int64_t popBuild = 0;  // agents of the strip when it was (re)built (auto kernel choice)
     float2 *posS = nullptr, *velS = nullptr, *auxS = nullptr, *posW = nullptr, *velW = nullptr, *auxW = nullptr;
     float *rk2S = nullptr, *rk2W = nullptr;
     float4 *propS = nullptr, *propW = nullptr;  // heterogeneous crowds only
@@ -277,7 +278,7 @@ struct orca_ctx {
     int lpRandom = 0;              // randomized LP constraint order (orca_set_lp_order)
     unsigned long long lpSeed = 0;
     int64_t lpStep0 = 0, lpMark = 0;  // step index t = lpStep0 + steps_total - lpMark
-    int variant = 0;
+    int variant = -1;  // -1: auto (pick_variant)
     int lp3Lanes = ORCA_LP3_GROUP;  // lanes per queued agent in the LP3 kernel (1 = thread)
     // strip rebalance: by-id active flags, all-gather records, fill reports
     uint8_t* activeBuf = nullptr;
@@ -425,6 +426,17 @@ void drop_graph(orca_ctx* c) {
     c->graphKey.clear();
 }
 
+// auto (-1): below ~24k agents per strip the step is latency bound (too few warps to hide a
+// thread's chain of dependent loads) and the 8-lane group per agent wins; above, one thread
+// per agent (measured crossover)
+#ifndef ORCA_AUTO_GROUP_BELOW
+#define ORCA_AUTO_GROUP_BELOW 24000
+#endif
+int pick_variant(const orca_ctx* c, const Domain& d) {
+    if (c->variant >= 0) return c->variant;
+    return (d.popBuild < ORCA_AUTO_GROUP_BELOW) ? 1 : 0;
+}
+
 // Everything a captured step body depends on: the kernel arguments of every strip (device
 // pointers, grid, model), launch sizes, the exchange buffers and the kernel selection.  A
 // cached graph is replayed only while this is unchanged, so orca_set_agents with the same
@@ -443,6 +455,8 @@ std::vector<unsigned char> graph_key(orca_ctx* c) {
         put(&a, sizeof a);
         put(&d.capW, sizeof d.capW);
         put(&d.nbins, sizeof d.nbins);
+        const int v = pick_variant(c, d);
+        put(&v, sizeof v);
         for (const ExAlloc* x : {&d.sendL, &d.sendR, &d.recvL, &d.recvR, &d.recvL1, &d.recvR1}) {
             put(&x->base, sizeof x->base);
             put(&x->bytes, sizeof x->bytes);
@@ -478,11 +492,12 @@ template <bool DRY>
 void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
     const int k = c->p.maxNeighbors;
-    if (c->variant == 1 && !c->het && !c->lpRandom)  // (group kernel: homogeneous, nearest-first)
+    const int variant = pick_variant(c, d);
+    if (variant == 1 && !c->het && !c->lpRandom)  // (group kernel: homogeneous, nearest-first)
         k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
-    else if (c->variant == 3)  // work-unit LP2 (P:84-89 ablation)
+    else if (variant == 3)  // work-unit LP2 (P:84-89 ablation)
         k_step<DRY, 0, true><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
-    else if (c->variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
+    else if (variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
         k_step<DRY, 0><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
     else if (k <= 10)  // register top-k list
         k_step<DRY, 10><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
@@ -886,6 +901,8 @@ orca_status build_domains(orca_ctx* c, int64_t n, const float2* sp, const float2
         d.nbins = ((int64_t)(d.g.e1 - d.g.e0) * g.ny) << g.lgS;
         int64_t sel = 0;
         for (int x = d.g.e0; x < d.g.e1; ++x) sel += colCount[x];
+        d.popBuild = 0;
+        for (int x = d.g.c0; x < d.g.c1; ++x) d.popBuild += colCount[x];
         // single strip: exact; strips: headroom for density drift between re-partitions
         const int64_t capW = (c->world == 1) ? std::max<int64_t>(n, 1) : sel + sel / 2 + 4096;
         if (capW > ((int64_t)1 << 30)) return fail(ORCA_ERR_CAPACITY, "strip too large");
@@ -1765,7 +1782,7 @@ orca_status orca_get_active(orca_ctx* c, uint8_t* active) {
 }
 
 orca_status orca_set_variant(orca_ctx* c, int32_t variant) {
-    if (!c || variant < 0 || variant > 3) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be 0, 1, 2 or 3");
+    if (!c || variant < -1 || variant > 3) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be -1, 0, 1, 2 or 3");
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->variant = variant;

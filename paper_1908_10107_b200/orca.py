@@ -328,8 +328,8 @@ class Orca:
         return a.astype(bool)
 
     def set_variant(self, variant: int):
-        """0 = thread per agent, 1 = 8-lane group per agent, 2 = register top-k list,
-        3 = work-unit LP2; all give the same results bit for bit."""
+        """-1 = automatic (default), 0 = thread per agent, 1 = 8-lane group per agent,
+        2 = register top-k list, 3 = work-unit LP2; all give the same results."""
         _check(_lib.orca_set_variant(self._ctx, variant))
 
     def stream(self) -> int:

@@ -22,10 +22,15 @@ def main():
     ap.add_argument("--configs", default="uniform_1m,dense")
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--ns", default="", help="agent counts (uniform-type configs), comma-separated")
     a = ap.parse_args()
     variants = [int(x) for x in a.variants.split(",")]
+    jobs = []
     for cfg in a.configs.split(","):
-        w = W.make(cfg)
+        for n in ([int(x) for x in a.ns.split(",")] if a.ns else [None]):
+            jobs.append((cfg, n))
+    for cfg, nn in jobs:
+        w = W.make(cfg, n=nn)
         for k in [int(x) for x in a.ks.split(",")]:
             p = dict(w["params"], maxNeighbors=k)
             ctx = O.Orca(p)

@@ -76,6 +76,14 @@ def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, variant=No
     # neighbours (bit-exact)
     assert np.array_equal(cnt[ids], ref["cnt"])
     assert np.array_equal(nb[ids], ref["nbr"])
+    # the automatic kernel choice (variant -1) and the one-thread-per-agent kernel (0) agree
+    # bit for bit, so the oracle comparison below covers both
+    if variant is None:
+        o.set_variant(0)
+        v0, fl0, nb0, cnt0 = o.debug_step()
+        o.set_variant(-1)
+        assert np.array_equal(v0, v) and np.array_equal(nb0, nb) and np.array_equal(cnt0, cnt)
+        assert np.array_equal(fl0 & 1, fl & 1)
     # velocities
     ov = ref["vel"]
     gv = v[ids].astype(np.float64)
@@ -605,6 +613,7 @@ def test_work_unit_lp_bit_identical_k_sweep(orca):
     for k in (1, 2, 3, 5, 9, 16, 17, 31, 32):
         a, _ = _ctx(orca, w, maxNeighbors=k)
         b, _ = _ctx(orca, w, maxNeighbors=k)
+        a.set_variant(0)
         b.set_variant(3)
         ra, rb = a.debug_step(), b.debug_step()
         for x, y in zip(ra, rb):
