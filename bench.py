@@ -417,11 +417,11 @@ def run_ours(args):
     ctx.set_lp3_lanes(args.lp3_lanes)
 
     # ---- e2e through the public API with pinned host buffers: every step uploads the
-    # state (orca_set_agents: H2D, grid, partition, binning), steps once and reads the
-    # result back (orca_get_state, or this rank's strip via orca_get_local_state).  The
+    # kinematic state (orca_set_state: H2D of pos + vel, re-binning), steps once and reads
+    # the result back (orca_get_state, or this rank's strip via orca_get_local_state).  The
     # uploaded state is the simulation as it stands after the device-timed runs (a
-    # checkpoint reload), so e2e and value time the same phase of the workload rather than
-    # the collision-rich first step from the random initial velocities.
+    # checkpoint reload of the same crowd), so e2e and value time the same phase of the
+    # workload rather than the collision-rich first step from the random initial velocities.
     hp = torch.empty((n_total, 2), dtype=torch.float32).pin_memory()
     hv = torch.empty((n_total, 2), dtype=torch.float32).pin_memory()
     hq = torch.from_numpy(w["pref"]).pin_memory()
@@ -437,7 +437,7 @@ def run_ours(args):
             gv[ids_] = v_
         hp.copy_(torch.from_numpy(gp))
         hv.copy_(torch.from_numpy(gv))
-    e2e_state = "state after the timed steps (checkpoint reload)"
+    e2e_state = "state after the timed steps, re-uploaded every step with orca_set_state (pos + vel)"
     if not (torch.isfinite(hp).all() and torch.isfinite(hv).all()):  # removed agents: initial state
         hp.copy_(torch.from_numpy(w["pos"]))
         hv.copy_(torch.from_numpy(w["vel"]))
@@ -466,7 +466,7 @@ def run_ours(args):
     t0 = time.perf_counter()
     d2h = 0
     for _ in range(ne):
-        ctx.set_agents(hp, hv, hq)
+        ctx.set_state(hp, hv)
         ctx.step(1)
         m = readback()
         d2h += m * (16 if world == 1 else 20)
@@ -476,7 +476,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
     e2e = {"value": n_total * ne / el, "unit": "agent-updates/s",
-           "h2d_bytes_per_step": int(hp.numel() * 4 * 3), "d2h_bytes_per_step": int(d2h // ne),
+           "h2d_bytes_per_step": int(hp.numel() * 4 * 2), "d2h_bytes_per_step": int(d2h // ne),
            "ms_per_step": 1000.0 * el / ne, "wall_clock": True, "input": e2e_state}
 
     # ---- roofline of the dominant kernel (k_step): ALU bound

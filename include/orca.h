@@ -109,6 +109,16 @@ void orca_destroy(orca_ctx *ctx);
 orca_status orca_set_agents(orca_ctx *ctx, int64_t n, const float *pos, const float *vel,
                             const float *prefVel);
 
+/* Replace the positions and velocities (float[2n] by id, host or device) of the loaded
+ * agents and keep everything else: preferred velocities or goals, per-agent properties,
+ * removals (entries of removed agents are ignored), counters, the LP-order step index and
+ * each agent's search-radius hint.  The grid stays unless the new positions leave its
+ * interior (then it is re-derived, reading Q12).  The per-frame upload of an application
+ * that moves agents itself, or reloads a checkpoint of the same crowd.  Multi-rank
+ * contexts: every rank calls it with the same arrays.  Synchronises.  Errors: NOT_READY,
+ * INVALID_ARGUMENT (NULL, NaN/Inf for an agent present), CAPACITY, CUDA, NCCL. */
+orca_status orca_set_state(orca_ctx *ctx, const float *pos, const float *vel);
+
 /* Goal seeking ("The agent's velocity is in the direction of the goal location,
  * scaled to the walking speed"): goal float[2n] by id; from the next step on, the
  * preferred velocity is recomputed every step as g*min(1, prefSpeed/|g|), g = goal - pos.

@@ -953,9 +953,21 @@ orca_status refresh_props(orca_ctx* c) {
 // partition on the frozen grid.  Goals / preferred velocities (aux), per-agent properties,
 // removals, search-radius history, counters and the LP-order step index carry over; the
 // step results do not depend on the partition (bit-identical to one strip).
-orca_status rebalance(orca_ctx* c, bool regrid) {
+orca_status ensure_report(orca_ctx* c) {
+    const int need = 3 * (int)c->doms.size() + 4;
+    if (c->reportCap < need) {
+        dfree(c->report);
+        CK(cudaMalloc(&c->report, (size_t)need * sizeof(int)));
+        c->reportCap = need;
+    }
+    return ORCA_OK;
+}
+
+// Every strip's owned agents back to by-id arrays in the stage (pos | vel | aux), their
+// search-radius hints (outA) and active flags -- all-gathered between ranks (collective).
+orca_status gather_state(orca_ctx* c) {
     const int64_t n = c->nGlobal;
-    if (n == 0) return ORCA_OK;
+    CKS(ensure_report(c));
     if (c->activeCap < n) {
         dfree(c->activeBuf);
         CK(cudaMalloc(&c->activeBuf, (size_t)n));
@@ -998,6 +1010,15 @@ orca_status rebalance(orca_ctx* c, bool regrid) {
             all, cap * c->world, sp, sv, sa, hist, c->activeBuf);
         CK(cudaGetLastError());
     }
+    return ORCA_OK;
+}
+
+orca_status rebalance(orca_ctx* c, bool regrid) {
+    const int64_t n = c->nGlobal;
+    if (n == 0) return ORCA_OK;
+    CKS(gather_state(c));
+    float2 *sp = c->stage, *sv = c->stage + n, *sa = c->stage + 2 * n;
+    float* hist = reinterpret_cast<float*>(c->outA);
     if (regrid) {  // a new frozen grid around the agents still in the simulation
         float mn[2], mx[2];
         CKS(stage_bounds(c, sp, sv, sa, n, mn, mx, c->activeBuf));
@@ -1255,6 +1276,39 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     CKS(derive_grid(c, n, mn, mx));
     c->nGlobal = n;
     return build_domains(c, n, sp, sv, sa, hist, nullptr);
+}
+
+orca_status orca_set_state(orca_ctx* c, const float* pos, const float* vel) {
+    if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    const int64_t n = c->nGlobal;
+    if (n > 0 && (!pos || !vel)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    if (n == 0) return ORCA_OK;
+    // everything but the kinematic state stays: preferred velocities or goals, per-agent
+    // properties, removals, search-radius hints (by id), counters, the LP-order step index
+    CKS(gather_state(c));
+    float2 *sp = c->stage, *sv = c->stage + n, *sa = c->stage + 2 * n;
+    float* hist = reinterpret_cast<float*>(c->outA);
+    CK(copy_in(c, sp, pos, n));
+    CK(copy_in(c, sv, vel, n));
+    float mn[2], mx[2];
+    CKS(stage_bounds(c, sp, sv, sa, n, mn, mx, c->activeBuf));  // finiteness of the agents present
+    const Grid& g = c->gg;
+    const bool inside = !(mn[0] <= mx[0]) ||
+                        (mn[0] >= g.ox + g.cs && mn[1] >= g.oy + g.cs && (double)mx[0] < g.ox + (double)g.cs * (g.nx - 1) &&
+                         (double)mx[1] < g.oy + (double)g.cs * (g.ny - 1));
+    if (!inside) {  // the new state leaves the grid's interior: re-derive it (reading Q12)
+        const float reach = 64.0f * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
+        CKS(derive_grid(c, n, mn, mx, 1 + (int)std::ceil(reach / c->p.neighborDist)));
+        c->regrids += 1;
+    }
+    *c->gridFlagHost = 0;
+    c->ready = false;
+    CKS(build_domains(c, n, sp, sv, sa, hist, c->activeBuf));
+    CKS(refresh_props(c));
+    return ORCA_OK;
 }
 
 orca_status orca_set_goals(orca_ctx* c, const float* goal, float prefSpeed) {

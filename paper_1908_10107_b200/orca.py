@@ -28,7 +28,7 @@ EXPORTS = [
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
     "orca_set_lp_order", "orca_set_lp3_lanes", "orca_rebalance", "orca_set_transport",
-    "orca_get_transport",
+    "orca_get_transport", "orca_set_state",
 ]
 
 
@@ -94,6 +94,7 @@ def _load():
         "orca_rebalance": [vp],
         "orca_set_transport": [vp, i32],
         "orca_get_transport": [vp, P(i32)],
+        "orca_set_state": [vp, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -198,6 +199,10 @@ class Orca:
         n = (pos.shape[0] if pos.ndim == 2 else pos.shape[0] // 2)
         _check(_lib.orca_set_agents(self._ctx, n, _ptr(pos), _ptr(vel), _ptr(pref)))
         self.n = n
+
+    def set_state(self, pos, vel):
+        """New positions / velocities of the loaded agents (by id); everything else stays."""
+        _check(_lib.orca_set_state(self._ctx, _ptr(_as_f32(pos)), _ptr(_as_f32(vel))))
 
     def set_goals(self, goals, pref_speed: float):
         _check(_lib.orca_set_goals(self._ctx, _ptr(_as_f32(goals)), pref_speed))

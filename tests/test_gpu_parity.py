@@ -844,3 +844,64 @@ def test_expanding_crowd_regrids(orca, strips):
     assert np.array_equal(na, nb) and np.array_equal(ca, cb) and np.array_equal(va, vb)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("strips", [0, 3])
+def test_set_state_keeps_the_rest(orca, strips):
+    """orca_set_state with the current state continues the run bit for bit (goals, removal,
+    per-agent properties, randomized LP order, counters all kept); with another state it
+    steps exactly like a fresh context configured the same way."""
+    w = W.make("uniform", n=12000, rho=0.3)
+    n = len(w["pos"])
+    rng = np.random.default_rng(21)
+    goals = (w["pos"] + rng.uniform(-40, 40, w["pos"].shape)).astype(np.float32)
+    props = _het_props(n, seed=4)
+
+    def make():
+        o = orca.Orca(w["params"], strips=strips)
+        o.set_agents(w["pos"], w["vel"], w["pref"])
+        o.set_goals(goals, 1.0)
+        o.set_goal_removal(1.5)
+        o.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+        o.set_lp_order(True, 9, 0)
+        return o
+
+    a, b = make(), make()
+    a.step(30)
+    b.step(30)
+    pos, vel = b.get_state()
+    b.set_state(pos, vel)  # removed agents read NaN: ignored
+    a.step(20)
+    b.step(20)
+    sa, sb = a.get_state(), b.get_state()
+    assert np.array_equal(sa[0], sb[0], equal_nan=True) and np.array_equal(sa[1], sb[1], equal_nan=True)
+    assert a.count() == b.count() < n
+    ta, tb = a.stats(), b.stats()
+    for key in ("infeasible", "collision_pairs", "removed"):
+        assert ta[key] == tb[key], key
+    # a present agent with NaN is refused
+    bad = sb[0].copy()
+    bad[np.nonzero(b.active())[0][0]] = np.nan
+    with pytest.raises(orca.OrcaError):
+        b.set_state(bad, sb[1])
+    for o in (a, b):
+        o.close()
+
+
+def test_set_state_new_state_equals_fresh_context(orca):
+    w = W.make("uniform", n=8000, rho=0.3)
+    w2 = W.make("uniform", n=8000, rho=0.45, salt=2)
+    a, p = _ctx(orca, w)
+    a.step(5)
+    a.set_state(w2["pos"], w2["vel"])  # the grid is re-derived if needed
+    b = orca.Orca(p)
+    b.set_agents(w2["pos"], w2["vel"], w["pref"])
+    ra, rb = a.debug_step(), b.debug_step()
+    for x, y in zip(ra, rb):
+        assert np.array_equal(x, y)
+    a.step(10)
+    b.step(10)
+    sa, sb = a.get_state(), b.get_state()
+    assert np.array_equal(sa[0], sb[0]) and np.array_equal(sa[1], sb[1])
+    a.close()
+    b.close()
