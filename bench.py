@@ -256,6 +256,36 @@ def suite(orca, torch, peak_tops):
                      "infeasible_per_step": st["infeasible"] / max(1, st["steps"]),
                      "remaining": ctx.count() if w.get("goals") is not None else n}
         ctx.close()
+    # the paper's crossing experiments: agents walk to their goals and
+    # leave there; steps until everyone has left (or a cap) and the device time per step
+    rng = np.random.default_rng(7)
+    for name, w, het in (("two_way_2500", W.make("two_way"), False),
+                         ("two_way_2500_heterogeneous", W.make("two_way"), True),
+                         ("eight_way_10k", W.make("eight_way"), False)):
+        n = len(w["pos"])
+        ctx = orca.Orca(w["params"])
+        ctx.set_agents(w["pos"], w["vel"], w["pref"])
+        ctx.set_goals(w["goals"], w["pref_speed"])
+        ctx.set_goal_removal(w["params"]["radius"])
+        if het:  # radius and desired speed each uniform over 3 values, max = 1.25 x desired
+            desired = rng.choice([1.0, 1.33, 2.0], n).astype(np.float32)
+            ctx.set_agent_props(rng.choice([0.5, 0.75, 1.0], n).astype(np.float32), 1.25 * desired, desired)
+        stream = torch.cuda.ExternalStream(ctx.stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps, cap = 0, 4000
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        while ctx.count() > 0 and steps < cap:
+            ctx.step(100)
+            steps += 100
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        torch.cuda.synchronize()
+        st = ctx.stats()
+        out[name] = {"n_agents": n, "steps_run": steps, "remaining": ctx.count(), "removed": st["removed"],
+                     "ms_per_step": e0.elapsed_time(e1) / steps, "infeasible_per_step": st["infeasible"] / steps}
+        ctx.close()
     # per-step trace dump (f4): 100 steps of 100k agents with every frame copied to
     # pinned host memory on the copy stream, against the same 100 steps without frames
     w = W.make("uniform")

@@ -493,7 +493,7 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
     const int k = c->p.maxNeighbors;
     const int variant = pick_variant(c, d);
-    if (variant == 1 && !c->het && !c->lpRandom)  // (group kernel: homogeneous, nearest-first)
+    if (variant == 1)  // 8-lane group per agent
         k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
     else if (variant == 3)  // work-unit LP2 (P:84-89 ablation)
         k_step<DRY, 0, true><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);

@@ -205,6 +205,10 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
         const float2 vi = a.velS[i];
         const float2 aux = a.auxS[i];
         const uint32_t idi = a.idS[i];
+        // per-agent (radius, maxSpeed, prefSpeed) of heterogeneous crowds
+        const bool het = a.propS != nullptr;
+        const float4 pr = het ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
+        const float ri = pr.x, vmaxi = pr.y, vprefi = (pr.z >= 0.0f) ? pr.z : a.m.prefSpeed;
         const int cx = cell_coord(pi.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
         const int lgS = a.g.lgS;
         const int nyS = a.g.ny << lgS;
@@ -304,16 +308,29 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
         if (!DRY && G.gl == 0) a.rk2W[ws] = fk;
 
         // ---- 3. half-planes, one lane per neighbour (Fig. 1) ----------------------
+        if (DRY && a.dbgNbr)  // neighbours in (distance, id) order
+            for (int q = G.gl; q < cnt; q += kG) a.dbgNbr[(size_t)idi * k + q] = (int32_t)a.idS[lj[q]];
+        if (a.m.lpRandom && cnt > 1) {  // randomized LP order (reading Q8): one lane shuffles
+            __syncwarp(G.gmask);
+            if (G.gl == 0) lp_shuffle(const_cast<uint32_t*>(lj), 1, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
+            __syncwarp(G.gmask);
+        }
         for (int q = G.gl; q < cnt; q += kG) {
             const uint32_t j = lj[q];
             const float2 pj = a.posS[j];
             const float2 vj = a.velS[j];
             const uint32_t idj = a.idS[j];
-            if (DRY && a.dbgNbr) a.dbgNbr[(size_t)idi * k + q] = (int32_t)idj;
             float nx, ny, s;
             int coll;
-            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, idj, a.m.R, a.m.R2D, a.m, nx, ny,
-                            s, coll);  // homogeneous only (heterogeneous crowds run variant 0)
+            // combined radius R = r_i + r_j (Fig. 1(a)); per agent when heterogeneous
+            float Rp = a.m.R;
+            double R2p = a.m.R2D;
+            if (het) {
+                const double Rd = (double)ri + (double)a.propS[j].x;
+                R2p = Rd * Rd;
+                Rp = (float)Rd;
+            }
+            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, idj, Rp, R2p, a.m, nx, ny, s, coll);
             nColl += coll;
             Lnx[q] = nx;
             Lny[q] = ny;
@@ -326,7 +343,7 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
         if (a.m.goals) {
             const float gx = aux.x - pi.x, gy = aux.y - pi.y;
             const float gl = sqrtf(fmaf(gx, gx, gy * gy));
-            const float sc = (gl > a.m.prefSpeed) ? a.m.prefSpeed / gl : 1.0f;
+            const float sc = (gl > vprefi) ? vprefi / gl : 1.0f;
             px = gx * sc;
             py = gy * sc;
         } else {
@@ -334,7 +351,7 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
             py = aux.y;
         }
         float vx, vy;
-        const int f = lp2_group(G, Lnx, Lny, Ls, cnt, a.m.maxSpeed, px, py, vx, vy, fl, wChecks, wLp1);
+        const int f = lp2_group(G, Lnx, Lny, Ls, cnt, vmaxi, px, py, vx, vy, fl, wChecks, wLp1);
         // flags of all lanes of the group
         fl |= __shfl_xor_sync(G.gmask, fl, 4);
         fl |= __shfl_xor_sync(G.gmask, fl, 2);
@@ -359,8 +376,7 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
             if (a.dbgNbr)
                 for (int q = cnt + G.gl; q < k; q += kG) a.dbgNbr[(size_t)idi * k + q] = -1;
         } else if (!deferred && G.gl == 0) {
-            finish_agent(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk,
-                         make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f));
+            finish_agent(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk, pr);
         }
     }
     // ---- counters: one lane per agent counts ---------------------------------------------

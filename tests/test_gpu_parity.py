@@ -905,3 +905,30 @@ def test_set_state_new_state_equals_fresh_context(orca):
     assert np.array_equal(sa[0], sb[0]) and np.array_equal(sa[1], sb[1])
     a.close()
     b.close()
+
+
+def test_group_variant_heterogeneous_and_random_order(orca):
+    """The 8-lane group kernel (variant 1, the automatic choice for small crowds) handles
+    per-agent radii/speeds and the randomized LP order bit-identically to variant 0."""
+    w = W.make("uniform", n=9000, rho=0.35)
+    n = len(w["pos"])
+    rng = np.random.default_rng(17)
+    goals = (w["pos"] + rng.uniform(-50, 50, w["pos"].shape)).astype(np.float32)
+    props = _het_props(n, seed=12)
+    ctxs = []
+    for v in (0, 1):
+        o, _ = _ctx(orca, w)
+        o.set_variant(v)
+        o.set_goals(goals, 1.0)
+        o.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+        o.set_lp_order(True, 77, 3)
+        ctxs.append(o)
+    r = [o.debug_step() for o in ctxs]
+    assert np.array_equal(r[0][2], r[1][2]) and np.array_equal(r[0][3], r[1][3])
+    assert np.array_equal(r[0][0], r[1][0]) and np.array_equal(r[0][1] & 1, r[1][1] & 1)
+    for o in ctxs:
+        o.step(25)
+    s = [o.get_state() for o in ctxs]
+    assert np.array_equal(s[0][0], s[1][0]) and np.array_equal(s[0][1], s[1][1])
+    for o in ctxs:
+        o.close()
