@@ -160,8 +160,16 @@ orca_status orca_set_agent_props(orca_ctx *ctx, const float *radius, const float
  * Synchronises.  Errors: NOT_READY. */
 orca_status orca_get_active(orca_ctx *ctx, uint8_t *active);
 
-/* Enqueue n_steps >= 0 synchronous steps on the context stream (one CUDA graph replay;
- * no host synchronisation).  Errors: NOT_READY, INVALID_ARGUMENT, CUDA, NCCL. */
+/* Enqueue n_steps >= 0 synchronous steps on the context stream: CUDA graphs of up to 64
+ * step bodies, replayed, and re-captured only when a captured argument changed.  Before each
+ * chunk of up to 64 steps, two maintenance checks run:
+ *   - the grid is re-derived (reading Q12) once an agent reached its outer cell ring (a
+ *     host-mapped flag: no synchronisation unless it is set);
+ *   - strip contexts read one small fill report (a synchronisation) and re-partition when a
+ *     strip could outgrow its buffers within the chunk (orca_rebalance).
+ * Multi-rank contexts: every rank calls it with the same n_steps.  Errors: NOT_READY,
+ * INVALID_ARGUMENT, CUDA, NCCL, CAPACITY, INTERNAL (an exchange timed out: a neighbour
+ * rank did not step). */
 orca_status orca_step(orca_ctx *ctx, int32_t n_steps);
 
 /* Trace dump ("saving the agent data for each simulation step to a binary file",
