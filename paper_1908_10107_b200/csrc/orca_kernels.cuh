@@ -546,6 +546,65 @@ __device__ __forceinline__ int lp2(const Lines& L, int T, int n, float r, float 
     return n;
 }
 
+// Constraint order for LP2 (reading Q8: the feasible optimum is the unique projection, so
+// any order reaches it; only the LP1 re-solve work depends on it).  Lines that the start
+// point v0 (pref clipped to the disc) violates go first: 1 = the most violated one only,
+// 2 = all violated ones in neighbour order, 3 = all violated ones by decreasing violation.
+// The rest keep their neighbour order.  Swept r01z (`profiles/sweep_lppen_r01z.txt`): 1 is
+// -1.7 % at 1M, -2 % at 100k, -1 % dense; 2 and 3 are slower (+3 %, +6 %: the partition costs
+// more than the re-solves it saves).  Off under the randomized order (orca_set_lp_order).
+#ifndef ORCA_LP_PEN
+#define ORCA_LP_PEN 1
+#endif
+__device__ __forceinline__ void line_move(const Lines& L, int T, int from, int to) {
+    // line `from` to slot `to` (to <= from), slots [to, from) shift up by one
+    const float nx = L.nx[from * T], ny = L.ny[from * T], s = L.s[from * T];
+    for (int m = from; m > to; --m) {
+        L.nx[m * T] = L.nx[(m - 1) * T];
+        L.ny[m * T] = L.ny[(m - 1) * T];
+        L.s[m * T] = L.s[(m - 1) * T];
+    }
+    L.nx[to * T] = nx;
+    L.ny[to * T] = ny;
+    L.s[to * T] = s;
+}
+
+template <int MODE>
+__device__ __forceinline__ void pen_order(const Lines& L, int T, int n, float r, float optx, float opty) {
+    float v0x = optx, v0y = opty;
+    const float l2 = fmaf(optx, optx, opty * opty);
+    if (l2 > r * r) {
+        const float sc = r / sqrtf(l2);
+        v0x = optx * sc;
+        v0y = opty * sc;
+    }
+    auto pen = [&](int q) { return L.s[q * T] - fmaf(L.nx[q * T], v0x, L.ny[q * T] * v0y); };
+    if (MODE == 1) {
+        int best = 0;
+        float pb = pen(0);
+        for (int q = 1; q < n; ++q) {
+            const float p = pen(q);
+            if (p > pb) {
+                pb = p;
+                best = q;
+            }
+        }
+        if (best > 0 && pb > 0.0f) line_move(L, T, best, 0);
+        return;
+    }
+    int w = 0;  // violated lines so far, in slots [0, w)
+    for (int q = 0; q < n; ++q) {
+        const float p = pen(q);
+        if (p > 0.0f) {
+            int to = w;
+            if (MODE == 3)
+                while (to > 0 && pen(to - 1) < p) --to;
+            if (to < q) line_move(L, T, q, to);
+            ++w;
+        }
+    }
+}
+
 // Warp-synchronised LP2 / LP3: the same arithmetic as lp2 / lp3, but every
 // lane in `mask` runs the same number (kmax) of constraint iterations -- lines it does not
 // have are skipped -- with a reconvergence point after each, so the lanes that re-solve on
@@ -1344,6 +1403,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         }
         float vx, vy;
         if (CNT) w.lines += (uint32_t)cnt;
+        if (ORCA_LP_PEN && !a.m.lpRandom && cnt > 1) pen_order<ORCA_LP_PEN>(L, T, cnt, vmaxi, px, py);
         const int f = WU ? lp2_wu<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                          : ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                                         : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
@@ -1527,6 +1587,50 @@ __global__ void k_unpermute(const uint32_t* __restrict__ binStart, Grid g, const
         if (posOut) posOut[id] = posS[i];
         if (velOut) velOut[id] = velS[i];
     }
+}
+
+// orca_set_state_async (one strip): every loaded agent, in its current sorted order, takes
+// its new position / velocity by id from the upload and is binned into the work arrays
+// exactly as the step epilogue bins its result (finish_agent): prefVel or goal, search-
+// radius hint and per-agent properties travel along; k_scan + k_scatter then sort.  A
+// non-finite input raises *bad (reported by orca_io_wait); an agent in the grid's outer
+// cell ring or beyond (clamped: still exact, reading Q12) raises *gridFlag, so the grid is
+// re-derived before a later step without a synchronisation here.
+__global__ void k_reload(const uint32_t* __restrict__ binStart, Grid g, const uint32_t* __restrict__ idS,
+                         const float2* __restrict__ auxS, const float* __restrict__ rk2S,
+                         const float4* __restrict__ propS, const float2* __restrict__ pos,
+                         const float2* __restrict__ vel, float2* __restrict__ posW, float2* __restrict__ velW,
+                         float2* __restrict__ auxW, uint32_t* __restrict__ idW, float* __restrict__ rk2W,
+                         float4* __restrict__ propW, uint32_t* __restrict__ cellW, uint32_t* __restrict__ rankW,
+                         uint32_t* __restrict__ count, int* __restrict__ ctr, int* gridFlag, int* bad) {
+    const int2 r = owned_range(binStart, g);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr[CT_NOWN] = r.y - r.x;
+        ctr[CT_EXTRA] = 0;
+    }
+    bool nonfinite = false, ring = false;
+    for (int i = r.x + blockIdx.x * blockDim.x + threadIdx.x; i < r.y; i += gridDim.x * blockDim.x) {
+        const int w = i - r.x;
+        const uint32_t id = idS[i];
+        const float2 p = pos[id];
+        const float2 v = vel[id];
+        nonfinite |= !(isfinite(p.x) && isfinite(p.y) && isfinite(v.x) && isfinite(v.y));
+        const int cx = cell_coord(p.x, g.ox, g.csD, g.invCs, g.nx);
+        const int sy = subrow_coord(p.y, g);
+        const int cyc = sy >> g.lgS;
+        ring |= cx == 0 || cx == g.nx - 1 || cyc == 0 || cyc == g.ny - 1;
+        const uint32_t c = bin_of(cx, sy, g);
+        posW[w] = p;
+        velW[w] = v;
+        auxW[w] = auxS[i];
+        idW[w] = id;
+        rk2W[w] = rk2S[i];
+        if (propW) propW[w] = propS[i];
+        cellW[w] = c;
+        rankW[w] = atomicAdd(&count[c], 1u);
+    }
+    if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+    if (__any_sync(0xffffffffu, ring) && (threadIdx.x & 31) == 0) *gridFlag = 1;
 }
 
 __global__ void k_fill1(int n, float* __restrict__ out, float v) {

@@ -350,6 +350,10 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
             px = aux.x;
             py = aux.y;
         }
+        if (ORCA_LP_PEN && !a.m.lpRandom && cnt > 1) {  // the constraint order of k_step
+            if (G.gl == 0) pen_order<ORCA_LP_PEN>(Lines{Lnx, Lny, Ls}, 1, cnt, vmaxi, px, py);
+            __syncwarp(G.gmask);
+        }
         float vx, vy;
         const int f = lp2_group(G, Lnx, Lny, Ls, cnt, vmaxi, px, py, vx, vy, fl, wChecks, wLp1);
         // flags of all lanes of the group
