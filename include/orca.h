@@ -184,6 +184,33 @@ orca_status orca_step_trace(orca_ctx *ctx, int32_t n_steps, float *frames, float
  * be NULL).  Synchronises.  Errors: NOT_READY, CUDA. */
 orca_status orca_get_state(orca_ctx *ctx, float *pos, float *vel);
 
+/* ---- asynchronous per-step I/O ---------------------------------------------------------
+ * The same operations as orca_set_state / orca_get_state (each iteration observes the
+ * agents' positions and velocities; the per-step state leaves the GPU), enqueued
+ * without any host synchronisation, so that an application streaming state in and out
+ * every frame overlaps step s with the upload of frame s+1 and the read-back of frame s-1
+ * (host->device and device->host run on two copy streams; two slots each, so at most two
+ * uploads and two read-backs are in flight).  Pass pinned host memory (or device memory)
+ * for the overlap; pageable memory works but is staged synchronously by CUDA.
+ *
+ * orca_set_state_async: pos, vel float[2n] by id, as orca_set_state.  The caller must not
+ * modify them until orca_io_wait returns.  The grid stays; positions outside its interior
+ * are clamped for the steps already enqueued (exact, reading Q12) and the grid is re-derived
+ * before a later step.  A NaN/Inf is reported by orca_io_wait, or earlier by an orca_step
+ * that re-derives the grid first (INVALID_ARGUMENT; the context then needs orca_set_agents).  Strip contexts (more than one strip) take the synchronous
+ * orca_set_state.  Errors: NOT_READY, INVALID_ARGUMENT (NULL), OUT_OF_MEMORY, CUDA.
+ *
+ * orca_get_state_async: the state after all previously enqueued steps into caller buffers
+ * float[2n] (either may be NULL), valid once orca_io_wait returns.  Loopback strip contexts
+ * take the synchronous orca_get_state.  Errors: NOT_READY, INVALID_ARGUMENT (multi-rank),
+ * OUT_OF_MEMORY, CUDA.
+ *
+ * orca_io_wait: blocks until every enqueued upload, step and read-back is complete.
+ * Errors: INVALID_ARGUMENT (a non-finite upload, see above), CUDA. */
+orca_status orca_set_state_async(orca_ctx *ctx, const float *pos, const float *vel);
+orca_status orca_get_state_async(orca_ctx *ctx, float *pos, float *vel);
+orca_status orca_io_wait(orca_ctx *ctx);
+
 /* Number of agents currently held (multi-GPU: held by this rank). */
 orca_status orca_get_count(orca_ctx *ctx, int64_t *n);
 

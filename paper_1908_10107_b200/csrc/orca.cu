@@ -295,6 +295,16 @@ struct orca_ctx {
     int* gridFlagDev = nullptr;
     int64_t regrids = 0;
     unsigned char* ipcStage = nullptr;  // device staging of the cudaIpc handles for the all-gather
+    // asynchronous per-step I/O (orca_set_state_async / orca_get_state_async / orca_io_wait):
+    // uploads on ioIn and read-backs on ioOut overlap the steps on `stream`; two slots each
+    cudaStream_t ioIn = nullptr, ioOut = nullptr;
+    cudaEvent_t inReady[2] = {}, inFree[2] = {}, outReady[2] = {}, outFree[2] = {};
+    float2* inBuf[2] = {};   // pos | vel by id, 2 x nGlobal
+    float2* outBuf[2] = {};  // pos | vel by id, 2 x nGlobal
+    int64_t ioCap = 0;
+    int inSlot = 0, outSlot = 0;
+    int* ioBadHost = nullptr;  // host-mapped: a non-finite value in an asynchronous upload
+    int* ioBadDev = nullptr;
 };
 
 namespace {
@@ -1087,6 +1097,34 @@ orca_status maybe_rebalance(orca_ctx* c) {
     return rebalance(c, need == 2);
 }
 
+// Streams, events, the host-mapped error word and the two upload / read-back slots of the
+// asynchronous I/O path, sized for the loaded agent count.
+orca_status io_init(orca_ctx* c) {
+    if (!c->ioIn) {
+        CK(cudaStreamCreateWithFlags(&c->ioIn, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->ioOut, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b)
+            for (cudaEvent_t* e : {&c->inReady[b], &c->inFree[b], &c->outReady[b], &c->outFree[b]})
+                CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CK(cudaHostAlloc(&c->ioBadHost, sizeof(int), cudaHostAllocMapped));
+        *c->ioBadHost = 0;
+        CK(cudaHostGetDevicePointer(&c->ioBadDev, c->ioBadHost, 0));
+    }
+    if (c->ioCap < c->nGlobal) {
+        CK(cudaStreamSynchronize(c->ioIn));
+        CK(cudaStreamSynchronize(c->ioOut));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int b = 0; b < 2; ++b) {
+            dfree(c->inBuf[b]);
+            dfree(c->outBuf[b]);
+            CK(cudaMalloc(&c->inBuf[b], (size_t)c->nGlobal * 2 * sizeof(float2)));
+            CK(cudaMalloc(&c->outBuf[b], (size_t)c->nGlobal * 2 * sizeof(float2)));
+        }
+        c->ioCap = c->nGlobal;
+    }
+    return ORCA_OK;
+}
+
 }  // namespace
 
 // =============================================================================== ABI
@@ -1227,6 +1265,18 @@ void orca_destroy(orca_ctx* c) {
         cudaStreamSynchronize(c->copyStream);
         cudaStreamDestroy(c->copyStream);
     }
+    for (cudaStream_t s : {c->ioIn, c->ioOut})
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    for (int b = 0; b < 2; ++b) {
+        for (cudaEvent_t e : {c->inReady[b], c->inFree[b], c->outReady[b], c->outFree[b]})
+            if (e) cudaEventDestroy(e);
+        dfree(c->inBuf[b]);
+        dfree(c->outBuf[b]);
+    }
+    if (c->ioBadHost) cudaFreeHost(c->ioBadHost);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
@@ -1240,6 +1290,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     if (n > 0 && (!pos || !vel || !pref)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
+    if (c->ioBadHost) *c->ioBadHost = 0;  // a refused asynchronous upload is superseded
     *c->gridFlagHost = 0;  // a new grid is derived below
     // same agent count as the loaded state: keep each agent's last k-th neighbour distance
     // as its first search radius (a hint; the selection is exact for any radius)
@@ -1308,6 +1359,36 @@ orca_status orca_set_state(orca_ctx* c, const float* pos, const float* vel) {
     c->ready = false;
     CKS(build_domains(c, n, sp, sv, sa, hist, c->activeBuf));
     CKS(refresh_props(c));
+    return ORCA_OK;
+}
+
+orca_status orca_set_state_async(orca_ctx* c, const float* pos, const float* vel) {
+    if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    const int64_t n = c->nGlobal;
+    if (n > 0 && (!pos || !vel)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
+    if (c->world > 1 || c->doms.size() != 1) return orca_set_state(c, pos, vel);  // strips: synchronous
+    if (n == 0) return ORCA_OK;
+    CK(cudaSetDevice(c->device));
+    CKS(io_init(c));
+    const int b = c->inSlot;
+    c->inSlot ^= 1;
+    float2* buf = c->inBuf[b];
+    // upload (copy stream) once the step that last read this slot is done with it
+    CK(cudaStreamWaitEvent(c->ioIn, c->inFree[b], 0));
+    CK(cudaMemcpyAsync(buf, pos, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->ioIn));
+    CK(cudaMemcpyAsync(buf + n, vel, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->ioIn));
+    CK(cudaEventRecord(c->inReady[b], c->ioIn));
+    // re-bin on the step stream: k_reload -> scan -> scatter (no host synchronisation)
+    CK(cudaStreamWaitEvent(c->stream, c->inReady[b], 0));
+    Domain& d = c->doms[0];
+    k_reload<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(
+        d.binStart, d.g, d.idS, d.auxS, d.rk2S, c->het ? d.propS : nullptr, buf, buf + n, d.posW, d.velW, d.auxW,
+        d.idW, d.rk2W, c->het ? d.propW : nullptr, d.cellW, d.rankW, d.count, d.ctr, c->gridFlagDev, c->ioBadDev);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->inFree[b], c->stream));
+    CK(enqueue_scan(c, d, false));
+    CK(enqueue_scatter(c, d, 0));
     return ORCA_OK;
 }
 
@@ -1432,6 +1513,51 @@ orca_status orca_get_state(orca_ctx* c, float* pos, float* vel) {
         if (vel) CK(cudaMemcpyAsync(vel, c->outB, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
+    return ORCA_OK;
+}
+
+orca_status orca_get_state_async(orca_ctx* c, float* pos, float* vel) {
+    if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    if (c->world > 1 && !c->loopback)
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "multi-rank context: use orca_get_local_state");
+    if (c->doms.size() != 1) return orca_get_state(c, pos, vel);  // loopback strips: synchronous
+    const int64_t n = c->nGlobal;
+    if (n == 0 || (!pos && !vel)) return ORCA_OK;
+    CK(cudaSetDevice(c->device));
+    CKS(io_init(c));
+    const int b = c->outSlot;
+    c->outSlot ^= 1;
+    float2* ob = c->outBuf[b];
+    Domain& d = c->doms[0];
+    // un-permute on the step stream once the read-back that last used this slot is done
+    CK(cudaStreamWaitEvent(c->stream, c->outFree[b], 0));
+    if (c->removeR > 0.0f)  // agents removed at their goal read as NaN
+        k_fill2<<<cap_blocks(2 * n, 256), 256, 0, c->stream>>>((int)(2 * n), ob, NAN);
+    k_unpermute<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.idS, d.posS, d.velS,
+                                                               pos ? ob : nullptr, vel ? ob + n : nullptr);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->outReady[b], c->stream));
+    // read back on the copy stream
+    CK(cudaStreamWaitEvent(c->ioOut, c->outReady[b], 0));
+    if (pos) CK(cudaMemcpyAsync(pos, ob, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->ioOut));
+    if (vel) CK(cudaMemcpyAsync(vel, ob + n, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->ioOut));
+    CK(cudaEventRecord(c->outFree[b], c->ioOut));
+    return ORCA_OK;
+}
+
+orca_status orca_io_wait(orca_ctx* c) {
+    if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
+    CK(cudaSetDevice(c->device));
+    if (c->ioIn) CK(cudaStreamSynchronize(c->ioIn));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->ioOut) CK(cudaStreamSynchronize(c->ioOut));
+    if (c->ioBadHost && *(volatile int*)c->ioBadHost) {
+        *c->ioBadHost = 0;
+        c->ready = false;
+        return fail(ORCA_ERR_INVALID_ARGUMENT,
+                    "NaN/Inf in an orca_set_state_async upload; load the agents again with orca_set_agents");
+    }
     return ORCA_OK;
 }
 

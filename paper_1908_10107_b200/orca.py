@@ -28,7 +28,8 @@ EXPORTS = [
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
     "orca_set_lp_order", "orca_set_lp3_lanes", "orca_rebalance", "orca_set_transport",
-    "orca_get_transport", "orca_set_state",
+    "orca_get_transport", "orca_set_state", "orca_set_state_async", "orca_get_state_async",
+    "orca_io_wait",
 ]
 
 
@@ -95,6 +96,9 @@ def _load():
         "orca_set_transport": [vp, i32],
         "orca_get_transport": [vp, P(i32)],
         "orca_set_state": [vp, vp, vp],
+        "orca_set_state_async": [vp, vp, vp],
+        "orca_get_state_async": [vp, vp, vp],
+        "orca_io_wait": [vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -141,6 +145,17 @@ def _as_f32(a):
     return a  # torch tensors: caller supplies float32 contiguous
 
 
+def _io_arg(a):
+    """Buffers of the asynchronous calls are used as they are (no conversion copy that could
+    be freed while the transfer is in flight)."""
+    if a is None:
+        return None
+    dt = getattr(a, "dtype", None)
+    if str(dt) not in ("float32", "torch.float32"):
+        raise TypeError("asynchronous I/O buffers must be float32")
+    return a
+
+
 def make_params(timeStep=0.25, neighborDist=15.0, maxNeighbors=10, timeHorizon=5.0, radius=0.5,
                 maxSpeed=1.33) -> Params:
     return Params(timeStep, neighborDist, maxNeighbors, timeHorizon, radius, maxSpeed)
@@ -172,6 +187,7 @@ class Orca:
             params = make_params(**params)
         self.params = params
         self._ctx = ctypes.c_void_p()
+        self._io_keep = []
         self.strips = max(1, strips)
         if strips:
             _check(_lib.orca_create_strips(ctypes.byref(params), device, strips, ctypes.byref(self._ctx)))
@@ -203,6 +219,26 @@ class Orca:
     def set_state(self, pos, vel):
         """New positions / velocities of the loaded agents (by id); everything else stays."""
         _check(_lib.orca_set_state(self._ctx, _ptr(_as_f32(pos)), _ptr(_as_f32(vel))))
+
+    def set_state_async(self, pos, vel):
+        """orca_set_state_async: enqueue the upload + re-binning without synchronising.  pos / vel
+        must be float32 C-contiguous (pinned torch tensors for the overlap) and stay untouched
+        until io_wait()."""
+        self._io_keep.extend((_io_arg(pos), _io_arg(vel)))
+        _check(_lib.orca_set_state_async(self._ctx, _ptr(pos), _ptr(vel)))
+
+    def get_state_async(self, pos=None, vel=None):
+        """orca_get_state_async: enqueue the read-back of the state after the enqueued steps into
+        pos / vel (float32 C-contiguous, either None); valid after io_wait()."""
+        self._io_keep.extend((_io_arg(pos), _io_arg(vel)))
+        _check(_lib.orca_get_state_async(self._ctx, _ptr(pos), _ptr(vel)))
+
+    def io_wait(self):
+        """orca_io_wait: every enqueued upload, step and read-back is complete."""
+        try:
+            _check(_lib.orca_io_wait(self._ctx))
+        finally:
+            self._io_keep.clear()
 
     def set_goals(self, goals, pref_speed: float):
         _check(_lib.orca_set_goals(self._ctx, _ptr(_as_f32(goals)), pref_speed))

@@ -1,0 +1,177 @@
+"""Asynchronous per-step I/O (orca_set_state_async / orca_get_state_async / orca_io_wait):
+the pipelined upload -> step -> read-back loop gives the synchronous loop's results bit for
+bit, including goals, removal at the goal, per-agent properties, the randomized LP order and
+states that leave the grid (clamped for the enqueued steps, re-gridded later)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_1908_10107_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orca():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1908_10107_b200 import build
+    build.build()
+    from paper_1908_10107_b200 import orca as O
+    return O
+
+
+def _props(n, seed):
+    rng = np.random.default_rng(seed)
+    radius = rng.choice([0.5, 0.75, 1.0], n).astype(np.float32)
+    desired = rng.choice([1.0, 1.33, 2.0], n).astype(np.float32)
+    return radius, (1.25 * desired).astype(np.float32), desired
+
+
+def _states(w, steps, seed, far_step=None):
+    """Per-step uploads: the initial state jittered (one of them shifted 400 m away)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for s in range(steps):
+        p = (w["pos"] + rng.normal(0, 0.3, w["pos"].shape)).astype(np.float32)
+        v = (w["vel"] + rng.normal(0, 0.1, w["vel"].shape)).astype(np.float32)
+        if s == far_step:
+            p = (p + np.float32(400.0)).astype(np.float32)
+        out.append((p, v))
+    return out
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_async_loop_equals_sync_loop(orca, full):
+    import torch
+    w = W.make("uniform", n=30000 if full else 6000, rho=0.3)
+    n = len(w["pos"])
+    rng = np.random.default_rng(3)
+    goals = (w["pos"] + rng.uniform(-30, 30, w["pos"].shape)).astype(np.float32)
+    props = _props(n, 8)
+
+    def make():
+        o = orca.Orca(w["params"])
+        o.set_agents(w["pos"], w["vel"], w["pref"])
+        if full:
+            o.set_goals(goals, 1.0)
+            o.set_goal_removal(2.0)
+            o.set_agent_props(*props)
+            o.set_lp_order(True, 5, 0)
+        return o
+
+    K = 12
+    ups = _states(w, K, seed=11, far_step=7)
+    a, b = make(), make()
+    ref = []
+    for p, v in ups:
+        a.set_state(p, v)
+        a.step(1)
+        ref.append(a.get_state())
+    hp = [torch.from_numpy(p).pin_memory() for p, _ in ups]
+    hv = [torch.from_numpy(v).pin_memory() for _, v in ups]
+    op = [torch.empty((n, 2), dtype=torch.float32).pin_memory() for _ in range(K)]
+    ov = [torch.empty((n, 2), dtype=torch.float32).pin_memory() for _ in range(K)]
+    for s in range(K):
+        b.set_state_async(hp[s], hv[s])
+        b.step(1)
+        b.get_state_async(op[s], ov[s])
+    b.io_wait()
+    for s in range(K):
+        assert np.array_equal(ref[s][0], op[s].numpy(), equal_nan=True), s
+        assert np.array_equal(ref[s][1], ov[s].numpy(), equal_nan=True), s
+    # the shifted upload was stepped on the old grid (clamped); the grid follows later
+    b.step(2)
+    a.step(2)
+    sa, sb = a.get_state(), b.get_state()
+    assert np.array_equal(sa[0], sb[0], equal_nan=True) and np.array_equal(sa[1], sb[1], equal_nan=True)
+    assert a.count() == b.count()
+    if full:
+        assert a.count() < n  # removal happened
+    ta, tb = a.stats(), b.stats()
+    for key in ("infeasible", "collision_pairs", "removed"):
+        assert ta[key] == tb[key], key
+    a.close()
+    b.close()
+
+
+def test_async_numpy_and_device_buffers(orca):
+    """Device tensors and plain float32 numpy arrays are accepted too."""
+    import torch
+    w = W.make("uniform", n=5000, rho=0.2)
+    a, b = orca.Orca(w["params"]), orca.Orca(w["params"])
+    for o in (a, b):
+        o.set_agents(w["pos"], w["vel"], w["pref"])
+    a.step(3)
+    ra = a.get_state()
+    dp = torch.from_numpy(w["pos"]).cuda()
+    dv = torch.from_numpy(w["vel"]).cuda()
+    b.set_state_async(dp, dv)
+    b.step(3)
+    pos = np.empty_like(w["pos"])
+    vel = np.empty_like(w["vel"])
+    b.get_state_async(pos, vel)
+    b.io_wait()
+    assert np.array_equal(ra[0], pos) and np.array_equal(ra[1], vel)
+    with pytest.raises(TypeError):
+        b.set_state_async(w["pos"].astype(np.float64), w["vel"])
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("value", [np.inf, np.nan])
+def test_async_nonfinite_upload_reported(orca, value):
+    w = W.make("uniform", n=4000, rho=0.2)
+    o = orca.Orca(w["params"])
+    o.set_agents(w["pos"], w["vel"], w["pref"])
+    bad = w["pos"].copy()
+    bad[17, 1] = value
+    o.set_state_async(bad, w["vel"])
+    raised = 0
+    try:  # (an Inf lies beyond the grid: a step that re-derives it first reports it)
+        o.step(1)
+    except orca.OrcaError:
+        raised += 1
+    try:
+        o.io_wait()
+    except orca.OrcaError:
+        raised += 1
+    assert raised
+    with pytest.raises(orca.OrcaError):  # NOT_READY until the agents are loaded again
+        o.step(1)
+    o.set_agents(w["pos"], w["vel"], w["pref"])
+    o.step(1)
+    o.io_wait()
+    o.close()
+
+
+def test_async_empty_and_strips_fallback(orca):
+    """n = 0 is a no-op; a loopback strips context takes the synchronous path."""
+    w = W.make("uniform", n=9000, rho=0.3)
+    e = orca.Orca(w["params"])
+    z = np.zeros((0, 2), np.float32)
+    e.set_agents(z, z, z)
+    e.set_state_async(z, z)
+    e.get_state_async(z, z)
+    e.io_wait()
+    e.close()
+    a = orca.Orca(w["params"])
+    s = orca.Orca(w["params"], strips=3)
+    for o in (a, s):
+        o.set_agents(w["pos"], w["vel"], w["pref"])
+        o.step(2)
+    ups = _states(w, 1, seed=5)[0]
+    a.set_state(*ups)
+    s.set_state_async(*ups)
+    a.step(2)
+    s.step(2)
+    pos = np.empty_like(w["pos"])
+    vel = np.empty_like(w["vel"])
+    s.get_state_async(pos, vel)
+    s.io_wait()
+    ra = a.get_state()
+    assert np.array_equal(ra[0], pos) and np.array_equal(ra[1], vel)
+    a.close()
+    s.close()
