@@ -29,6 +29,10 @@ using namespace orca;
 namespace {
 
 constexpr int kSubRowsLog2 = 3;  // 8 sort sub-rows per cell
+#ifndef ORCA_SUBCOLS_LOG2
+#define ORCA_SUBCOLS_LOG2 2
+#endif
+constexpr int kSubColsLog2 = ORCA_SUBCOLS_LOG2;  // 2^this fine columns per cell
 
 int scan_tiles(int64_t C) { return (int)((C + kScanTile - 1) / kScanTile); }
 int cap_blocks(int64_t n, int threads) {
@@ -651,10 +655,10 @@ orca_status check_overflow(orca_ctx* c) {
 
 // owned range [o0, o1) of a domain (host read; synchronises)
 orca_status owned_range_host(orca_ctx* c, Domain& d, int* o0, int* o1) {
-    const int64_t nyS = (int64_t)d.g.ny << d.g.lgS;
+    const int64_t cb = d.g.colBins;
     uint32_t v[2];
-    CK(cudaMemcpyAsync(&v[0], d.binStart + (d.g.c0 - d.g.e0) * nyS, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(&v[1], d.binStart + (d.g.c1 - d.g.e0) * nyS, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&v[0], d.binStart + (d.g.c0 - d.g.e0) * cb, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&v[1], d.binStart + (d.g.c1 - d.g.e0) * cb, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     *o0 = (int)v[0];
     *o1 = (int)v[1];
@@ -739,6 +743,7 @@ orca_status derive_grid(orca_ctx* c, int64_t n, const float mn[2], const float m
     Grid g{};
     g.cs = cs;
     g.lgS = kSubRowsLog2;
+    g.lgC = kSubColsLog2;
     if (n == 0) {
         g.ox = g.oy = 0.0f;
         g.nx = g.ny = 1;
@@ -749,7 +754,7 @@ orca_status derive_grid(orca_ctx* c, int64_t n, const float mn[2], const float m
         g.oy = oy;
         const double tx = std::floor(((double)mx[0] - (double)g.ox) / (double)cs) + margin + 1;
         const double ty = std::floor(((double)mx[1] - (double)g.oy) / (double)cs) + margin + 1;
-        if (tx > 1e9 || ty > 1e9 || tx * ty * (double)(1 << kSubRowsLog2) > (double)(1 << 28))
+        if (tx > 1e9 || ty > 1e9 || tx * ty * (double)(1 << (kSubRowsLog2 + kSubColsLog2)) > (double)(1 << 28))
             return fail(ORCA_ERR_CAPACITY, "grid would exceed 2^28 sort bins");
         g.nx = (int)tx;
         g.ny = (int)ty;
@@ -758,6 +763,9 @@ orca_status derive_grid(orca_ctx* c, int64_t n, const float mn[2], const float m
     g.invCs = 1.0 / (double)cs;
     g.csSub = (double)cs / (double)(1 << g.lgS);
     g.invCsSub = (double)(1 << g.lgS) / (double)cs;
+    g.csSubX = (double)cs / (double)(1 << g.lgC);
+    g.invCsSubX = (double)(1 << g.lgC) / (double)cs;
+    g.colBins = (g.ny << g.lgS) << g.lgC;
     c->gg = g;
     return ORCA_OK;
 }
@@ -908,7 +916,7 @@ orca_status build_domains(orca_ctx* c, int64_t n, const float2* sp, const float2
         d.g.e1 = std::min(d.g.c1 + 1, g.nx);
         d.g.hasL = s > 0;
         d.g.hasR = s < c->world - 1;
-        d.nbins = ((int64_t)(d.g.e1 - d.g.e0) * g.ny) << g.lgS;
+        d.nbins = (int64_t)(d.g.e1 - d.g.e0) * g.colBins;
         int64_t sel = 0;
         for (int x = d.g.e0; x < d.g.e1; ++x) sel += colCount[x];
         d.popBuild = 0;

@@ -49,9 +49,12 @@ struct WorkT {
 struct Grid {
     float ox, oy, cs;  // origin, cell size (fp32 values; widened exactly to fp64)
     int nx, ny;        // dims (cells of size cs = r_obs)
-    int lgS;           // each cell is split into 2^lgS sub-rows for the sort order
+    int lgS;           // each cell is split into 2^lgS sub-rows for the sort order ...
+    int lgC;           // ... and 2^lgC sub-columns (fine columns)
+    int colBins;       // sort bins per cell column: 2^lgC fine columns x (ny << lgS) sub-rows
     double csD, invCs;        // fl64(cs), fl64(1/cs)
     double csSub, invCsSub;   // cs / 2^lgS (exact), 2^lgS / cs
+    double csSubX, invCsSubX; // cs / 2^lgC (exact), 2^lgC / cs
     // strip of this domain: owned columns [c0, c1); the local bins cover
     // columns [e0, e1) = owned plus one ghost column on each side that exists
     int c0, c1, e0, e1;
@@ -105,11 +108,18 @@ __device__ __forceinline__ int subrow_coord(float y, const Grid& g) {
     return floor_div_clamped(__dsub_rn((double)y, (double)g.oy), g.csSub, g.invCsSub, g.ny << g.lgS);
 }
 
-// Local bin id of the sort order: column-major over (cx - e0, sub-row), so the owned
-// strip is one contiguous id range, a coarse cell is 2^lgS consecutive bins, and each
-// column run of the 3x3 stencil is ordered by y at sub-row granularity.
-__device__ __forceinline__ uint32_t bin_of(int cx, int sy, const Grid& g) {
-    return (uint32_t)(cx - g.e0) * (uint32_t)(g.ny << g.lgS) + (uint32_t)sy;
+// Fine column of x: floor((x - ox) / (cs / 2^lgC)), clamped, by the same exact rule; the
+// fine column >> lgC is exactly the clamped cell column (cell_coord).
+__device__ __forceinline__ int finecol_coord(float x, const Grid& g) {
+    return floor_div_clamped(__dsub_rn((double)x, (double)g.ox), g.csSubX, g.invCsSubX, g.nx << g.lgC);
+}
+
+// Local bin id of the sort order: column-major over (fine column - 2^lgC e0, sub-row), so
+// the owned strip (cell columns [c0, c1)) is one contiguous id range, a cell column is
+// colBins consecutive bins, and each fine column's run is ordered by y at sub-row
+// granularity: the agents within a distance of (x, y) lie in a few short runs.
+__device__ __forceinline__ uint32_t bin_of(int fx, int sy, const Grid& g) {
+    return (uint32_t)(fx - (g.e0 << g.lgC)) * (uint32_t)(g.ny << g.lgS) + (uint32_t)sy;
 }
 
 constexpr uint32_t kInvalid = 0xffffffffu;  // work entry that left the strip
@@ -147,14 +157,15 @@ __global__ void k_select(int n, const float2* __restrict__ pos, const float2* __
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         if (active && !active[i]) continue;  // removed at its goal
         const float2 p = pos[i];
-        const int cx = cell_coord(p.x, g.ox, g.csD, g.invCs, g.nx);
+        const int fx = finecol_coord(p.x, g);
+        const int cx = fx >> g.lgC;  // = cell_coord(p.x, ...)
         if (cx < g.e0 || cx >= g.e1) continue;
         const int w = atomicAdd(&ctr[CT_EXTRA], 1);
         if (w >= capW) {
             atomicOr(&ctr[CT_OVF], OVF_WORK);
             continue;
         }
-        const uint32_t c = bin_of(cx, subrow_coord(p.y, g), g);
+        const uint32_t c = bin_of(fx, subrow_coord(p.y, g), g);
         posW[w] = p;
         velW[w] = vel[i];
         auxW[w] = aux[i];
@@ -169,8 +180,8 @@ __global__ void k_select(int n, const float2* __restrict__ pos, const float2* __
 // first search radius of the next orca_set_agents with the same agent count.
 __global__ void k_hist_by_id(const uint32_t* __restrict__ binStart, Grid g, const uint32_t* __restrict__ idS,
                              const float* __restrict__ rk2S, float* __restrict__ out) {
-    const int nyS = g.ny << g.lgS;
-    const int o0 = (int)binStart[(g.c0 - g.e0) * nyS], o1 = (int)binStart[(g.c1 - g.e0) * nyS];
+    const int cb = g.colBins;
+    const int o0 = (int)binStart[(g.c0 - g.e0) * cb], o1 = (int)binStart[(g.c1 - g.e0) * cb];
     for (int i = o0 + blockIdx.x * blockDim.x + threadIdx.x; i < o1; i += gridDim.x * blockDim.x)
         out[idS[i]] = rk2S[i];
 }
@@ -182,8 +193,8 @@ __global__ void k_gather_state(const uint32_t* __restrict__ binStart, Grid g, co
                                const float2* __restrict__ auxS, const float* __restrict__ rk2S,
                                float2* __restrict__ pos, float2* __restrict__ vel, float2* __restrict__ aux,
                                float* __restrict__ rk2, uint8_t* __restrict__ active) {
-    const int nyS = g.ny << g.lgS;
-    const int o0 = (int)binStart[(g.c0 - g.e0) * nyS], o1 = (int)binStart[(g.c1 - g.e0) * nyS];
+    const int cb = g.colBins;
+    const int o0 = (int)binStart[(g.c0 - g.e0) * cb], o1 = (int)binStart[(g.c1 - g.e0) * cb];
     for (int i = o0 + blockIdx.x * blockDim.x + threadIdx.x; i < o1; i += gridDim.x * blockDim.x) {
         const uint32_t id = idS[i];
         pos[id] = posS[i];
@@ -200,8 +211,8 @@ __global__ void k_pack_owned(const uint32_t* __restrict__ binStart, Grid g, cons
                              const float2* __restrict__ posS, const float2* __restrict__ velS,
                              const float2* __restrict__ auxS, const float* __restrict__ rk2S,
                              float4* __restrict__ out, int cap) {
-    const int nyS = g.ny << g.lgS;
-    const int o0 = (int)binStart[(g.c0 - g.e0) * nyS], o1 = (int)binStart[(g.c1 - g.e0) * nyS];
+    const int cb = g.colBins;
+    const int o0 = (int)binStart[(g.c0 - g.e0) * cb], o1 = (int)binStart[(g.c1 - g.e0) * cb];
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < cap; q += gridDim.x * blockDim.x) {
         const int i = o0 + q;
         if (i < o1) {
@@ -233,9 +244,9 @@ __global__ void k_unpack_gathered(const float4* __restrict__ in, int total, floa
 // Fill report of a strip: owned agents and the populations of its two edge columns.
 __global__ void k_fill_report(const uint32_t* __restrict__ binStart, Grid g, int* __restrict__ out) {
     if (threadIdx.x != 0) return;
-    const int nyS = g.ny << g.lgS;
-    const int b0 = (int)binStart[(g.c0 - g.e0) * nyS], b1 = (int)binStart[(g.c0 - g.e0 + 1) * nyS];
-    const int b2 = (int)binStart[(g.c1 - 1 - g.e0) * nyS], b3 = (int)binStart[(g.c1 - g.e0) * nyS];
+    const int cb = g.colBins;
+    const int b0 = (int)binStart[(g.c0 - g.e0) * cb], b1 = (int)binStart[(g.c0 - g.e0 + 1) * cb];
+    const int b2 = (int)binStart[(g.c1 - 1 - g.e0) * cb], b3 = (int)binStart[(g.c1 - g.e0) * cb];
     out[0] = b3 - b0;
     out[1] = b1 - b0;
     out[2] = b3 - b2;
@@ -889,7 +900,7 @@ struct StepArgs {
     int pad1;
     int* gridFlag;  // host-mapped: set when an agent enters the grid's outer cell ring
 };
-static_assert(sizeof(Grid) == 80 && sizeof(Model) == 96 && sizeof(ExBuf) % 8 == 0, "padding-free layouts");
+static_assert(sizeof(Grid) == 104 && sizeof(Model) == 96 && sizeof(ExBuf) % 8 == 0, "padding-free layouts");
 
 #ifndef ORCA_STEP_THREADS
 #define ORCA_STEP_THREADS 128
@@ -1057,14 +1068,14 @@ __device__ __forceinline__ void push_halo(const ExBuf& x, int* ctr, float2 p, fl
 }
 
 // Append one entry to the work buffers at nOwn + extra (ghosts, immigrants).
-__device__ __forceinline__ void append_work(const StepArgs& a, int nOwn, int cx, int sy, float2 p, float2 v, float2 aux,
+__device__ __forceinline__ void append_work(const StepArgs& a, int nOwn, int fx, int sy, float2 p, float2 v, float2 aux,
                                             uint32_t id, float rk2, float4 pr) {
     const int e = nOwn + atomicAdd(&a.ctr[CT_EXTRA], 1);
     if (e >= a.capW) {
         atomicOr(&a.ctr[CT_OVF], OVF_WORK);
         return;
     }
-    const uint32_t c = bin_of(cx, sy, a.g);
+    const uint32_t c = bin_of(fx, sy, a.g);
     a.posW[e] = p;
     a.velW[e] = v;
     a.auxW[e] = aux;
@@ -1094,14 +1105,15 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
             return;
         }
     }
-    const int cx = cell_coord(pn.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
+    const int fx = finecol_coord(pn.x, a.g);
+    const int cx = fx >> a.g.lgC;  // = cell_coord(pn.x, ...)
     const int sy = subrow_coord(pn.y, a.g);
     if (a.gridFlag) {  // the outer ring: beyond it positions are clamped -> re-derive the grid
         const int cyc = sy >> a.g.lgS;
         if (cx == 0 || cx == a.g.nx - 1 || cyc == 0 || cyc == a.g.ny - 1) *a.gridFlag = 1;
     }
     if (cx >= a.g.c0 && cx < a.g.c1) {
-        const uint32_t c = bin_of(cx, sy, a.g);
+        const uint32_t c = bin_of(fx, sy, a.g);
         a.posW[w] = pn;
         a.velW[w] = vn;
         a.auxW[w] = aux;
@@ -1126,15 +1138,12 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
             x.mrk2[s] = rk2;
             x.mprop[s] = pr;
         }
-        append_work(a, nOwn, cx, sy, pn, vn, aux, id, INFINITY, pr);
+        append_work(a, nOwn, fx, sy, pn, vn, aux, id, INFINITY, pr);
     }
 }
 
-// warp reconvergence points in k_step: after the column scans (COLS) and
-// at the once-per-agent phase boundaries (PHASES); the one before the final merge is always on
-#ifndef ORCA_SYNC_COLS
-#define ORCA_SYNC_COLS 0
-#endif
+// warp reconvergence points in k_step at the once-per-agent phase
+// boundaries (PHASES); the one before the final merge is always on
 #ifndef ORCA_SYNC_PHASES
 #define ORCA_SYNC_PHASES 0  // swept: 1M 0.495 ms (0) vs 0.529 ms (1)
 #endif
@@ -1162,9 +1171,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     const Lines L{reinterpret_cast<float*>(L0), reinterpret_cast<float*>(L1), reinterpret_cast<float*>(Bf)};
 
     // owned agents are the contiguous sorted range of columns [c0, c1)
-    const int nyS0 = a.g.ny << a.g.lgS;
-    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * nyS0];
-    const int o1 = (int)a.binStart[(a.g.c1 - a.g.e0) * nyS0];
+    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * a.g.colBins];
+    const int o1 = (int)a.binStart[(a.g.c1 - a.g.e0) * a.g.colBins];
     const int ws = blockIdx.x * T + tid;  // work slot
     const int i = o0 + ws;                // sorted index
     const bool active = i < o1;
@@ -1204,9 +1212,9 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             const int rlo = max(cy - 1, 0) << lgS;              // first sub-row of the 3 rows
             const int rhi = (min(cy + 1, a.g.ny - 1) + 1) << lgS; // one past the last
             const int c0 = max(cx - 1, 0), c1 = min(cx + 1, a.g.nx - 1);
-            int ncand = 0;
-            for (int col = c0; col <= c1; ++col)
-                ncand += (int)a.binStart[(col - a.g.e0) * nyS + rhi] - (int)a.binStart[(col - a.g.e0) * nyS + rlo];
+            const int lgC = a.g.lgC;
+            const int fe0 = a.g.e0 << lgC;                              // first local fine column
+            const int f0 = c0 << lgC, f1 = ((c1 + 1) << lgC) - 1;       // fine columns of the stencil
             float thr = a.m.nd2Fup;
             bool guessed = false;
             const float rk2p = a.rk2S[i];
@@ -1218,10 +1226,13 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                     thr = b;
                     guessed = true;
                 }
-            } else if (ncand > 4 * k) {
+            } else {
+                int ncand = 0;  // agents in the 3x3 stencil
+                for (int fc = f0; fc <= f1; ++fc)
+                    ncand += (int)a.binStart[(fc - fe0) * nyS + rhi] - (int)a.binStart[(fc - fe0) * nyS + rlo];
                 // r^2 = 2.2 k / (pi rho), rho = ncand / (9 cs^2): ~22 expected hits for k = 10
                 const float g = ORCA_COLD_LAMBDA * (float)k * 9.0f * a.g.cs * a.g.cs / (3.14159265f * (float)ncand);
-                if (g < thr) {
+                if (ncand > 4 * k && g < thr) {
                     thr = g;
                     guessed = true;
                 }
@@ -1247,8 +1258,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             if (KR > 0 && mode == 0) reg_clear<(KR > 0 ? KR : 1)>(R);
             for (int pass = 0; pass < 3; ++pass) {
                 const float thrPass = thr;
-                // sub-row window and side columns for this pass
-                int lo = rlo, hi = rhi - 1, cl = c0, cr = c1;
+                // sub-row window and fine-column range for this pass
+                int lo = rlo, hi = rhi - 1, fa = f0, fb = f1;
                 if (guessed) {
                     const float rg = sqrtf(thr) * (1.0f + 1e-6f) + 1e-6f;
                     // sub-rows s with [oy + s h, oy + (s+1) h) within rg of y (h = cs/2^lgS):
@@ -1257,19 +1268,16 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                     const double rs = (double)rg * a.g.invCsSub + 1e-6;
                     lo = max(lo, (int)fmax(floor(ty - rs), -2.0));
                     hi = min(hi, (int)fmin(floor(ty + rs), (double)nyS + 2.0));
-                    const double xl = (double)a.g.ox + (double)cx * (double)a.g.cs;  // cell's left edge
-                    if ((double)pi.x - xl > (double)rg) cl = cx;                       // left column beyond rg
-                    if (xl + (double)a.g.cs - (double)pi.x > (double)rg) cr = cx;     // right column beyond rg
+                    // fine columns within rg of x, the same way
+                    const double tx = __dmul_rn(__dsub_rn((double)pi.x, (double)a.g.ox), a.g.invCsSubX);
+                    const double rsx = (double)rg * a.g.invCsSubX + 1e-6;
+                    fa = max(fa, (int)fmax(floor(tx - rsx), -2.0));
+                    fb = min(fb, (int)fmin(floor(tx + rsx), (double)(a.g.nx << lgC) + 2.0));
                 }
                 int nb = 0;
-                for (int q = 0; q < 3; ++q) {
-                    // reconverge between the column runs (first pass of the first mode:
-                    // every active lane comes here exactly three times)
-                    if (ORCA_SYNC_COLS && pass == 0 && mode == ((KR > 0) ? 0 : 1)) __syncwarp(activeMask);
-                    const int col = (q == 0) ? cx : (q == 1 ? cx - 1 : cx + 1);  // own column first
-                    if (col < cl || col > cr) continue;
-                    const int b = (int)a.binStart[(col - a.g.e0) * nyS + lo];
-                    const int e = (int)a.binStart[(col - a.g.e0) * nyS + hi + 1];
+                for (int fc = fa; fc <= fb; ++fc) {  // one run per fine column
+                    const int b = (int)a.binStart[(fc - fe0) * nyS + lo];
+                    const int e = (int)a.binStart[(fc - fe0) * nyS + hi + 1];
                     if (CNT) w.cand += (uint32_t)(e - b);
                     int j = b;
                     for (; j + 1 < e; j += 2) {  // 2-way unrolled: two loads in flight
@@ -1494,8 +1502,8 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
     const Lines P{base + 3 * k * T, base + 4 * k * T, base + 5 * k * T};
     const int nq = (int)*a.qCount;
     if ((int)blockIdx.x * T >= nq) return;  // block-uniform: nothing queued for this block
-    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * (a.g.ny << a.g.lgS)];
-    const int nOwn = (int)a.binStart[(a.g.c1 - a.g.e0) * (a.g.ny << a.g.lgS)] - o0;
+    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * a.g.colBins];
+    const int nOwn = (int)a.binStart[(a.g.c1 - a.g.e0) * a.g.colBins] - o0;
     int cInf = 0, cDeg = 0, cG1 = 0, cG2 = 0, cG3 = 0;
     // one queue entry per thread, grid-stride over the device-side count (block-uniform
     // trip count); lanes of a warp reconverge inside lp3_sync
@@ -1572,8 +1580,8 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
 // ------------------------------------------------------------------ state utilities
 // owned sorted range [o0, o1) of a domain
 __device__ __forceinline__ int2 owned_range(const uint32_t* __restrict__ binStart, const Grid& g) {
-    const int nyS = g.ny << g.lgS;
-    return make_int2((int)binStart[(g.c0 - g.e0) * nyS], (int)binStart[(g.c1 - g.e0) * nyS]);
+    const int cb = g.colBins;
+    return make_int2((int)binStart[(g.c0 - g.e0) * cb], (int)binStart[(g.c1 - g.e0) * cb]);
 }
 
 // owned agents -> id-ordered outputs (pos, vel; either nullable); optional local export
@@ -1615,11 +1623,12 @@ __global__ void k_reload(const uint32_t* __restrict__ binStart, Grid g, const ui
         const float2 p = pos[id];
         const float2 v = vel[id];
         nonfinite |= !(isfinite(p.x) && isfinite(p.y) && isfinite(v.x) && isfinite(v.y));
-        const int cx = cell_coord(p.x, g.ox, g.csD, g.invCs, g.nx);
+        const int fx = finecol_coord(p.x, g);
+        const int cx = fx >> g.lgC;
         const int sy = subrow_coord(p.y, g);
         const int cyc = sy >> g.lgS;
         ring |= cx == 0 || cx == g.nx - 1 || cyc == 0 || cyc == g.ny - 1;
-        const uint32_t c = bin_of(cx, sy, g);
+        const uint32_t c = bin_of(fx, sy, g);
         posW[w] = p;
         velW[w] = v;
         auxW[w] = auxS[i];
@@ -1802,12 +1811,12 @@ __global__ void k_receive(StepArgs a, ExBuf rL0, ExBuf rL1, ExBuf rR0, ExBuf rR1
             mig = false;
         }
         const float2 p = mig ? x->mpos[q] : x->hpos[q];
-        const int cx = cell_coord(p.x, a.g.ox, a.g.csD, a.g.invCs, a.g.nx);
+        const int fx = finecol_coord(p.x, a.g);
         const int sy = subrow_coord(p.y, a.g);
         if (mig)
-            append_work(a, nOwn, cx, sy, p, x->mvel[q], x->maux[q], x->mid[q], x->mrk2[q], x->mprop[q]);
+            append_work(a, nOwn, fx, sy, p, x->mvel[q], x->maux[q], x->mid[q], x->mrk2[q], x->mprop[q]);
         else
-            append_work(a, nOwn, cx, sy, p, x->hvel[q], make_float2(0.0f, 0.0f), x->hid[q], INFINITY,
+            append_work(a, nOwn, fx, sy, p, x->hvel[q], make_float2(0.0f, 0.0f), x->hid[q], INFINITY,
                         make_float4(x->hrad[q], 0.0f, 0.0f, 0.0f));
     }
 }

@@ -221,8 +221,8 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3_grp(StepArgs a) {
     float* Pny = Pnx + k;
     float* Ps = Pny + k;
     const int nq = (int)*a.qCount;
-    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * (a.g.ny << a.g.lgS)];
-    const int nOwn = (int)a.binStart[(a.g.c1 - a.g.e0) * (a.g.ny << a.g.lgS)] - o0;
+    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * a.g.colBins];
+    const int nOwn = (int)a.binStart[(a.g.c1 - a.g.e0) * a.g.colBins] - o0;
     int cInf = 0, cDeg = 0, cG1 = 0, cG2 = 0, cG3 = 0;
     // persistent grid (a few waves of groups), group-uniform stride over the queue
     for (int q = blockIdx.x * PPB + slot; q < nq; q += gridDim.x * PPB) {

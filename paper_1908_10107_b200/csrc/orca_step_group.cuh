@@ -185,9 +185,8 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
     float* Lny = Lnx + k;
     float* Ls = Lny + k;
 
-    const int nyS0 = a.g.ny << a.g.lgS;
-    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * nyS0];
-    const int o1 = (int)a.binStart[(a.g.c1 - a.g.e0) * nyS0];
+    const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * a.g.colBins];
+    const int o1 = (int)a.binStart[(a.g.c1 - a.g.e0) * a.g.colBins];
     const int ws = blockIdx.x * kGroupAgents + ag;
     const int i = o0 + ws;
     const bool active = i < o1;  // group-uniform
@@ -219,9 +218,9 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
             const int rlo = max(cy - 1, 0) << lgS;
             const int rhi = (min(cy + 1, a.g.ny - 1) + 1) << lgS;
             const int c0 = max(cx - 1, 0), c1 = min(cx + 1, a.g.nx - 1);
-            int ncand = 0;
-            for (int col = c0; col <= c1; ++col)
-                ncand += (int)a.binStart[(col - a.g.e0) * nyS + rhi] - (int)a.binStart[(col - a.g.e0) * nyS + rlo];
+            const int lgC = a.g.lgC;
+            const int fe0 = a.g.e0 << lgC;                         // first local fine column
+            const int f0 = c0 << lgC, f1 = ((c1 + 1) << lgC) - 1;  // fine columns of the stencil
             float thr = a.m.nd2Fup;
             bool guessed = false;
             const float rk2p = a.rk2S[i];
@@ -233,34 +232,36 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
                     thr = b;
                     guessed = true;
                 }
-            } else if (ncand > 4 * k) {
+            } else {
+                int ncand = 0;  // agents in the 3x3 stencil
+                for (int fc = f0; fc <= f1; ++fc)
+                    ncand += (int)a.binStart[(fc - fe0) * nyS + rhi] - (int)a.binStart[(fc - fe0) * nyS + rlo];
                 const float g = 2.2f * (float)k * 9.0f * a.g.cs * a.g.cs / (3.14159265f * (float)ncand);
-                if (g < thr) {
+                if (ncand > 4 * k && g < thr) {
                     thr = g;
                     guessed = true;
                 }
             }
             for (int pass = 0; pass < 2; ++pass) {
                 const float thrPass = thr;
-                int lo = rlo, hi = rhi - 1, cl = c0, cr = c1;
+                int lo = rlo, hi = rhi - 1, fa = f0, fb = f1;
                 if (guessed) {
                     const float rg = sqrtf(thr) * (1.0f + 1e-6f) + 1e-6f;
                     const double ty = __dmul_rn(__dsub_rn((double)pi.y, (double)a.g.oy), a.g.invCsSub);
                     const double rs = (double)rg * a.g.invCsSub + 1e-6;
                     lo = max(lo, (int)fmax(floor(ty - rs), -2.0));
                     hi = min(hi, (int)fmin(floor(ty + rs), (double)nyS + 2.0));
-                    const double xl = (double)a.g.ox + (double)cx * (double)a.g.cs;
-                    if ((double)pi.x - xl > (double)rg) cl = cx;
-                    if (xl + (double)a.g.cs - (double)pi.x > (double)rg) cr = cx;
+                    const double tx = __dmul_rn(__dsub_rn((double)pi.x, (double)a.g.ox), a.g.invCsSubX);
+                    const double rsx = (double)rg * a.g.invCsSubX + 1e-6;
+                    fa = max(fa, (int)fmax(floor(tx - rsx), -2.0));
+                    fb = min(fb, (int)fmin(floor(tx + rsx), (double)(a.g.nx << lgC) + 2.0));
                 }
                 cnt = 0;
                 useA = true;
                 int nb = 0;
-                for (int q = 0; q < 3; ++q) {
-                    const int col = (q == 0) ? cx : (q == 1 ? cx - 1 : cx + 1);
-                    if (col < cl || col > cr) continue;
-                    const int b = (int)a.binStart[(col - a.g.e0) * nyS + lo];
-                    const int e = (int)a.binStart[(col - a.g.e0) * nyS + hi + 1];
+                for (int fc = fa; fc <= fb; ++fc) {  // one run per fine column
+                    const int b = (int)a.binStart[(fc - fe0) * nyS + lo];
+                    const int e = (int)a.binStart[(fc - fe0) * nyS + hi + 1];
                     if (DRY) wCand += (uint32_t)max(e - b, 0);
                     for (int j0 = b; j0 < e; j0 += kG) {
                         const int j = j0 + G.gl;
