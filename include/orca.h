@@ -231,10 +231,12 @@ orca_status orca_debug_step(orca_ctx *ctx, float *vnew, uint8_t *flags, int32_t 
                             int32_t *cnt);
 
 /* Work of one step on the current state, counted by an instrumented dry run of the same
- * kernel (not applied): out[0] candidates read from the 3x3 bins, out[1] half-planes
- * built, out[2] LP constraint checks, out[3] LP1 inner iterations, out[4] LP3 projected
- * lines.  Used for the ALU roofline.  Synchronises. */
-orca_status orca_debug_work(orca_ctx *ctx, int64_t out[5]);
+ * kernel (not applied): out[0] candidates the kernel read (its fine-column runs within the
+ * search radius), out[1] half-planes built, out[2] LP constraint checks, out[3] LP1 inner
+ * iterations, out[4] LP3 projected lines, out[5] agents in the 3x3 bins around every agent
+ * (the paper's candidate set, P:94 / P:98: SURVEY §8(d)'s c_cand).  Used for the ALU
+ * roofline.  Synchronises. */
+orca_status orca_debug_work(orca_ctx *ctx, int64_t out[6]);
 
 /* Counters (synchronises).  orca_reset_stats zeroes them. */
 orca_status orca_get_stats(orca_ctx *ctx, orca_stats *out);

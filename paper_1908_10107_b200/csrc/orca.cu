@@ -28,7 +28,10 @@ using namespace orca;
 
 namespace {
 
-constexpr int kSubRowsLog2 = 3;  // 8 sort sub-rows per cell
+#ifndef ORCA_SUBROWS_LOG2
+#define ORCA_SUBROWS_LOG2 3
+#endif
+constexpr int kSubRowsLog2 = ORCA_SUBROWS_LOG2;  // 2^this sort sub-rows per cell
 #ifndef ORCA_SUBCOLS_LOG2
 #define ORCA_SUBCOLS_LOG2 2
 #endif
@@ -1694,11 +1697,11 @@ orca_status orca_debug_step(orca_ctx* c, float* vnew, uint8_t* flags, int32_t* n
     return ORCA_OK;
 }
 
-orca_status orca_debug_work(orca_ctx* c, int64_t out[5]) {
+orca_status orca_debug_work(orca_ctx* c, int64_t out[6]) {
     if (!c || !out) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
-    for (int q = 0; q < 5; ++q) out[q] = 0;
+    for (int q = 0; q < 6; ++q) out[q] = 0;
     if (c->nGlobal == 0) return ORCA_OK;
     Work* dW = nullptr;
     CK(cudaMalloc(&dW, sizeof(Work)));
@@ -1708,6 +1711,10 @@ orca_status orca_debug_work(orca_ctx* c, int64_t out[5]) {
         StepArgs a = make_args(c, d);
         a.work = dW;
         e = dry_step(c, d, a);
+        if (e == cudaSuccess) {
+            k_stencil_count<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.binStart, d.g, d.posS, &dW->stencil);
+            e = cudaGetLastError();
+        }
     }
     Work h{};
     if (e == cudaSuccess) e = cudaMemcpyAsync(&h, dW, sizeof(Work), cudaMemcpyDeviceToHost, c->stream);
@@ -1719,6 +1726,7 @@ orca_status orca_debug_work(orca_ctx* c, int64_t out[5]) {
     out[2] = (int64_t)h.checks;
     out[3] = (int64_t)h.lp1;
     out[4] = (int64_t)h.proj;
+    out[5] = (int64_t)h.stencil;
     return ORCA_OK;
 }
 

@@ -36,11 +36,12 @@ enum { ST_INFEASIBLE = 0, ST_DEGENERATE, ST_G1, ST_G2, ST_G3, ST_COLLISION, ST_R
 // Work counters of an instrumented dry step (orca_debug_work): per-launch totals used by
 // the bench's ALU roofline.
 struct Work {
-    unsigned long long cand;   // candidates read from the 3x3 bins (message reads)
+    unsigned long long cand;   // candidates read (the fine-column runs within the search radius)
     unsigned long long lines;  // ORCA half-planes built
     unsigned long long checks; // LP2 constraint checks (incl. inside LP3)
     unsigned long long lp1;    // LP1 inner iterations
     unsigned long long proj;   // LP3 projected lines
+    unsigned long long stencil;  // agents in the 3x3 cell stencil of each agent (SURVEY §8(d) c_cand)
 };
 struct WorkT {
     uint32_t cand, lines, checks, lp1, proj;
@@ -1595,6 +1596,29 @@ __global__ void k_unpermute(const uint32_t* __restrict__ binStart, Grid g, const
         if (posOut) posOut[id] = posS[i];
         if (velOut) velOut[id] = velS[i];
     }
+}
+
+// The paper's candidate count: agents in the 3x3 bins around every owned agent ("For
+// those within the same or neighboring partitioning bins, it calculates whether they are
+// within the observation radius").  The per-unit figure c_cand of SURVEY §8(d)'s
+// algorithmic work model; the step itself reads only the fine-column runs within its search
+// radius.
+__global__ void k_stencil_count(const uint32_t* __restrict__ binStart, Grid g, const float2* __restrict__ posS,
+                                unsigned long long* __restrict__ out) {
+    const int2 r = owned_range(binStart, g);
+    const int nyS = g.ny << g.lgS, fe0 = g.e0 << g.lgC;
+    unsigned long long sum = 0;
+    for (int i = r.x + blockIdx.x * blockDim.x + threadIdx.x; i < r.y; i += gridDim.x * blockDim.x) {
+        const float2 p = posS[i];
+        const int cx = cell_coord(p.x, g.ox, g.csD, g.invCs, g.nx);
+        const int cy = subrow_coord(p.y, g) >> g.lgS;
+        const int rlo = max(cy - 1, 0) << g.lgS, rhi = (min(cy + 1, g.ny - 1) + 1) << g.lgS;
+        const int f0 = max(cx - 1, 0) << g.lgC, f1 = (min(cx + 1, g.nx - 1) + 1) << g.lgC;
+        for (int fc = f0; fc < f1; ++fc)
+            sum += binStart[(fc - fe0) * nyS + rhi] - binStart[(fc - fe0) * nyS + rlo];
+    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0 && sum) atomicAdd(out, sum);
 }
 
 // orca_set_state_async (one strip): every loaded agent, in its current sorted order, takes

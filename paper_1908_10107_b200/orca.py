@@ -316,9 +316,9 @@ class Orca:
         return v, fl, nb[:, :k], cnt
 
     def work(self) -> dict:
-        out = (ctypes.c_int64 * 5)()
+        out = (ctypes.c_int64 * 6)()
         _check(_lib.orca_debug_work(self._ctx, out))
-        return dict(cand=out[0], lines=out[1], checks=out[2], lp1=out[3], proj=out[4])
+        return dict(cand=out[0], lines=out[1], checks=out[2], lp1=out[3], proj=out[4], stencil=out[5])
 
     def stats(self) -> dict:
         s = Stats()
