@@ -821,16 +821,55 @@ __device__ __forceinline__ void lp3(const Lines& L, const Lines& P, int T, int n
     }
 }
 
+// Directional LP2 of LP3's projected problem (lp2 with dirOpt), warp-synchronised like
+// lp2_sync: the lanes of `mask` (all at the same LP3 line, so kmax = that line's index is
+// uniform) run kmax constraint iterations with a reconvergence point after each, so the
+// LP1 re-solves at the same projected line run together.
+#ifndef ORCA_SYNC_LP3_INNER
+#define ORCA_SYNC_LP3_INNER 0  // swept r01ae: 1 is +1.4 % (1M), +3 % (dense)
+#endif
+template <bool CNT>
+__device__ __forceinline__ int lp2_dir_sync(const Lines& P, int T, int m, int kmax, float r, float dx, float dy,
+                                            float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask) {
+    vx = dx * r;
+    vy = dy * r;
+    int failed = m;
+    for (int i = 0; i < kmax; ++i) {
+        if (i < m && failed == m) {
+            if (CNT) ++w.checks;
+            const float pen = P.s[i * T] - fmaf(P.nx[i * T], vx, P.ny[i * T] * vy);
+            if (pen > 0.0f) {
+                const float tx = vx, ty = vy;
+                if (!lp1<CNT>(P, T, i, r, dx, dy, true, vx, vy, fl, w)) {
+                    vx = tx;
+                    vy = ty;
+                    failed = i;
+                }
+            }
+        }
+        __syncwarp(mask);
+    }
+    return failed;
+}
+
 // lp3 with a uniform kmax-iteration outer loop and a reconvergence point per line (see
-// lp2_sync); the inner projected LP2 is per lane.
+// lp2_sync); the inner projected LP2 is lp2_dir_sync over the lanes at the same line.
 template <bool CNT>
 __device__ __forceinline__ void lp3_sync(const Lines& L, const Lines& P, int T, int n, int begin, int kmax, float r,
                                          float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask) {
     float dist = 0.0f;
     for (int i = 0; i < kmax; ++i) {
+        bool part = false;
+        float nix = 0.0f, niy = 0.0f, si = 0.0f;
         if (i >= begin && i < n) {
-            const float nix = L.nx[i * T], niy = L.ny[i * T], si = L.s[i * T];
-            if (si - fmaf(nix, vx, niy * vy) > dist) {
+            nix = L.nx[i * T];
+            niy = L.ny[i * T];
+            si = L.s[i * T];
+            part = si - fmaf(nix, vx, niy * vy) > dist;
+        }
+        const unsigned pm = ORCA_SYNC_LP3_INNER ? __ballot_sync(mask, part) : 0u;
+        {
+            if (part) {
                 int m = 0;
                 for (int j = 0; j < i; ++j) {
                     const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
@@ -848,7 +887,9 @@ __device__ __forceinline__ void lp3_sync(const Lines& L, const Lines& P, int T, 
                     ++m;
                 }
                 const float tx = vx, ty = vy;
-                if (lp2<CNT>(P, T, m, r, nix, niy, true, vx, vy, fl, w) < m) {
+                const int fm = ORCA_SYNC_LP3_INNER ? lp2_dir_sync<CNT>(P, T, m, i, r, nix, niy, vx, vy, fl, w, pm)
+                                                   : lp2<CNT>(P, T, m, r, nix, niy, true, vx, vy, fl, w);
+                if (fm < m) {
                     vx = tx;
                     vy = ty;
                 }
@@ -1148,6 +1189,9 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
 #ifndef ORCA_SYNC_PHASES
 #define ORCA_SYNC_PHASES 0  // swept: 1M 0.495 ms (0) vs 0.529 ms (1)
 #endif
+#ifndef ORCA_MARGIN
+#define ORCA_MARGIN 1.0f  // 1: the rigorous displacement bound (first pass always exact)
+#endif
 #ifndef ORCA_COLD_LAMBDA
 #define ORCA_COLD_LAMBDA 1.6f  // no history: guessed radius holds ~this x k agents on average (r01q)
 #endif
@@ -1220,7 +1264,12 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             bool guessed = false;
             const float rk2p = a.rk2S[i];
             if (rk2p < a.m.nd2Fup) {
-                const float marg = 2.0002f * a.m.maxSpeedAll * a.m.dt + 4e-7f * (fabsf(pi.x) + fabsf(pi.y)) + 1e-5f;
+                // this agent moved |v_i| dt since the k-th distance was measured (its stored
+                // velocity is its last displacement), a neighbour at most maxSpeed dt; the guess
+                // is only a hint (the exactness test below decides), ORCA_MARGIN scales it
+                const float vi2 = sqrtf(fmaf(vi.x, vi.x, vi.y * vi.y));
+                const float marg = ORCA_MARGIN * (1.0002f * (vi2 + a.m.maxSpeedAll) * a.m.dt) +
+                                   4e-7f * (fabsf(pi.x) + fabsf(pi.y)) + 1e-5f;
                 const float r = sqrtf(rk2p) * (1.0f + 1e-5f) + marg;
                 const float b = r * r * (1.0f + 1e-3f);
                 if (b < thr) {
