@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--no-multicore", action="store_true", help="skip the all-cores oracle baseline")
     ap.add_argument("--shared-gpu", action="store_true",
                     help="test only: all ranks on GPU 0 (gloo for torch, ORCA_NCCL_LIB=tests/fake_nccl for liborca)")
-    ap.add_argument("--lp3-lanes", type=int, default=1, help="lanes per infeasible agent in the LP3 kernel")
+    ap.add_argument("--lp3-lanes", type=int, default=-1, help="lanes per infeasible agent in the LP3 kernel (-1: auto)")
     ap.add_argument("--variant", type=int, default=-1, help="-1: auto (default), 0: thread per agent, 1: 8-lane group per agent, 2: register top-k, "
                          "3: work-unit LP2")
     return ap.parse_args()

@@ -281,12 +281,13 @@ struct orca_ctx {
     std::vector<std::pair<int, cudaGraphExec_t>> graphs;
     std::vector<unsigned char> graphKey;  // graph_key() the cached graphs were captured with
     cudaEvent_t ev[8] = {};
+    cudaEvent_t chunkEv[2] = {};  // after the last two step chunks (orca_step's grid check)
     int smemBytes = 0, lp3Smem = 0, groupSmem = 0;
     int lpRandom = 0;              // randomized LP constraint order (orca_set_lp_order)
     unsigned long long lpSeed = 0;
     int64_t lpStep0 = 0, lpMark = 0;  // step index t = lpStep0 + steps_total - lpMark
     int variant = -1;  // -1: auto (pick_variant)
-    int lp3Lanes = ORCA_LP3_GROUP;  // lanes per queued agent in the LP3 kernel (1 = thread)
+    int lp3Lanes = -1;  // lanes per queued agent in the LP3 kernel (1 = thread, -1 = auto)
     // strip rebalance: by-id active flags, all-gather records, fill reports
     uint8_t* activeBuf = nullptr;
     int64_t activeCap = 0;
@@ -454,6 +455,17 @@ int pick_variant(const orca_ctx* c, const Domain& d) {
     return (d.popBuild < ORCA_AUTO_GROUP_BELOW) ? 1 : 0;
 }
 
+// LP3 lanes, auto (-1): an 8-lane group per queued agent below ~250k agents per strip (the
+// queue is then too short to fill the GPU with one thread per agent: 100k -3.5 %), one
+// thread per agent above (1M: 1 lane 0.37 ms vs 8 lanes 0.42 ms)
+#ifndef ORCA_AUTO_LP3_GROUP_BELOW
+#define ORCA_AUTO_LP3_GROUP_BELOW 250000
+#endif
+int pick_lp3_lanes(const orca_ctx* c, const Domain& d) {
+    if (c->lp3Lanes > 0) return c->lp3Lanes;
+    return (d.popBuild < ORCA_AUTO_LP3_GROUP_BELOW) ? 8 : 1;
+}
+
 // Everything a captured step body depends on: the kernel arguments of every strip (device
 // pointers, grid, model), launch sizes, the exchange buffers and the kernel selection.  A
 // cached graph is replayed only while this is unchanged, so orca_set_agents with the same
@@ -474,6 +486,8 @@ std::vector<unsigned char> graph_key(orca_ctx* c) {
         put(&d.nbins, sizeof d.nbins);
         const int v = pick_variant(c, d);
         put(&v, sizeof v);
+        const int l3 = pick_lp3_lanes(c, d);
+        put(&l3, sizeof l3);
         for (const ExAlloc* x : {&d.sendL, &d.sendR, &d.recvL, &d.recvR, &d.recvL1, &d.recvR1}) {
             put(&x->base, sizeof x->base);
             put(&x->bytes, sizeof x->bytes);
@@ -485,7 +499,7 @@ std::vector<unsigned char> graph_key(orca_ctx* c) {
 }
 
 // LP3 on the queue (same results bit for bit): a GW-lane group per agent on a persistent
-// grid (ORCA_LP3_GROUP > 1), else one thread per agent on a capacity grid
+// grid (pick_lp3_lanes > 1), else one thread per agent on a capacity grid
 template <bool DRY, int GW>
 void launch_lp3_grp(orca_ctx* c, Domain& d, StepArgs& a) {
     constexpr int ppb = kStepThreads / GW;
@@ -496,7 +510,7 @@ void launch_lp3_grp(orca_ctx* c, Domain& d, StepArgs& a) {
 
 template <bool DRY>
 void launch_lp3(orca_ctx* c, Domain& d, StepArgs& a) {
-    switch (c->lp3Lanes) {
+    switch (pick_lp3_lanes(c, d)) {
         case 4: launch_lp3_grp<DRY, 4>(c, d, a); break;
         case 8: launch_lp3_grp<DRY, 8>(c, d, a); break;
         case 16: launch_lp3_grp<DRY, 16>(c, d, a); break;
@@ -1047,8 +1061,9 @@ orca_status rebalance(orca_ctx* c, bool regrid) {
             mn[0] = mx[0] = c->gg.ox + c->gg.cs;
             mn[1] = mx[1] = c->gg.oy + c->gg.cs;
         }
-        // margin: a 64-step chunk moves agents up to 64 maxSpeed dt before the next check
-        const float reach = 64.0f * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
+        // margin: agents move up to 128 maxSpeed dt before the next check sees them (a chunk of
+        // <= 64 steps is checked once the chunk after it is queued, orca_step)
+        const float reach = 128.0f * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
         CKS(derive_grid(c, n, mn, mx, 1 + (int)std::ceil(reach / c->p.neighborDist)));
         c->regrids += 1;
     } else {
@@ -1290,6 +1305,8 @@ void orca_destroy(orca_ctx* c) {
     if (c->ioBadHost) cudaFreeHost(c->ioBadHost);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : c->chunkEv)
+        if (e) cudaEventDestroy(e);
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -1362,7 +1379,7 @@ orca_status orca_set_state(orca_ctx* c, const float* pos, const float* vel) {
                         (mn[0] >= g.ox + g.cs && mn[1] >= g.oy + g.cs && (double)mx[0] < g.ox + (double)g.cs * (g.nx - 1) &&
                          (double)mx[1] < g.oy + (double)g.cs * (g.ny - 1));
     if (!inside) {  // the new state leaves the grid's interior: re-derive it (reading Q12)
-        const float reach = 64.0f * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
+        const float reach = 128.0f * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
         CKS(derive_grid(c, n, mn, mx, 1 + (int)std::ceil(reach / c->p.neighborDist)));
         c->regrids += 1;
     }
@@ -1437,9 +1454,15 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
     // one graph of up to kChunk step bodies, replayed
     const int kChunk = 64;
     int remaining = n_steps;
-    while (remaining > 0) {
+    if (c->world == 1 && !c->chunkEv[0])
+        for (auto& e : c->chunkEv) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int q = 0; remaining > 0; ++q) {
         const int s = std::min(remaining, kChunk);
-        CKS(maybe_rebalance(c));  // strips only: capacities for the next chunk
+        // one strip: the outer-ring flag of chunk q-2 is final once that chunk is done, so a long
+        // call re-derives the grid while it runs (chunk q-1 keeps the GPU busy meanwhile); the
+        // first two chunks of a call only read the flag (no synchronisation for short calls)
+        if (c->world == 1 && q >= 2) CK(cudaEventSynchronize(c->chunkEv[q & 1]));
+        CKS(maybe_rebalance(c));  // grid check; strips: capacities for the next chunk
         {
             std::vector<unsigned char> key = graph_key(c);
             if (key != c->graphKey) {
@@ -1468,6 +1491,7 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
             c->graphs.emplace_back(s, exec);
         }
         CK(cudaGraphLaunch(exec, c->stream));
+        if (c->world == 1) CK(cudaEventRecord(c->chunkEv[q & 1], c->stream));
         remaining -= s;
     }
     c->host_steps += n_steps;
@@ -1936,8 +1960,8 @@ orca_status orca_rebalance(orca_ctx* c) {
 }
 
 orca_status orca_set_lp3_lanes(orca_ctx* c, int32_t lanes) {
-    if (!c || (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16))
-        return fail(ORCA_ERR_INVALID_ARGUMENT, "lanes must be 1, 4, 8 or 16");
+    if (!c || (lanes != -1 && lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16))
+        return fail(ORCA_ERR_INVALID_ARGUMENT, "lanes must be -1 (auto), 1, 4, 8 or 16");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);

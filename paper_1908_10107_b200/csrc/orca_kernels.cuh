@@ -1316,13 +1316,15 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                     // ty in fp64 is accurate to ~1e-12 sub-rows, covered by the 1e-6 margin
                     const double ty = __dmul_rn(__dsub_rn((double)pi.y, (double)a.g.oy), a.g.invCsSub);
                     const double rs = (double)rg * a.g.invCsSub + 1e-6;
-                    lo = max(lo, (int)fmax(floor(ty - rs), -2.0));
-                    hi = min(hi, (int)fmin(floor(ty + rs), (double)nyS + 2.0));
-                    // fine columns within rg of x, the same way
+                    lo = max(lo, (int)fmin(fmax(floor(ty - rs), 0.0), (double)(nyS - 1)));
+                    hi = min(hi, (int)fmin(fmax(floor(ty + rs), 0.0), (double)(nyS - 1)));
+                    // fine columns within rg of x, the same way.  Both windows are clamped like
+                    // the agents' own bins, so an agent outside the grid searches the edge bins
+                    // its neighbours are clamped into (floor and clamp are monotone)
                     const double tx = __dmul_rn(__dsub_rn((double)pi.x, (double)a.g.ox), a.g.invCsSubX);
                     const double rsx = (double)rg * a.g.invCsSubX + 1e-6;
-                    fa = max(fa, (int)fmax(floor(tx - rsx), -2.0));
-                    fb = min(fb, (int)fmin(floor(tx + rsx), (double)(a.g.nx << lgC) + 2.0));
+                    fa = max(fa, (int)fmin(fmax(floor(tx - rsx), 0.0), (double)((a.g.nx << lgC) - 1)));
+                    fb = min(fb, (int)fmin(fmax(floor(tx + rsx), 0.0), (double)((a.g.nx << lgC) - 1)));
                 }
                 int nb = 0;
                 for (int fc = fa; fc <= fb; ++fc) {  // one run per fine column

@@ -12,9 +12,6 @@
 
 namespace orca {
 
-#ifndef ORCA_LP3_GROUP
-#define ORCA_LP3_GROUP 1  // default lanes per queued agent (1 = k_lp3; groups measured slower, §12)
-#endif
 
 template <int GW>
 struct Grp {

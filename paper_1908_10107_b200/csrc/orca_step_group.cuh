@@ -249,12 +249,12 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
                     const float rg = sqrtf(thr) * (1.0f + 1e-6f) + 1e-6f;
                     const double ty = __dmul_rn(__dsub_rn((double)pi.y, (double)a.g.oy), a.g.invCsSub);
                     const double rs = (double)rg * a.g.invCsSub + 1e-6;
-                    lo = max(lo, (int)fmax(floor(ty - rs), -2.0));
-                    hi = min(hi, (int)fmin(floor(ty + rs), (double)nyS + 2.0));
+                    lo = max(lo, (int)fmin(fmax(floor(ty - rs), 0.0), (double)(nyS - 1)));
+                    hi = min(hi, (int)fmin(fmax(floor(ty + rs), 0.0), (double)(nyS - 1)));
                     const double tx = __dmul_rn(__dsub_rn((double)pi.x, (double)a.g.ox), a.g.invCsSubX);
                     const double rsx = (double)rg * a.g.invCsSubX + 1e-6;
-                    fa = max(fa, (int)fmax(floor(tx - rsx), -2.0));
-                    fb = min(fb, (int)fmin(floor(tx + rsx), (double)(a.g.nx << lgC) + 2.0));
+                    fa = max(fa, (int)fmin(fmax(floor(tx - rsx), 0.0), (double)((a.g.nx << lgC) - 1)));
+                    fb = min(fb, (int)fmin(fmax(floor(tx + rsx), 0.0), (double)((a.g.nx << lgC) - 1)));
                 }
                 cnt = 0;
                 useA = true;

@@ -354,7 +354,7 @@ class Orca:
         _check(_lib.orca_rebalance(self._ctx))
 
     def set_lp3_lanes(self, lanes: int):
-        """Lanes per infeasible agent in the LP3 kernel: 1 (thread), 4, 8 or 16; same results."""
+        """Lanes per infeasible agent in the LP3 kernel: -1 (auto), 1 (thread), 4, 8 or 16; same results."""
         _check(_lib.orca_set_lp3_lanes(self._ctx, lanes))
 
     def set_lp_order(self, randomized: bool, seed: int = 0, first_step: int = 0):
