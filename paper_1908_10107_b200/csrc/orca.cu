@@ -279,7 +279,9 @@ struct orca_ctx {
     int64_t host_steps = 0, host_updates = 0;
     int64_t steps_total = 0;  // steps since creation (never reset): the LP-order step index
     std::vector<std::pair<int, cudaGraphExec_t>> graphs;
-    std::vector<unsigned char> graphKey;  // graph_key() the cached graphs were captured with
+    std::vector<int64_t> graphGen;        // keyGen each cached graph was captured under
+    std::vector<unsigned char> graphKey;  // graph_key() of the current generation
+    int64_t keyGen = 0;
     cudaEvent_t ev[8] = {};
     cudaEvent_t chunkEv[2] = {};  // after the last two step chunks (orca_step's grid check)
     int smemBytes = 0, lp3Smem = 0, groupSmem = 0;
@@ -441,6 +443,7 @@ orca_status dom_alloc(orca_ctx* c, Domain& d, int capW, int64_t nbins, int capM,
 void drop_graph(orca_ctx* c) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.second);
     c->graphs.clear();
+    c->graphGen.clear();
     c->graphKey.clear();
 }
 
@@ -1465,31 +1468,56 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
         CKS(maybe_rebalance(c));  // grid check; strips: capacities for the next chunk
         {
             std::vector<unsigned char> key = graph_key(c);
-            if (key != c->graphKey) {
-                drop_graph(c);
+            if (key != c->graphKey) {  // new arguments: cached graphs are updated on next use
                 c->graphKey = std::move(key);
+                c->keyGen += 1;
             }
         }
-        cudaGraphExec_t exec = nullptr;
-        for (auto& g : c->graphs)
-            if (g.first == s) exec = g.second;
-        if (!exec) {
-            if (c->graphs.size() >= 4) {
-                cudaGraphExecDestroy(c->graphs.front().second);
-                c->graphs.erase(c->graphs.begin());
-            }
+        int slot = -1;
+        for (size_t g = 0; g < c->graphs.size(); ++g)
+            if (c->graphs[g].first == s) slot = (int)g;
+        if (slot < 0 || c->graphGen[slot] != c->keyGen) {
             cudaGraph_t gr;
             CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
             orca_status st = ORCA_OK;
-            for (int q = 0; q < s && st == ORCA_OK; ++q) st = enqueue_step(c, nullptr);
+            for (int t = 0; t < s && st == ORCA_OK; ++t) st = enqueue_step(c, nullptr);
             cudaError_t e2 = cudaStreamEndCapture(c->stream, &gr);
             if (st != ORCA_OK) return st;
             if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
-            cudaError_t e = cudaGraphInstantiate(&exec, gr, 0);
+            bool updated = false;
+            if (slot >= 0) {
+                // same step body with new arguments (a re-grid, a rebalance, a reload): update
+                // the instantiated graph in place -- much cheaper than instantiating it again
+                cudaGraphExecUpdateResultInfo info;
+                updated = cudaGraphExecUpdate(c->graphs[slot].second, gr, &info) == cudaSuccess;
+                if (!updated) {
+                    (void)cudaGetLastError();
+                    cudaGraphExecDestroy(c->graphs[slot].second);
+                    c->graphs.erase(c->graphs.begin() + slot);
+                    c->graphGen.erase(c->graphGen.begin() + slot);
+                    slot = -1;
+                }
+            }
+            if (!updated) {
+                if (c->graphs.size() >= 4) {
+                    cudaGraphExecDestroy(c->graphs.front().second);
+                    c->graphs.erase(c->graphs.begin());
+                    c->graphGen.erase(c->graphGen.begin());
+                }
+                cudaGraphExec_t ex = nullptr;
+                cudaError_t e = cudaGraphInstantiate(&ex, gr, 0);
+                if (e != cudaSuccess) {
+                    cudaGraphDestroy(gr);
+                    return cuda_fail(e, "cudaGraphInstantiate");
+                }
+                c->graphs.emplace_back(s, ex);
+                c->graphGen.push_back(c->keyGen);
+                slot = (int)c->graphs.size() - 1;
+            }
+            c->graphGen[slot] = c->keyGen;
             cudaGraphDestroy(gr);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-            c->graphs.emplace_back(s, exec);
         }
+        cudaGraphExec_t exec = c->graphs[slot].second;
         CK(cudaGraphLaunch(exec, c->stream));
         if (c->world == 1) CK(cudaEventRecord(c->chunkEv[q & 1], c->stream));
         remaining -= s;
