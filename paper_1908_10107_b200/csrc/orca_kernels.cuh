@@ -1071,8 +1071,22 @@ __device__ __forceinline__ void reg_merge(RegList<KR>& L, int& cnt, const uint32
     }
 }
 
+// Exact (kappa, id) order of candidates ja and jb around agent pi (fp64 keys).
+__device__ __forceinline__ bool exact_less(uint32_t ja, uint32_t jb, float2 pi, const float2* __restrict__ posS,
+                                           const uint32_t* __restrict__ idS) {
+    const double ka = exact_key(posS[ja], pi), kb = exact_key(posS[jb], pi);
+    if (ka != kb) return ka < kb;
+    return idS[ja] < idS[jb];
+}
+
 // Merge the nb buffered candidates (j, fp32 d2) into the sorted top-k list (Lf = fp32 d2
-// bits, Lj = j).  Returns the new list length.
+// bits, Lj = j).  Returns the new list length.  With f > 1e-30 (the relative error bound of
+// the fp32 d2 holds) a list entry o is surely farther if f (1 + 2^-19) < o and surely nearer
+// if o < f (1 - 2^-19) -- one compare per step on the insertion path; only the band between
+// takes the exact fp64 keys (ORCA_FAST_MERGE; 0 = cand_less at every step).
+#ifndef ORCA_FAST_MERGE
+#define ORCA_FAST_MERGE 1
+#endif
 __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int cnt, int k, const uint32_t* Bf,
                                                 const float* Bff, int nb, float2 pi, const Model& m,
                                                 const float2* __restrict__ posS, const uint32_t* __restrict__ idS) {
@@ -1081,6 +1095,26 @@ __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int 
         const uint32_t j = Bf[b * T];
         const float f = buf_d2(Bff, b, j, pi, posS);
         if (!in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
+        if (ORCA_FAST_MERGE && f > 1e-30f) {
+            const float fhi = f * (1.0f + 0x1p-19f), flo = f * (1.0f - 0x1p-19f);
+            int p = cnt;
+            if (cnt == k) {  // beyond the k-th: rejected
+                const float o = __uint_as_float(Lf[(k - 1) * T]);
+                if (!(fhi < o) && (o < flo || !exact_less(j, Lj[(k - 1) * T], pi, posS, idS))) continue;
+                p = k - 1;
+            }
+            while (p > 0) {
+                const float o = __uint_as_float(Lf[(p - 1) * T]);
+                if (!(fhi < o) && (o < flo || !exact_less(j, Lj[(p - 1) * T], pi, posS, idS))) break;
+                Lf[p * T] = __float_as_uint(o);
+                Lj[p * T] = Lj[(p - 1) * T];
+                --p;
+            }
+            Lf[p * T] = __float_as_uint(f);
+            Lj[p * T] = j;
+            if (cnt < k) ++cnt;
+            continue;
+        }
         if (cnt == k && !cand_less(f, j, __uint_as_float(Lf[(k - 1) * T]), Lj[(k - 1) * T], pi, posS, idS))
             continue;
         int p = (cnt < k) ? cnt : k - 1;
