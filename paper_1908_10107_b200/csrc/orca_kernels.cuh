@@ -1573,6 +1573,10 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
 }
 
 // ------------------------------------------------------------ LP3 on the queue
+#ifndef ORCA_LP3_SORT
+#define ORCA_LP3_SORT 1
+#endif
+#define ORCA_MAX_K_DEV 32  // = ORCA_MAX_K (include/orca.h); buckets 0..32 by failure index
 // One thread per queued (infeasible) agent, grid-stride over the device-side queue
 // count; same smem column layout as k_step (lines, then projected lines).
 template <bool DRY>
@@ -1591,11 +1595,47 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
     const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * a.g.colBins];
     const int nOwn = (int)a.binStart[(a.g.c1 - a.g.e0) * a.g.colBins] - o0;
     int cInf = 0, cDeg = 0, cG1 = 0, cG2 = 0, cG3 = 0;
+#if ORCA_LP3_SORT
+    __shared__ int sHist[ORCA_MAX_K_DEV + 2];
+    __shared__ int sPerm[T];
+#endif
     // one queue entry per thread, grid-stride over the device-side count (block-uniform
     // trip count); lanes of a warp reconverge inside lp3_sync
     for (int qb = blockIdx.x * T; qb < nq; qb += gridDim.x * T) {
+#if ORCA_LP3_SORT
+    // block-local counting sort of the block's entries by LP2 failure index f, so the lanes
+    // of a warp start the least-penetration loop at (nearly) the same line
+    const int nv = min(T, nq - qb);
+    for (int h = tid; h < ORCA_MAX_K_DEV + 2; h += T) sHist[h] = 0;
+    __syncthreads();
+    int key = ORCA_MAX_K_DEV + 1, rk = 0;
+    if (tid < nv) {
+        key = (a.qEntry[qb + tid].y >> 8) & 0xff;
+        rk = atomicAdd(&sHist[key], 1);
+    }
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the <= 34 bucket counts
+        int v0 = sHist[tid], v1 = (tid + 32 < ORCA_MAX_K_DEV + 2) ? sHist[tid + 32] : 0;
+        int incl = v0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        sHist[tid] = incl - v0;
+        if (tid + 32 < ORCA_MAX_K_DEV + 2) sHist[tid + 32] = tot;  // (only bucket 33 = inactive)
+        (void)v1;
+    }
+    __syncthreads();
+    if (tid < nv) sPerm[sHist[key] + rk] = qb + tid;
+    __syncthreads();
+    const bool act = tid < nv;
+    const int q = act ? sPerm[tid] : 0;
+#else
     const int q = qb + tid;
     const bool act = q < nq;
+#endif
     const unsigned qmask = __ballot_sync(0xffffffffu, act);
     if (act) {
         const int4 e = a.qEntry[q];
