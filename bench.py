@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--no-suite", action="store_true", help="skip the other BASELINE workloads (N=1 only)")
     ap.add_argument("--no-multicore", action="store_true", help="skip the all-cores oracle baseline")
     ap.add_argument("--shared-gpu", action="store_true",
