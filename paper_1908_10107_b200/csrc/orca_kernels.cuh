@@ -411,7 +411,7 @@ __device__ __forceinline__ void lp_shuffle(uint32_t* x, int T, int c, unsigned l
 // Agent i against neighbour j, R = r_i + r_j.  Branch predicates in fp64 exactly as the
 // oracle's expression trees; geometry in fp32 Hessian form.  Returns flag bits
 // (FL_G1) and sets *collision.
-__device__ __forceinline__ uint32_t orca_line(float xi, float yi, float vxi, float vyi, float xj, float yj,
+__device__ __forceinline__ uint32_t orca_line_branchy(float xi, float yi, float vxi, float vyi, float xj, float yj,
                                               float vxj, float vyj, uint32_t idi, uint32_t idj, float R, double R2D,
                                               const Model& m, float& nx, float& ny, float& s, int& collision) {
     const double rpx = __dsub_rn((double)xj, (double)xi);
@@ -469,6 +469,60 @@ __device__ __forceinline__ uint32_t orca_line(float xi, float yi, float vxi, flo
         s = fmaf(nx, vxi, ny * vyi) + 0.5f * (R * m.invDtF - wl);
     }
     return fl;
+}
+
+// The same half-plane with the three cases folded into selects (ORCA_LINE_BF, default): the
+// fp64 predicates are evaluated exactly as above (same expression trees, so the same branch
+// decisions bit for bit), then one sqrt and one reciprocal serve whichever case holds -- the
+// lanes of a warp stay converged whatever mix of cut-off / leg / collision pairs they meet.
+// Only the coincident collision (w = 0, reading Q15) keeps a branch.
+#ifndef ORCA_LINE_BF
+#define ORCA_LINE_BF 1
+#endif
+__device__ __forceinline__ uint32_t orca_line_bf(float xi, float yi, float vxi, float vyi, float xj, float yj,
+                                                 float vxj, float vyj, uint32_t idi, uint32_t idj, float R, double R2D,
+                                                 const Model& m, float& nx, float& ny, float& s, int& collision) {
+    const double rpx = __dsub_rn((double)xj, (double)xi);
+    const double rpy = __dsub_rn((double)yj, (double)yi);
+    const double rvx = __dsub_rn((double)vxi, (double)vxj);
+    const double rvy = __dsub_rn((double)vyi, (double)vyj);
+    const double d2 = __dadd_rn(__dmul_rn(rpx, rpx), __dmul_rn(rpy, rpy));
+    const bool coll = !(d2 > R2D);
+    const double invH = coll ? m.invDtD : m.invTauD;  // horizon dt (collision, Q4) or tau
+    const double wx = __dsub_rn(rvx, __dmul_rn(invH, rpx));
+    const double wy = __dsub_rn(rvy, __dmul_rn(invH, rpy));
+    const double wl2 = __dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy));
+    const double dot1 = __dadd_rn(__dmul_rn(wx, rpx), __dmul_rn(wy, rpy));
+    const bool cut = coll || (dot1 < 0.0 && __dmul_rn(dot1, dot1) > __dmul_rn(R2D, wl2));  // w-normal cases
+    const double detw = __dsub_rn(__dmul_rn(rpx, wy), __dmul_rn(rpy, wx));
+    collision = coll ? 1 : 0;
+    if (coll && wl2 == 0.0) {  // coincident, equal velocity (reading Q15)
+        nx = (idi < idj) ? -1.0f : 1.0f;
+        ny = 0.0f;
+        s = fmaf(nx, vxi, ny * vyi) + 0.5f * (R * m.invDtF);
+        return FL_G1;
+    }
+    // cut-off / collision: n = w/|w|, s = n.v_i + (R/h - |w|)/2;  legs: n from the leg
+    // direction (left: det > 0, ties right, Q5), s = n.(v_i + v_j)/2
+    const float sq = sqrtf((float)(cut ? wl2 : __dsub_rn(d2, R2D)));  // |w| or the leg length
+    const float inv = 1.0f / (cut ? sq : (float)d2);
+    const float px = (float)rpx, py = (float)rpy;
+    const float sg = (detw > 0.0) ? 1.0f : -1.0f;
+    const float lnx = -(px * R + sg * py * sq) * inv;
+    const float lny = (sg * px * sq - py * R) * inv;
+    nx = cut ? (float)wx * inv : lnx;
+    ny = cut ? (float)wy * inv : lny;
+    const float invHF = coll ? m.invDtF : m.invTauF;
+    s = cut ? fmaf(nx, vxi, ny * vyi) + 0.5f * (R * invHF - sq) : 0.5f * fmaf(nx, vxi + vxj, ny * (vyi + vyj));
+    return 0u;
+}
+
+__device__ __forceinline__ uint32_t orca_line(float xi, float yi, float vxi, float vyi, float xj, float yj, float vxj,
+                                              float vyj, uint32_t idi, uint32_t idj, float R, double R2D,
+                                              const Model& m, float& nx, float& ny, float& s, int& collision) {
+    if (ORCA_LINE_BF)
+        return orca_line_bf(xi, yi, vxi, vyi, xj, yj, vxj, vyj, idi, idj, R, R2D, m, nx, ny, s, collision);
+    return orca_line_branchy(xi, yi, vxi, vyi, xj, yj, vxj, vyj, idi, idj, R, R2D, m, nx, ny, s, collision);
 }
 
 // ------------------------------------------------------------------- LP
