@@ -445,6 +445,22 @@ def run_ours(args):
             acc += ctx.step_timed(1)[0]
         variant_ms[str(v)] = acc / max(3, args.steps // 4)
     ctx.set_variant(args.variant)
+    # LP constraint order A/B (reading Q8; same optimum, different work), variant 0; and the
+    # work-unit variant 3 in the sequential order, where its work units run
+    order_ms = {}
+    for name, mode, v in (("greedy", 0, 0), ("sequential", 2, 0), ("randomized", 1, 0),
+                          ("sequential_work_units", 2, 3)):
+        ctx.set_variant(v)
+        ctx.set_lp_order(mode, 1, 0)
+        ctx.step(2)
+        acc = 0.0
+        for s in range(max(3, args.steps // 4)):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            acc += ctx.step_timed(1)[0]
+        order_ms[name] = acc / max(3, args.steps // 4)
+    ctx.set_lp_order(0)
+    ctx.set_variant(args.variant)
     # LP3 kernel lanes per infeasible agent A/B (same results bit for bit)
     lp3_ms = {}
     for lanes in (1, 4, 8, 16):
@@ -600,7 +616,7 @@ def run_ours(args):
         # neighbour with the peer-memory exchange)
         "gpu_launches": (4 if world == 1 else
                          5 + ((2 if 0 < rank < world - 1 else 1) if ctx.transport() == 0 else 0)) * args.steps,
-        "kernel_variant": args.variant, "k_step_ms_by_variant": variant_ms,
+        "kernel_variant": args.variant, "k_step_ms_by_variant": variant_ms, "k_step_ms_by_lp_order": order_ms,
         "lp3_lanes": args.lp3_lanes, "k_step_ms_by_lp3_lanes": lp3_ms,
         "roofline": roofline, "hbm_context": hbm,
         "stats": st,

@@ -134,16 +134,22 @@ orca_status orca_set_goals(orca_ctx *ctx, const float *goal, float prefSpeed);
 orca_status orca_set_goal_removal(orca_ctx *ctx, float radius);
 
 /* Constraint order of the per-agent LP ("based on the randomized incremental linear
- * program solver of Seidel"; reading Q8).  randomized = 0 (default): nearest
- * neighbour first.  randomized = 1: the half-planes of agent `id` at step `t` are processed
- * in the Fisher-Yates order of the counter-based hash of (seed, t, id) -- splitmix64
- * finaliser, spelled out in DESIGN.md §3 -- where t = first_step for the next orca_step and
- * grows by one per step (orca_set_agents does not reset it: to resume a checkpoint taken at
- * step t, pass first_step = t).  The feasible optimum does not depend on the order; only
- * infeasible agents with a non-unique least-penetration velocity can.  Persists across
- * orca_set_agents.  Synchronises.  Errors: INVALID_ARGUMENT (randomized not 0/1,
- * first_step outside [0, 2^31 - 2^24)). */
-orca_status orca_set_lp_order(orca_ctx *ctx, int32_t randomized, uint64_t seed, int64_t first_step);
+ * program solver of Seidel"; reading Q8).  The feasible optimum does not depend on
+ * the order; only the work does, and infeasible agents with a non-unique least-penetration
+ * velocity can.
+ *   mode 0 (default): greedy -- at each step the most violated half-plane not yet processed
+ *          goes next, re-solved against the processed ones only; the LP ends as soon as no
+ *          remaining half-plane is violated.
+ *   mode 1: randomized -- the half-planes of agent `id` at step `t` are processed in the
+ *          Fisher-Yates order of the counter-based hash of (seed, t, id) -- splitmix64
+ *          finaliser, spelled out in DESIGN.md §3 -- where t = first_step for the next
+ *          orca_step and grows by one per step (orca_set_agents does not reset it: to resume
+ *          a checkpoint taken at step t, pass first_step = t).
+ *   mode 2: neighbour order (nearest first), the sequential incremental LP as the oracle
+ *          runs it; the work-unit kernel variant (orca_set_variant 3) runs in modes 1 and 2.
+ * Persists across orca_set_agents.  Synchronises.  Errors: INVALID_ARGUMENT (mode not
+ * 0/1/2, first_step outside [0, 2^31 - 2^24)). */
+orca_status orca_set_lp_order(orca_ctx *ctx, int32_t mode, uint64_t seed, int64_t first_step);
 
 /* Heterogeneous crowds ("an equal chance of being of radius 0.5 m, 0.75 m or 1 m ...
  * desired speed of 1 m/s, 1.33 m/s or 2 m/s. The maximum speed is adjusted to be 125% of

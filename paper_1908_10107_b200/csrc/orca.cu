@@ -285,7 +285,7 @@ struct orca_ctx {
     cudaEvent_t ev[8] = {};
     cudaEvent_t chunkEv[2] = {};  // after the last two step chunks (orca_step's grid check)
     int smemBytes = 0, lp3Smem = 0, groupSmem = 0;
-    int lpRandom = 0;              // randomized LP constraint order (orca_set_lp_order)
+    int lpMode = 0;  // LP constraint order (orca_set_lp_order): 0 greedy, 1 randomized, 2 neighbour order
     unsigned long long lpSeed = 0;
     int64_t lpStep0 = 0, lpMark = 0;  // step index t = lpStep0 + steps_total - lpMark
     int variant = -1;  // -1: auto (pick_variant)
@@ -345,7 +345,8 @@ Model make_model(const orca_ctx* c) {
     m.prefSpeed = c->prefSpeed;
     m.removeR2 = (c->goals && c->removeR > 0.0f) ? c->removeR * c->removeR : 0.0f;
     m.maxSpeedAll = c->het ? std::max(c->maxSpeedAll, p.maxSpeed) : p.maxSpeed;
-    m.lpRandom = c->lpRandom;
+    m.lpRandom = c->lpMode == 1 ? 1 : 0;
+    m.lpGreedy = c->lpMode == 0 ? 1 : 0;
     m.lpSeed = c->lpSeed;
     return m;
 }
@@ -1997,14 +1998,14 @@ orca_status orca_set_lp3_lanes(orca_ctx* c, int32_t lanes) {
     return ORCA_OK;
 }
 
-orca_status orca_set_lp_order(orca_ctx* c, int32_t randomized, uint64_t seed, int64_t first_step) {
-    if (!c || (randomized != 0 && randomized != 1)) return fail(ORCA_ERR_INVALID_ARGUMENT, "randomized must be 0 or 1");
+orca_status orca_set_lp_order(orca_ctx* c, int32_t mode, uint64_t seed, int64_t first_step) {
+    if (!c || mode < 0 || mode > 2) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be 0, 1 or 2");
     if (first_step < 0 || first_step >= ((int64_t)1 << 31) - ((int64_t)1 << 24))
         return fail(ORCA_ERR_INVALID_ARGUMENT, "first_step out of range");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
-    c->lpRandom = randomized;
+    c->lpMode = mode;
     c->lpSeed = seed;
     c->lpStep0 = first_step;
     c->lpMark = c->steps_total;

@@ -78,6 +78,8 @@ struct Model {
     float maxSpeedAll;            // largest maxSpeed of any agent (history search bound)
     int lpRandom;                 // 1: randomized LP constraint order (reading Q8)
     unsigned long long lpSeed;
+    int lpGreedy;                 // 1: LP2 takes the most violated remaining half-plane next (Q8)
+    int pad1;
 };
 
 // ------------------------------------------------------------------ cell (reading Q11)
@@ -612,63 +614,67 @@ __device__ __forceinline__ int lp2(const Lines& L, int T, int n, float r, float 
     return n;
 }
 
-// Constraint order for LP2 (reading Q8: the feasible optimum is the unique projection, so
-// any order reaches it; only the LP1 re-solve work depends on it).  Lines that the start
-// point v0 (pref clipped to the disc) violates go first: 1 = the most violated one only,
-// 2 = all violated ones in neighbour order, 3 = all violated ones by decreasing violation.
-// The rest keep their neighbour order.  Swept r01z (`profiles/sweep_lppen_r01z.txt`): 1 is
-// -1.7 % at 1M, -2 % at 100k, -1 % dense; 2 and 3 are slower (+3 %, +6 %: the partition costs
-// more than the re-solves it saves).  Off under the randomized order (orca_set_lp_order).
-#ifndef ORCA_LP_PEN
-#define ORCA_LP_PEN 1
-#endif
-__device__ __forceinline__ void line_move(const Lines& L, int T, int from, int to) {
-    // line `from` to slot `to` (to <= from), slots [to, from) shift up by one
-    const float nx = L.nx[from * T], ny = L.ny[from * T], s = L.s[from * T];
-    for (int m = from; m > to; --m) {
-        L.nx[m * T] = L.nx[(m - 1) * T];
-        L.ny[m * T] = L.ny[(m - 1) * T];
-        L.s[m * T] = L.s[(m - 1) * T];
-    }
-    L.nx[to * T] = nx;
-    L.ny[to * T] = ny;
-    L.s[to * T] = s;
+// Greedy constraint order (lp order mode 0, the default; reading Q8).  Seidel's incremental
+// LP reaches the same optimum for any order of the half-planes, so at every step t
+// this LP2 takes, among the half-planes not yet processed (slots [t, n)), the one the current
+// point violates most (the first in slot order among equal violations), swaps it into slot t
+// and re-solves LP1 on it against the processed slots [0, t) only.  When no remaining
+// half-plane is violated the current point is the optimum: it is optimal for the processed
+// set and satisfies the rest.  An LP1 failure at step t is an infeasible LP whose first t
+// slots are the processed ones -- exactly what LP3 (begin = t) expects.  Compared with the
+// sequential order this re-solves only against the few binding half-planes, and the lanes of
+// a warp take their steps together (one reconvergence point per step).
+__device__ __forceinline__ void line_swap(const Lines& L, int T, int a, int b) {
+    const float ax = L.nx[a * T], ay = L.ny[a * T], as = L.s[a * T];
+    L.nx[a * T] = L.nx[b * T];
+    L.ny[a * T] = L.ny[b * T];
+    L.s[a * T] = L.s[b * T];
+    L.nx[b * T] = ax;
+    L.ny[b * T] = ay;
+    L.s[b * T] = as;
 }
 
-template <int MODE>
-__device__ __forceinline__ void pen_order(const Lines& L, int T, int n, float r, float optx, float opty) {
-    float v0x = optx, v0y = opty;
+template <bool CNT>
+__device__ __forceinline__ int lp2_greedy(const Lines& L, int T, int n, int kmax, float r, float optx, float opty,
+                                          float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask) {
     const float l2 = fmaf(optx, optx, opty * opty);
     if (l2 > r * r) {
         const float sc = r / sqrtf(l2);
-        v0x = optx * sc;
-        v0y = opty * sc;
+        vx = optx * sc;
+        vy = opty * sc;
+    } else {
+        vx = optx;
+        vy = opty;
     }
-    auto pen = [&](int q) { return L.s[q * T] - fmaf(L.nx[q * T], v0x, L.ny[q * T] * v0y); };
-    if (MODE == 1) {
-        int best = 0;
-        float pb = pen(0);
-        for (int q = 1; q < n; ++q) {
-            const float p = pen(q);
-            if (p > pb) {
-                pb = p;
-                best = q;
+    int failed = n;
+    bool done = n == 0;
+    for (int t = 0; t < kmax; ++t) {
+        if (!__any_sync(mask, !done)) break;  // (also the per-step reconvergence point)
+        if (done) continue;
+        float best = 0.0f;
+        int bi = -1;
+        for (int q = t; q < n; ++q) {
+            if (CNT) ++w.checks;
+            const float pen = L.s[q * T] - fmaf(L.nx[q * T], vx, L.ny[q * T] * vy);
+            if (pen > best) {
+                best = pen;
+                bi = q;
             }
         }
-        if (best > 0 && pb > 0.0f) line_move(L, T, best, 0);
-        return;
-    }
-    int w = 0;  // violated lines so far, in slots [0, w)
-    for (int q = 0; q < n; ++q) {
-        const float p = pen(q);
-        if (p > 0.0f) {
-            int to = w;
-            if (MODE == 3)
-                while (to > 0 && pen(to - 1) < p) --to;
-            if (to < q) line_move(L, T, q, to);
-            ++w;
+        if (bi < 0) {
+            done = true;
+            continue;
+        }
+        if (bi != t) line_swap(L, T, t, bi);
+        const float tx = vx, ty = vy;
+        if (!lp1<CNT>(L, T, t, r, optx, opty, false, vx, vy, fl, w)) {
+            vx = tx;
+            vy = ty;
+            failed = t;
+            done = true;
         }
     }
+    return failed;
 }
 
 // Warp-synchronised LP2 / LP3: the same arithmetic as lp2 / lp3, but every
@@ -996,7 +1002,7 @@ struct StepArgs {
     int pad1;
     int* gridFlag;  // host-mapped: set when an agent enters the grid's outer cell ring
 };
-static_assert(sizeof(Grid) == 104 && sizeof(Model) == 96 && sizeof(ExBuf) % 8 == 0, "padding-free layouts");
+static_assert(sizeof(Grid) == 104 && sizeof(Model) == 104 && sizeof(ExBuf) % 8 == 0, "padding-free layouts");
 
 #ifndef ORCA_STEP_THREADS
 #define ORCA_STEP_THREADS 128
@@ -1551,10 +1557,12 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         }
         float vx, vy;
         if (CNT) w.lines += (uint32_t)cnt;
-        if (ORCA_LP_PEN && !a.m.lpRandom && cnt > 1) pen_order<ORCA_LP_PEN>(L, T, cnt, vmaxi, px, py);
-        const int f = WU ? lp2_wu<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
-                         : ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
-                                        : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
+        // LP order (reading Q8): greedy (mode 0, default) or the sequential incremental LP over
+        // the neighbour / randomized order (modes 2 / 1; the work-unit variant's own loop)
+        const int f = a.m.lpGreedy ? lp2_greedy<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
+                      : WU         ? lp2_wu<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
+                      : ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
+                                     : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
         if (f < cnt) {
             // infeasible: queue the agent with its half-planes and LP2 point; k_lp3
             // runs the least-penetration LP on a compacted set of agents (full warps)

@@ -163,6 +163,67 @@ __device__ __forceinline__ int lp2_group(const GroupCtx& G, const float* nx, con
     }
 }
 
+// lp2_greedy (orca_kernels.cuh) over the group: the lanes evaluate the remaining half-planes
+// (slot t + lane, + 8, ...), a group reduction picks the largest violation (the lowest slot
+// among equal ones, as the sequential scan does), lane 0 swaps it into slot t, and
+// lp1_group re-solves against slots [0, t).  Same choices, same arithmetic, same result.
+__device__ __forceinline__ int lp2_group_greedy(const GroupCtx& G, float* nx, float* ny, float* sv, int n, float r,
+                                                float optx, float opty, float& vx, float& vy, uint32_t& fl,
+                                                uint32_t& checks, uint32_t& lp1it) {
+    const float l2 = fmaf(optx, optx, opty * opty);
+    if (l2 > r * r) {
+        const float sc = r / sqrtf(l2);
+        vx = optx * sc;
+        vy = opty * sc;
+    } else {
+        vx = optx;
+        vy = opty;
+    }
+    for (int t = 0; t < n; ++t) {
+        float best = 0.0f;
+        int bi = -1;
+        for (int q = t + G.gl; q < n; q += kG) {
+            const float pen = sv[q] - fmaf(nx[q], vx, ny[q] * vy);
+            if (pen > best) {
+                best = pen;
+                bi = q;
+            }
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            const float ob = __shfl_xor_sync(G.gmask, best, o);
+            const int oi = __shfl_xor_sync(G.gmask, bi, o);
+            if (oi >= 0 && (bi < 0 || ob > best || (ob == best && oi < bi))) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        checks += (uint32_t)(n - t);
+        if (bi < 0) return n;
+        if (bi != t) {
+            __syncwarp(G.gmask);
+            if (G.gl == 0) {
+                const float ax = nx[t], ay = ny[t], as = sv[t];
+                nx[t] = nx[bi];
+                ny[t] = ny[bi];
+                sv[t] = sv[bi];
+                nx[bi] = ax;
+                ny[bi] = ay;
+                sv[bi] = as;
+            }
+            __syncwarp(G.gmask);
+        }
+        lp1it += (uint32_t)t;
+        const float tx = vx, ty = vy;
+        if (!lp1_group(G, nx, ny, sv, t, r, optx, opty, false, vx, vy, fl)) {
+            vx = tx;
+            vy = ty;
+            return t;
+        }
+    }
+    return n;
+}
+
 template <bool DRY>
 __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
     extern __shared__ __align__(16) unsigned char smemg[];
@@ -351,12 +412,9 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
             px = aux.x;
             py = aux.y;
         }
-        if (ORCA_LP_PEN && !a.m.lpRandom && cnt > 1) {  // the constraint order of k_step
-            if (G.gl == 0) pen_order<ORCA_LP_PEN>(Lines{Lnx, Lny, Ls}, 1, cnt, vmaxi, px, py);
-            __syncwarp(G.gmask);
-        }
         float vx, vy;
-        const int f = lp2_group(G, Lnx, Lny, Ls, cnt, vmaxi, px, py, vx, vy, fl, wChecks, wLp1);
+        const int f = a.m.lpGreedy ? lp2_group_greedy(G, Lnx, Lny, Ls, cnt, vmaxi, px, py, vx, vy, fl, wChecks, wLp1)
+                                   : lp2_group(G, Lnx, Lny, Ls, cnt, vmaxi, px, py, vx, vy, fl, wChecks, wLp1);
         // flags of all lanes of the group
         fl |= __shfl_xor_sync(G.gmask, fl, 4);
         fl |= __shfl_xor_sync(G.gmask, fl, 2);

@@ -357,11 +357,12 @@ class Orca:
         """Lanes per infeasible agent in the LP3 kernel: -1 (auto), 1 (thread), 4, 8 or 16; same results."""
         _check(_lib.orca_set_lp3_lanes(self._ctx, lanes))
 
-    def set_lp_order(self, randomized: bool, seed: int = 0, first_step: int = 0):
-        """LP constraint order (reading Q8): False = nearest first; True = the
-        counter-based Fisher-Yates order of (seed, t, id), t = first_step for the next step
-        and +1 per step (the oracle's lp_seed / lp_step)."""
-        _check(_lib.orca_set_lp_order(self._ctx, 1 if randomized else 0, seed, first_step))
+    def set_lp_order(self, mode, seed: int = 0, first_step: int = 0):
+        """LP constraint order (reading Q8): 0 / False = greedy (most violated next, the
+        default); 1 / True = the counter-based Fisher-Yates order of (seed, t, id), t =
+        first_step for the next step and +1 per step (the oracle's lp_seed / lp_step); 2 =
+        neighbour order, sequential (the oracle's default order)."""
+        _check(_lib.orca_set_lp_order(self._ctx, int(mode), seed, first_step))
 
     def active(self):
         a = np.empty(self.n, np.uint8)

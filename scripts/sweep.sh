@@ -11,7 +11,7 @@ import json, sys
 f, cfg, r = sys.argv[1], sys.argv[2], sys.argv[3]
 try:
     d = json.loads(r)
-    print(f"{f:40s} {cfg:12s} ms/step {d['ms_per_step']:.4f}  k_step {d['roofline']['stage_ms']['k_step+k_lp3']:.4f}  variants {d['k_step_ms_by_variant']} lp3 {d.get('k_step_ms_by_lp3_lanes')}")
+    print(f"{f:40s} {cfg:12s} ms/step {d['ms_per_step']:.4f}  k_step {d['roofline']['stage_ms']['k_step+k_lp3']:.4f}  order {d.get('k_step_ms_by_lp_order')} variants {d['k_step_ms_by_variant']} lp3 {d.get('k_step_ms_by_lp3_lanes')}")
 except Exception as e:
     print(f, cfg, "FAILED", r[:200])
 PY

@@ -48,7 +48,8 @@ def _oracle_params(oracle, p):
     return oracle.make_params(**p)
 
 
-def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, variant=None, lp3_lanes=None, **over):
+def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, variant=None, lp3_lanes=None, order=None,
+                 **over):
     """One step from the state in w on both sides; returns a report dict and asserts the
     bar.  agents: optional sample of ids for large inputs (oracle computes one by one).
     lp: optional (seed, step) of the randomized LP order (reading Q8)."""
@@ -59,6 +60,8 @@ def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, variant=No
         o.set_lp3_lanes(lp3_lanes)
     if lp is not None:
         o.set_lp_order(True, lp[0], lp[1])
+    if order is not None:
+        o.set_lp_order(order)
     op = _oracle_params(oracle, p)
     origin, cs, dims = o.grid()
     oorigin, odims = oracle.grid_derive(w["pos"], op.neighborDist)
@@ -352,17 +355,21 @@ def test_strips_goals_circle(orca):
     b.close()
 
 
+@pytest.mark.parametrize("order", [0, 2])
 @pytest.mark.parametrize("config,n,rho", [("uniform", 20000, 0.25), ("dense", 20000, None), ("uniform", 5000, 0.02)])
-def test_variants_bit_identical(orca, config, n, rho):
+def test_variants_bit_identical(orca, config, n, rho, order):
     """Thread-per-agent with a shared-memory (0) or register (2) top-k list, the
     8-lane-group-per-agent kernel (1) and the work-unit LP2 (3): same neighbours, velocities
     and trajectories bit for bit (exact comparators; the group and work-unit LPs use exact
-    min/max reductions).  The work-unit LP also reproduces every flag and work counter."""
+    min/max reductions), in the greedy LP order (0, default) and the sequential neighbour
+    order (2, where variant 3 runs the work units).  The work-unit LP also reproduces every
+    flag and work counter."""
     w = W.make(config, n=n, rho=rho) if rho else W.make(config, n=n)
     ctxs = []
     for v in (0, 1, 2, 3):
         o, p = _ctx(orca, w)
         o.set_variant(v)
+        o.set_lp_order(order)
         ctxs.append(o)
     r = [o.debug_step() for o in ctxs]
     for q in (1, 2, 3):
@@ -596,14 +603,14 @@ def test_work_unit_lp_parity(orca, oracle, case):
     LP-heaviest inputs: the dense crowd, the circle's central crush and k = 32 (segments of
     32 lanes, one problem per round)."""
     if case == "dense":
-        compare_step(orca, oracle, W.make("dense", n=4000), variant=3)
+        compare_step(orca, oracle, W.make("dense", n=4000), variant=3, order=2)
     elif case == "k32":
-        compare_step(orca, oracle, W.make("uniform", n=3000, rho=0.5), variant=3, maxNeighbors=32)
+        compare_step(orca, oracle, W.make("uniform", n=3000, rho=0.5), variant=3, order=2, maxNeighbors=32)
     else:
         w = W.make("circle")
         op = oracle.make_params(**w["params"])
         pos, vel, _ = oracle.run(op, w["pos"], w["vel"], goals=w["goals"], pref_speed=1.0, steps=300)
-        compare_step(orca, oracle, dict(w, pos=pos, vel=vel), variant=3)
+        compare_step(orca, oracle, dict(w, pos=pos, vel=vel), variant=3, order=2)
 
 
 def test_work_unit_lp_bit_identical_k_sweep(orca):
@@ -615,6 +622,8 @@ def test_work_unit_lp_bit_identical_k_sweep(orca):
         b, _ = _ctx(orca, w, maxNeighbors=k)
         a.set_variant(0)
         b.set_variant(3)
+        for o in (a, b):  # the work-unit loop runs in the sequential orders
+            o.set_lp_order(2)
         ra, rb = a.debug_step(), b.debug_step()
         for x, y in zip(ra, rb):
             assert np.array_equal(x, y), k
