@@ -912,6 +912,61 @@ __device__ __forceinline__ int lp2_dir_sync(const Lines& P, int T, int m, int km
     return failed;
 }
 
+// LP3 in the greedy order (lp order mode 0; reading Q8): Seidel's incremental 3-D LP for the
+// least-penetration velocity reaches the same penetration for any insertion order, so
+// at each step the half-plane penetrated most beyond the running penetration `dist` among
+// slots [t, n) (lowest slot among equals) is swapped into slot t and the projected LP over the
+// processed slots [0, t) runs; when none exceeds dist the point is optimal.  One
+// reconvergence point per step.
+template <bool CNT>
+__device__ __forceinline__ void lp3_greedy(const Lines& L, const Lines& P, int T, int n, int begin, int kmax, float r,
+                                           float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask) {
+    float dist = 0.0f;
+    bool done = begin >= n;
+    for (int t = 0; t < kmax; ++t) {  // uniform trip count over the lanes of `mask`
+        if (!__any_sync(mask, !done)) break;
+        if (done || t < begin) continue;
+        float best = dist;
+        int bi = -1;
+        for (int q = t; q < n; ++q) {
+            const float pen = L.s[q * T] - fmaf(L.nx[q * T], vx, L.ny[q * T] * vy);
+            if (pen > best) {
+                best = pen;
+                bi = q;
+            }
+        }
+        if (CNT) w.checks += (uint32_t)(n - t);
+        if (bi < 0) {
+            done = true;
+            continue;
+        }
+        if (bi != t) line_swap(L, T, t, bi);
+        const float nix = L.nx[t * T], niy = L.ny[t * T], si = L.s[t * T];
+        int m = 0;
+        for (int j = 0; j < t; ++j) {
+            const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
+            const float det = fmaf(nix, njy, -niy * njx);
+            if (fabsf(det) <= kEps && fmaf(nix, njx, niy * njy) > 0.0f) {
+                if (fabsf(sj - si) <= 2e-5f * r + 1e-6f) fl |= FL_G2;
+                continue;
+            }
+            if (CNT) ++w.proj;
+            const float dx = njx - nix, dy = njy - niy;
+            const float il = 1.0f / sqrtf(fmaf(dx, dx, dy * dy));
+            P.nx[m * T] = dx * il;
+            P.ny[m * T] = dy * il;
+            P.s[m * T] = (sj - si) * il;
+            ++m;
+        }
+        const float tx = vx, ty = vy;
+        if (lp2<CNT>(P, T, m, r, nix, niy, true, vx, vy, fl, w) < m) {
+            vx = tx;  // floating-point failure: keep the current point
+            vy = ty;
+        }
+        dist = si - fmaf(nix, vx, niy * vy);
+    }
+}
+
 // lp3 with a uniform kmax-iteration outer loop and a reconvergence point per line (see
 // lp2_sync); the inner projected LP2 is lp2_dir_sync over the lanes at the same line.
 template <bool CNT>
@@ -1712,7 +1767,9 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
             L.s[m * T] = l.z;
         }
         const float4 pr = a.propS ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
-        if (ORCA_SYNC_LP)
+        if (a.m.lpGreedy)
+            lp3_greedy<CNT>(L, P, T, cnt, f, k, pr.y, vx, vy, fl, w, qmask);
+        else if (ORCA_SYNC_LP)
             lp3_sync<CNT>(L, P, T, cnt, f, k, pr.y, vx, vy, fl, w, qmask);
         else
             lp3<CNT>(L, P, T, cnt, f, pr.y, vx, vy, fl, w);

@@ -146,11 +146,48 @@ __device__ __forceinline__ int lp2_grp(const Grp<GW>& G, const float* nx, const 
 // / |n_j - n_i| of the earlier lines are built one per lane (compacted in j order) and the
 // direction-optimal LP2 along n_i runs on them.
 template <int GW, bool CNT>
-__device__ __forceinline__ void lp3_grp(const Grp<GW>& G, const float* Lnx, const float* Lny, const float* Ls,
-                                        float* Pnx, float* Pny, float* Ps, int n, int begin, float r, float& vx,
-                                        float& vy, uint32_t& fl, WorkT& w) {
+__device__ __forceinline__ void lp3_grp(const Grp<GW>& G, float* Lnx, float* Lny, float* Ls, float* Pnx, float* Pny,
+                                        float* Ps, int n, int begin, float r, bool greedy, float& vx, float& vy,
+                                        uint32_t& fl, WorkT& w) {
     float dist = 0.0f;
     for (int i = begin; i < n; ++i) {
+        if (greedy) {
+            // lp3_greedy's choice: the largest penetration beyond dist among slots [i, n)
+            // (lowest slot among equals), swapped into slot i; none: the point is optimal
+            float best = dist;
+            int bi = -1;
+            for (int q = i + G.gl; q < n; q += GW) {
+                const float pen = Ls[q] - fmaf(Lnx[q], vx, Lny[q] * vy);
+                if (pen > best) {
+                    best = pen;
+                    bi = q;
+                }
+            }
+#pragma unroll
+            for (int o = GW / 2; o > 0; o >>= 1) {
+                const float ob = __shfl_xor_sync(G.mask, best, o);
+                const int oi = __shfl_xor_sync(G.mask, bi, o);
+                if (oi >= 0 && (bi < 0 || ob > best || (ob == best && oi < bi))) {
+                    best = ob;
+                    bi = oi;
+                }
+            }
+            if (CNT) w.checks += (uint32_t)(n - i);
+            if (bi < 0) break;
+            if (bi != i) {
+                __syncwarp(G.mask);
+                if (G.gl == 0) {
+                    const float ax = Lnx[i], ay = Lny[i], as = Ls[i];
+                    Lnx[i] = Lnx[bi];
+                    Lny[i] = Lny[bi];
+                    Ls[i] = Ls[bi];
+                    Lnx[bi] = ax;
+                    Lny[bi] = ay;
+                    Ls[bi] = as;
+                }
+                __syncwarp(G.mask);
+            }
+        }
         const float nix = Lnx[i], niy = Lny[i], si = Ls[i];
         if (!(si - fmaf(nix, vx, niy * vy) > dist)) continue;
         int m = 0;
@@ -236,7 +273,7 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3_grp(StepArgs a) {
         }
         __syncwarp(G.mask);
         const float4 pr = a.propS ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
-        lp3_grp<GW, CNT>(G, Lnx, Lny, Ls, Pnx, Pny, Ps, cnt, f, pr.y, vx, vy, fl, w);
+        lp3_grp<GW, CNT>(G, Lnx, Lny, Ls, Pnx, Pny, Ps, cnt, f, pr.y, a.m.lpGreedy != 0, vx, vy, fl, w);
         float dl = 0.0f;
         for (int m = G.gl; m < cnt; m += GW) dl = fmaxf(dl, Ls[m] - fmaf(Lnx[m], vx, Lny[m] * vy));
         dl = grp_max(G, dl);
