@@ -259,8 +259,8 @@ orca_status orca_set_variant(orca_ctx *ctx, int32_t variant);
 
 /* Lanes per queued infeasible agent in the least-penetration kernel: 1 = one thread
  * per agent, 4 / 8 / 16 = a lane group per agent (projected lines one per lane, LP1 bounds
- * by an exact group scan), -1 = automatic (default: 8 below ~250k agents per strip, else 1,
- * chosen by measurement).  Same results bit for bit.
+ * by an exact group scan), -1 = automatic (default; one thread per agent at every size since
+ * the greedy LP3, chosen by measurement).  Same results bit for bit.
  * Errors: INVALID_ARGUMENT. */
 orca_status orca_set_lp3_lanes(orca_ctx *ctx, int32_t lanes);
 

@@ -459,11 +459,12 @@ int pick_variant(const orca_ctx* c, const Domain& d) {
     return (d.popBuild < ORCA_AUTO_GROUP_BELOW) ? 1 : 0;
 }
 
-// LP3 lanes, auto (-1): an 8-lane group per queued agent below ~250k agents per strip (the
-// queue is then too short to fill the GPU with one thread per agent: 100k -3.5 %), one
-// thread per agent above (1M: 1 lane 0.37 ms vs 8 lanes 0.42 ms)
+// LP3 lanes, auto (-1): an 8-lane group per queued agent below ORCA_AUTO_LP3_GROUP_BELOW
+// agents per strip, one thread per agent above.  With the sequential LP3 the groups won below
+// ~250k (100k -3.5 %, r01af); with the greedy LP3 one thread per agent wins at every size
+// (100k -10 %, corridor -3 %, r01ap), so the threshold is 0
 #ifndef ORCA_AUTO_LP3_GROUP_BELOW
-#define ORCA_AUTO_LP3_GROUP_BELOW 250000
+#define ORCA_AUTO_LP3_GROUP_BELOW 0
 #endif
 int pick_lp3_lanes(const orca_ctx* c, const Domain& d) {
     if (c->lp3Lanes > 0) return c->lp3Lanes;

@@ -547,7 +547,7 @@ __device__ __forceinline__ bool lp1(const Lines& L, int T, int no, float r, floa
     float tL = -sq, tR = sq;
     const float Dx = niy, Dy = -nix;  // line direction; base point s_i n_i
 #ifndef ORCA_LP1_UNROLL
-#define ORCA_LP1_UNROLL 4  // swept r01r: 1M -0.4 %, dense -1.4 %, 100k -2 % vs 1
+#define ORCA_LP1_UNROLL 1  // r01r: 4 was best with the sequential LP; with the greedy LP 1 is -1.3 % (r01ao)
 #endif
 #define ORCA_STR_(x) #x
 #define ORCA_XSTR_(x) ORCA_STR_(x)
@@ -1691,7 +1691,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
 
 // ------------------------------------------------------------ LP3 on the queue
 #ifndef ORCA_LP3_SORT
-#define ORCA_LP3_SORT 1
+#define ORCA_LP3_SORT 0  // r01aj: -0.8 % with the sequential LP3; with the greedy LP3 +2.2 % (r01ao)
 #endif
 #define ORCA_MAX_K_DEV 32  // = ORCA_MAX_K (include/orca.h); buckets 0..32 by failure index
 // One thread per queued (infeasible) agent, grid-stride over the device-side queue

@@ -4,7 +4,7 @@
 OUT=gpurun_out; mkdir -p $OUT
 for F in "$@"; do
   ORCA_NVCC_EXTRA="$F" python -c "from paper_1908_10107_b200 import build as B; B.build(force=True)" > /dev/null 2>&1 || { echo "build failed: $F"; continue; }
-  for CFG in uniform_1m uniform dense; do
+  for CFG in ${SWEEP_CFGS:-uniform_1m uniform dense}; do
     R=$(timeout 150 python bench.py --config $CFG --steps 10 --warmup 3 --no-cpu-baseline --no-suite --e2e-steps 1 2>/dev/null | tail -1)
     python - "$F" "$CFG" "$R" <<'PY'
 import json, sys
