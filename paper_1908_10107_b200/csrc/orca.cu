@@ -549,7 +549,7 @@ cudaError_t enqueue_scan(orca_ctx* c, Domain& d, bool zero) {
         cudaError_t e = cudaMemsetAsync(d.scanStatus, 0, (tiles + 2) * sizeof(unsigned long long), c->stream);
         if (e != cudaSuccess) return e;
     }
-    k_scan<<<tiles, 1024, 0, c->stream>>>(d.count, d.binStart, (int)d.nbins, d.scanStatus,
+    k_scan<<<tiles, kScanThreads, 0, c->stream>>>(d.count, d.binStart, (int)d.nbins, d.scanStatus,
                                           reinterpret_cast<unsigned int*>(d.scanStatus + tiles));
     return cudaGetLastError();
 }

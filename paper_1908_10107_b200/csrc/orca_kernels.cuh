@@ -259,9 +259,17 @@ __global__ void k_fill_report(const uint32_t* __restrict__ binStart, Grid g, int
 // (1024 threads x 4).  status[] (64-bit: flag << 62 | value) and the tile ticket must be
 // zero at launch.  Writes binStart[0..C] and re-zeroes count for the next histogram.
 constexpr unsigned long long kAggFlag = 1ull << 62, kIncFlag = 2ull << 62, kValMask = (1ull << 62) - 1;
-constexpr int kScanTile = 4096;
+#ifndef ORCA_SCAN_ITEMS
+#define ORCA_SCAN_ITEMS 4  // bins per thread (multiple of 4); tile = 1024 x this
+#endif
+#ifndef ORCA_SCAN_THREADS
+#define ORCA_SCAN_THREADS 1024  // threads per scan tile (a multiple of 32, <= 1024)
+#endif
+constexpr int kScanItems = ORCA_SCAN_ITEMS;
+constexpr int kScanThreads = ORCA_SCAN_THREADS;
+constexpr int kScanTile = kScanThreads * kScanItems;
 
-__global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uint32_t* __restrict__ binStart, int C,
+__global__ void __launch_bounds__(kScanThreads) k_scan(uint32_t* __restrict__ count, uint32_t* __restrict__ binStart, int C,
                                                unsigned long long* __restrict__ status,
                                                unsigned int* __restrict__ ticket) {
     __shared__ uint32_t warpSums[32];
@@ -271,16 +279,21 @@ __global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uin
     __syncthreads();
     const int tile = (int)tileS;
     const int base = tile * kScanTile;
-    uint32_t v[4];
-    const int i0 = base + tid * 4;
-    if (i0 + 3 < C) {
-        const uint4 q = *reinterpret_cast<const uint4*>(count + i0);
-        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    uint32_t v[kScanItems];
+    const int i0 = base + tid * kScanItems;
+    if (i0 + kScanItems - 1 < C) {
+#pragma unroll
+        for (int c = 0; c < kScanItems / 4; ++c) {
+            const uint4 q = *reinterpret_cast<const uint4*>(count + i0 + 4 * c);
+            v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
+        }
     } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = (i0 + q < C) ? count[i0 + q] : 0u;
+        for (int q = 0; q < kScanItems; ++q) v[q] = (i0 + q < C) ? count[i0 + q] : 0u;
     }
-    const uint32_t local = v[0] + v[1] + v[2] + v[3];
+    uint32_t local = 0;
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) local += v[q];
     uint32_t incl = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -290,7 +303,7 @@ __global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uin
     if (lane == 31) warpSums[wid] = incl;
     __syncthreads();
     if (wid == 0) {
-        const uint32_t w = warpSums[lane];
+        const uint32_t w = (lane < kScanThreads / 32) ? warpSums[lane] : 0u;
         uint32_t wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -339,14 +352,14 @@ __global__ void __launch_bounds__(1024) k_scan(uint32_t* __restrict__ count, uin
     __syncthreads();
     uint32_t run = prefixS + warpSums[wid] + incl - local;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kScanItems; ++q) {
         if (i0 + q < C) {
             binStart[i0 + q] = run;
             count[i0 + q] = 0u;
         }
         run += v[q];
     }
-    if ((C - 1) / 4 == tile * 1024 + tid) binStart[C] = run;  // owner of element C-1
+    if ((C - 1) / kScanItems == tile * kScanThreads + tid) binStart[C] = run;  // owner of element C-1
 }
 
 // Counting-sort scatter of the nOwn + extra work entries (invalid = emigrated) into the
