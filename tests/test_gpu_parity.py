@@ -597,6 +597,24 @@ def test_randomized_order_resume_and_strips(orca):
 
 
 # ------------------------------------------------ work-unit LP2 (§8(f3))
+@pytest.mark.parametrize("order", [0, 2])
+@pytest.mark.parametrize("case", ["dense", "circle_crush", "k32"])
+def test_lp_orders_vs_oracle(orca, oracle, case, order):
+    """The greedy LP order (0, default: most violated half-plane next, in LP2 and LP3) and the
+    sequential neighbour order (2, the oracle's) both reach the oracle's optimum within 1e-4 and
+    its least penetration on the LP-heaviest inputs (reading Q8)."""
+    if case == "dense":
+        r = compare_step(orca, oracle, W.make("dense", n=4000), variant=0, order=order)
+    elif case == "k32":
+        r = compare_step(orca, oracle, W.make("uniform", n=3000, rho=0.5), variant=0, order=order, maxNeighbors=32)
+    else:
+        w = W.make("circle")
+        op = oracle.make_params(**w["params"])
+        pos, vel, _ = oracle.run(op, w["pos"], w["vel"], goals=w["goals"], pref_speed=1.0, steps=300)
+        r = compare_step(orca, oracle, dict(w, pos=pos, vel=vel), variant=0, order=order)
+    assert r["n_inf"] > 0
+
+
 @pytest.mark.parametrize("case", ["dense", "circle_crush", "k32"])
 def test_work_unit_lp_parity(orca, oracle, case):
     """Variant 3 (idle lanes evaluate other lanes' LP1 constraints) against the oracle on the
