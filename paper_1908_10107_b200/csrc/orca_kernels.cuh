@@ -1703,6 +1703,9 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
 }
 
 // ------------------------------------------------------------ LP3 on the queue
+#ifndef ORCA_LP3_LOAD_UNROLL
+#define ORCA_LP3_LOAD_UNROLL 4  // r01au: 1M -0.4 %, 100k -2 %, dense -1 % vs 1
+#endif
 #ifndef ORCA_LP3_SORT
 #define ORCA_LP3_SORT 0  // r01aj: -0.8 % with the sequential LP3; with the greedy LP3 +2.2 % (r01ao)
 #endif
@@ -1773,6 +1776,9 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
         const int cnt = e.y & 0xff, f = (e.y >> 8) & 0xff;
         uint32_t fl = (uint32_t)(e.y >> 16);
         float vx = __int_as_float(e.z), vy = __int_as_float(e.w);
+        // the queued half-planes (L2-resident, written by k_step): unrolled so several loads
+        // are in flight before the shared-memory stores wait on them
+        _Pragma(ORCA_XSTR_(unroll ORCA_LP3_LOAD_UNROLL))
         for (int m = 0; m < cnt; ++m) {
             const float4 l = a.qLines[(size_t)m * a.qcap + q];
             L.nx[m * T] = l.x;
