@@ -254,7 +254,8 @@ orca_status orca_reset_stats(orca_ctx *ctx);
  * shared-memory top-k list, 1 = an 8-lane group per agent, 2 = one thread per agent with a
  * register top-k list (k <= 16; else shared memory), 3 = variant 0 with the paper's
  * work-unit LP2 (lanes that need no re-solve evaluate the constraints of lanes
- * that do).  Errors: INVALID_ARGUMENT. */
+ * that do) in the sequential LP orders (orca_set_lp_order modes 1 and 2; in the greedy order
+ * it runs variant 0's LP).  Errors: INVALID_ARGUMENT. */
 orca_status orca_set_variant(orca_ctx *ctx, int32_t variant);
 
 /* Lanes per queued infeasible agent in the least-penetration kernel: 1 = one thread
