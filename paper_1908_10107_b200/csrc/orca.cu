@@ -448,11 +448,11 @@ void drop_graph(orca_ctx* c) {
     c->graphKey.clear();
 }
 
-// auto (-1): below ~24k agents per strip the step is latency bound (too few warps to hide a
+// auto (-1): below ~17k agents per strip the step is latency bound (too few warps to hide a
 // thread's chain of dependent loads) and the 8-lane group per agent wins; above, one thread
 // per agent (measured crossover)
 #ifndef ORCA_AUTO_GROUP_BELOW
-#define ORCA_AUTO_GROUP_BELOW 24000
+#define ORCA_AUTO_GROUP_BELOW 17000  // r01x: 24000; re-measured r01ax with the greedy LP: 15k v1, 20k v0
 #endif
 int pick_variant(const orca_ctx* c, const Domain& d) {
     if (c->variant >= 0) return c->variant;
