@@ -503,14 +503,34 @@ std::vector<unsigned char> graph_key(orca_ctx* c) {
     return k;
 }
 
+// Launch of a step-chain kernel with the programmatic-dependent-launch attribute (one strip:
+// the chain is k_step -> k_lp3 -> k_scan -> k_scatter -> next k_step, every kernel opens with
+// pdl_entry()), so each kernel's launch overlaps its predecessor's tail.  Strips keep plain
+// launches (exchange kernels and NCCL calls sit in the chain).  Errors surface through
+// cudaGetLastError at the call sites.
+template <typename... KArgs, typename... Args>
+void launch_k(orca_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (ORCA_PDL && c->world == 1) ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // LP3 on the queue (same results bit for bit): a GW-lane group per agent on a persistent
 // grid (pick_lp3_lanes > 1), else one thread per agent on a capacity grid
 template <bool DRY, int GW>
 void launch_lp3_grp(orca_ctx* c, Domain& d, StepArgs& a) {
     constexpr int ppb = kStepThreads / GW;
     const int blocks = (int)std::min<int64_t>((d.capW + ppb - 1) / ppb, 148 * 16);
-    k_lp3_grp<DRY, GW><<<std::max(blocks, 1), kStepThreads, lp3_grp_words(c->p.maxNeighbors) * 4 * ppb, c->stream>>>(
-        a);
+    launch_k(c, k_lp3_grp<DRY, GW>, dim3(std::max(blocks, 1)), dim3(kStepThreads),
+             (size_t)lp3_grp_words(c->p.maxNeighbors) * 4 * ppb, a);
 }
 
 template <bool DRY>
@@ -519,7 +539,7 @@ void launch_lp3(orca_ctx* c, Domain& d, StepArgs& a) {
         case 4: launch_lp3_grp<DRY, 4>(c, d, a); break;
         case 8: launch_lp3_grp<DRY, 8>(c, d, a); break;
         case 16: launch_lp3_grp<DRY, 16>(c, d, a); break;
-        default: k_lp3<DRY><<<lp3_blocks(d.capW), kStepThreads, c->lp3Smem, c->stream>>>(a);
+        default: launch_k(c, k_lp3<DRY>, dim3(lp3_blocks(d.capW)), dim3(kStepThreads), (size_t)c->lp3Smem, a);
     }
 }
 
@@ -530,15 +550,16 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int k = c->p.maxNeighbors;
     const int variant = pick_variant(c, d);
     if (variant == 1)  // 8-lane group per agent
-        k_step_group<DRY><<<(d.capW + kGroupAgents - 1) / kGroupAgents, kGroupThreads, c->groupSmem, c->stream>>>(a);
+        launch_k(c, k_step_group<DRY>, dim3((d.capW + kGroupAgents - 1) / kGroupAgents), dim3(kGroupThreads),
+                 (size_t)c->groupSmem, a);
     else if (variant == 3)  // work-unit LP2 (P:84-89 ablation)
-        k_step<DRY, 0, true><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
+        launch_k(c, k_step<DRY, 0, true>, dim3(blocks), dim3(kStepThreads), (size_t)c->smemBytes, a);
     else if (variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
-        k_step<DRY, 0><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
+        launch_k(c, k_step<DRY, 0, false>, dim3(blocks), dim3(kStepThreads), (size_t)c->smemBytes, a);
     else if (k <= 10)  // register top-k list
-        k_step<DRY, 10><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
+        launch_k(c, k_step<DRY, 10, false>, dim3(blocks), dim3(kStepThreads), (size_t)c->smemBytes, a);
     else
-        k_step<DRY, 16><<<blocks, kStepThreads, c->smemBytes, c->stream>>>(a);
+        launch_k(c, k_step<DRY, 16, false>, dim3(blocks), dim3(kStepThreads), (size_t)c->smemBytes, a);
 }
 
 // zero: clear the status words, tile ticket and LP3 queue count first (at set-up); in the
@@ -549,17 +570,15 @@ cudaError_t enqueue_scan(orca_ctx* c, Domain& d, bool zero) {
         cudaError_t e = cudaMemsetAsync(d.scanStatus, 0, (tiles + 2) * sizeof(unsigned long long), c->stream);
         if (e != cudaSuccess) return e;
     }
-    k_scan<<<tiles, kScanThreads, 0, c->stream>>>(d.count, d.binStart, (int)d.nbins, d.scanStatus,
-                                          reinterpret_cast<unsigned int*>(d.scanStatus + tiles));
+    launch_k(c, k_scan, dim3(tiles), dim3(kScanThreads), 0, d.count, d.binStart, (int)d.nbins, d.scanStatus,
+             reinterpret_cast<unsigned int*>(d.scanStatus + tiles));
     return cudaGetLastError();
 }
 
 cudaError_t enqueue_scatter(orca_ctx* c, Domain& d, int bump) {
-    k_scatter<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.ctr, bump, d.cellW, d.rankW, d.binStart, d.posW, d.velW,
-                                                              d.auxW, d.idW, d.rk2W, d.posS, d.velS, d.auxS, d.idS,
-                                                              d.rk2S, d.capW, c->het ? d.propW : nullptr,
-                                                              c->het ? d.propS : nullptr, d.scanStatus,
-                                                              scan_tiles(d.nbins) + 2);
+    launch_k(c, k_scatter, dim3(cap_blocks(d.capW, 256)), dim3(256), 0, d.ctr, bump, d.cellW, d.rankW, d.binStart,
+             d.posW, d.velW, d.auxW, d.idW, d.rk2W, d.posS, d.velS, d.auxS, d.idS, d.rk2S, d.capW,
+             c->het ? d.propW : nullptr, c->het ? d.propS : nullptr, d.scanStatus, scan_tiles(d.nbins) + 2);
     return cudaGetLastError();
 }
 

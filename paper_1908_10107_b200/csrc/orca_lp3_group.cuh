@@ -236,6 +236,7 @@ __host__ __device__ constexpr int lp3_grp_words(int k) { return 6 * k + 1; }
 
 template <bool DRY, int GW>
 __global__ void __launch_bounds__(kStepThreads) k_lp3_grp(StepArgs a) {
+    pdl_entry();
     constexpr bool CNT = DRY;
     constexpr int PPB = kStepThreads / GW;  // queued agents per block
     WorkT w{0, 0, 0, 0, 0};

@@ -226,6 +226,7 @@ __device__ __forceinline__ int lp2_group_greedy(const GroupCtx& G, float* nx, fl
 
 template <bool DRY>
 __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char smemg[];
     const int k = a.m.k;
     const int tid = threadIdx.x;
