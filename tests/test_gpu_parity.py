@@ -180,6 +180,29 @@ def test_tie_lattice_neighbors(orca, oracle):
     compare_step(orca, oracle, w)
 
 
+@pytest.mark.parametrize("ulp", [False, True])
+def test_subcell_boundary_lattice(orca, oracle, ulp):
+    """Agents exactly on the sort's fine-column (cs/4) and sub-row (cs/8) boundaries -- and one
+    fp32 ulp either side of them -- with many exact distance ties: the search windows of the
+    sub-cell runs still give the bit-exact cells and (kappa, id) neighbour lists."""
+    cs = 4.0
+    xs = np.arange(40, dtype=np.float32) * np.float32(cs / 4)
+    ys = np.arange(40, dtype=np.float32) * np.float32(cs / 8)
+    pos = np.stack(np.meshgrid(xs, ys, indexing="ij"), -1).reshape(-1, 2).astype(np.float32)
+    pos += np.float32(cs)  # the grid origin is min - cs: boundaries at whole multiples
+    if ulp:
+        rng = np.random.default_rng(4)
+        pick = rng.random(pos.shape) < 0.3
+        up = rng.random(pos.shape) < 0.5
+        pos = np.where(pick, np.where(up, np.nextafter(pos, np.float32(np.inf)),
+                                      np.nextafter(pos, np.float32(-np.inf))), pos).astype(np.float32)
+    rng = np.random.default_rng(5)
+    pref = rng.uniform(-1, 1, pos.shape).astype(np.float32)
+    w = dict(pos=pos, vel=np.zeros_like(pos), pref=pref, goals=None,
+             params=dict(W.DEFAULT_PARAMS, neighborDist=cs, radius=0.2))
+    compare_step(orca, oracle, w, max_deg=len(pos))
+
+
 def test_coincident_agents(orca, oracle):
     """Coincident agents with equal velocity (reading Q15, g1): deterministic +-x push."""
     rng = np.random.default_rng(9)
