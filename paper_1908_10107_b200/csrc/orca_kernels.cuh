@@ -445,7 +445,7 @@ __device__ __forceinline__ void lp_shuffle(uint32_t* x, int T, int c, unsigned l
 // oracle's expression trees; geometry in fp32 Hessian form.  Returns flag bits
 // (FL_G1) and sets *collision.
 __device__ __forceinline__ uint32_t orca_line_branchy(float xi, float yi, float vxi, float vyi, float xj, float yj,
-                                              float vxj, float vyj, uint32_t idi, uint32_t idj, float R, double R2D,
+                                              float vxj, float vyj, uint32_t idi, const uint32_t* __restrict__ idS, uint32_t j, float R, double R2D,
                                               const Model& m, float& nx, float& ny, float& s, int& collision) {
     const double rpx = __dsub_rn((double)xj, (double)xi);
     const double rpy = __dsub_rn((double)yj, (double)yi);
@@ -489,7 +489,7 @@ __device__ __forceinline__ uint32_t orca_line_branchy(float xi, float yi, float 
         const double wl2 = __dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy));
         float wl;
         if (wl2 == 0.0) {  // coincident, equal velocity (reading Q15)
-            nx = (idi < idj) ? -1.0f : 1.0f;
+            nx = (idi < idS[j]) ? -1.0f : 1.0f;  // (the id only here: loaded lazily)
             ny = 0.0f;
             wl = 0.0f;
             fl |= FL_G1;
@@ -513,7 +513,7 @@ __device__ __forceinline__ uint32_t orca_line_branchy(float xi, float yi, float 
 #define ORCA_LINE_BF 1
 #endif
 __device__ __forceinline__ uint32_t orca_line_bf(float xi, float yi, float vxi, float vyi, float xj, float yj,
-                                                 float vxj, float vyj, uint32_t idi, uint32_t idj, float R, double R2D,
+                                                 float vxj, float vyj, uint32_t idi, const uint32_t* __restrict__ idS, uint32_t j, float R, double R2D,
                                                  const Model& m, float& nx, float& ny, float& s, int& collision) {
     const double rpx = __dsub_rn((double)xj, (double)xi);
     const double rpy = __dsub_rn((double)yj, (double)yi);
@@ -530,7 +530,7 @@ __device__ __forceinline__ uint32_t orca_line_bf(float xi, float yi, float vxi, 
     const double detw = __dsub_rn(__dmul_rn(rpx, wy), __dmul_rn(rpy, wx));
     collision = coll ? 1 : 0;
     if (coll && wl2 == 0.0) {  // coincident, equal velocity (reading Q15)
-        nx = (idi < idj) ? -1.0f : 1.0f;
+        nx = (idi < idS[j]) ? -1.0f : 1.0f;  // (the id only here: loaded lazily)
         ny = 0.0f;
         s = fmaf(nx, vxi, ny * vyi) + 0.5f * (R * m.invDtF);
         return FL_G1;
@@ -551,11 +551,11 @@ __device__ __forceinline__ uint32_t orca_line_bf(float xi, float yi, float vxi, 
 }
 
 __device__ __forceinline__ uint32_t orca_line(float xi, float yi, float vxi, float vyi, float xj, float yj, float vxj,
-                                              float vyj, uint32_t idi, uint32_t idj, float R, double R2D,
+                                              float vyj, uint32_t idi, const uint32_t* __restrict__ idS, uint32_t j, float R, double R2D,
                                               const Model& m, float& nx, float& ny, float& s, int& collision) {
     if (ORCA_LINE_BF)
-        return orca_line_bf(xi, yi, vxi, vyi, xj, yj, vxj, vyj, idi, idj, R, R2D, m, nx, ny, s, collision);
-    return orca_line_branchy(xi, yi, vxi, vyi, xj, yj, vxj, vyj, idi, idj, R, R2D, m, nx, ny, s, collision);
+        return orca_line_bf(xi, yi, vxi, vyi, xj, yj, vxj, vyj, idi, idS, j, R, R2D, m, nx, ny, s, collision);
+    return orca_line_branchy(xi, yi, vxi, vyi, xj, yj, vxj, vyj, idi, idS, j, R, R2D, m, nx, ny, s, collision);
 }
 
 // ------------------------------------------------------------------- LP
@@ -1611,7 +1611,6 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             const uint32_t j = L1[q * T];
             const float2 pj = a.posS[j];
             const float2 vj = a.velS[j];
-            const uint32_t idj = a.idS[j];
             float nx, ny, s;
             int coll;
             // combined radius R = r_i + r_j (Fig. 1(a)); per agent when heterogeneous
@@ -1622,7 +1621,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 R2p = Rd * Rd;
                 Rp = (float)Rd;
             }
-            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, idj, Rp, R2p, a.m, nx, ny, s, coll);
+            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, a.idS, j, Rp, R2p, a.m, nx, ny, s, coll);
             nColl += coll;
             L.nx[q * T] = nx;
             L.ny[q * T] = ny;

@@ -382,7 +382,6 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
             const uint32_t j = lj[q];
             const float2 pj = a.posS[j];
             const float2 vj = a.velS[j];
-            const uint32_t idj = a.idS[j];
             float nx, ny, s;
             int coll;
             // combined radius R = r_i + r_j (Fig. 1(a)); per agent when heterogeneous
@@ -393,7 +392,7 @@ __global__ void __launch_bounds__(kGroupThreads, 8) k_step_group(StepArgs a) {
                 R2p = Rd * Rd;
                 Rp = (float)Rd;
             }
-            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, idj, Rp, R2p, a.m, nx, ny, s, coll);
+            fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, a.idS, j, Rp, R2p, a.m, nx, ny, s, coll);
             nColl += coll;
             Lnx[q] = nx;
             Lny[q] = ny;
