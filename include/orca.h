@@ -24,7 +24,10 @@
  *     copies inputs (the caller keeps ownership of its buffers) and writes outputs into
  *     caller-allocated buffers.
  *   - A context is used by one host thread at a time.  orca_step is asynchronous on the
- *     context's stream; every getter synchronises that stream.
+ *     context's stream (a call of more than two 64-step chunks waits for chunk q-2 before
+ *     queuing chunk q, to re-derive the grid while it runs); every getter synchronises that
+ *     stream.  orca_set_state_async / orca_get_state_async do not synchronise: their buffers
+ *     are in use until orca_io_wait returns.
  *   - On error, orca_last_error() returns a thread-local human-readable message.
  */
 #ifndef ORCA_H
