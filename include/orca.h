@@ -338,6 +338,14 @@ orca_status orca_set_transport(orca_ctx *ctx, int32_t mode);
  * every rank when some pair of neighbouring GPUs cannot map each other's memory. */
 orca_status orca_get_transport(orca_ctx *ctx, int32_t *mode);
 
+/* The kernels one step launches for this context's first strip, as chosen for the loaded
+ * agents: info[0] = step kernel variant (0, 1, 2 or 3), info[1] = lanes per
+ * agent of the least-penetration kernel (0 = LP3 runs inside the step kernel, no k_lp3
+ * launch), info[2] = CUDA kernels launched per step and strip (step kernel, k_lp3 unless
+ * inline, k_scan, k_scatter, plus k_receive and one k_push per neighbour for strips with
+ * the peer-memory exchange), info[3] = the transport.  Errors: INVALID_ARGUMENT, NOT_READY. */
+orca_status orca_get_launch_info(orca_ctx *ctx, int32_t info[4]);
+
 orca_status orca_get_strips(orca_ctx *ctx, int32_t *bounds);
 
 #ifdef __cplusplus

@@ -351,6 +351,8 @@ Model make_model(const orca_ctx* c) {
     return m;
 }
 
+bool pick_lp3_inline(const orca_ctx* c, const Domain& d);
+
 StepArgs make_args(orca_ctx* c, Domain& d) {
     StepArgs a{};
     a.g = d.g;
@@ -379,6 +381,7 @@ StepArgs make_args(orca_ctx* c, Domain& d) {
     a.qEntry = d.qEntry;
     a.qLines = d.qLines;
     a.qcap = d.capW;
+    a.lp3Inline = pick_lp3_inline(c, d) ? 1 : 0;
     a.gridFlag = c->gridFlagDev;
     a.qCount = reinterpret_cast<unsigned int*>(d.scanStatus + scan_tiles(d.nbins) + 1);
     return a;
@@ -471,6 +474,16 @@ int pick_lp3_lanes(const orca_ctx* c, const Domain& d) {
     return (d.popBuild < ORCA_AUTO_LP3_GROUP_BELOW) ? 8 : 1;
 }
 
+// LP3 inside k_step (StepArgs::lp3Inline) for strips below ORCA_AUTO_LP3_INLINE_BELOW agents
+// on the thread-per-agent kernels: there the step is latency bound and the
+// separate k_lp3 launch is a serial tail; the group kernel always queues.
+#ifndef ORCA_AUTO_LP3_INLINE_BELOW
+#define ORCA_AUTO_LP3_INLINE_BELOW 125000  // r01bi: k_step+k_lp3 50k 0.054 -> 0.046, 100k 0.058 -> 0.051 ms; 150k+ slower
+#endif
+bool pick_lp3_inline(const orca_ctx* c, const Domain& d) {
+    return pick_variant(c, d) != 1 && d.popBuild < ORCA_AUTO_LP3_INLINE_BELOW;
+}
+
 // Everything a captured step body depends on: the kernel arguments of every strip (device
 // pointers, grid, model), launch sizes, the exchange buffers and the kernel selection.  A
 // cached graph is replayed only while this is unchanged, so orca_set_agents with the same
@@ -535,6 +548,7 @@ void launch_lp3_grp(orca_ctx* c, Domain& d, StepArgs& a) {
 
 template <bool DRY>
 void launch_lp3(orca_ctx* c, Domain& d, StepArgs& a) {
+    if (a.lp3Inline) return;  // k_step finished its infeasible agents
     switch (pick_lp3_lanes(c, d)) {
         case 4: launch_lp3_grp<DRY, 4>(c, d, a); break;
         case 8: launch_lp3_grp<DRY, 8>(c, d, a); break;
@@ -549,17 +563,19 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
     const int k = c->p.maxNeighbors;
     const int variant = pick_variant(c, d);
+    // inline LP3 needs the projected half-planes: 3k more words per thread
+    const size_t smem = (size_t)c->smemBytes + (a.lp3Inline ? (size_t)3 * std::max(k, 1) * 4 * kStepThreads : 0);
     if (variant == 1)  // 8-lane group per agent
         launch_k(c, k_step_group<DRY>, dim3((d.capW + kGroupAgents - 1) / kGroupAgents), dim3(kGroupThreads),
                  (size_t)c->groupSmem, a);
     else if (variant == 3)  // work-unit LP2 (P:84-89 ablation)
-        launch_k(c, k_step<DRY, 0, true>, dim3(blocks), dim3(kStepThreads), (size_t)c->smemBytes, a);
+        launch_k(c, k_step<DRY, 0, true>, dim3(blocks), dim3(kStepThreads), smem, a);
     else if (variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
-        launch_k(c, k_step<DRY, 0, false>, dim3(blocks), dim3(kStepThreads), (size_t)c->smemBytes, a);
+        launch_k(c, k_step<DRY, 0, false>, dim3(blocks), dim3(kStepThreads), smem, a);
     else if (k <= 10)  // register top-k list
-        launch_k(c, k_step<DRY, 10, false>, dim3(blocks), dim3(kStepThreads), (size_t)c->smemBytes, a);
+        launch_k(c, k_step<DRY, 10, false>, dim3(blocks), dim3(kStepThreads), smem, a);
     else
-        launch_k(c, k_step<DRY, 16, false>, dim3(blocks), dim3(kStepThreads), (size_t)c->smemBytes, a);
+        launch_k(c, k_step<DRY, 16, false>, dim3(blocks), dim3(kStepThreads), smem, a);
 }
 
 // zero: clear the status words, tile ticket and LP3 queue count first (at set-up); in the
@@ -733,8 +749,9 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
                              (const void*)k_step<false, 10>, (const void*)k_step<true, 10>,
                              (const void*)k_step<false, 16>, (const void*)k_step<true, 16>,
                              (const void*)k_step<false, 0, true>, (const void*)k_step<true, 0, true>};
+    const int stepSmemMax = c->smemBytes + 3 * std::max(params->maxNeighbors, 1) * 4 * kStepThreads;  // + inline LP3
     for (const void* f : stepFns)
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smemBytes);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, stepSmemMax);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
     if (e == cudaSuccess)
@@ -1990,6 +2007,23 @@ orca_status orca_set_transport(orca_ctx* c, int32_t mode) {
 orca_status orca_get_transport(orca_ctx* c, int32_t* mode) {
     if (!c || !mode) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
     *mode = c->transport;
+    return ORCA_OK;
+}
+
+orca_status orca_get_launch_info(orca_ctx* c, int32_t info[4]) {
+    if (!c || !info) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
+    if (!c->ready || c->doms.empty()) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    const Domain& d = c->doms[0];
+    const bool inl = pick_lp3_inline(c, d);
+    int n = inl ? 3 : 4;
+    if (d.g.hasL || d.g.hasR) {  // strips: k_receive, and k_push per neighbour (peer memory)
+        n += 1;
+        if (c->transport == 0) n += (d.g.hasL ? 1 : 0) + (d.g.hasR ? 1 : 0);
+    }
+    info[0] = pick_variant(c, d);
+    info[1] = inl ? 0 : pick_lp3_lanes(c, d);
+    info[2] = n;
+    info[3] = c->transport;
     return ORCA_OK;
 }
 

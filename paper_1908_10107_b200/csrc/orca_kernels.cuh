@@ -1085,7 +1085,7 @@ struct StepArgs {
     float4* qLines;        // line m of entry q at [m * qcap + q] = (nx, ny, s, 0)
     unsigned int* qCount;  // zeroed before every step
     int qcap;
-    int pad1;
+    int lp3Inline;  // 1: k_step finishes its infeasible agents itself (small strips; no k_lp3)
     int* gridFlag;  // host-mapped: set when an agent enters the grid's outer cell ring
 };
 static_assert(sizeof(Grid) == 104 && sizeof(Model) == 104 && sizeof(ExBuf) % 8 == 0, "padding-free layouts");
@@ -1649,7 +1649,23 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                       : WU         ? lp2_wu<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                       : ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                                      : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
-        if (f < cnt) {
+        if (a.lp3Inline) {
+            // small strips (latency bound, spare issue slots): the least-penetration LP
+            // runs here on the half-planes in shared memory -- the same lp3 as k_lp3, so the
+            // same result -- and the agent is finished below like a feasible one
+            const unsigned lmask = __ballot_sync(activeMask, f < cnt);
+            if (f < cnt) {
+                fl |= FL_INFEASIBLE;
+                const Lines P{Bff, Bff + k * T, Bff + 2 * k * T};  // launched with 3k more words
+                if (a.m.lpGreedy)
+                    lp3_greedy<CNT>(L, P, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask);
+                else
+                    lp3_sync<CNT>(L, P, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask);
+                float dl = 0.0f;
+                for (int m = 0; m < cnt; ++m) dl = fmaxf(dl, L.s[m * T] - fmaf(L.nx[m * T], vx, L.ny[m * T] * vy));
+                if (dl > 0.0f && dl < 1e-6f) fl |= FL_G3;
+            }
+        } else if (f < cnt) {
             // infeasible: queue the agent with its half-planes and LP2 point; k_lp3
             // runs the least-penetration LP on a compacted set of agents (full warps)
             fl |= FL_INFEASIBLE;

@@ -29,7 +29,7 @@ EXPORTS = [
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
     "orca_set_lp_order", "orca_set_lp3_lanes", "orca_rebalance", "orca_set_transport",
     "orca_get_transport", "orca_set_state", "orca_set_state_async", "orca_get_state_async",
-    "orca_io_wait",
+    "orca_io_wait", "orca_get_launch_info",
 ]
 
 
@@ -99,6 +99,7 @@ def _load():
         "orca_set_state_async": [vp, vp, vp],
         "orca_get_state_async": [vp, vp, vp],
         "orca_io_wait": [vp],
+        "orca_get_launch_info": [vp, P(i32)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -347,6 +348,12 @@ class Orca:
         m = ctypes.c_int32()
         _check(_lib.orca_get_transport(self._ctx, ctypes.byref(m)))
         return m.value
+
+    def launch_info(self) -> dict:
+        """orca_get_launch_info: the kernels one step launches (first strip)."""
+        out = (ctypes.c_int32 * 4)()
+        _check(_lib.orca_get_launch_info(self._ctx, out))
+        return dict(variant=out[0], lp3_lanes=out[1], kernels_per_step=out[2], transport=out[3])
 
     def rebalance(self):
         """Re-partition the strips from the current state (automatic when a strip nears its
