@@ -11,6 +11,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1127,7 +1129,12 @@ orca_status maybe_rebalance(orca_ctx* c) {
         if (!*outside) return ORCA_OK;
         CK(cudaStreamSynchronize(c->stream));
         *outside = 0;
-        return rebalance(c, true);
+        const auto t0 = std::chrono::steady_clock::now();
+        const orca_status st = rebalance(c, true);
+        if (std::getenv("ORCA_DEBUG_TIMING"))
+            std::fprintf(stderr, "[orca] regrid %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        return st;
     }
     const int nd = (int)c->doms.size();
     if (c->reportCap < 3 * nd + 4) {
@@ -1515,6 +1522,7 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
         for (size_t g = 0; g < c->graphs.size(); ++g)
             if (c->graphs[g].first == s) slot = (int)g;
         if (slot < 0 || c->graphGen[slot] != c->keyGen) {
+            const auto tg0 = std::chrono::steady_clock::now();
             cudaGraph_t gr;
             CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
             orca_status st = ORCA_OK;
@@ -1554,6 +1562,9 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
             }
             c->graphGen[slot] = c->keyGen;
             cudaGraphDestroy(gr);
+            if (std::getenv("ORCA_DEBUG_TIMING"))
+                std::fprintf(stderr, "[orca] graph %d steps %s %.3f ms\n", s, updated ? "updated" : "instantiated",
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tg0).count());
         }
         cudaGraphExec_t exec = c->graphs[slot].second;
         CK(cudaGraphLaunch(exec, c->stream));
