@@ -565,8 +565,10 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
     const int k = c->p.maxNeighbors;
     const int variant = pick_variant(c, d);
-    // inline LP3 needs the projected half-planes: 3k more words per thread
-    const size_t smem = (size_t)c->smemBytes + (a.lp3Inline ? (size_t)3 * std::max(k, 1) * 4 * kStepThreads : 0);
+    // inline LP3 needs the projected half-planes (3k words per thread after s, partly in the
+    // free tail of the candidate buffer): max(0, 3k - ORCA_BUF_EXTRA) more words per thread
+    const size_t smem = (size_t)c->smemBytes +
+                        (a.lp3Inline ? (size_t)std::max(0, 3 * k - ORCA_BUF_EXTRA) * 4 * kStepThreads : 0);
     if (variant == 1)  // 8-lane group per agent
         launch_k(c, k_step_group<DRY>, dim3((d.capW + kGroupAgents - 1) / kGroupAgents), dim3(kGroupThreads),
                  (size_t)c->groupSmem, a);

@@ -1656,7 +1656,10 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             const unsigned lmask = __ballot_sync(activeMask, f < cnt);
             if (f < cnt) {
                 fl |= FL_INFEASIBLE;
-                const Lines P{Bff, Bff + k * T, Bff + 2 * k * T};  // launched with 3k more words
+                // projected half-planes right after s in the (now free) candidate buffer and
+                // beyond it: the launch adds max(0, 3k - ORCA_BUF_EXTRA) words per thread
+                float* Pb = reinterpret_cast<float*>(Bf + k * T);
+                const Lines P{Pb, Pb + k * T, Pb + 2 * k * T};
                 if (a.m.lpGreedy)
                     lp3_greedy<CNT>(L, P, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask);
                 else
