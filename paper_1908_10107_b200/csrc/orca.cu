@@ -480,7 +480,7 @@ int pick_lp3_lanes(const orca_ctx* c, const Domain& d) {
 // on the thread-per-agent kernels: there the step is latency bound and the
 // separate k_lp3 launch is a serial tail; the group kernel always queues.
 #ifndef ORCA_AUTO_LP3_INLINE_BELOW
-#define ORCA_AUTO_LP3_INLINE_BELOW 125000  // r01bi: k_step+k_lp3 50k 0.054 -> 0.046, 100k 0.058 -> 0.051 ms; 150k+ slower
+#define ORCA_AUTO_LP3_INLINE_BELOW 125000  // ~ one wave of k_step blocks (148 SMs x 7 x 128); r01bk: 100k 0.058 -> 0.051, 125k 0.062 -> 0.056, 150k 0.067 -> 0.080 ms
 #endif
 bool pick_lp3_inline(const orca_ctx* c, const Domain& d) {
     return pick_variant(c, d) != 1 && d.popBuild < ORCA_AUTO_LP3_INLINE_BELOW;
