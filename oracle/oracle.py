@@ -92,6 +92,8 @@ def lib():
         L.or_lp3.restype = None
         L.or_penetration.argtypes = [P(Line), ctypes.c_int, f64p]
         L.or_penetration.restype = ctypes.c_double
+        L.or_solve.argtypes = [P(Line), ctypes.c_int, ctypes.c_double, f64p, f64p, f64p]
+        L.or_solve.restype = ctypes.c_uint32
         L.or_step.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float, P(Agents),
                               P(LpOrder), f32p, i32p, ctypes.c_int64, i64p, f64p, f64p, u8p, f64p, i32p, i32p]
         L.or_run.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float, P(Agents),
@@ -196,6 +198,17 @@ def solve(lines, r, pref):
         v, d3 = lp3(lines, f, r, v)
         return v, True, d | d3
     return v, False, d
+
+
+def solve_classify(lines, r, pref):
+    """or_solve: the step's solve of one agent plus its flags (INFEASIBLE, G2, G3, G4).
+    Returns (v, flags, delta)."""
+    arr, n = _lines(lines)
+    o = np.ascontiguousarray(pref, np.float64)
+    v = np.zeros(2, np.float64)
+    d = ctypes.c_double(0.0)
+    fl = lib().or_solve(arr, n, r, _p(o, ctypes.c_double), _p(v, ctypes.c_double), ctypes.byref(d))
+    return v, int(fl), d.value
 
 
 def penetration(lines, v):

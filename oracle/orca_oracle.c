@@ -394,6 +394,30 @@ static int solve_agent(const or_line *L, int n, double maxSpeed, const double pr
     return 0;
 }
 
+/* The solve and its classification (SURVEY 8(c) degenerate classes; DESIGN reading Q21):
+ * infeasible, g2 (raised inside LP1/LP3), g3 (0 < delta < 1e-6 after LP3) and g4 (a
+ * reversed-order re-solve reaches the same delta, within 1e-9, at a v more than 1e-6
+ * away: the least-penetration argmin is not unique). */
+uint32_t or_solve(const or_line *L, int n, double maxSpeed, const double pref[2], double v[2], double *delta) {
+    uint32_t diag = 0;
+    or_line Lrev[32];
+    int infeasible = solve_agent(L, n, maxSpeed, pref, v, &diag);
+    double dl = or_penetration(L, n, v);
+    if (infeasible) {
+        diag |= OR_FLAG_INFEASIBLE;
+        if (dl > 0.0 && dl < OR_G3_EPS) diag |= OR_FLAG_G3_MARGINAL;
+        for (int a = 0; a < n; ++a) Lrev[a] = L[n - 1 - a];
+        double v2[2];
+        uint32_t d2 = 0;
+        solve_agent(Lrev, n, maxSpeed, pref, v2, &d2);
+        double dl2 = or_penetration(L, n, v2);
+        if (fabs(dl2 - dl) <= 1e-9 && hypot(v2[0] - v[0], v2[1] - v[1]) > 1e-6)
+            diag |= OR_FLAG_G4_NONUNIQUE;
+    }
+    if (delta) *delta = dl;
+    return diag;
+}
+
 /* ---------------------------------------------------------------------------------- */
 /* One synchronous step (reading Q13: all reads are of the pre-step state). */
 /* ---------------------------------------------------------------------------------- */
@@ -459,7 +483,7 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, c
     bins_t b;
     if (bins_build(&b, n, pos, origin, p->neighborDist, dims) != 0) return -1;
     cand_t *cand = (cand_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(cand_t));
-    or_line L[32], Lrev[32];
+    or_line L[32];
     int32_t nb[32];
     for (int64_t q = 0; q < m; ++q) {
         const int64_t i = agents ? agents[q] : q;
@@ -496,20 +520,8 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, c
          *    penetration */
         double pv[2], v[2];
         pref_of(pos, pref, goals, prefSpeed, ag, i, pv);
-        int infeasible = solve_agent(L, c, maxSpeed, pv, v, &diag);
-        double dl = or_penetration(L, c, v);
-        if (infeasible) {
-            diag |= OR_FLAG_INFEASIBLE;
-            if (dl > 0.0 && dl < OR_G3_EPS) diag |= OR_FLAG_G3_MARGINAL;
-            /* g4: a reversed-order re-solve reaching the same delta at another v */
-            for (int32_t a = 0; a < c; ++a) Lrev[a] = L[c - 1 - a];
-            double v2[2];
-            uint32_t d2 = 0;
-            solve_agent(Lrev, c, maxSpeed, pv, v2, &d2);
-            double dl2 = or_penetration(L, c, v2);
-            if (fabs(dl2 - dl) <= 1e-9 && hypot(v2[0] - v[0], v2[1] - v[1]) > 1e-6)
-                diag |= OR_FLAG_G4_NONUNIQUE;
-        }
+        double dl;
+        diag |= or_solve(L, c, maxSpeed, pv, v, &dl);
         /* 4. integrate ("take the chosen velocity"; explicit Euler) */
         vnew[2 * q] = v[0];
         vnew[2 * q + 1] = v[1];

@@ -129,6 +129,14 @@ void or_lp3(const or_line *lines, int n, int begin, double r, double v[2], uint3
 /* Maximum penetration max(0, max_j det(d_j, p_j - v)) of v into the lines. */
 double or_penetration(const or_line *lines, int n, const double v[2]);
 
+/* One agent's velocity solve as or_step does it: LP2 over the lines in the given
+ * order, LP3 from the failure index, then the classification: returns the flags
+ * (INFEASIBLE, G2, G3, G4; n <= 32), writes v and delta = or_penetration(lines, v).
+ * Pins: g4 fires on a non-unique least-penetration argmin (S:123 pair) and not on a
+ * unique one (empty triangle); g2 fires on near-parallel pairs crossing inside the disc. */
+uint32_t or_solve(const or_line *lines, int n, double maxSpeed, const double pref[2], double v[2],
+                  double *delta);
+
 /* ---- one synchronous time step (reading Q13) ---------------------------- */
 
 /* Computes, for every agent i in `agents` (or all agents when agents == NULL, m ignored),

@@ -546,3 +546,122 @@ def test_randomized_order_same_optimum(oracle):
     moved = sum(not np.array_equal(oracle.lp_permutation(2024, 5, i, int(c)), np.arange(c))
                 for i, c in enumerate(b["cnt"]) if c > 1)
     assert moved > 0.9 * np.count_nonzero(b["cnt"] > 1)
+
+
+# --------------------------------------- degenerate classes g2 / g4
+def _rot_line(line, th, q):
+    """`line` (point, unit direction) rotated by th about the point q (which it contains)."""
+    c, s = math.cos(th), math.sin(th)
+    dx, dy = line[2], line[3]
+    return [q[0], q[1], c * dx - s * dy, s * dx + c * dy]
+
+
+def _argmin_diameter(lines, r, slack, res=801):
+    """Diameter of {v in the disc : max penetration(v) <= grid best + slack} on a dense grid:
+    large iff the least-penetration argmin is not unique (up to the grid)."""
+    n, s = pins._halfplane_form(lines)
+    g = np.linspace(-r, r, res)
+    X, Y = np.meshgrid(g, g, indexing="ij")
+    inside = X * X + Y * Y <= r * r
+    V = np.stack([X[inside], Y[inside]], axis=1)
+    pen = np.maximum(np.max(s[None, :] - V @ n.T, axis=1), 0.0)
+    near = V[pen <= pen.min() + slack]
+    return float(np.max(np.ptp(near, axis=0)))
+
+
+def test_g4_fires_on_non_unique_lp3_argmin(oracle):
+    """g4: a least-penetration problem whose argmin is a segment.  The
+    S:123 pair {x >= 1, x <= -1} is minimised (delta = 1) by every point of x = 0 in the
+    disc; likewise {y >= 0.5, y <= -0.5, x <= 1.5} along y = 0.  The grid search confirms
+    the argmin set is a long segment, and the oracle flags g4."""
+    cases = [
+        [[1.0, 0.0, 0.0, -1.0], [-1.0, 0.0, 0.0, 1.0]],
+        [[0.0, 0.5, 1.0, 0.0], [0.0, -0.5, -1.0, 0.0], [1.5, 0.0, 0.0, 1.0]],
+    ]
+    for lines in cases:
+        assert _argmin_diameter(lines, 2.0, 1e-9) > 1.0  # independent: non-unique argmin
+        v, fl, d = oracle.solve_classify(lines, 2.0, [0.3, 0.1])
+        assert fl & oracle.FLAG_INFEASIBLE
+        assert fl & oracle.FLAG_G4, (lines, fl)
+        assert abs(d - pins.penetration_np(lines, v)) < 1e-12
+        assert abs(d - (1.0 if len(lines) == 2 else 0.5)) < 1e-9
+
+
+def test_g4_silent_on_unique_lp3_argmin(oracle):
+    """A unique least-penetration argmin never raises g4: the symmetric empty triangle (S:125,
+    v = 0, delta = 0.5) and 200 generic random infeasible problems, whose near-argmin sets
+    (grid, slack 1e-3) stay a few grid cells wide."""
+    tri = []
+    for a in (90.0, 210.0, 330.0):
+        n = np.array([math.cos(math.radians(a)), math.sin(math.radians(a))])
+        tri.append([0.5 * n[0], 0.5 * n[1], n[1], -n[0]])
+    v, fl, d = oracle.solve_classify(tri, 1.33, [0.2, 0.1])
+    assert fl & oracle.FLAG_INFEASIBLE and not fl & oracle.FLAG_G4
+    assert np.hypot(*v) < 1e-9 and abs(d - 0.5) < 1e-9
+    assert _argmin_diameter(tri, 1.33, 1e-3) < 0.02
+    rng = np.random.default_rng(44)
+    tested = 0
+    while tested < 200:
+        m = int(rng.integers(3, 12))
+        ang = rng.uniform(0, 2 * np.pi, m)
+        n = np.stack([np.cos(ang), np.sin(ang)], 1)
+        s = rng.uniform(0.2, 1.2, m)
+        lines = np.concatenate([s[:, None] * n, np.stack([n[:, 1], -n[:, 0]], 1)], axis=1)
+        v, fl, d = oracle.solve_classify(lines, 1.33, rng.uniform(-1, 1, 2))
+        if not fl & oracle.FLAG_INFEASIBLE:
+            continue
+        assert not fl & oracle.FLAG_G4, lines
+        if tested < 40:
+            assert _argmin_diameter(lines, 1.33, 1e-3, res=401) < 0.2
+        tested += 1
+
+
+def test_g2_near_parallel_crossing_inside_disc(oracle):
+    """g2 (reading Q9): lines 5e-6 rad apart crossing INSIDE the speed disc.  A solver with
+    the GPU's parallel tolerance (|det| <= 1e-5 -> "parallel": fail if the point lies on the
+    wrong side, else skip) declares LP1 infeasible here, while the exact problem is
+    feasible (vertex enumeration) -- the decision can flip, so the agent is flagged."""
+    A = [0.5, 0.0, 0.0, -1.0]                      # permitted x >= 0.5
+    q = np.array([0.5, 0.2])                       # the crossing, |q| < r
+    B = _rot_line(A, 5e-6, q)
+    B[0] -= 0.1 * B[2]                             # B's point 0.1 along B from the crossing
+    B[1] -= 0.1 * B[3]
+    den = A[2] * B[3] - A[3] * B[2]                 # det(D_A, D_B)
+    num = A[2] * (B[1] - A[1]) - A[3] * (B[0] - A[0])  # det(D_A, P_B - P_A)
+    assert abs(den) <= 1e-5 and num < 0.0          # the eps-solver's "parallel, pointing away"
+    assert pins.lp_vertex_enumeration([A, B], 1.33, [0.0, 0.0]) is not None  # exactly feasible
+    f, v, diag = oracle.lp2([A, B], 1.33, [0.0, 0.0])
+    assert f == 2 and diag & oracle.FLAG_G2
+    ve = pins.lp_vertex_enumeration([A, B], 1.33, [0.0, 0.0])
+    assert np.allclose(v, ve, atol=1e-9)
+    # the same pair, the other way round, in the least-penetration LP (same-direction pair
+    # whose bisector crosses the disc) with a third line making the problem infeasible
+    C = [-0.5, 0.0, 0.0, 1.0]
+    v3, d3 = oracle.lp3([A, C, B], 2, 1.33, np.array([0.0, 0.0]))
+    assert d3 & oracle.FLAG_G2
+
+
+def test_g2_silent_when_crossing_outside_disc_or_angle_large(oracle):
+    """No g2 when (a) the lines are as nearly parallel (5e-6 rad) but cross far outside the
+    disc -- the eps-solver's parallel rule and the exact crossing then decide alike -- or
+    (b) they cross inside the disc at 3e-5 rad, above the GPU tolerance (both solvers
+    intersect)."""
+    A = [0.5, 0.0, 0.0, -1.0]
+    for q, th in (((0.5, 100.0), 5e-6), ((0.5, -100.0), -5e-6), ((0.5, 0.2), 3e-5), ((0.5, 0.2), -3e-5)):
+        B = _rot_line(A, th, q)
+        # move B's point to the disc (the crossing stays at q)
+        t = -(B[0] * B[2] + B[1] * B[3])
+        B = [B[0] + t * B[2], B[1] + t * B[3], B[2], B[3]]
+        den = A[2] * B[3] - A[3] * B[2]
+        num = A[2] * (B[1] - A[1]) - A[3] * (B[0] - A[0])
+        cross_in_disc = math.hypot(*q) < 1.33
+        if abs(den) <= 1e-5:
+            assert not cross_in_disc
+            # the eps rule (fail iff num < 0) agrees with the exact feasibility of {A, B}
+            # on B's chord: exact LP1 on B clipped by A
+            exact_ok = pins.lp_vertex_enumeration([A, B], 1.33, [B[0], B[1]]) is not None
+            assert exact_ok == (num >= 0.0)
+        for order in ([A, B], [B, A]):
+            for pref in ([0.0, 0.0], [1.0, 0.3], [-1.0, -0.5]):
+                f, v, diag = oracle.lp2(order, 1.33, pref)
+                assert not diag & oracle.FLAG_G2, (q, th, pref)
