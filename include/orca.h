@@ -264,9 +264,18 @@ orca_status orca_set_variant(orca_ctx *ctx, int32_t variant);
 /* Lanes per queued infeasible agent in the least-penetration kernel: 1 = one thread
  * per agent, 4 / 8 / 16 = a lane group per agent (projected lines one per lane, LP1 bounds
  * by an exact group scan), -1 = automatic (default; one thread per agent at every size since
- * the greedy LP3, chosen by measurement).  Same results bit for bit.
- * Errors: INVALID_ARGUMENT. */
+ * the greedy LP3, chosen by measurement).  Same results bit for bit.  Only
+ * strips whose LP3 is queued use it: where LP3 runs inside the step kernel (see
+ * orca_set_lp3_inline) this setting has no effect.  Errors: INVALID_ARGUMENT. */
 orca_status orca_set_lp3_lanes(orca_ctx *ctx, int32_t lanes);
+
+/* Where the least-penetration LP of infeasible agents runs: -1 = automatic (default:
+ * inside the thread-per-agent step kernel for strips that fit one wave of its blocks at the
+ * occupancy the extra shared memory allows -- computed at orca_create from the CUDA
+ * occupancy API for the context's k -- else queued for the k_lp3 kernel), 0 = always queued
+ * (k_lp3, honouring orca_set_lp3_lanes), 1 = always inside the step kernel.  The 8-lane group
+ * variant always queues.  Same results bit for bit.  Synchronises.  Errors: INVALID_ARGUMENT. */
+orca_status orca_set_lp3_inline(orca_ctx *ctx, int32_t mode);
 
 /* The context's cudaStream_t (as void*), e.g. for CUDA-event timing by the caller. */
 orca_status orca_get_stream(orca_ctx *ctx, void **stream);
@@ -314,8 +323,6 @@ orca_status orca_create_strips(const orca_params *params, int32_t device, int32_
 orca_status orca_partition_columns(const int64_t *colCount, int32_t nx, int32_t world,
                                    int32_t *bounds);
 
-/* Owned column ranges of the strips held by this context: bounds int32[2 * strips held]
- * = (c0, c1) pairs.  Errors: NOT_READY. */
 /* Re-partition the strips from the current state (agent-count quantiles of the columns
  * on the frozen grid) and re-size their buffers.  Done automatically before every chunk of
  * up to 64 steps when a strip could outgrow its capacities within the chunk (a crowd
@@ -338,14 +345,18 @@ orca_status orca_set_transport(orca_ctx *ctx, int32_t mode);
  * every rank when some pair of neighbouring GPUs cannot map each other's memory. */
 orca_status orca_get_transport(orca_ctx *ctx, int32_t *mode);
 
-/* The kernels one step launches for this context's first strip, as chosen for the loaded
- * agents: info[0] = step kernel variant (0, 1, 2 or 3), info[1] = lanes per
- * agent of the least-penetration kernel (0 = LP3 runs inside the step kernel, no k_lp3
- * launch), info[2] = CUDA kernels launched per step and strip (step kernel, k_lp3 unless
- * inline, k_scan, k_scatter, plus k_receive and one k_push per neighbour for strips with
- * the peer-memory exchange), info[3] = the transport.  Errors: INVALID_ARGUMENT, NOT_READY. */
+/* The kernels one step launches, as chosen for the loaded agents:
+ * info[0] = step kernel variant of the first strip (0, 1, 2 or 3), info[1] = lanes per
+ * agent of the first strip's least-penetration kernel (0 = LP3 runs inside the step kernel,
+ * no k_lp3 launch), info[2] = this library's CUDA kernels launched per step, summed over
+ * the strips this context holds (per strip: step kernel, k_lp3 unless inline, k_scan,
+ * k_scatter, plus k_receive and one k_push per neighbour with the peer-memory exchange;
+ * NCCL's own kernels under transport 1 are not counted), info[3] = the transport.
+ * Errors: INVALID_ARGUMENT, NOT_READY. */
 orca_status orca_get_launch_info(orca_ctx *ctx, int32_t info[4]);
 
+/* Owned column ranges of the strips held by this context: bounds int32[2 * strips held]
+ * = (c0, c1) pairs.  Errors: INVALID_ARGUMENT, NOT_READY. */
 orca_status orca_get_strips(orca_ctx *ctx, int32_t *bounds);
 
 #ifdef __cplusplus

@@ -95,7 +95,8 @@ def lib():
         L.or_solve.argtypes = [P(Line), ctypes.c_int, ctypes.c_double, f64p, f64p, f64p]
         L.or_solve.restype = ctypes.c_uint32
         L.or_step.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float, P(Agents),
-                              P(LpOrder), f32p, i32p, ctypes.c_int64, i64p, f64p, f64p, u8p, f64p, i32p, i32p]
+                              P(LpOrder), f32p, i32p, ctypes.c_int64, i64p, f64p, f64p, u8p, f64p, i32p, i32p,
+                              f64p, f64p]
         L.or_run.argtypes = [P(Params), ctypes.c_int64, f32p, f32p, f32p, f32p, ctypes.c_float, P(Agents),
                              P(LpOrder), ctypes.c_int32]
         L.or_lp_permutation.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, i32p]
@@ -246,7 +247,7 @@ def _agents(props):
 
 
 def step(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, origin=None, dims=None,
-         agents=None, want_nbrs=False, props=None, lp_seed=None, lp_step=0):
+         agents=None, want_nbrs=False, props=None, lp_seed=None, lp_step=0, vtest=None):
     """One synchronous step from the given fp32 state.  If origin/dims are None the grid is
     derived from `pos` (as at set_agents).  props: optional per-agent radius / maxSpeed /
     prefSpeed arrays.  lp_seed: None = nearest-first LP order, else the randomized
@@ -275,14 +276,19 @@ def step(params: Params, pos, vel, pref=None, goals=None, pref_speed=1.0, origin
     delta = np.zeros(m, np.float64)
     nbr = np.full((m, max(k, 1)), -1, np.int32) if want_nbrs else None
     cnt = np.zeros(m, np.int32) if want_nbrs else None
+    vt = None if vtest is None else np.ascontiguousarray(vtest, np.float64).reshape(m, 2)
+    dt = None if vtest is None else np.zeros(m, np.float64)
     rc = lib().or_step(ctypes.byref(params), n, _p(pos, ctypes.c_float), _p(vel, ctypes.c_float),
                        _p(pref, ctypes.c_float), _p(goals, ctypes.c_float), pref_speed, agp,
                        _order(lp_seed, lp_step), _p(origin, ctypes.c_float), _p(dims, ctypes.c_int32), m, _p(ag, ctypes.c_int64),
                        _p(vnew, ctypes.c_double), _p(pnew, ctypes.c_double), _p(flags, ctypes.c_uint8),
-                       _p(delta, ctypes.c_double), _p(nbr, ctypes.c_int32), _p(cnt, ctypes.c_int32))
+                       _p(delta, ctypes.c_double), _p(nbr, ctypes.c_int32), _p(cnt, ctypes.c_int32),
+                       _p(vt, ctypes.c_double), _p(dt, ctypes.c_double))
     if rc != 0:
         raise ValueError("or_step failed")
     out = dict(vel=vnew, pos=pnew, flags=flags, delta=delta, origin=origin, dims=dims)
+    if vtest is not None:
+        out["dtest"] = dt
     if want_nbrs:
         out["nbr"] = nbr[:, :k]
         out["cnt"] = cnt

@@ -474,7 +474,7 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, c
             const float *goals, float prefSpeed, const or_agents *ag, const or_lp_order *order,
             const float origin[2], const int32_t dims[2],
             int64_t m, const int64_t *agents, double *vnew, double *pnew, uint8_t *flags,
-            double *delta, int32_t *nbr, int32_t *cnt) {
+            double *delta, int32_t *nbr, int32_t *cnt, const double *vtest, double *dtest) {
     if (!params_ok(p) || n < 0 || (n > 0 && (!pos || !vel || (!pref && !goals)))) return -1;
     if (!agents) m = n;
     if (m < 0) return -1;
@@ -531,6 +531,8 @@ int or_step(const or_params *p, int64_t n, const float *pos, const float *vel, c
         }
         if (flags) flags[q] = (uint8_t)diag;
         if (delta) delta[q] = dl;
+        /* a candidate velocity (e.g. the product's) judged on this agent's own lines */
+        if (vtest && dtest) dtest[q] = or_penetration(L, c, vtest + 2 * q);
         if (nbr) {
             for (int32_t a = 0; a < k; ++a) nbr[q * k + a] = (a < c) ? nb[a] : -1;
         }
@@ -559,8 +561,7 @@ int64_t or_run(const or_params *p, int64_t n, float *pos, float *vel, const floa
             ord.step = order->step + s;
         }
         if (or_step(p, n, pos, vel, pref, goals, prefSpeed, ag, order ? &ord : NULL, origin, dims, 0, NULL, vn, pn,
-                    fl, NULL,
-                    NULL, NULL) != 0) {
+                    fl, NULL, NULL, NULL, NULL, NULL) != 0) {
             infeasible = -1;
             break;
         }

@@ -145,12 +145,15 @@ uint32_t or_solve(const or_line *lines, int n, double maxSpeed, const double pre
  * g = goal - pos (reading Q16); otherwise pref is used as given.
  * Outputs are indexed like `agents` (or by agent id when agents == NULL):
  *   vnew[2m], pnew[2m] (fp64), flags[m], delta[m] (max penetration at vnew),
- *   nbr[m*k] / cnt[m] (nullable).  Returns 0 or -1 on bad arguments. */
+ *   nbr[m*k] / cnt[m] (nullable).  vtest[2m] (nullable): velocities to judge -- dtest[q]
+ *   receives their maximum penetration into agent q's own half-planes (the parity tests'
+ *   infeasible-agent check).  Returns 0 or -1 on bad arguments. */
 int or_step(const or_params *p, int64_t n, const float *pos, const float *vel,
             const float *pref, const float *goals, float prefSpeed, const or_agents *ag,
             const or_lp_order *order, const float origin[2],
             const int32_t dims[2], int64_t m, const int64_t *agents, double *vnew,
-            double *pnew, uint8_t *flags, double *delta, int32_t *nbr, int32_t *cnt);
+            double *pnew, uint8_t *flags, double *delta, int32_t *nbr, int32_t *cnt,
+            const double *vtest, double *dtest);
 
 /* Runs nsteps full steps in place on fp32 state (state is fp32 between steps, as in the
  * product ABI): vel <- fl32(v'), pos <- fl32(p + dt*v').  The grid is derived once from

@@ -25,8 +25,21 @@ def nvcc() -> str:
     return "nvcc"
 
 
+STAMP = LIB + ".flags"  # the nvcc flags the library was built with (ORCA_NVCC_EXTRA sweeps)
+
+
+def _flags() -> str:
+    return " ".join(NVCC_FLAGS + os.environ.get("ORCA_NVCC_EXTRA", "").split())
+
+
 def stale() -> bool:
     if not os.path.exists(LIB):
+        return True
+    try:
+        with open(STAMP) as f:
+            if f.read() != _flags():
+                return True  # built with other flags (e.g. a sweep's -D overrides)
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(d) > t for d in DEPS if os.path.exists(d))
@@ -43,6 +56,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building liborca.so")
     if verbose:
         sys.stderr.write(r.stderr)
+    with open(STAMP, "w") as f:
+        f.write(_flags())
     return LIB
 
 

@@ -292,6 +292,8 @@ struct orca_ctx {
     int64_t lpStep0 = 0, lpMark = 0;  // step index t = lpStep0 + steps_total - lpMark
     int variant = -1;  // -1: auto (pick_variant)
     int lp3Lanes = -1;  // lanes per queued agent in the LP3 kernel (1 = thread, -1 = auto)
+    int lp3InlineMode = -1;  // orca_set_lp3_inline: -1 auto (strips up to inlineBelow agents), 0 queue, 1 inline
+    int64_t inlineBelow = 0;  // one wave of k_step blocks with the inline-LP3 shared memory (orca_create)
     // strip rebalance: by-id active flags, all-gather records, fill reports
     uint8_t* activeBuf = nullptr;
     int64_t activeCap = 0;
@@ -480,10 +482,16 @@ int pick_lp3_lanes(const orca_ctx* c, const Domain& d) {
 // on the thread-per-agent kernels: there the step is latency bound and the
 // separate k_lp3 launch is a serial tail; the group kernel always queues.
 #ifndef ORCA_AUTO_LP3_INLINE_BELOW
-#define ORCA_AUTO_LP3_INLINE_BELOW 125000  // ~ one wave of k_step blocks (148 SMs x 7 x 128); r01bk: 100k 0.058 -> 0.051, 125k 0.062 -> 0.056, 150k 0.067 -> 0.080 ms
+#define ORCA_AUTO_LP3_INLINE_BELOW 1000000000  // cap on top of the measured rule below (no cap)
+// The rule: inline while the strip fits ONE wave of k_step blocks at the occupancy the inline
+// shared memory allows (cudaOccupancyMaxActiveBlocksPerMultiprocessor x SMs x block size,
+// computed in orca_create for the context's k).  At k = 10: 7 blocks/SM -> 132,608 agents;
+// r01bk: 100k 0.058 -> 0.051, 125k 0.062 -> 0.056 ms inline, 150k 0.067 -> 0.080 (two waves).
 #endif
 bool pick_lp3_inline(const orca_ctx* c, const Domain& d) {
-    return pick_variant(c, d) != 1 && d.popBuild < ORCA_AUTO_LP3_INLINE_BELOW;
+    if (pick_variant(c, d) == 1) return false;  // the group kernel always queues
+    if (c->lp3InlineMode >= 0) return c->lp3InlineMode == 1;
+    return d.popBuild <= std::min<int64_t>(c->inlineBelow, ORCA_AUTO_LP3_INLINE_BELOW);
 }
 
 // Everything a captured step body depends on: the kernel arguments of every strip (device
@@ -765,6 +773,15 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
         e = cudaFuncSetAttribute(k_step_group<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->groupSmem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_step_group<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->groupSmem);
+    if (e == cudaSuccess) {
+        // inline-LP3 threshold: one wave of k_step blocks with the inline shared memory
+        const int k = params->maxNeighbors;
+        const size_t smemInl = (size_t)c->smemBytes + (size_t)std::max(0, 3 * k - ORCA_BUF_EXTRA) * 4 * kStepThreads;
+        int blocks = 0, sms = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step<false, 0, false>, kStepThreads, smemInl);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        c->inlineBelow = (int64_t)blocks * sms * kStepThreads;
+    }
     if (e != cudaSuccess) return cuda_fail(e, "orca_create");
     return ORCA_OK;
 }
@@ -2026,17 +2043,30 @@ orca_status orca_get_transport(orca_ctx* c, int32_t* mode) {
 orca_status orca_get_launch_info(orca_ctx* c, int32_t info[4]) {
     if (!c || !info) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
     if (!c->ready || c->doms.empty()) return fail(ORCA_ERR_NOT_READY, "set_agents first");
-    const Domain& d = c->doms[0];
-    const bool inl = pick_lp3_inline(c, d);
-    int n = inl ? 3 : 4;
-    if (d.g.hasL || d.g.hasR) {  // strips: k_receive, and k_push per neighbour (peer memory)
-        n += 1;
-        if (c->transport == 0) n += (d.g.hasL ? 1 : 0) + (d.g.hasR ? 1 : 0);
+    // summed over the context's strips (each strip launches its own chain; strips may differ in
+    // the inline-LP3 choice); NCCL's own kernels (transport 1) are not ours and not counted
+    int n = 0;
+    for (const Domain& d : c->doms) {
+        n += pick_lp3_inline(c, d) ? 3 : 4;
+        if (d.g.hasL || d.g.hasR) {  // strips: k_receive, and k_push per neighbour (peer memory)
+            n += 1;
+            if (c->transport == 0) n += (d.g.hasL ? 1 : 0) + (d.g.hasR ? 1 : 0);
+        }
     }
+    const Domain& d = c->doms[0];
     info[0] = pick_variant(c, d);
-    info[1] = inl ? 0 : pick_lp3_lanes(c, d);
+    info[1] = pick_lp3_inline(c, d) ? 0 : pick_lp3_lanes(c, d);
     info[2] = n;
     info[3] = c->transport;
+    return ORCA_OK;
+}
+
+orca_status orca_set_lp3_inline(orca_ctx* c, int32_t mode) {
+    if (!c || mode < -1 || mode > 1) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be -1 (auto), 0 or 1");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    drop_graph(c);
+    c->lp3InlineMode = mode;
     return ORCA_OK;
 }
 

@@ -27,7 +27,7 @@ EXPORTS = [
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
-    "orca_set_lp_order", "orca_set_lp3_lanes", "orca_rebalance", "orca_set_transport",
+    "orca_set_lp_order", "orca_set_lp3_lanes", "orca_set_lp3_inline", "orca_rebalance", "orca_set_transport",
     "orca_get_transport", "orca_set_state", "orca_set_state_async", "orca_get_state_async",
     "orca_io_wait", "orca_get_launch_info",
 ]
@@ -92,6 +92,7 @@ def _load():
         "orca_step_trace": [vp, i32, vp, vp],
         "orca_set_lp_order": [vp, i32, ctypes.c_uint64, i64],
         "orca_set_lp3_lanes": [vp, i32],
+        "orca_set_lp3_inline": [vp, i32],
         "orca_rebalance": [vp],
         "orca_set_transport": [vp, i32],
         "orca_get_transport": [vp, P(i32)],
@@ -359,6 +360,10 @@ class Orca:
         """Re-partition the strips from the current state (automatic when a strip nears its
         capacities; every rank must call it together)."""
         _check(_lib.orca_rebalance(self._ctx))
+
+    def set_lp3_inline(self, mode: int):
+        """-1 automatic, 0 always queue for k_lp3, 1 always inside the step kernel."""
+        _check(_lib.orca_set_lp3_inline(self._ctx, mode))
 
     def set_lp3_lanes(self, lanes: int):
         """Lanes per infeasible agent in the LP3 kernel: -1 (auto), 1 (thread), 4, 8 or 16; same results."""

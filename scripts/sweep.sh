@@ -17,3 +17,6 @@ except Exception as e:
 PY
   done
 done | tee $OUT/sweep.txt
+# leave the default build behind (build.py also rebuilds on a flags mismatch)
+python -c "from paper_1908_10107_b200 import build as B; B.build(force=True)" > /dev/null 2>&1
+

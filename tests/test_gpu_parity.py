@@ -15,6 +15,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
+import oracle_par
 import pins
 from paper_1908_10107_b200 import workloads as W
 
@@ -72,10 +73,11 @@ def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, variant=No
     assert np.array_equal(cx, ocx) and np.array_equal(cy, ocy)
     # one step (dry) on the GPU
     v, fl, nb, cnt = o.debug_step()
-    ref = oracle.step(op, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"),
-                      pref_speed=w.get("pref_speed", 1.0), agents=agents, want_nbrs=True,
-                      lp_seed=None if lp is None else lp[0], lp_step=0 if lp is None else lp[1])
     ids = np.arange(len(w["pos"])) if agents is None else np.asarray(agents)
+    ref = oracle_par.step(op, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"),
+                          pref_speed=w.get("pref_speed", 1.0), agents=agents, want_nbrs=True,
+                          lp_seed=None if lp is None else lp[0], lp_step=0 if lp is None else lp[1],
+                          vtest=v[ids].astype(np.float64))
     # neighbours (bit-exact)
     assert np.array_equal(cnt[ids], ref["cnt"])
     assert np.array_equal(nb[ids], ref["nbr"])
@@ -94,15 +96,9 @@ def compare_step(orca, oracle, w, agents=None, max_deg=None, lp=None, variant=No
     deg = (ref["flags"] & oracle.FLAG_DEGENERATE) != 0
     bad = (err > VTOL) & ~deg
     k = p["maxNeighbors"]
-    # infeasible: penetration of the GPU answer on the oracle's lines
+    # infeasible: penetration of the GPU answer on the oracle's own lines (every agent)
     inf = (ref["flags"] & oracle.FLAG_INFEASIBLE) != 0
-    worst_pen_gap = 0.0
-    for q in np.nonzero(inf)[0][:400]:
-        i = ids[q]
-        lines = [oracle.orca_line(w["pos"][i], w["vel"][i], w["pos"][j], w["vel"][j], i, j, p["radius"],
-                                  p["timeHorizon"], p["timeStep"])[0] for j in ref["nbr"][q][:ref["cnt"][q]]]
-        gap = pins.penetration_np(lines, gv[q]) - ref["delta"][q]
-        worst_pen_gap = max(worst_pen_gap, gap)
+    worst_pen_gap = float((ref["dtest"] - ref["delta"])[inf].max()) if inf.any() else 0.0
     speed = np.hypot(gv[:, 0], gv[:, 1])
     report = dict(n=len(ids), max_err=float(err[~deg].max()) if (~deg).any() else 0.0,
                   n_bad=int(bad.sum()), n_deg=int(deg.sum()), n_inf=int(inf.sum()),
@@ -200,7 +196,8 @@ def test_subcell_boundary_lattice(orca, oracle, ulp):
     pref = rng.uniform(-1, 1, pos.shape).astype(np.float32)
     w = dict(pos=pos, vel=np.zeros_like(pos), pref=pref, goals=None,
              params=dict(W.DEFAULT_PARAMS, neighborDist=cs, radius=0.2))
-    compare_step(orca, oracle, w, max_deg=len(pos))
+    rep = compare_step(orca, oracle, w)
+    print("subcell lattice", ulp, rep)
 
 
 def test_coincident_agents(orca, oracle):
@@ -295,16 +292,132 @@ def test_multistep_invariants_circle(orca):
     o.close()
 
 
-# ------------------------------------------------------- full sizes, sampled outputs
-@pytest.mark.parametrize("config", ["uniform", "uniform_1m", "dense"])
-def test_full_size_sampled(orca, oracle, config):
-    """BASELINE sizes in the bench's launch configuration; the oracle recomputes a random
-    sample of agents one by one on the full state."""
+# ------------------------------------------------------- full sizes, every agent
+def check_warm_state(o, oracle, p, pref=None, goals=None, pref_speed=1.0, props=None, label=""):
+    """The context's CURRENT state (after real GPU steps: the history search radius, the
+    bench's automatic kernel choice and launch configuration) against the oracle on that
+    same fp32 state and frozen grid, for EVERY active agent: cells and neighbour lists
+    bit-exact, velocities within 1e-4 outside the degenerate set, infeasible agents'
+    penetration on the oracle's lines, a real step equal to the dry step, positions.  Ids of
+    removed agents (NaN) are left out on both sides: the oracle steps the active crowd."""
+    pos, vel = o.get_state()
+    act = np.isfinite(pos[:, 0])
+    aid = np.nonzero(act)[0]
+    origin, cs, dims = o.grid()
+    origin32 = np.asarray(origin, np.float32)
+    op = oracle.make_params(**p)
+    cx, cy = o.debug_cells()
+    ocx, ocy = oracle.cells(pos[aid], origin32, op.neighborDist, np.asarray(dims, np.int32))
+    assert np.array_equal(cx[aid], ocx) and np.array_equal(cy[aid], ocy), label
+    v, fl, nb, cnt = o.debug_step()
+    sub = lambda a: None if a is None else np.ascontiguousarray(a[aid])
+    sprops = None if props is None else {k_: sub(v_) for k_, v_ in props.items()}
+    ref = oracle_par.step(op, pos[aid], vel[aid], pref=sub(pref), goals=sub(goals), pref_speed=pref_speed,
+                          origin=origin32, dims=np.asarray(dims, np.int32), want_nbrs=True, props=sprops,
+                          vtest=v[aid].astype(np.float64))
+    onb = np.where(ref["nbr"] >= 0, aid[np.maximum(ref["nbr"], 0)], -1)  # compacted -> global ids
+    assert np.array_equal(cnt[aid], ref["cnt"]), label
+    assert np.array_equal(nb[aid], onb), label
+    gv = v[aid].astype(np.float64)
+    err = np.max(np.abs(gv - ref["vel"]), axis=1)
+    deg = (ref["flags"] & oracle.FLAG_DEGENERATE) != 0
+    inf = (ref["flags"] & oracle.FLAG_INFEASIBLE) != 0
+    bad = (err > VTOL) & ~deg
+    gap = float((ref["dtest"] - ref["delta"])[inf].max()) if inf.any() else 0.0
+    vmax = np.float64(p["maxSpeed"]) if props is None else props["maxSpeed"][aid].astype(np.float64)
+    speed = np.hypot(gv[:, 0], gv[:, 1])
+    report = dict(label=label, n=len(aid), max_err=float(err[~deg].max()) if (~deg).any() else 0.0,
+                  n_bad=int(bad.sum()), excluded_degenerate=int(deg.sum()), n_inf=int(inf.sum()),
+                  gpu_inf=int(((fl[aid] & 1) != 0).sum()), worst_pen_gap=gap,
+                  g1=int(((ref["flags"] & oracle.FLAG_G1) != 0).sum()),
+                  g2=int(((ref["flags"] & oracle.FLAG_G2) != 0).sum()),
+                  g4=int(((ref["flags"] & oracle.FLAG_G4) != 0).sum()))
+    print("parity", report)
+    assert report["n_bad"] == 0, (report, aid[np.nonzero(bad)[0][:10]])
+    assert report["excluded_degenerate"] <= max(1, 0.001 * len(aid)), report
+    assert gap <= VTOL, report
+    assert np.all(speed <= vmax * (1 + 1e-6) + 1e-7), report
+    o.step(1)
+    pos1, vel1 = o.get_state()
+    still = np.isfinite(pos1[aid, 0])  # (removal after this step)
+    assert np.array_equal(vel1[aid][still], v[aid][still]), label
+    pexp = ref["pos"]
+    ptol = p["timeStep"] * VTOL + np.spacing(np.abs(pexp).max(axis=1).astype(np.float32)).astype(np.float64)
+    perr = np.max(np.abs(pos1[aid].astype(np.float64) - pexp), axis=1)
+    assert np.all((perr <= ptol + 1e-12) | deg | ~still), perr[still].max()
+    return report
+
+
+@pytest.mark.parametrize("config", ["uniform", "dense", "uniform_1m"])
+def test_full_size_every_agent(orca, oracle, config):
+    """BASELINE sizes (C2 100k, C3 500k, C2' 1M) in the bench's launch configuration (the
+    automatic kernel choice: inline LP3 at 100k, k_step + k_lp3 above), from a state warmed
+    by 20 real GPU steps (history search radius), every agent against the oracle."""
     w = W.make(config)
-    rng = np.random.default_rng(123)
-    ag = np.sort(rng.choice(len(w["pos"]), 1500, replace=False))
-    rep = compare_step(orca, oracle, w, agents=ag)
-    assert rep["n"] == 1500
+    o, p = _ctx(orca, w)
+    o.step(20)
+    rep = check_warm_state(o, oracle, p, pref=w["pref"], label=config)
+    assert rep["n"] == len(w["pos"])
+    o.close()
+
+
+def test_full_size_heterogeneous_goals_removal(orca, oracle):
+    """§8(f1)+(f2) at the C2 size: 100k agents with per-agent radius / maxSpeed / desired
+    speed, goal seeking and removal at the goal, after 20 GPU steps in which
+    agents have left; the oracle steps the remaining crowd, every agent compared."""
+    w = W.make("uniform")
+    n = len(w["pos"])
+    rng = np.random.default_rng(31)
+    goals = (w["pos"] + rng.uniform(-12, 12, w["pos"].shape)).astype(np.float32)
+    props = _het_props(n, seed=13)
+    o, p = _ctx(orca, dict(w, goals=goals, pref_speed=1.0))
+    o.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+    o.set_goal_removal(0.75)
+    o.step(20)
+    assert 0 < o.stats()["removed"] < n // 2
+    n_active = o.count()
+    rep = check_warm_state(o, oracle, p, pref=w["pref"], goals=goals, props=props, label="het+goals+removal 100k")
+    assert rep["n"] == n_active
+    o.close()
+
+
+def test_max_speed_zero(orca, oracle):
+    """maxSpeed = 0 (allowed by orca_create): the speed disc is a point, every agent's LP is
+    infeasible unless all its half-planes admit v = 0; both sides return v = 0 exactly and
+    nobody moves."""
+    w = W.make("uniform", n=3000, rho=0.3)
+    rep = compare_step(orca, oracle, w, maxSpeed=0.0)
+    o, p = _ctx(orca, w, maxSpeed=0.0)
+    o.step(3)
+    pos, vel = o.get_state()
+    assert np.all(vel == 0.0) and np.array_equal(pos, w["pos"])
+    o.close()
+    print("maxSpeed=0", rep)
+
+
+def test_c4_4m_eight_strips_bit_identical_and_oracle(orca, oracle):
+    """C4 (BASELINE configs[4]): 4M agents in 8 loopback strips (halo + migration through the
+    exchange buffers) equal one strip bit for bit over 72 steps; the final
+    state is then checked against the oracle for every agent."""
+    w = W.make("uniform_4m")
+    n = len(w["pos"])
+    a, p = _ctx(orca, w)
+    b = orca.Orca(p, strips=8)
+    b.set_agents(w["pos"], w["vel"], w["pref"])
+    for chunk in (1, 7, 64):
+        a.step(chunk)
+        b.step(chunk)
+        pa, va = a.get_state()
+        pb, vb = b.get_state()
+        assert np.array_equal(pa, pb) and np.array_equal(va, vb), chunk
+    assert b.count() == n
+    sa, sb = a.stats(), b.stats()
+    for key in ("infeasible", "degenerate", "collision_pairs"):
+        assert sa[key] == sb[key], key
+    b.close()
+    rep = check_warm_state(a, oracle, p, pref=w["pref"], label="C4 4M")
+    assert rep["n"] == n
+    a.close()
 
 
 def test_history_bound_path_consistent(orca):
@@ -678,13 +791,20 @@ def test_work_unit_lp_bit_identical_k_sweep(orca):
 def test_lp3_lanes_bit_identical(orca, config, n, k):
     """The least-penetration kernel with 1 (thread), 4, 8 or 16 lanes per agent: the same
     velocities, flags, work counters, trajectories and statistics bit for bit (k = 32 runs
-    LP1/projection chunks beyond one group width)."""
+    LP1/projection chunks beyond one group width).  These sizes would run LP3 inside the step
+    kernel, so the queued path is forced (orca_set_lp3_inline(0)) for the lane settings; the
+    last context keeps the automatic (inline) choice, which must agree as well."""
     w = W.make(config, n=n) if config == "dense" else W.make(config, n=n, rho=0.6)
     ctxs = []
     for lanes in (1, 4, 8, 16, -1):  # -1: automatic
         o, _ = _ctx(orca, w, maxNeighbors=k)
         o.set_lp3_lanes(lanes)
+        o.set_lp3_inline(0)
+        assert o.launch_info()["lp3_lanes"] == (1 if lanes == -1 else lanes)
         ctxs.append(o)
+    o, _ = _ctx(orca, w, maxNeighbors=k)
+    assert o.launch_info()["lp3_lanes"] == 0  # inline
+    ctxs.append(o)
     r = [o.debug_step() for o in ctxs]
     assert np.count_nonzero(r[0][1] & 1) > 0
     wk = [o.work() for o in ctxs]
