@@ -44,6 +44,19 @@ OPS = dict(stencil=5, lines=50, checks=15, lp1=15, proj=15)
 OPS_EXEC = dict(cand=5, lines=40, checks=4, lp1=8, proj=10)
 
 
+def source_sha() -> str:
+    """sha256 of the CUDA sources + C header: ties an ncu capture (profiles/traffic.json) to
+    the revision it measured (scripts/ncu_extract.py writes the same hash)."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_1908_10107_b200", "csrc")
+    for f in sorted(os.listdir(csrc)) + ["../../include/orca.h"]:
+        if f.endswith((".cu", ".cuh", ".h")):
+            with open(os.path.join(csrc, f), "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -52,10 +65,11 @@ def parse():
     ap.add_argument("--config", default="uniform_1m")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=6.0, help="single-thread oracle sample (cpu_baseline)")
+    ap.add_argument("--ref-seconds", type=float, default=150.0,
+                    help="--impl reference: time budget of the timed full oracle steps")
     ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--no-suite", action="store_true", help="skip the other BASELINE workloads (N=1 only)")
-    ap.add_argument("--no-multicore", action="store_true", help="skip the all-cores oracle baseline")
     ap.add_argument("--shared-gpu", action="store_true",
                     help="test only: all ranks on GPU 0 (gloo for torch, ORCA_NCCL_LIB=tests/fake_nccl for liborca)")
     ap.add_argument("--lp3-lanes", type=int, default=-1, help="lanes per infeasible agent in the LP3 kernel (-1: auto)")
@@ -159,70 +173,78 @@ def oracle_rate(w, seconds, rng_seed=0):
     return m / el, m, el
 
 
-_MC = {}
-
-
-def _mc_worker(chunk):
-    from oracle import oracle as O
-    w = _MC["w"]
-    p = O.make_params(**w["params"])
-    O.step(p, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"), pref_speed=w.get("pref_speed", 1.0),
-           agents=chunk)
-    return len(chunk)
-
-
-def oracle_rate_multicore(w, seconds, rate1):
-    """The same oracle on all host cores: P forked processes step disjoint parts of one agent
-    sample of the same state (each builds the bins of the full state, as a real multi-core
-    run would); wall-clock of the whole pool.  Returns (agents/s, sample, elapsed, P)."""
-    import multiprocessing as mp
-    try:
-        procs = len(os.sched_getaffinity(0))
-    except AttributeError:
-        procs = os.cpu_count() or 1
-    n = len(w["pos"])
-    m = int(min(n, max(2000, rate1 * seconds * procs * 0.7)))
-    rng = np.random.default_rng(12345)
-    sample = np.sort(rng.choice(n, m, replace=False))
-    chunks = np.array_split(sample, procs * 2)
-    _MC["w"] = w
-    ctx = mp.get_context("fork")
-    with ctx.Pool(procs) as pool:
-        pool.map(_mc_worker, chunks[:procs])  # warm the workers (imports, library load)
-        t0 = time.perf_counter()
-        done = sum(pool.map(_mc_worker, chunks))
-        el = time.perf_counter() - t0
-    return done / el, done, el, procs
-
-
 def run_reference(args):
+    """This tier's reference arm: the fp64 oracle (oracle/, unchanged) stepping the WHOLE
+    crowd of the bench workload, every step a full synchronous step of all agents, on all host
+    cores (forked workers on disjoint agent slices of the same pre-step state; oracle/par.py).
+    W warm-up and K timed steps as asked, unless K would not fit the time budget: then as many
+    full timed steps as fit (at least one), and `steps` reports what ran."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    from oracle import oracle as O, par
     w, rho = workload(args.config)
     n = len(w["pos"])
-    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        oracle_rate(w, per_step / 4)
-    rates, samples, els = [], [], []
-    for s in range(args.steps):
-        r, m, el = oracle_rate(w, per_step, rng_seed=s + 1)
-        rates.append(r)
-        samples.append(m)
-        els.append(el)
-    value = float(np.sum(samples) / np.sum(els))
+    p = O.make_params(**w["params"])
+    po = par.ParallelOracle(p, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"),
+                            pref_speed=w.get("pref_speed", 1.0))
+    warm = min(args.warmup, 1)
+    t_warm = po.step(warm) if warm else 0.0
+    per = t_warm / warm if warm else None
+    budget = args.ref_seconds
+    steps = args.steps if per is None else max(1, min(args.steps, int(budget / max(per, 1e-9))))
+    el = po.step(steps)
+    po.close()
+    value = n * steps / el
     line = {
         "impl": "reference", "metric": "agent-updates/s", "value": value, "unit": "agent-updates/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * n / value, "higher_is_better": True, "scaling": "strong",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "steps_requested": args.steps,
+        "warmup_requested": args.warmup,
+        "ms_per_step": 1000.0 * el / steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w["name"], "n_agents": n, "rho": rho, **w["params"]},
-        "cpu_baseline": {"value": value, "unit": "agent-updates/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{int(np.mean(samples))} random agents of the {n}-agent state per step "
-                                   f"(one step each, full-state bins), single thread"},
+        "cpu_baseline": {"value": value, "unit": "agent-updates/s", "cores": po.procs, "kind": "oracle",
+                         "cpu_model": par.cpu_model(),
+                         "sample": f"{steps} full synchronous steps of all {n} agents (after {warm} warm-up step), "
+                                   f"agents split over {po.procs} forked processes per step, {el:.1f} s"},
         "e2e": {"value": value, "unit": "agent-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def oracle_baselines(w, seconds):
+    """cpu_baseline of the bench line (rank 0, N = 1): the oracle as it stands on the host
+    cores -- one full step of the whole workload on all cores, and a single-thread sample of
+    the same state for the per-core rate -- plus the BASELINE's small configs run in full
+    (C0 circle 1000 steps, C1 corridor 600 steps)."""
+    from oracle import oracle as O, par
+    from paper_1908_10107_b200 import workloads as W
+    n = len(w["pos"])
+    p = O.make_params(**w["params"])
+    po = par.ParallelOracle(p, w["pos"], w["vel"], pref=w["pref"], goals=w.get("goals"),
+                            pref_speed=w.get("pref_speed", 1.0))
+    el = po.step(1)
+    po.close()
+    r1, m1, el1 = oracle_rate(w, seconds)
+    out = {"value": n / el, "unit": "agent-updates/s", "cores": po.procs, "kind": "oracle",
+           "cpu_model": par.cpu_model(),
+           "sample": f"one full synchronous step of all {n} agents of the initial state, agents split over "
+                     f"{po.procs} forked processes, {el:.1f} s",
+           "single_thread": {"value": r1, "cores": 1,
+                             "sample": f"{m1} random agents of the same state, one thread, {el1:.1f} s"}}
+    configs = {}
+    for name, steps in (("circle", 1000), ("corridor", 600)):
+        wc = W.make(name)
+        pc = O.make_params(**wc["params"])
+        poc = par.ParallelOracle(pc, wc["pos"], wc["vel"], pref=wc["pref"], goals=wc.get("goals"),
+                                 pref_speed=wc.get("pref_speed", 1.0), procs=1 if name == "circle" else None)
+        elc = poc.step(steps)
+        configs[wc["name"]] = {"n_agents": len(wc["pos"]), "steps": steps, "seconds": elc,
+                               "ms_per_frame": 1000.0 * elc / steps,
+                               "agent_updates_per_s": len(wc["pos"]) * steps / elc, "cores": poc.procs}
+        poc.close()
+    out["configs_full_runs"] = configs
+    return out
 
 
 def suite(orca, torch, peak_tops):
@@ -341,7 +363,9 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
-    assert world == args.gpus or world == 1, "launch N>1 with torchrun"
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     if args.shared_gpu:  # test mode: every rank on GPU 0, liborca's NCCL from ORCA_NCCL_LIB
         local = 0
     torch.cuda.set_device(local)
@@ -432,6 +456,11 @@ def run_ours(args):
             flush.zero_()
         stage += np.array(ctx.step_timed(1))
     stage /= args.steps
+    comm = None
+    if world > 1:  # liborca's communicator size and the exchange time, per rank
+        parts = [None] * world
+        dist.all_gather_object(parts, (ctx.comm_info()["comm_ranks"], float(stage[3])))
+        comm = {"comm_ranks": [q[0] for q in parts], "exchange_ms_per_rank": [q[1] for q in parts]}
     work1 = ctx.work()
     work = {k: 0.5 * (work0[k] + work1[k]) for k in work0}
     # kernel variant A/B (same results bit for bit): fused-step ms per step
@@ -462,10 +491,13 @@ def run_ours(args):
         order_ms[name] = acc / max(3, args.steps // 4)
     ctx.set_lp_order(0)
     ctx.set_variant(args.variant)
-    # LP3 kernel lanes per infeasible agent A/B (same results bit for bit)
+    # LP3 kernel lanes per infeasible agent A/B (same results bit for bit), on the queued path
+    # (orca_set_lp3_inline(0)); "inline" = LP3 inside k_step, the automatic choice below one
+    # wave of k_step blocks
     lp3_ms = {}
-    for lanes in (1, 4, 8, 16):
-        ctx.set_lp3_lanes(lanes)
+    for lanes in (1, 4, 8, 16, "inline"):
+        ctx.set_lp3_inline(1 if lanes == "inline" else 0)
+        ctx.set_lp3_lanes(1 if lanes == "inline" else lanes)
         ctx.step(2)
         acc = 0.0
         for s in range(max(3, args.steps // 4)):
@@ -474,6 +506,7 @@ def run_ours(args):
             acc += ctx.step_timed(1)[0]
         lp3_ms[str(lanes)] = acc / max(3, args.steps // 4)
     ctx.set_lp3_lanes(args.lp3_lanes)
+    ctx.set_lp3_inline(-1)
 
     # ---- e2e through the public API with pinned host buffers: every step uploads the
     # kinematic state (orca_set_state: H2D of pos + vel, re-binning), steps once and reads
@@ -570,31 +603,43 @@ def run_ours(args):
                       "once (pipelined: H2D of step s+1 and D2H of step s-1 overlap step s)",
                "synchronous": e2e_sync_line}
 
-    # ---- roofline of the dominant kernel (k_step): ALU bound
+    # ---- roofline of the dominant kernel (k_step): ALU bound.  peak = the FP32
+    # FFMA lane-op rate measured in this run by orca_probe_alu (at the clock it ran at)
     pk, pk_kind = peaks()
+    probe = orca.probe_alu(local)
     ops = sum(OPS[k] * work[k] for k in OPS)
     t_step = stage[0] / 1000.0
     achieved = ops / t_step / 1e12
-    peak = SMS * FP32_LANES_PER_SM * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    traffic, ncu = None, None
+    peak = probe["fp32_lane_ops_per_s"] / 1e12
+    nominal = SMS * FP32_LANES_PER_SM * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    traffic, ncu, traffic_note = None, None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             ent = json.load(open(tpath)).get(args.config, {})
-            traffic = ent.get("k_step_dram_bytes")
-            keep = ("issue_slots_busy_pct", "avg_active_threads_per_warp", "achieved_occupancy_pct",
-                    "fma_pipe_active_pct", "alu_pipe_active_pct", "fp64_pipe_active_pct", "report")
-            ncu = {k: v for k, v in ent.get("k_step_ncu", {}).items() if k in keep} or None
-        except Exception:
-            traffic, ncu = None, None
+            kn = ent.get("k_step_ncu", {})
+            if kn.get("source_sha") == source_sha():
+                traffic = ent.get("k_step_dram_bytes")
+                keep = ("issue_slots_busy_pct", "avg_active_threads_per_warp", "achieved_occupancy_pct",
+                        "fma_pipe_active_pct", "alu_pipe_active_pct", "fp64_pipe_active_pct", "warp_instructions",
+                        "duration_ns", "report", "source_sha")
+                ncu = {k: v for k, v in kn.items() if k in keep} or None
+            else:
+                traffic_note = "profiles/traffic.json was captured from another source revision: not used"
+        except Exception as e:  # noqa: BLE001
+            traffic_note = f"profiles/traffic.json unreadable: {e}"
     ops_exec = sum(OPS_EXEC[k] * work[k] for k in OPS_EXEC)
     roofline = {"bound": "alu", "kernel": "k_step(+k_lp3)", "achieved": achieved, "peak": peak, "unit": "Tlane-op/s",
-                "frac": achieved / peak, "traffic": traffic, "ncu": ncu,
+                "frac": achieved / peak, "frac_executed": ops_exec / t_step / 1e12 / peak,
+                "traffic": traffic, "traffic_note": traffic_note, "ncu": ncu,
                 "work_model": "SURVEY §8(d): 5 c_cand(3x3 bins) + 50 half-planes + 15 LP inner iterations per agent-step",
                 "executed": {"achieved": ops_exec / t_step / 1e12, "frac": ops_exec / t_step / 1e12 / peak,
                              "ops_per_launch": ops_exec,
                              "model": "5 candidates read + 40 half-planes + 4 checks + 8 LP1 it + 10 LP3 proj"},
-                "peak_source": f"148 SMs x 128 FP32 lanes x sm_max_mhz ({pk_kind} MEASURED_PEAKS.json)",
+                "peak_source": "measured in this run: orca_probe_alu FP32 FFMA lane-ops/s "
+                               f"(probe SM clock {probe['sm_mhz']:.0f} MHz, {probe['fp32_lanes_per_sm_clk']:.1f} "
+                               "FMA lanes/SM/clk)",
+                "peak_nominal": nominal, "probe": probe,
                 "ops_per_launch": ops, "work_per_launch": work,
                 "stage_ms": {"k_step+k_lp3": stage[0], "k_scan": stage[1], "k_scatter": stage[2],
                              "exchange": stage[3]}}
@@ -618,7 +663,7 @@ def run_ours(args):
         "gpu_launches": launch_info["kernels_per_step"] * args.steps, "launch_info": launch_info,
         "kernel_variant": args.variant, "k_step_ms_by_variant": variant_ms, "k_step_ms_by_lp_order": order_ms,
         "lp3_lanes": args.lp3_lanes, "k_step_ms_by_lp3_lanes": lp3_ms,
-        "roofline": roofline, "hbm_context": hbm,
+        "roofline": roofline, "hbm_context": hbm, "comm": comm,
         "stats": st,
     }
     line["e2e"] = e2e
@@ -626,16 +671,7 @@ def run_ours(args):
         c = clk.summary()
         line["clocks"] = c
         if world == 1 and not args.no_cpu_baseline:
-            r, m, el = oracle_rate(w, args.cpu_seconds)
-            line["cpu_baseline"] = {"value": r, "unit": "agent-updates/s", "cores": 1, "kind": "oracle",
-                                    "sample": f"{m} random agents of the initial {n_total}-agent state, one step, "
-                                              f"single thread, {el:.1f} s"}
-            if not args.no_multicore:
-                rm, mm, elm, procs = oracle_rate_multicore(w, args.cpu_seconds / 2, r)
-                line["cpu_baseline_multicore"] = {
-                    "value": rm, "unit": "agent-updates/s", "cores": procs, "kind": "oracle x P processes",
-                    "sample": f"{mm} random agents of the initial {n_total}-agent state split over {procs} forked "
-                              f"processes (each bins the full state), one step, {elm:.1f} s wall"}
+            line["cpu_baseline"] = oracle_baselines(w, args.cpu_seconds)
     ctx.close()
     if rank == 0:
         if world == 1 and not args.no_suite:
@@ -645,8 +681,20 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def relaunch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: start the N ranks itself (one
+    process per GPU, torch.distributed.run on 127.0.0.1) with the same arguments."""
+    import secrets
+    port = os.environ.get("MASTER_PORT") or str(29500 + secrets.randbelow(2000))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", port, os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

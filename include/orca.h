@@ -332,12 +332,14 @@ orca_status orca_partition_columns(const int64_t *colCount, int32_t nx, int32_t 
  * contexts: no-op.  Synchronises.  Errors: NOT_READY, CUDA, NCCL, CAPACITY. */
 orca_status orca_rebalance(orca_ctx *ctx);
 
-/* Transport of the per-step strip exchange: 0 (default) = peer memory -- a
+/* Transport of the per-step strip exchange: 0 = peer memory (default of
+ * in-process loopback strips) -- a
  * k_push kernel stores exactly the used halo/migration records into the neighbour's receive
  * buffer (cudaIpc mapping over NVLink between ranks; the neighbour strip's buffer in
  * loopback) and raises an arrival flag the neighbour's k_receive waits on (bounded: a
  * missing neighbour step is an error, never a hang); 1 = NCCL send/recv of the whole
- * buffers (loopback: device copies), the baseline.  Multi-rank contexts: every rank must
+ * buffers (loopback: device copies; the default of orca_create_dist until an NVLink
+ * measurement shows the peer-memory path faster).  Multi-rank contexts: every rank must
  * call it together.  Synchronises.  Errors: INVALID_ARGUMENT, CUDA, NCCL. */
 orca_status orca_set_transport(orca_ctx *ctx, int32_t mode);
 
@@ -358,6 +360,20 @@ orca_status orca_get_launch_info(orca_ctx *ctx, int32_t info[4]);
 /* Owned column ranges of the strips held by this context: bounds int32[2 * strips held]
  * = (c0, c1) pairs.  Errors: INVALID_ARGUMENT, NOT_READY. */
 orca_status orca_get_strips(orca_ctx *ctx, int32_t *bounds);
+
+/* The context's ranks: info[0] = world, info[1] = rank, info[2] = the rank count of
+ * liborca's own NCCL communicator as NCCL reports it (ncclCommCount; -1 if the library
+ * lacks the call; 1 for single-rank contexts).  Errors: INVALID_ARGUMENT. */
+orca_status orca_get_comm_info(orca_ctx *ctx, int32_t info[3]);
+
+/* Measured ALU denominators of the roofline (SURVEY §8(d) "confirm with an
+ * FFMA microbenchmark at the run's clock"): on `device`, 8 independent FMA chains per
+ * thread, 2048 threads per SM; out[0] = FP32 FFMA lane-ops/s, out[1] = FP64 DFMA lane-ops/s,
+ * out[2] = the SM clock (MHz) the FP32 probe ran at (clock64 over its duration), out[3] =
+ * FP32 FMA lanes per SM per clock implied by out[0] and out[2] (128 on B200).  Best of two
+ * ~1 ms launches each; synchronises the device.  Not part of the step.
+ * Errors: INVALID_ARGUMENT, CUDA. */
+orca_status orca_probe_alu(int32_t device, double out[4]);
 
 #ifdef __cplusplus
 }

@@ -110,15 +110,22 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*errStr)(ncclResult_t) = nullptr;
+    ncclResult_t (*commCount)(ncclComm_t, int*) = nullptr;  // optional
 };
 
 NcclApi& nccl() {
     static NcclApi api;
     if (api.tried) return api;
     api.tried = true;
-    // ORCA_NCCL_LIB: an alternative implementation of the same API (the tests' host-staged
-    // stand-in, tests/fake_nccl, lets several processes share one GPU)
+#ifdef ORCA_TEST_HOOKS
+    // TEST BUILD ONLY (liborca_test.so, build.py test_hooks=True): ORCA_NCCL_LIB names an
+    // alternative implementation of the same API -- the tests' host-staged stand-in
+    // tests/fake_nccl, which lets several processes share one GPU.  The product liborca.so
+    // always uses the process's libnccl.so.2.
     const char* alt = getenv("ORCA_NCCL_LIB");
+#else
+    const char* alt = nullptr;
+#endif
     void* h = (alt && *alt) ? dlopen(alt, RTLD_NOW | RTLD_LOCAL) : dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
     if (!h && !(alt && *alt)) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
@@ -143,6 +150,7 @@ NcclApi& nccl() {
     api.allGather = (decltype(api.allGather))sym("ncclAllGather");
     api.errStr = (decltype(api.errStr))sym("ncclGetErrorString");
     api.ok = ok;
+    api.commCount = (decltype(api.commCount))dlsym(h, "ncclCommCount");
     if (!ok) api.err = "libnccl.so.2 lacks a required symbol";
     return api;
 }
@@ -302,7 +310,9 @@ struct orca_ctx {
     int* report = nullptr;
     int reportCap = 0;
     int64_t rebalances = 0;
-    int transport = 0;  // 0: peer memory (k_push / cudaIpc), 1: NCCL send/recv (loopback: copies)
+    int transport = 0;  // 0: peer memory (k_push / cudaIpc), 1: NCCL send/recv (loopback: copies);
+                        // orca_create_dist defaults to 1, loopback strips to 0
+    int commRanks = 1;  // ranks in the NCCL communicator (ncclCommCount; -1 unknown)
     // set (host-mapped, no synchronisation) when an agent enters the grid's outer cell ring:
     // the grid is re-derived before the next chunk of steps (reading Q12)
     int* gridFlagHost = nullptr;
@@ -603,10 +613,13 @@ cudaError_t enqueue_scan(orca_ctx* c, Domain& d, bool zero) {
     return cudaGetLastError();
 }
 
-cudaError_t enqueue_scatter(orca_ctx* c, Domain& d, int bump) {
+// props: move the per-agent properties too (false right after k_select, which does not
+// write them: refresh_props then gathers them by id into the new sorted order)
+cudaError_t enqueue_scatter(orca_ctx* c, Domain& d, int bump, bool props = true) {
     launch_k(c, k_scatter, dim3(cap_blocks(d.capW, 256)), dim3(256), 0, d.ctr, bump, d.cellW, d.rankW, d.binStart,
              d.posW, d.velW, d.auxW, d.idW, d.rk2W, d.posS, d.velS, d.auxS, d.idS, d.rk2S, d.capW,
-             c->het ? d.propW : nullptr, c->het ? d.propS : nullptr, d.scanStatus, scan_tiles(d.nbins) + 2);
+             (c->het && props) ? d.propW : nullptr, (c->het && props) ? d.propS : nullptr, d.scanStatus,
+             scan_tiles(d.nbins) + 2);
     return cudaGetLastError();
 }
 
@@ -1016,7 +1029,7 @@ orca_status build_domains(orca_ctx* c, int64_t n, const float2* sp, const float2
                                                                 d.capW, hist, active);
         CK(cudaGetLastError());
         CK(enqueue_scan(c, d, true));
-        CK(enqueue_scatter(c, d, 0));
+        CK(enqueue_scatter(c, d, 0, false));
     }
     CK(cudaStreamSynchronize(c->stream));
     CKS(check_overflow(c));
@@ -1221,6 +1234,34 @@ orca_status io_init(orca_ctx* c) {
 }  // namespace
 
 // =============================================================================== ABI
+
+// ------------------------------------------------------------------ ALU peak probe
+// Measured denominators of the ALU roofline: kProbeChains independent FMA
+// chains per thread (enough ILP to cover the FMA latency), 2048 threads per SM.  Block 0's
+// thread 0 brackets its run with clock64() so the caller also gets the SM clock the probe ran
+// at.  The results are written so the compiler cannot drop the chains.
+constexpr int kProbeChains = 8;
+template <typename T>
+__global__ void __launch_bounds__(256) k_probe_fma(T* out, int iters, T a, T b, long long* cyc) {
+    long long c0 = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) c0 = clock64();
+    T x[kProbeChains];
+#pragma unroll
+    for (int q = 0; q < kProbeChains; ++q) x[q] = (T)(threadIdx.x + q);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+#pragma unroll
+            for (int q = 0; q < kProbeChains; ++q) x[q] = x[q] * a + b;
+        }
+    }
+    T acc = 0;
+#pragma unroll
+    for (int q = 0; q < kProbeChains; ++q) acc += x[q];
+    if (acc == (T)-1.2345) out[blockIdx.x] = acc;  // practically never; keeps the chains live
+    if (blockIdx.x == 0 && threadIdx.x == 0) cyc[0] = clock64() - c0;
+}
+
 extern "C" {
 
 const char* orca_status_string(orca_status s) {
@@ -1327,6 +1368,15 @@ orca_status orca_create_dist(const orca_params* params, int32_t device, int32_t 
     }
     c->world = world;
     c->rank = rank;
+    // NCCL send/recv is the default exchange between ranks: the fused
+    // peer-memory transport (orca_set_transport(0)) is selectable, but no NVLink measurement
+    // has shown it faster yet
+    c->transport = 1;
+    c->commRanks = -1;
+    if (N.commCount) {
+        int cnt = -1;
+        if (N.commCount(c->comm, &cnt) == ncclSuccess) c->commRanks = cnt;
+    }
     c->doms.resize(1);
     *out = c;
     return ORCA_OK;
@@ -2061,6 +2111,14 @@ orca_status orca_get_launch_info(orca_ctx* c, int32_t info[4]) {
     return ORCA_OK;
 }
 
+orca_status orca_get_comm_info(orca_ctx* c, int32_t info[3]) {
+    if (!c || !info) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
+    info[0] = c->world;
+    info[1] = c->rank;
+    info[2] = c->world > 1 ? c->commRanks : 1;
+    return ORCA_OK;
+}
+
 orca_status orca_set_lp3_inline(orca_ctx* c, int32_t mode) {
     if (!c || mode < -1 || mode > 1) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be -1 (auto), 0 or 1");
     CK(cudaSetDevice(c->device));
@@ -2138,6 +2196,58 @@ orca_status orca_set_variant(orca_ctx* c, int32_t variant) {
 orca_status orca_get_stream(orca_ctx* c, void** stream) {
     if (!c || !stream) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
     *stream = (void*)c->stream;
+    return ORCA_OK;
+}
+
+orca_status orca_probe_alu(int32_t device, double out[4]) {
+    if (!out) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(ORCA_ERR_INVALID_ARGUMENT, "no such CUDA device");
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const int blocks = sms * 8, threads = 256;
+    void* buf = nullptr;
+    long long* cyc = nullptr;
+    CK(cudaMalloc(&buf, (size_t)blocks * sizeof(double)));
+    CK(cudaMalloc(&cyc, sizeof(long long)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double best32 = 0.0, best64 = 0.0, mhz = 0.0;
+    for (int pass = 0; pass < 4; ++pass) {
+        const bool f64 = pass & 1;
+        const int iters = f64 ? 256 : 1024;
+        CK(cudaEventRecord(e0, 0));
+        if (f64)
+            k_probe_fma<double><<<blocks, threads>>>((double*)buf, iters, 0.999999, 1e-7, cyc);
+        else
+            k_probe_fma<float><<<blocks, threads>>>((float*)buf, iters, 0.999999f, 1e-7f, cyc);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(e1, 0));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        const double ops = (double)blocks * threads * iters * 16.0 * kProbeChains;  // FMA lane-ops
+        const double rate = ops / (ms * 1e-3);
+        if (f64) {
+            best64 = std::max(best64, rate);
+        } else if (rate > best32) {
+            best32 = rate;
+            long long c = 0;
+            CK(cudaMemcpy(&c, cyc, sizeof c, cudaMemcpyDeviceToHost));
+            mhz = (double)c / (ms * 1e-3) / 1e6;  // block 0 spans ~the whole launch
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    cudaFree(cyc);
+    out[0] = best32;
+    out[1] = best64;
+    out[2] = mhz;
+    out[3] = (mhz > 0.0) ? best32 / (mhz * 1e6 * sms) : 0.0;  // FP32 FMA lanes per SM per clock
     return ORCA_OK;
 }
 

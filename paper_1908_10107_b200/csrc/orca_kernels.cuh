@@ -804,6 +804,7 @@ __device__ __forceinline__ int lp2_wu(const Lines& L, int T, int n, int kmax, fl
         const int myRank = __popc(V & ((1u << lane) - 1u));  // owners: rank among V
         __shared__ unsigned char wuOwner[1024];                // problem rank -> owner lane
         const int wb = threadIdx.x & ~31;
+        __syncwarp(mask);  // every lane's reads of the previous line's owners are done (racecheck)
         if (need) wuOwner[wb + myRank] = (unsigned char)lane;
         __syncwarp(mask);
         const int seg = lane / S, j = lane - seg * S;

@@ -14,6 +14,9 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "liborca.so")
+# tests only: ORCA_LIB selects another build of this same library -- liborca_test.so, built
+# with -DORCA_TEST_HOOKS so the multi-process tests can swap in their NCCL stand-in
+LIB_PATH = os.environ.get("ORCA_LIB") or LIB_PATH
 
 ORCA_MAX_K = 32
 STATUS = {0: "ok", 1: "invalid argument", 2: "not ready", 3: "out of memory", 4: "CUDA error",
@@ -29,7 +32,7 @@ EXPORTS = [
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
     "orca_set_lp_order", "orca_set_lp3_lanes", "orca_set_lp3_inline", "orca_rebalance", "orca_set_transport",
     "orca_get_transport", "orca_set_state", "orca_set_state_async", "orca_get_state_async",
-    "orca_io_wait", "orca_get_launch_info",
+    "orca_io_wait", "orca_get_launch_info", "orca_probe_alu", "orca_get_comm_info",
 ]
 
 
@@ -101,6 +104,8 @@ def _load():
         "orca_get_state_async": [vp, vp, vp],
         "orca_io_wait": [vp],
         "orca_get_launch_info": [vp, P(i32)],
+        "orca_probe_alu": [i32, P(ctypes.c_double)],
+        "orca_get_comm_info": [vp, P(i32)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -170,6 +175,13 @@ def partition_columns(col_count, world: int):
     _check(_lib.orca_partition_columns(cc.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(cc), world,
                                        b.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
     return b
+
+
+def probe_alu(device: int = 0) -> dict:
+    """orca_probe_alu: measured FP32 / FP64 FMA lane-op rates and the SM clock they ran at."""
+    out = (ctypes.c_double * 4)()
+    _check(_lib.orca_probe_alu(device, out))
+    return dict(fp32_lane_ops_per_s=out[0], fp64_lane_ops_per_s=out[1], sm_mhz=out[2], fp32_lanes_per_sm_clk=out[3])
 
 
 def nccl_unique_id() -> bytes:
@@ -355,6 +367,12 @@ class Orca:
         out = (ctypes.c_int32 * 4)()
         _check(_lib.orca_get_launch_info(self._ctx, out))
         return dict(variant=out[0], lp3_lanes=out[1], kernels_per_step=out[2], transport=out[3])
+
+    def comm_info(self) -> dict:
+        """orca_get_comm_info: world, rank and the rank count of liborca's NCCL communicator."""
+        out = (ctypes.c_int32 * 3)()
+        _check(_lib.orca_get_comm_info(self._ctx, out))
+        return dict(world=out[0], rank=out[1], comm_ranks=out[2])
 
     def rebalance(self):
         """Re-partition the strips from the current state (automatic when a strip nears its

@@ -60,7 +60,9 @@ def main():
     ent = data.setdefault(workload, {})
     if "dram_read_bytes" in got and "dram_write_bytes" in got:
         ent[f"{prefix}_dram_bytes"] = got["dram_read_bytes"] + got["dram_write_bytes"]
-    ent[f"{prefix}_ncu"] = dict(got, report=os.path.basename(rep))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import source_sha  # the revision this capture measured (bench.py checks it)
+    ent[f"{prefix}_ncu"] = dict(got, report=os.path.basename(rep), source_sha=source_sha())
     json.dump(data, open(path, "w"), indent=1, sort_keys=True)
     print(json.dumps({workload: ent}, indent=1))
 

@@ -77,3 +77,13 @@ def test_no_cpu_fallback_without_library(tmp_path, monkeypatch):
     mod = importlib.util.module_from_spec(spec)
     with pytest.raises(ImportError):
         spec.loader.exec_module(mod)
+
+
+def test_nccl_test_seam_only_in_test_build(orca):
+    """The fake-NCCL hook (ORCA_NCCL_LIB) exists only in liborca_test.so (-DORCA_TEST_HOOKS);
+    the product library never loads another NCCL."""
+    from paper_1908_10107_b200 import build
+    test_lib = build.build(test_hooks=True)
+    prod = open(os.path.join(ROOT, "paper_1908_10107_b200", "liborca.so"), "rb").read()
+    assert b"ORCA_NCCL_LIB" not in prod
+    assert b"ORCA_NCCL_LIB" in open(test_lib, "rb").read()

@@ -20,6 +20,13 @@ FAKE_DIR = os.path.join(HERE, "fake_nccl")
 FAKE_LIB = os.path.join(FAKE_DIR, "libfakenccl.so")
 
 
+def _test_lib():
+    """liborca_test.so: the product sources built with -DORCA_TEST_HOOKS, the only build that
+    honours ORCA_NCCL_LIB (the product liborca.so never loads another NCCL)."""
+    from paper_1908_10107_b200 import build
+    return build.build(test_hooks=True)
+
+
 def _build_fake():
     src = os.path.join(FAKE_DIR, "fake_nccl.cu")
     if os.path.exists(FAKE_LIB) and os.path.getmtime(FAKE_LIB) >= os.path.getmtime(src):
@@ -48,7 +55,7 @@ def test_multirank_strips_bit_identical(orca, tmp_path, world, scenario, transpo
     1: ncclSend/ncclRecv of the whole buffers (through the stand-in)."""
     lib = _build_fake()
     uid = "/orca_fake_" + secrets.token_hex(8)
-    env = dict(os.environ, ORCA_NCCL_LIB=lib, ORCA_TEST_TRANSPORT=str(transport))
+    env = dict(os.environ, ORCA_NCCL_LIB=lib, ORCA_LIB=_test_lib(), ORCA_TEST_TRANSPORT=str(transport))
     procs, outs = [], []
     for r in range(world):
         out = str(tmp_path / f"rank{r}.npz")
@@ -99,7 +106,7 @@ def test_bench_multirank_shared_gpu(orca, tmp_path):
     one GPU through the fake NCCL: one valid JSON line from rank 0."""
     import json
     lib = _build_fake()
-    env = dict(os.environ, ORCA_NCCL_LIB=lib)
+    env = dict(os.environ, ORCA_NCCL_LIB=lib, ORCA_LIB=_test_lib())
     root = os.path.dirname(HERE)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(29600 + secrets.randbelow(300)), os.path.join(root, "bench.py"),
@@ -111,5 +118,28 @@ def test_bench_multirank_shared_gpu(orca, tmp_path):
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "strips2"
-    assert d["config"]["exchange"] == "peer-memory"
+    assert d["config"]["exchange"] == "nccl"  # the multi-rank default
+    assert d["comm"]["comm_ranks"] == [2, 2]  # every rank's liborca communicator holds 2 ranks
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["roofline"]["frac"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_self_launch_shared_gpu(orca):
+    """`python bench.py --gpus 2` WITHOUT torchrun starts its two ranks itself and reports
+    n_gpus 2; a rank count that disagrees with --gpus exits non-zero."""
+    import json
+    lib = _build_fake()
+    env = dict(os.environ, ORCA_NCCL_LIB=lib, ORCA_LIB=_test_lib())
+    env.pop("WORLD_SIZE", None)
+    root = os.path.dirname(HERE)
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+           "--config", "uniform", "--e2e-steps", "1", "--shared-gpu"]
+    r = subprocess.run(cmd, env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "strips2"
+    bad = subprocess.run(cmd, env=dict(env, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"), cwd=root,
+                         capture_output=True, text=True, timeout=300)
+    assert bad.returncode != 0

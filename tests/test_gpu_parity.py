@@ -803,7 +803,8 @@ def test_lp3_lanes_bit_identical(orca, config, n, k):
         assert o.launch_info()["lp3_lanes"] == (1 if lanes == -1 else lanes)
         ctxs.append(o)
     o, _ = _ctx(orca, w, maxNeighbors=k)
-    assert o.launch_info()["lp3_lanes"] == 0  # inline
+    li = o.launch_info()
+    assert li["lp3_lanes"] == (1 if li["variant"] == 1 else 0)  # inline unless the group variant
     ctxs.append(o)
     r = [o.debug_step() for o in ctxs]
     assert np.count_nonzero(r[0][1] & 1) > 0
