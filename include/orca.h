@@ -270,11 +270,15 @@ orca_status orca_set_variant(orca_ctx *ctx, int32_t variant);
 orca_status orca_set_lp3_lanes(orca_ctx *ctx, int32_t lanes);
 
 /* Where the least-penetration LP of infeasible agents runs: -1 = automatic (default:
- * inside the thread-per-agent step kernel for strips that fit one wave of its blocks at the
- * occupancy the extra shared memory allows -- computed at orca_create from the CUDA
- * occupancy API for the context's k -- else queued for the k_lp3 kernel), 0 = always queued
- * (k_lp3, honouring orca_set_lp3_lanes), 1 = always inside the step kernel.  The 8-lane group
- * variant always queues.  Same results bit for bit.  Synchronises.  Errors: INVALID_ARGUMENT. */
+ * inside the thread-per-agent step kernel on the block's queue (mode 2) for strips that fit
+ * one wave of its blocks at the occupancy its shared memory allows -- computed at
+ * orca_create from the CUDA occupancy API for the context's k -- else queued for the k_lp3
+ * kernel; measured), 0 = always queued
+ * (k_lp3, honouring orca_set_lp3_lanes), 1 = always inside the step kernel, each thread on
+ * its own agent, 2 = inside the step kernel on the block's compacted queue (after a block
+ * barrier, the block's infeasible agents are solved by its first threads, their projected
+ * half-planes in the shared-memory columns of finished agents).  The 8-lane group variant
+ * always queues.  Same results bit for bit.  Synchronises.  Errors: INVALID_ARGUMENT. */
 orca_status orca_set_lp3_inline(orca_ctx *ctx, int32_t mode);
 
 /* The context's cudaStream_t (as void*), e.g. for CUDA-event timing by the caller. */

@@ -365,7 +365,7 @@ Model make_model(const orca_ctx* c) {
     return m;
 }
 
-bool pick_lp3_inline(const orca_ctx* c, const Domain& d);
+int pick_lp3_mode(const orca_ctx* c, const Domain& d);
 
 StepArgs make_args(orca_ctx* c, Domain& d) {
     StepArgs a{};
@@ -395,7 +395,7 @@ StepArgs make_args(orca_ctx* c, Domain& d) {
     a.qEntry = d.qEntry;
     a.qLines = d.qLines;
     a.qcap = d.capW;
-    a.lp3Inline = pick_lp3_inline(c, d) ? 1 : 0;
+    a.lp3Inline = pick_lp3_mode(c, d);
     a.gridFlag = c->gridFlagDev;
     a.qCount = reinterpret_cast<unsigned int*>(d.scanStatus + scan_tiles(d.nbins) + 1);
     return a;
@@ -488,21 +488,27 @@ int pick_lp3_lanes(const orca_ctx* c, const Domain& d) {
     return (d.popBuild < ORCA_AUTO_LP3_GROUP_BELOW) ? 8 : 1;
 }
 
-// LP3 inside k_step (StepArgs::lp3Inline) for strips below ORCA_AUTO_LP3_INLINE_BELOW agents
-// on the thread-per-agent kernels: there the step is latency bound and the
-// separate k_lp3 launch is a serial tail; the group kernel always queues.
+// LP3 inside k_step (StepArgs::lp3Inline) for small strips on the thread-per-agent kernels
+// (DESIGN.md §12): there the step is latency bound and the separate k_lp3 launch is a serial
+// tail; the group kernel always queues.
 #ifndef ORCA_AUTO_LP3_INLINE_BELOW
 #define ORCA_AUTO_LP3_INLINE_BELOW 1000000000  // cap on top of the measured rule below (no cap)
-// The rule: inline while the strip fits ONE wave of k_step blocks at the occupancy the inline
-// shared memory allows (cudaOccupancyMaxActiveBlocksPerMultiprocessor x SMs x block size,
-// computed in orca_create for the context's k).  At k = 10: 7 blocks/SM -> 132,608 agents;
-// r01bk: 100k 0.058 -> 0.051, 125k 0.062 -> 0.056 ms inline, 150k 0.067 -> 0.080 (two waves).
+// The rule (r02h): LP3 on the block-local queue inside k_step (mode 2) while the strip fits ONE
+// wave of k_step blocks at the occupancy its shared memory allows (cudaOccupancyMax-
+// ActiveBlocksPerMultiprocessor x SMs x block size, computed in orca_create for the context's
+// k; 8 blocks/SM -> 151,552 agents at k = 10), else the k_lp3 kernel (mode 0).  Measured at
+// k = 10 (scripts/lp3_modes_probe.py, ms/step for modes 0 / 1 / 2): 100k 0.0676 / 0.0778 /
+// 0.0595, dense 500k 0.193 / 0.231 / 0.203, 1M 0.309 / 0.410 / 0.338 -- beyond one wave the
+// block barrier leaves one busy warp per block during its LP3 phase, while k_lp3 runs full warps.
 #endif
-bool pick_lp3_inline(const orca_ctx* c, const Domain& d) {
-    if (pick_variant(c, d) == 1) return false;  // the group kernel always queues
-    if (c->lp3InlineMode >= 0) return c->lp3InlineMode == 1;
-    return d.popBuild <= std::min<int64_t>(c->inlineBelow, ORCA_AUTO_LP3_INLINE_BELOW);
+// 0: queued for k_lp3, 1: inside k_step per thread, 2: inside k_step on the block's
+// compacted queue (orca_set_lp3_inline)
+int pick_lp3_mode(const orca_ctx* c, const Domain& d) {
+    if (pick_variant(c, d) == 1) return 0;  // the group kernel always queues
+    if (c->lp3InlineMode >= 0) return c->lp3InlineMode;
+    return d.popBuild <= std::min<int64_t>(c->inlineBelow, ORCA_AUTO_LP3_INLINE_BELOW) ? 2 : 0;
 }
+bool pick_lp3_inline(const orca_ctx* c, const Domain& d) { return pick_lp3_mode(c, d) != 0; }
 
 // Everything a captured step body depends on: the kernel arguments of every strip (device
 // pointers, grid, model), launch sizes, the exchange buffers and the kernel selection.  A
@@ -583,10 +589,12 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
     const int k = c->p.maxNeighbors;
     const int variant = pick_variant(c, d);
-    // inline LP3 needs the projected half-planes (3k words per thread after s, partly in the
-    // free tail of the candidate buffer): max(0, 3k - ORCA_BUF_EXTRA) more words per thread
+    // per-thread inline LP3 (mode 1) needs the projected half-planes: 3k more words per thread
+    // after the columns; the block queue (mode 2) only its small scratch area
     const size_t smem = (size_t)c->smemBytes +
-                        (a.lp3Inline ? (size_t)std::max(0, 3 * k - ORCA_BUF_EXTRA) * 4 * kStepThreads : 0);
+                        (a.lp3Inline == 1   ? (size_t)3 * k * 4 * kStepThreads
+                         : a.lp3Inline == 2 ? (size_t)step_lp3q_scratch_bytes(k)
+                                            : 0);
     if (variant == 1)  // 8-lane group per agent
         launch_k(c, k_step_group<DRY>, dim3((d.capW + kGroupAgents - 1) / kGroupAgents), dim3(kGroupThreads),
                  (size_t)c->groupSmem, a);
@@ -789,7 +797,7 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
     if (e == cudaSuccess) {
         // inline-LP3 threshold: one wave of k_step blocks with the inline shared memory
         const int k = params->maxNeighbors;
-        const size_t smemInl = (size_t)c->smemBytes + (size_t)std::max(0, 3 * k - ORCA_BUF_EXTRA) * 4 * kStepThreads;
+        const size_t smemInl = (size_t)c->smemBytes + (size_t)step_lp3q_scratch_bytes(k);  // mode 2
         int blocks = 0, sms = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step<false, 0, false>, kStepThreads, smemInl);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1243,11 +1251,13 @@ orca_status io_init(orca_ctx* c) {
 constexpr int kProbeChains = 8;
 template <typename T>
 __global__ void __launch_bounds__(256) k_probe_fma(T* out, int iters, T a, T b, long long* cyc) {
-    long long c0 = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) c0 = clock64();
+    long long c0;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c0));
     T x[kProbeChains];
+    // the chains start from a value that depends on the first clock read (c0 >> 62 is 0 in
+    // practice), so the compiler cannot hoist the FMAs above it
 #pragma unroll
-    for (int q = 0; q < kProbeChains; ++q) x[q] = (T)(threadIdx.x + q);
+    for (int q = 0; q < kProbeChains; ++q) x[q] = (T)(threadIdx.x + q + (int)(c0 >> 62));
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
@@ -1259,7 +1269,9 @@ __global__ void __launch_bounds__(256) k_probe_fma(T* out, int iters, T a, T b, 
 #pragma unroll
     for (int q = 0; q < kProbeChains; ++q) acc += x[q];
     if (acc == (T)-1.2345) out[blockIdx.x] = acc;  // practically never; keeps the chains live
-    if (blockIdx.x == 0 && threadIdx.x == 0) cyc[0] = clock64() - c0;
+    long long c1;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1) : "l"((long long)(acc != acc)));  // after acc
+    if (blockIdx.x == 0 && threadIdx.x == 0) cyc[0] = c1 - c0;
 }
 
 extern "C" {
@@ -2120,7 +2132,7 @@ orca_status orca_get_comm_info(orca_ctx* c, int32_t info[3]) {
 }
 
 orca_status orca_set_lp3_inline(orca_ctx* c, int32_t mode) {
-    if (!c || mode < -1 || mode > 1) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be -1 (auto), 0 or 1");
+    if (!c || mode < -1 || mode > 2) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be -1 (auto), 0, 1 or 2");
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);

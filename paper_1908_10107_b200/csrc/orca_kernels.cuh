@@ -559,19 +559,19 @@ __device__ __forceinline__ uint32_t orca_line(float xi, float yi, float vxi, flo
 }
 
 // ------------------------------------------------------------------- LP
-// Lines live in shared memory, one column per thread: element m of this thread's list
-// is at [m * T] of each pointer (bank = tid % 32 for every m -> conflict-free even under
-// divergence).
+// Lines live in shared memory, one column per thread: half-plane m of this thread is the
+// normal n[m * T] (a float2: one 64-bit access) and the offset s[m * T] (the same bank
+// pattern for every m -> conflict-free under divergence apart from the 64-bit half-warp split).
 struct Lines {
-    float* nx;
-    float* ny;
+    float2* n;
     float* s;
 };
 
 template <bool CNT>
 __device__ __forceinline__ bool lp1(const Lines& L, int T, int no, float r, float optx, float opty, bool dirOpt,
                                     float& vx, float& vy, uint32_t& fl, WorkT& w) {
-    const float nix = L.nx[no * T], niy = L.ny[no * T], si = L.s[no * T];
+    const float2 ni = L.n[no * T];
+    const float nix = ni.x, niy = ni.y, si = L.s[no * T];
     const float disc = (r - si) * (r + si);  // r^2 - s^2: distance of the chord
     if (disc < 0.0f) return false;
     const float sq = sqrtf(disc);
@@ -585,7 +585,8 @@ __device__ __forceinline__ bool lp1(const Lines& L, int T, int no, float r, floa
     _Pragma(ORCA_XSTR_(unroll ORCA_LP1_UNROLL))
     for (int j = 0; j < no; ++j) {
         if (CNT) ++w.lp1;
-        const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
+        const float2 nj = L.n[j * T];
+        const float njx = nj.x, njy = nj.y, sj = L.s[j * T];
         const float den = fmaf(njx, Dx, njy * Dy);
         const float num = sj - si * fmaf(njx, nix, njy * niy);
         if (fabsf(den) <= kEps) {
@@ -632,7 +633,8 @@ __device__ __forceinline__ int lp2(const Lines& L, int T, int n, float r, float 
     }
     for (int i = 0; i < n; ++i) {
         if (CNT) ++w.checks;
-        const float pen = L.s[i * T] - fmaf(L.nx[i * T], vx, L.ny[i * T] * vy);
+        const float2 ni = L.n[i * T];
+        const float pen = L.s[i * T] - fmaf(ni.x, vx, ni.y * vy);
         if (pen > 0.0f) {
             const float tx = vx, ty = vy;
             if (!lp1<CNT>(L, T, i, r, optx, opty, dirOpt, vx, vy, fl, w)) {
@@ -656,12 +658,11 @@ __device__ __forceinline__ int lp2(const Lines& L, int T, int n, float r, float 
 // sequential order this re-solves only against the few binding half-planes, and the lanes of
 // a warp take their steps together (one reconvergence point per step).
 __device__ __forceinline__ void line_swap(const Lines& L, int T, int a, int b) {
-    const float ax = L.nx[a * T], ay = L.ny[a * T], as = L.s[a * T];
-    L.nx[a * T] = L.nx[b * T];
-    L.ny[a * T] = L.ny[b * T];
+    const float2 an = L.n[a * T];
+    const float as = L.s[a * T];
+    L.n[a * T] = L.n[b * T];
     L.s[a * T] = L.s[b * T];
-    L.nx[b * T] = ax;
-    L.ny[b * T] = ay;
+    L.n[b * T] = an;
     L.s[b * T] = as;
 }
 
@@ -686,7 +687,8 @@ __device__ __forceinline__ int lp2_greedy(const Lines& L, int T, int n, int kmax
         int bi = -1;
         for (int q = t; q < n; ++q) {
             if (CNT) ++w.checks;
-            const float pen = L.s[q * T] - fmaf(L.nx[q * T], vx, L.ny[q * T] * vy);
+            const float2 nq = L.n[q * T];
+            const float pen = L.s[q * T] - fmaf(nq.x, vx, nq.y * vy);
             if (pen > best) {
                 best = pen;
                 bi = q;
@@ -732,7 +734,8 @@ __device__ __forceinline__ int lp2_sync(const Lines& L, int T, int n, int kmax, 
     for (int i = 0; i < kmax; ++i) {
         if (i < n && failed == n) {
             if (CNT) ++w.checks;
-            const float pen = L.s[i * T] - fmaf(L.nx[i * T], vx, L.ny[i * T] * vy);
+            const float2 ni = L.n[i * T];
+            const float pen = L.s[i * T] - fmaf(ni.x, vx, ni.y * vy);
             if (pen > 0.0f) {
                 const float tx = vx, ty = vy;
                 if (!lp1<CNT>(L, T, i, r, optx, opty, false, vx, vy, fl, w)) {
@@ -781,7 +784,8 @@ __device__ __forceinline__ int lp2_wu(const Lines& L, int T, int n, int kmax, fl
         bool need = false;
         if (i < n && failed == n) {
             if (CNT) ++w.checks;
-            need = L.s[i * T] - fmaf(L.nx[i * T], vx, L.ny[i * T] * vy) > 0.0f;
+            const float2 ni = L.n[i * T];
+            need = L.s[i * T] - fmaf(ni.x, vx, ni.y * vy) > 0.0f;
         }
         const unsigned V = __ballot_sync(mask, need);
         if (V == 0u) continue;
@@ -815,13 +819,15 @@ __device__ __forceinline__ int lp2_wu(const Lines& L, int T, int n, int kmax, fl
             const int o = valid ? (int)wuOwner[wb + p] : lane;  // owner lane of problem p
             const int d = o - lane;                              // column offset to the owner
             const float ro = __shfl_sync(mask, r, o);
-            const float nix = L.nx[i * T + d], niy = L.ny[i * T + d], si = L.s[i * T + d];
+            const float2 nid = L.n[i * T + d];
+            const float nix = nid.x, niy = nid.y, si = L.s[i * T + d];
             const float sq = sqrtf(fmaxf((ro - si) * (ro + si), 0.0f));
             float tL = -sq, tR = sq;
             bool parF = false, g2 = false;
             if (valid && j < i) {
                 const float Dx = niy, Dy = -nix;
-                const float njx = L.nx[j * T + d], njy = L.ny[j * T + d], sj = L.s[j * T + d];
+                const float2 njd = L.n[j * T + d];
+                const float njx = njd.x, njy = njd.y, sj = L.s[j * T + d];
                 const float den = fmaf(njx, Dx, njy * Dy);
                 const float num = sj - si * fmaf(njx, nix, njy * niy);
                 if (fabsf(den) <= kEps) {
@@ -855,7 +861,8 @@ __device__ __forceinline__ int lp2_wu(const Lines& L, int T, int n, int kmax, fl
             const float rL = __shfl_sync(mask, tL, src), rR = __shfl_sync(mask, tR, src);
             const int rc = __shfl_sync(mask, code, src);
             if (mine) {
-                const float oix = L.nx[i * T], oiy = L.ny[i * T], osi = L.s[i * T];
+                const float2 oin = L.n[i * T];
+                const float oix = oin.x, oiy = oin.y, osi = L.s[i * T];
                 if ((r - osi) * (r + osi) < 0.0f) {
                     failed = i;  // empty chord: the serial lp1 fails before any line
                 } else {
@@ -884,11 +891,13 @@ __device__ __forceinline__ void lp3(const Lines& L, const Lines& P, int T, int n
                                     float& vy, uint32_t& fl, WorkT& w) {
     float dist = 0.0f;
     for (int i = begin; i < n; ++i) {
-        const float nix = L.nx[i * T], niy = L.ny[i * T], si = L.s[i * T];
+        const float2 ni = L.n[i * T];
+        const float nix = ni.x, niy = ni.y, si = L.s[i * T];
         if (si - fmaf(nix, vx, niy * vy) > dist) {
             int m = 0;
             for (int j = 0; j < i; ++j) {
-                const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
+                const float2 nj = L.n[j * T];
+                const float njx = nj.x, njy = nj.y, sj = L.s[j * T];
                 const float det = fmaf(nix, njy, -niy * njx);
                 if (fabsf(det) <= kEps && fmaf(nix, njx, niy * njy) > 0.0f) {
                     // same direction: skipped; matters only if the lines nearly coincide
@@ -898,8 +907,7 @@ __device__ __forceinline__ void lp3(const Lines& L, const Lines& P, int T, int n
                 if (CNT) ++w.proj;
                 const float dx = njx - nix, dy = njy - niy;
                 const float il = 1.0f / sqrtf(fmaf(dx, dx, dy * dy));
-                P.nx[m * T] = dx * il;
-                P.ny[m * T] = dy * il;
+                P.n[m * T] = make_float2(dx * il, dy * il);
                 P.s[m * T] = (sj - si) * il;
                 ++m;
             }
@@ -929,7 +937,8 @@ __device__ __forceinline__ int lp2_dir_sync(const Lines& P, int T, int m, int km
     for (int i = 0; i < kmax; ++i) {
         if (i < m && failed == m) {
             if (CNT) ++w.checks;
-            const float pen = P.s[i * T] - fmaf(P.nx[i * T], vx, P.ny[i * T] * vy);
+            const float2 ni = P.n[i * T];
+            const float pen = P.s[i * T] - fmaf(ni.x, vx, ni.y * vy);
             if (pen > 0.0f) {
                 const float tx = vx, ty = vy;
                 if (!lp1<CNT>(P, T, i, r, dx, dy, true, vx, vy, fl, w)) {
@@ -951,7 +960,7 @@ __device__ __forceinline__ int lp2_dir_sync(const Lines& P, int T, int m, int km
 // processed slots [0, t) runs; when none exceeds dist the point is optimal.  One
 // reconvergence point per step.
 template <bool CNT>
-__device__ __forceinline__ void lp3_greedy(const Lines& L, const Lines& P, int T, int n, int begin, int kmax, float r,
+__device__ __forceinline__ void lp3_greedy(const Lines& L, const Lines& P, int T, int TP, int n, int begin, int kmax, float r,
                                            float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask) {
     float dist = 0.0f;
     bool done = begin >= n;
@@ -961,7 +970,8 @@ __device__ __forceinline__ void lp3_greedy(const Lines& L, const Lines& P, int T
         float best = dist;
         int bi = -1;
         for (int q = t; q < n; ++q) {
-            const float pen = L.s[q * T] - fmaf(L.nx[q * T], vx, L.ny[q * T] * vy);
+            const float2 nq = L.n[q * T];
+            const float pen = L.s[q * T] - fmaf(nq.x, vx, nq.y * vy);
             if (pen > best) {
                 best = pen;
                 bi = q;
@@ -973,10 +983,12 @@ __device__ __forceinline__ void lp3_greedy(const Lines& L, const Lines& P, int T
             continue;
         }
         if (bi != t) line_swap(L, T, t, bi);
-        const float nix = L.nx[t * T], niy = L.ny[t * T], si = L.s[t * T];
+        const float2 ni = L.n[t * T];
+        const float nix = ni.x, niy = ni.y, si = L.s[t * T];
         int m = 0;
         for (int j = 0; j < t; ++j) {
-            const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
+            const float2 nj = L.n[j * T];
+            const float njx = nj.x, njy = nj.y, sj = L.s[j * T];
             const float det = fmaf(nix, njy, -niy * njx);
             if (fabsf(det) <= kEps && fmaf(nix, njx, niy * njy) > 0.0f) {
                 if (fabsf(sj - si) <= 2e-5f * r + 1e-6f) fl |= FL_G2;
@@ -985,13 +997,12 @@ __device__ __forceinline__ void lp3_greedy(const Lines& L, const Lines& P, int T
             if (CNT) ++w.proj;
             const float dx = njx - nix, dy = njy - niy;
             const float il = 1.0f / sqrtf(fmaf(dx, dx, dy * dy));
-            P.nx[m * T] = dx * il;
-            P.ny[m * T] = dy * il;
-            P.s[m * T] = (sj - si) * il;
+            P.n[m * TP] = make_float2(dx * il, dy * il);
+            P.s[m * TP] = (sj - si) * il;
             ++m;
         }
         const float tx = vx, ty = vy;
-        if (lp2<CNT>(P, T, m, r, nix, niy, true, vx, vy, fl, w) < m) {
+        if (lp2<CNT>(P, TP, m, r, nix, niy, true, vx, vy, fl, w) < m) {
             vx = tx;  // floating-point failure: keep the current point
             vy = ty;
         }
@@ -1002,15 +1013,16 @@ __device__ __forceinline__ void lp3_greedy(const Lines& L, const Lines& P, int T
 // lp3 with a uniform kmax-iteration outer loop and a reconvergence point per line (see
 // lp2_sync); the inner projected LP2 is lp2_dir_sync over the lanes at the same line.
 template <bool CNT>
-__device__ __forceinline__ void lp3_sync(const Lines& L, const Lines& P, int T, int n, int begin, int kmax, float r,
+__device__ __forceinline__ void lp3_sync(const Lines& L, const Lines& P, int T, int TP, int n, int begin, int kmax, float r,
                                          float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask) {
     float dist = 0.0f;
     for (int i = 0; i < kmax; ++i) {
         bool part = false;
         float nix = 0.0f, niy = 0.0f, si = 0.0f;
         if (i >= begin && i < n) {
-            nix = L.nx[i * T];
-            niy = L.ny[i * T];
+            const float2 ni = L.n[i * T];
+            nix = ni.x;
+            niy = ni.y;
             si = L.s[i * T];
             part = si - fmaf(nix, vx, niy * vy) > dist;
         }
@@ -1019,7 +1031,8 @@ __device__ __forceinline__ void lp3_sync(const Lines& L, const Lines& P, int T, 
             if (part) {
                 int m = 0;
                 for (int j = 0; j < i; ++j) {
-                    const float njx = L.nx[j * T], njy = L.ny[j * T], sj = L.s[j * T];
+                    const float2 nj = L.n[j * T];
+                    const float njx = nj.x, njy = nj.y, sj = L.s[j * T];
                     const float det = fmaf(nix, njy, -niy * njx);
                     if (fabsf(det) <= kEps && fmaf(nix, njx, niy * njy) > 0.0f) {
                         if (fabsf(sj - si) <= 2e-5f * r + 1e-6f) fl |= FL_G2;
@@ -1028,14 +1041,13 @@ __device__ __forceinline__ void lp3_sync(const Lines& L, const Lines& P, int T, 
                     if (CNT) ++w.proj;
                     const float dx = njx - nix, dy = njy - niy;
                     const float il = 1.0f / sqrtf(fmaf(dx, dx, dy * dy));
-                    P.nx[m * T] = dx * il;
-                    P.ny[m * T] = dy * il;
-                    P.s[m * T] = (sj - si) * il;
+                    P.n[m * TP] = make_float2(dx * il, dy * il);
+                    P.s[m * TP] = (sj - si) * il;
                     ++m;
                 }
                 const float tx = vx, ty = vy;
-                const int fm = ORCA_SYNC_LP3_INNER ? lp2_dir_sync<CNT>(P, T, m, i, r, nix, niy, vx, vy, fl, w, pm)
-                                                   : lp2<CNT>(P, T, m, r, nix, niy, true, vx, vy, fl, w);
+                const int fm = ORCA_SYNC_LP3_INNER ? lp2_dir_sync<CNT>(P, TP, m, i, r, nix, niy, vx, vy, fl, w, pm)
+                                                   : lp2<CNT>(P, TP, m, r, nix, niy, true, vx, vy, fl, w);
                 if (fm < m) {
                     vx = tx;
                     vy = ty;
@@ -1108,6 +1120,10 @@ __host__ __device__ constexpr int step_buf_words(int k) { return k + ORCA_BUF_EX
 #ifndef ORCA_BUF1
 #define ORCA_BUF1 1  // 1: the buffer keeps j only; the merge recomputes the fp32 d2 (r01o: -8 %)
 #endif
+// projected half-plane columns of the block-queue LP3 beyond the per-thread columns (stride
+// kLp3Scratch): progress when no column is free (every agent of a block infeasible)
+constexpr int kLp3Scratch = 8;
+__host__ __device__ constexpr int step_lp3q_scratch_bytes(int k) { return 4 * 3 * k * kLp3Scratch; }
 __host__ __device__ constexpr int step_smem_per_thread(int k) {
     return 4 * (2 * k + (ORCA_BUF1 ? 1 : 2) * step_buf_words(k));
 }
@@ -1234,7 +1250,9 @@ __device__ __forceinline__ bool exact_less(uint32_t ja, uint32_t jb, float2 pi, 
 #ifndef ORCA_FAST_MERGE
 #define ORCA_FAST_MERGE 1
 #endif
-__device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int cnt, int k, const uint32_t* Bf,
+// List entries are (fp32 d2 bits, j) pairs in one 64-bit shared-memory slot each: a shift
+// step of the insertion is one 64-bit load and one 64-bit store.
+__device__ __forceinline__ int merge_candidates(uint2* Lst, int cnt, int k, const uint32_t* Bf,
                                                 const float* Bff, int nb, float2 pi, const Model& m,
                                                 const float2* __restrict__ posS, const uint32_t* __restrict__ idS) {
     constexpr int T = kStepThreads;
@@ -1246,32 +1264,47 @@ __device__ __forceinline__ int merge_candidates(uint32_t* Lf, uint32_t* Lj, int 
             const float fhi = f * (1.0f + 0x1p-19f), flo = f * (1.0f - 0x1p-19f);
             int p = cnt;
             if (cnt == k) {  // beyond the k-th: rejected
-                const float o = __uint_as_float(Lf[(k - 1) * T]);
-                if (!(fhi < o) && (o < flo || !exact_less(j, Lj[(k - 1) * T], pi, posS, idS))) continue;
+                const uint2 o = Lst[(k - 1) * T];
+                const float of = __uint_as_float(o.x);
+                if (!(fhi < of) && (of < flo || !exact_less(j, o.y, pi, posS, idS))) continue;
                 p = k - 1;
             }
+            uint2* q = Lst + p * T;
+            // fast path: shift while the entry below is surely farther (one fp32 compare)
             while (p > 0) {
-                const float o = __uint_as_float(Lf[(p - 1) * T]);
-                if (!(fhi < o) && (o < flo || !exact_less(j, Lj[(p - 1) * T], pi, posS, idS))) break;
-                Lf[p * T] = __float_as_uint(o);
-                Lj[p * T] = Lj[(p - 1) * T];
+                const uint2 o = q[-T];
+                if (!(fhi < __uint_as_float(o.x))) break;
+                *q = o;
+                q -= T;
                 --p;
             }
-            Lf[p * T] = __float_as_uint(f);
-            Lj[p * T] = j;
+            // the entry below is not surely farther: unless surely nearer, the exact fp64 keys
+            // decide (a near-tie, rare), and the shifting continues on them
+            while (p > 0) {
+                const uint2 o = q[-T];
+                const float of = __uint_as_float(o.x);
+                if (of < flo) break;
+                if (!(fhi < of) && !exact_less(j, o.y, pi, posS, idS)) break;
+                *q = o;
+                q -= T;
+                --p;
+            }
+            *q = make_uint2(__float_as_uint(f), j);
             if (cnt < k) ++cnt;
             continue;
         }
-        if (cnt == k && !cand_less(f, j, __uint_as_float(Lf[(k - 1) * T]), Lj[(k - 1) * T], pi, posS, idS))
-            continue;
+        if (cnt == k) {
+            const uint2 o = Lst[(k - 1) * T];
+            if (!cand_less(f, j, __uint_as_float(o.x), o.y, pi, posS, idS)) continue;
+        }
         int p = (cnt < k) ? cnt : k - 1;
-        while (p > 0 && cand_less(f, j, __uint_as_float(Lf[(p - 1) * T]), Lj[(p - 1) * T], pi, posS, idS)) {
-            Lf[p * T] = Lf[(p - 1) * T];
-            Lj[p * T] = Lj[(p - 1) * T];
+        while (p > 0) {
+            const uint2 o = Lst[(p - 1) * T];
+            if (!cand_less(f, j, __uint_as_float(o.x), o.y, pi, posS, idS)) break;
+            Lst[p * T] = o;
             --p;
         }
-        Lf[p * T] = __float_as_uint(f);
-        Lj[p * T] = j;
+        Lst[p * T] = make_uint2(__float_as_uint(f), j);
         if (cnt < k) ++cnt;
     }
     return cnt;
@@ -1391,11 +1424,10 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     const int tid = threadIdx.x;
     const int k = a.m.k;
     const int capB = step_buf_words(k);
-    uint32_t* L0 = reinterpret_cast<uint32_t*>(smem) + tid;  // list d2 / nx
-    uint32_t* L1 = L0 + k * T;                                  // list j  / ny
-    uint32_t* Bf = L1 + k * T;                                  // buffer j / s
-    float* Bff = reinterpret_cast<float*>(Bf + capB * T);       // buffer d2
-    const Lines L{reinterpret_cast<float*>(L0), reinterpret_cast<float*>(L1), reinterpret_cast<float*>(Bf)};
+    uint2* Lst = reinterpret_cast<uint2*>(smem) + tid;                    // list (d2, j) / normal n
+    uint32_t* Bf = reinterpret_cast<uint32_t*>(smem) + 2 * k * T + tid;    // buffer j / s
+    float* Bff = reinterpret_cast<float*>(Bf + capB * T);                  // buffer d2
+    const Lines L{reinterpret_cast<float2*>(Lst), reinterpret_cast<float*>(Bf)};
 
     // owned agents are the contiguous sorted range of columns [c0, c1)
     const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * a.g.colBins];
@@ -1411,6 +1443,16 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     uint32_t fl = 0;
     int nColl = 0;
     bool deferred = false;
+    // block-local LP3 queue (lp3Inline == 2): queue words of the block's
+    // infeasible agents and the thread columns that are free once their agent is finished
+    __shared__ uint32_t sQ[T];
+    __shared__ uint8_t sFree[T];
+    __shared__ int sQn;
+    const bool blockQ = a.lp3Inline == 2;
+    if (blockQ && tid == 0) sQn = 0;
+    if (blockQ) __syncthreads();
+    bool queued = false;
+    int cInfX = 0, cDegX = 0, cG1X = 0, cG2X = 0, cG3X = 0;  // agents this thread finished from the queue
     if (active) {
         const float2 pi = a.posS[i];
         const float2 vi = a.velS[i];
@@ -1480,11 +1522,11 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 if (KR > 0 && mode == 0)
                     reg_merge<(KR > 0 ? KR : 1)>(R, cnt, Bf, Bff, nb, pi, a.m, a.posS, tie);
                 else
-                    cnt = merge_candidates(L0, L1, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
+                    cnt = merge_candidates(Lst, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
             };
             auto kth = [&]() -> float {  // fp32 d2 of the k-th (valid when cnt >= k)
                 if (KR > 0 && mode == 0) return reg_f<(KR > 0 ? KR : 1)>(R, k - 1);
-                return __uint_as_float(L0[(k - 1) * T]);
+                return __uint_as_float(Lst[(k - 1) * T].x);
             };
           for (;;) {  // modes
             if (KR > 0 && mode == 0) reg_clear<(KR > 0 ? KR : 1)>(R);
@@ -1594,7 +1636,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             if (KR > 0 && mode == 0) {  // neighbour indices into the shared list slots
 #pragma unroll
                 for (int q = 0; q < (KR > 0 ? KR : 1); ++q)
-                    if (q < cnt) L1[q * T] = R.j[q];
+                    if (q < cnt) Lst[q * T] = make_uint2(__float_as_uint(R.f[q]), R.j[q]);
             }
         }
         if (!DRY) a.rk2W[ws] = fk;  // next step's search bound (read back by k_lp3 for queued agents)
@@ -1604,12 +1646,13 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         if (ORCA_SYNC_PHASES) __syncwarp(activeMask);
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
         if (DRY && a.dbgNbr)  // neighbours in (distance, id) order
-            for (int q = 0; q < cnt; ++q) a.dbgNbr[(size_t)idi * k + q] = (int32_t)a.idS[L1[q * T]];
+            for (int q = 0; q < cnt; ++q) a.dbgNbr[(size_t)idi * k + q] = (int32_t)a.idS[Lst[q * T].y];
         // optional randomized LP order (P:82 Seidel, reading Q8): permute the list first
-        if (a.m.lpRandom && cnt > 1) lp_shuffle(L1, T, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
+        if (a.m.lpRandom && cnt > 1)  // (the j of each 64-bit slot: stride 2T words)
+            lp_shuffle(reinterpret_cast<uint32_t*>(Lst) + 1, 2 * T, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
         // (half-plane q overwrites list slot q in place: j is read before the write)
         for (int q = 0; q < cnt; ++q) {
-            const uint32_t j = L1[q * T];
+            const uint32_t j = Lst[q * T].y;
             const float2 pj = a.posS[j];
             const float2 vj = a.velS[j];
             float nx, ny, s;
@@ -1624,8 +1667,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             }
             fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, a.idS, j, Rp, R2p, a.m, nx, ny, s, coll);
             nColl += coll;
-            L.nx[q * T] = nx;
-            L.ny[q * T] = ny;
+            L.n[q * T] = make_float2(nx, ny);
             L.s[q * T] = s;
         }
 
@@ -1650,23 +1692,48 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                       : WU         ? lp2_wu<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                       : ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                                      : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
-        if (a.lp3Inline) {
+        if (blockQ) {
+            if (f < cnt) {
+                // infeasible: into the block's queue; the least-penetration LP runs after
+                // the block barrier below on a compacted set of lanes.  The LP2 point waits in
+                // this thread's free buffer words (right after s)
+                fl |= FL_INFEASIBLE;
+                queued = true;
+                Bf[k * T] = __float_as_uint(vx);
+                Bf[(k + 1) * T] = __float_as_uint(vy);
+                const unsigned mask = __activemask();
+                const int lane = tid & 31;
+                const int leader = __ffs(mask) - 1;
+                int base = 0;
+                if (lane == leader) base = atomicAdd(&sQn, __popc(mask));
+                base = __shfl_sync(mask, base, leader);
+                sQ[base + __popc(mask & ((1u << lane) - 1u))] =
+                    (uint32_t)tid | ((uint32_t)cnt << 8) | ((uint32_t)f << 16) | (fl << 24);
+                if (DRY && a.dbgCnt) a.dbgCnt[idi] = cnt;
+                if (DRY && a.dbgNbr)
+                    for (int q2 = cnt; q2 < k; ++q2) a.dbgNbr[(size_t)idi * k + q2] = -1;
+            }
+        } else if (a.lp3Inline) {
             // small strips (latency bound, spare issue slots): the least-penetration LP
             // runs here on the half-planes in shared memory -- the same lp3 as k_lp3, so the
             // same result -- and the agent is finished below like a feasible one
             const unsigned lmask = __ballot_sync(activeMask, f < cnt);
             if (f < cnt) {
                 fl |= FL_INFEASIBLE;
-                // projected half-planes right after s in the (now free) candidate buffer and
-                // beyond it: the launch adds max(0, 3k - ORCA_BUF_EXTRA) words per thread
-                float* Pb = reinterpret_cast<float*>(Bf + k * T);
-                const Lines P{Pb, Pb + k * T, Pb + 2 * k * T};
+                // projected half-planes in the 3k words per thread the launch adds after the
+                // per-thread columns (their own interleaved layout: the candidate buffers of
+                // threads still selecting stay untouched)
+                float* Pb = reinterpret_cast<float*>(smem) + (2 * k + capB) * T;
+                const Lines P{reinterpret_cast<float2*>(Pb) + tid, Pb + 2 * k * T + tid};
                 if (a.m.lpGreedy)
-                    lp3_greedy<CNT>(L, P, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask);
+                    lp3_greedy<CNT>(L, P, T, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask);
                 else
-                    lp3_sync<CNT>(L, P, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask);
+                    lp3_sync<CNT>(L, P, T, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask);
                 float dl = 0.0f;
-                for (int m = 0; m < cnt; ++m) dl = fmaxf(dl, L.s[m * T] - fmaf(L.nx[m * T], vx, L.ny[m * T] * vy));
+                for (int m = 0; m < cnt; ++m) {
+                    const float2 nm = L.n[m * T];
+                    dl = fmaxf(dl, L.s[m * T] - fmaf(nm.x, vx, nm.y * vy));
+                }
                 if (dl > 0.0f && dl < 1e-6f) fl |= FL_G3;
             }
         } else if (f < cnt) {
@@ -1683,7 +1750,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             const int q = (int)base + __popc(mask & ((1u << lane) - 1u));
             a.qEntry[q] = make_int4(i, cnt | (f << 8) | ((int)fl << 16), __float_as_int(vx), __float_as_int(vy));
             for (int m = 0; m < cnt; ++m)
-                a.qLines[(size_t)m * a.qcap + q] = make_float4(L.nx[m * T], L.ny[m * T], L.s[m * T], 0.0f);
+                a.qLines[(size_t)m * a.qcap + q] = make_float4(L.n[m * T].x, L.n[m * T].y, L.s[m * T], 0.0f);
             if (DRY && a.dbgCnt) a.dbgCnt[idi] = cnt;
             if (DRY && a.dbgNbr)
                 for (int q2 = cnt; q2 < k; ++q2) a.dbgNbr[(size_t)idi * k + q2] = -1;
@@ -1691,8 +1758,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
 
         if (ORCA_SYNC_PHASES) __syncwarp(activeMask);
         // ---- 5. integrate (explicit Euler) + next step's binning ----------------------
-        if (deferred) {
-            // finished by k_lp3
+        if (deferred || queued) {
+            // finished by k_lp3 / by the block queue below
         } else if (DRY) {
             if (a.dbgV) a.dbgV[idi] = make_float2(vx, vy);
             if (a.dbgFlags) a.dbgFlags[idi] = (uint8_t)fl;
@@ -1701,6 +1768,86 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 for (int q = cnt; q < k; ++q) a.dbgNbr[(size_t)idi * k + q] = -1;
         } else {
             finish_agent(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk, pr);
+        }
+    }
+    if (blockQ) {
+        // ---- LP3 of the block's infeasible agents on compacted lanes -----------------
+        // Free columns: threads whose agent is finished (or that have none); an executor
+        // thread e runs queue entry e with the owner's half-planes (owner column) and its
+        // projected half-planes in free column sFree[e], then finishes the owner's agent.
+        {
+            const int lane = tid & 31;
+            const bool fr = !queued;
+            const unsigned fm = __ballot_sync(0xffffffffu, fr);
+            __shared__ int sWarpFree[T / 32];
+            if (lane == 0) sWarpFree[tid >> 5] = __popc(fm);
+            __syncthreads();
+            int off = 0;
+            for (int q = 0; q < (tid >> 5); ++q) off += sWarpFree[q];
+            if (fr) sFree[off + __popc(fm & ((1u << lane) - 1u))] = (uint8_t)tid;
+        }
+        __syncthreads();
+        // Rounds (block-uniform): executors e < nfree take free column sFree[e] for their
+        // projected half-planes, the next kLp3Scratch take a column of the small scratch area
+        // after the per-thread columns (stride kLp3Scratch), so every round makes progress even
+        // when every agent of the block is infeasible; the owners finished in a round free
+        // their columns for the next.  One round whenever at most half the block is queued.
+        const int nq = sQn;
+        int nfree = T - nq, done = 0;
+        const int o1b = o1;
+        float* scratch = reinterpret_cast<float*>(smem) + (2 * k + capB) * T;
+        while (done < nq) {
+            const int nexec = min(nq - done, nfree + kLp3Scratch);
+            const bool ex = tid < nexec;
+            const unsigned xmask = __ballot_sync(0xffffffffu, ex);
+            int owner = 0;
+            if (ex) {
+                const uint32_t e = sQ[done + tid];
+                owner = (int)(e & 0xffu);
+                const int cnt = (int)((e >> 8) & 0xffu), f = (int)((e >> 16) & 0xffu);
+                uint32_t fl2 = e >> 24;
+                float* sw = reinterpret_cast<float*>(smem);
+                const Lines Lo{reinterpret_cast<float2*>(sw) + owner, sw + 2 * k * T + owner};
+                const bool main = tid < nfree;
+                const int TP = main ? T : kLp3Scratch;
+                const int pcol = main ? (int)sFree[tid] : tid - nfree;
+                const Lines P = main ? Lines{reinterpret_cast<float2*>(sw) + pcol, sw + 2 * k * T + pcol}
+                                     : Lines{reinterpret_cast<float2*>(scratch) + pcol, scratch + 2 * k * TP + pcol};
+                float vx = sw[3 * k * T + owner];  // the LP2 point stashed after s
+                float vy = sw[(3 * k + 1) * T + owner];
+                const int wso = blockIdx.x * T + owner;
+                const int io = o0 + wso;
+                const float4 pr = a.propS ? a.propS[io] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
+                if (a.m.lpGreedy)
+                    lp3_greedy<CNT>(Lo, P, T, TP, cnt, f, k, pr.y, vx, vy, fl2, w, xmask);
+                else
+                    lp3_sync<CNT>(Lo, P, T, TP, cnt, f, k, pr.y, vx, vy, fl2, w, xmask);
+                float dl = 0.0f;
+                for (int m = 0; m < cnt; ++m) {
+                    const float2 nm = Lo.n[m * T];
+                    dl = fmaxf(dl, Lo.s[m * T] - fmaf(nm.x, vx, nm.y * vy));
+                }
+                if (dl > 0.0f && dl < 1e-6f) fl2 |= FL_G3;
+                const uint32_t ido = a.idS[io];
+                if (DRY) {
+                    if (a.dbgV) a.dbgV[ido] = make_float2(vx, vy);
+                    if (a.dbgFlags) a.dbgFlags[ido] = (uint8_t)fl2;
+                } else {
+                    finish_agent(a, wso, o1b - o0, a.posS[io], vx, vy, a.auxS[io], ido, a.rk2W[wso], pr);
+                }
+                cInfX += 1;
+                cDegX += (fl2 & (FL_G1 | FL_G2)) != 0;
+                cG1X += (fl2 & FL_G1) != 0;
+                cG2X += (fl2 & FL_G2) != 0;
+                cG3X += (fl2 & FL_G3) != 0;
+            }
+            done += nexec;
+            if (done < nq) {  // (block-uniform) another round: the finished owners' columns are free
+                __syncthreads();
+                if (ex) sFree[nfree + tid] = (uint8_t)owner;
+                nfree += nexec;
+                __syncthreads();
+            }
         }
     }
     if (DRY && a.work) {
@@ -1721,12 +1868,23 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         // per-warp counts (ballot + popc), one relaxed atomic per warp and counter; no
         // block barrier, so fast warps never wait for a slow LP in the same block
         const int lane = tid & 31;
-        if (deferred) fl = 0;  // counted by k_lp3 with its final flags
-        const int cInf = __popc(__ballot_sync(0xffffffffu, fl & FL_INFEASIBLE));
-        const int cDeg = __popc(__ballot_sync(0xffffffffu, fl & (FL_G1 | FL_G2)));
-        const int cG1 = __popc(__ballot_sync(0xffffffffu, fl & FL_G1));
-        const int cG2 = __popc(__ballot_sync(0xffffffffu, fl & FL_G2));
-        const int cG3 = __popc(__ballot_sync(0xffffffffu, fl & FL_G3));
+        if (deferred || queued) fl = 0;  // counted by k_lp3 / the queue executor with the final flags
+        int cInf = __popc(__ballot_sync(0xffffffffu, fl & FL_INFEASIBLE));
+        int cDeg = __popc(__ballot_sync(0xffffffffu, fl & (FL_G1 | FL_G2)));
+        int cG1 = __popc(__ballot_sync(0xffffffffu, fl & FL_G1));
+        int cG2 = __popc(__ballot_sync(0xffffffffu, fl & FL_G2));
+        int cG3 = __popc(__ballot_sync(0xffffffffu, fl & FL_G3));
+        if (blockQ) {
+            int x[5] = {cInfX, cDegX, cG1X, cG2X, cG3X};
+#pragma unroll
+            for (int r = 0; r < 5; ++r)
+                for (int o = 16; o > 0; o >>= 1) x[r] += __shfl_xor_sync(0xffffffffu, x[r], o);
+            cInf += x[0];
+            cDeg += x[1];
+            cG1 += x[2];
+            cG2 += x[3];
+            cG3 += x[4];
+        }
         int c = nColl;
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         if (lane == 0) {
@@ -1759,9 +1917,9 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
     constexpr int T = kStepThreads;
     const int tid = threadIdx.x;
     const int k = a.m.k;
-    float* base = reinterpret_cast<float*>(smem) + tid;
-    const Lines L{base, base + k * T, base + 2 * k * T};
-    const Lines P{base + 3 * k * T, base + 4 * k * T, base + 5 * k * T};
+    float* sw = reinterpret_cast<float*>(smem);
+    const Lines L{reinterpret_cast<float2*>(sw) + tid, sw + 2 * k * T + tid};                  // words [0, 3kT)
+    const Lines P{reinterpret_cast<float2*>(sw + 3 * k * T) + tid, sw + 5 * k * T + tid};      // words [3kT, 6kT)
     const int nq = (int)*a.qCount;
     if ((int)blockIdx.x * T >= nq) return;  // block-uniform: nothing queued for this block
     const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * a.g.colBins];
@@ -1820,19 +1978,21 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
         _Pragma(ORCA_XSTR_(unroll ORCA_LP3_LOAD_UNROLL))
         for (int m = 0; m < cnt; ++m) {
             const float4 l = a.qLines[(size_t)m * a.qcap + q];
-            L.nx[m * T] = l.x;
-            L.ny[m * T] = l.y;
+            L.n[m * T] = make_float2(l.x, l.y);
             L.s[m * T] = l.z;
         }
         const float4 pr = a.propS ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
         if (a.m.lpGreedy)
-            lp3_greedy<CNT>(L, P, T, cnt, f, k, pr.y, vx, vy, fl, w, qmask);
+            lp3_greedy<CNT>(L, P, T, T, cnt, f, k, pr.y, vx, vy, fl, w, qmask);
         else if (ORCA_SYNC_LP)
-            lp3_sync<CNT>(L, P, T, cnt, f, k, pr.y, vx, vy, fl, w, qmask);
+            lp3_sync<CNT>(L, P, T, T, cnt, f, k, pr.y, vx, vy, fl, w, qmask);
         else
             lp3<CNT>(L, P, T, cnt, f, pr.y, vx, vy, fl, w);
         float dl = 0.0f;
-        for (int m = 0; m < cnt; ++m) dl = fmaxf(dl, L.s[m * T] - fmaf(L.nx[m * T], vx, L.ny[m * T] * vy));
+        for (int m = 0; m < cnt; ++m) {
+            const float2 nm = L.n[m * T];
+            dl = fmaxf(dl, L.s[m * T] - fmaf(nm.x, vx, nm.y * vy));
+        }
         if (dl > 0.0f && dl < 1e-6f) fl |= FL_G3;
         const float2 pi = a.posS[i];
         const uint32_t idi = a.idS[i];

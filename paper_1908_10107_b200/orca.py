@@ -380,7 +380,8 @@ class Orca:
         _check(_lib.orca_rebalance(self._ctx))
 
     def set_lp3_inline(self, mode: int):
-        """-1 automatic, 0 always queue for k_lp3, 1 always inside the step kernel."""
+        """-1 automatic, 0 always queue for k_lp3, 1 inside the step kernel per thread, 2 inside
+        the step kernel on the block's compacted queue."""
         _check(_lib.orca_set_lp3_inline(self._ctx, mode))
 
     def set_lp3_lanes(self, lanes: int):

@@ -210,6 +210,12 @@ ncclResult_t ncclCommInitRank(ncclComm_t* out, int nranks, ncclUniqueId id, int 
     return ncclSuccess;
 }
 
+ncclResult_t ncclCommCount(const ncclComm_t c, int* count) {
+    if (!c || !count) return ncclInvalidArgument;
+    *count = c->n;
+    return ncclSuccess;
+}
+
 ncclResult_t ncclCommDestroy(ncclComm_t c) {
     if (!c) return ncclSuccess;
     cudaDeviceSynchronize();

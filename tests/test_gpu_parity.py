@@ -826,6 +826,45 @@ def test_lp3_lanes_bit_identical(orca, config, n, k):
         o.close()
 
 
+@pytest.mark.parametrize("config,n,k,het", [("dense", 20000, 10, False), ("uniform", 30000, 32, True),
+                                            ("uniform", 3001, 3, False), ("dense", 40000, 10, True)])
+def test_lp3_modes_bit_identical(orca, config, n, k, het):
+    """Where LP3 runs -- the k_lp3 kernel (0), per thread inside k_step (1), k_step's block-local
+    compacted queue (2, two rounds when more than half a block is infeasible) -- changes
+    nothing: dry-step velocities / flags / lists / work counters and 15 real steps (state and
+    statistics) bit for bit, with heterogeneous agents and goals too."""
+    w = W.make(config, n=n) if config == "dense" else W.make(config, n=n, rho=0.6)
+    rng = np.random.default_rng(3)
+    ctxs = []
+    for mode in (0, 1, 2):
+        o, _ = _ctx(orca, w, maxNeighbors=k)
+        o.set_variant(0)
+        if het:
+            props = _het_props(n, seed=21)
+            o.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+            o.set_goals((w["pos"] + rng.uniform(-30, 30, w["pos"].shape)).astype(np.float32), 1.0)
+            rng = np.random.default_rng(3)
+        o.set_lp3_inline(mode)
+        assert o.launch_info()["lp3_lanes"] == (1 if mode == 0 else 0)
+        ctxs.append(o)
+    r = [o.debug_step() for o in ctxs]
+    assert np.count_nonzero(r[0][1] & 1) > 0
+    wk = [o.work() for o in ctxs]
+    for q in (1, 2):
+        for x, y in zip(r[0], r[q]):
+            assert np.array_equal(x, y), q
+        assert wk[0] == wk[q], q
+    for o in ctxs:
+        o.step(15)
+    s = [o.get_state() for o in ctxs]
+    st = [o.stats() for o in ctxs]
+    for q in (1, 2):
+        assert np.array_equal(s[0][0], s[q][0]) and np.array_equal(s[0][1], s[q][1]), q
+        assert st[0] == st[q], q
+    for o in ctxs:
+        o.close()
+
+
 @pytest.mark.parametrize("lanes", [4, 16])
 def test_lp3_group_vs_oracle(orca, oracle, lanes):
     """The group LP3 kernels against the oracle on the dense crowd (many infeasible LPs)."""
