@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -1245,9 +1246,11 @@ orca_status io_init(orca_ctx* c) {
 
 // ------------------------------------------------------------------ ALU peak probe
 // Measured denominators of the ALU roofline: kProbeChains independent FMA
-// chains per thread (enough ILP to cover the FMA latency), 2048 threads per SM.  Block 0's
-// thread 0 brackets its run with clock64() so the caller also gets the SM clock the probe ran
-// at.  The results are written so the compiler cannot drop the chains.
+// chains per thread (enough ILP to cover the FMA latency), 2048 threads per SM.  Every block
+// records its SM id and its first / last clock64(); the host takes, per SM, the span from the
+// earliest start to the latest end (the per-SM cycle counter runs at the SM clock), so the
+// caller also gets the SM clock the probe ran at.  The results are written so the compiler
+// cannot drop the chains.
 constexpr int kProbeChains = 8;
 template <typename T>
 __global__ void __launch_bounds__(256) k_probe_fma(T* out, int iters, T a, T b, long long* cyc) {
@@ -1271,7 +1274,14 @@ __global__ void __launch_bounds__(256) k_probe_fma(T* out, int iters, T a, T b, 
     if (acc == (T)-1.2345) out[blockIdx.x] = acc;  // practically never; keeps the chains live
     long long c1;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1) : "l"((long long)(acc != acc)));  // after acc
-    if (blockIdx.x == 0 && threadIdx.x == 0) cyc[0] = c1 - c0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        cyc[3 * blockIdx.x] = c0;
+        cyc[3 * blockIdx.x + 1] = c1;
+        cyc[3 * blockIdx.x + 2] = smid;
+    }
 }
 
 extern "C" {
@@ -2223,11 +2233,12 @@ orca_status orca_probe_alu(int32_t device, double out[4]) {
     void* buf = nullptr;
     long long* cyc = nullptr;
     CK(cudaMalloc(&buf, (size_t)blocks * sizeof(double)));
-    CK(cudaMalloc(&cyc, sizeof(long long)));
+    CK(cudaMalloc(&cyc, (size_t)blocks * 3 * sizeof(long long)));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     double best32 = 0.0, best64 = 0.0, mhz = 0.0;
+    std::vector<long long> h((size_t)blocks * 3);
     for (int pass = 0; pass < 4; ++pass) {
         const bool f64 = pass & 1;
         const int iters = f64 ? 256 : 1024;
@@ -2247,9 +2258,17 @@ orca_status orca_probe_alu(int32_t device, double out[4]) {
             best64 = std::max(best64, rate);
         } else if (rate > best32) {
             best32 = rate;
-            long long c = 0;
-            CK(cudaMemcpy(&c, cyc, sizeof c, cudaMemcpyDeviceToHost));
-            mhz = (double)c / (ms * 1e-3) / 1e6;  // block 0 spans ~the whole launch
+            CK(cudaMemcpy(h.data(), cyc, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+            std::vector<long long> lo(1024, LLONG_MAX), hi(1024, LLONG_MIN);
+            for (int q = 0; q < blocks; ++q) {
+                const int sm = (int)(h[3 * q + 2] & 1023);
+                lo[sm] = std::min(lo[sm], h[3 * q]);
+                hi[sm] = std::max(hi[sm], h[3 * q + 1]);
+            }
+            long long span = 0;  // the busiest SM's cycles from its first block start to last end
+            for (int q = 0; q < 1024; ++q)
+                if (hi[q] > lo[q]) span = std::max(span, hi[q] - lo[q]);
+            mhz = (double)span / (ms * 1e-3) / 1e6;
         }
     }
     cudaEventDestroy(e0);
