@@ -258,7 +258,10 @@ orca_status orca_reset_stats(orca_ctx *ctx);
  * register top-k list (k <= 16; else shared memory), 3 = variant 0 with the paper's
  * work-unit LP2 (lanes that need no re-solve evaluate the constraints of lanes
  * that do) in the sequential LP orders (orca_set_lp_order modes 1 and 2; in the greedy order
- * it runs variant 0's LP).  Errors: INVALID_ARGUMENT. */
+ * it runs variant 0's LP), 4 = two lanes per agent (each scans every other candidate into its
+ * own top-k list, the lists are merged exactly, the lanes build every other half-plane and
+ * share the greedy LP2; k <= 14 and the greedy order, else it runs as 0).  Same results bit
+ * for bit.  Errors: INVALID_ARGUMENT. */
 orca_status orca_set_variant(orca_ctx *ctx, int32_t variant);
 
 /* Lanes per queued infeasible agent in the least-penetration kernel: 1 = one thread
@@ -346,6 +349,16 @@ orca_status orca_rebalance(orca_ctx *ctx);
  * measurement shows the peer-memory path faster).  Multi-rank contexts: every rank must
  * call it together.  Synchronises.  Errors: INVALID_ARGUMENT, CUDA, NCCL. */
 orca_status orca_set_transport(orca_ctx *ctx, int32_t mode);
+
+/* Halo overlap of the strips (SURVEY §8(e) "interior columns compute during the
+ * exchange"): the agents of the two boundary columns on each side of a strip -- every agent
+ * that can end the step in an edge column or leave the strip, since maxSpeed * timeStep < one
+ * column -- step first; the exchange and k_receive then run on a second stream while the
+ * interior columns step, joined before the next binning.  -1 = automatic (default: on for
+ * strips of >= 4 columns on the thread-per-agent kernels), 0 = off, 1 = on where possible.
+ * Overlapping strips run LP3 on the block queue (orca_set_lp3_inline mode 2).  Results are
+ * bit-identical either way.  Synchronises.  Errors: INVALID_ARGUMENT. */
+orca_status orca_set_overlap(orca_ctx *ctx, int32_t mode);
 
 /* The transport in use (0 / 1 as above).  A multi-rank context falls back from 0 to 1 on
  * every rank when some pair of neighbouring GPUs cannot map each other's memory. */

@@ -261,6 +261,11 @@ struct Domain {
 struct orca_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // strips' halo overlap (orca_set_overlap): the exchange and k_receive run on `side` while
+    // the interior columns step on `stream` (fork / join by events, inside the step graphs)
+    cudaStream_t side = nullptr;
+    cudaEvent_t evFork = nullptr, evJoin = nullptr;
+    int overlapMode = -1;  // -1 auto (on for strips), 0 off, 1 on
     orca_params p{};
     bool ready = false, goals = false;
     float prefSpeed = 0.0f;
@@ -303,6 +308,7 @@ struct orca_ctx {
     int lp3Lanes = -1;  // lanes per queued agent in the LP3 kernel (1 = thread, -1 = auto)
     int lp3InlineMode = -1;  // orca_set_lp3_inline: -1 auto (strips up to inlineBelow agents), 0 queue, 1 inline
     int64_t inlineBelow = 0;  // one wave of k_step blocks with the inline-LP3 shared memory (orca_create)
+    int64_t pairBelow = 0;    // one wave of the lane-pair k_step (variant 4) blocks (orca_create)
     // strip rebalance: by-id active flags, all-gather records, fill reports
     uint8_t* activeBuf = nullptr;
     int64_t activeCap = 0;
@@ -406,9 +412,9 @@ orca_status dom_alloc(orca_ctx* c, Domain& d, int capW, int64_t nbins, int capM,
     if (capW > d.capW) {
         float2** f2[] = {&d.posS, &d.velS, &d.auxS, &d.posW, &d.velW, &d.auxW};
         uint32_t** u4[] = {&d.idS, &d.idW, &d.cellW, &d.rankW};
-        for (auto p : f2) {
+        for (auto p : f2) {  // (+2 spare entries: the staged copies round runs up to 16 bytes)
             dfree(*p);
-            CK(cudaMalloc(p, (size_t)capW * sizeof(float2)));
+            CK(cudaMalloc(p, (size_t)(capW + 2) * sizeof(float2)));
         }
         for (auto p : u4) {
             dfree(*p);
@@ -466,15 +472,24 @@ void drop_graph(orca_ctx* c) {
     c->graphKey.clear();
 }
 
-// auto (-1): below ~17k agents per strip the step is latency bound (too few warps to hide a
-// thread's chain of dependent loads) and the 8-lane group per agent wins; above, one thread
-// per agent (measured crossover)
+// auto (-1): while a strip fits one wave of the lane-pair kernel (variant 4: 64 agents per
+// block; blocks/SM from the occupancy API x SMs, orca_create) the step is latency bound and
+// halving each warp's dependency chain wins; above, one thread per agent (variant 0).
+// Measured r02m (whole-step ms, v0 / v1 / v4, block-queue LP3 for v0 and v4): 5k 0.047 /
+// 0.047 / 0.041, 10k 0.049 / 0.049 / 0.043, 20k 0.049 / 0.064 / 0.043, 50k 0.055 / 0.095 /
+// 0.049, 70k 0.057 / 0.117 / 0.051; 100k v0 0.063 / v4 0.076 (two waves).  The 8-lane group
+// (variant 1, r01x's choice below 17k) no longer wins anywhere: explicit only.
 #ifndef ORCA_AUTO_GROUP_BELOW
-#define ORCA_AUTO_GROUP_BELOW 17000  // r01x: 24000; re-measured r01ax with the greedy LP: 15k v1, 20k v0
+#define ORCA_AUTO_GROUP_BELOW 0
 #endif
+// variant 4 (two lanes per agent) needs k <= 14 (the merged list in one buffer column) and
+// the greedy LP order; elsewhere it runs as variant 0
+bool pair_ok(const orca_ctx* c) { return c->p.maxNeighbors <= 14 && c->lpMode == 0; }
 int pick_variant(const orca_ctx* c, const Domain& d) {
-    if (c->variant >= 0) return c->variant;
-    return (d.popBuild < ORCA_AUTO_GROUP_BELOW) ? 1 : 0;
+    int v = c->variant;
+    if (v < 0) v = (d.popBuild < ORCA_AUTO_GROUP_BELOW) ? 1 : (d.popBuild <= c->pairBelow) ? 4 : 0;
+    if (v == 4 && !pair_ok(c)) v = 0;
+    return v;
 }
 
 // LP3 lanes, auto (-1): an 8-lane group per queued agent below ORCA_AUTO_LP3_GROUP_BELOW
@@ -504,12 +519,25 @@ int pick_lp3_lanes(const orca_ctx* c, const Domain& d) {
 #endif
 // 0: queued for k_lp3, 1: inside k_step per thread, 2: inside k_step on the block's
 // compacted queue (orca_set_lp3_inline)
+bool overlap_on(const orca_ctx* c, const Domain& d);
 int pick_lp3_mode(const orca_ctx* c, const Domain& d) {
-    if (pick_variant(c, d) == 1) return 0;  // the group kernel always queues
-    if (c->lp3InlineMode >= 0) return c->lp3InlineMode;
+    const int v = pick_variant(c, d);
+    if (v == 1) return 0;  // the group kernel always queues
+    if (overlap_on(c, d)) return 2;  // the boundary agents' LP3 must finish inside their launch
+    if (c->lp3InlineMode >= 0) return (v == 4 && c->lp3InlineMode == 1) ? 2 : c->lp3InlineMode;
     return d.popBuild <= std::min<int64_t>(c->inlineBelow, ORCA_AUTO_LP3_INLINE_BELOW) ? 2 : 0;
 }
 bool pick_lp3_inline(const orca_ctx* c, const Domain& d) { return pick_lp3_mode(c, d) != 0; }
+
+// Halo overlap: the strip's boundary columns (two on each side: every agent
+// that can end the step in an edge column or leave the strip, since maxSpeed dt < one
+// column) step first, then their exchange and k_receive run on the side stream while the
+// interior columns step.  Needs >= 4 owned columns and the thread-per-agent kernels.
+bool overlap_on(const orca_ctx* c, const Domain& d) {
+    if (c->world == 1 || c->overlapMode == 0 || !(d.g.hasL || d.g.hasR)) return false;
+    if (pick_variant(c, d) == 1 || d.g.c1 - d.g.c0 < 4) return false;
+    return true;
+}
 
 // Everything a captured step body depends on: the kernel arguments of every strip (device
 // pointers, grid, model), launch sizes, the exchange buffers and the kernel selection.  A
@@ -521,8 +549,8 @@ std::vector<unsigned char> graph_key(orca_ctx* c) {
         const unsigned char* b = static_cast<const unsigned char*>(p);
         k.insert(k.end(), b, b + n);
     };
-    const int hdr[7] = {c->variant, c->lp3Lanes, c->smemBytes, c->world, c->loopback ? 1 : 0, (int)c->doms.size(),
-                        c->transport};
+    const int hdr[8] = {c->variant, c->lp3Lanes, c->smemBytes, c->world, c->loopback ? 1 : 0, (int)c->doms.size(),
+                        c->transport, c->overlapMode};
     put(hdr, sizeof hdr);
     for (Domain& d : c->doms) {
         const StepArgs a = make_args(c, d);
@@ -601,6 +629,9 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
                  (size_t)c->groupSmem, a);
     else if (variant == 3)  // work-unit LP2 (P:84-89 ablation)
         launch_k(c, k_step<DRY, 0, true>, dim3(blocks), dim3(kStepThreads), smem, a);
+    else if (variant == 4)  // two lanes per agent: 64 agents per block
+        launch_k(c, k_step<DRY, 0, false, true>, dim3((d.capW + kStepThreads / 2 - 1) / (kStepThreads / 2)),
+                 dim3(kStepThreads), smem, a);
     else if (variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
         launch_k(c, k_step<DRY, 0, false>, dim3(blocks), dim3(kStepThreads), smem, a);
     else if (k <= 10)  // register top-k list
@@ -635,14 +666,14 @@ cudaError_t enqueue_scatter(orca_ctx* c, Domain& d, int bump, bool props = true)
 // Neighbour exchange of one step: every strip sends its L/R buffers and receives its
 // neighbours'.  Loopback: device copies between the strips of this context.  NCCL: one
 // group of send/recv with ranks +-1.
-orca_status enqueue_exchange(orca_ctx* c) {
+orca_status enqueue_exchange(orca_ctx* c, cudaStream_t st) {
     if (c->world == 1) return ORCA_OK;
     if (c->transport == 0) {  // peer memory: exact-size remote stores + arrival flags
         for (Domain& d : c->doms) {
             if (d.g.hasL)
-                k_push<<<kPushBlocks, 256, 0, c->stream>>>(d.sendL.b, d.peerL[0], d.peerL[1], d.ctr, d.pushDone);
+                k_push<<<kPushBlocks, 256, 0, st>>>(d.sendL.b, d.peerL[0], d.peerL[1], d.ctr, d.pushDone);
             if (d.g.hasR)
-                k_push<<<kPushBlocks, 256, 0, c->stream>>>(d.sendR.b, d.peerR[0], d.peerR[1], d.ctr, d.pushDone + 1);
+                k_push<<<kPushBlocks, 256, 0, st>>>(d.sendR.b, d.peerR[0], d.peerR[1], d.ctr, d.pushDone + 1);
         }
         CK(cudaGetLastError());
         return ORCA_OK;
@@ -653,10 +684,10 @@ orca_status enqueue_exchange(orca_ctx* c) {
             Domain& d = c->doms[s];
             if (d.g.hasR)
                 CK(cudaMemcpyAsync(c->doms[s + 1].recvL.base, d.sendR.base, d.sendR.bytes, cudaMemcpyDeviceToDevice,
-                                   c->stream));
+                                   st));
             if (d.g.hasL)
                 CK(cudaMemcpyAsync(c->doms[s - 1].recvR.base, d.sendL.base, d.sendL.bytes, cudaMemcpyDeviceToDevice,
-                                   c->stream));
+                                   st));
         }
         return ORCA_OK;
     }
@@ -665,12 +696,12 @@ orca_status enqueue_exchange(orca_ctx* c) {
     ncclResult_t r = N.groupStart();
     if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
     if (d.g.hasL) {
-        r = N.send(d.sendL.base, d.sendL.bytes, ncclUint8, c->rank - 1, c->comm, c->stream);
-        if (r == ncclSuccess) r = N.recv(d.recvL.base, d.recvL.bytes, ncclUint8, c->rank - 1, c->comm, c->stream);
+        r = N.send(d.sendL.base, d.sendL.bytes, ncclUint8, c->rank - 1, c->comm, st);
+        if (r == ncclSuccess) r = N.recv(d.recvL.base, d.recvL.bytes, ncclUint8, c->rank - 1, c->comm, st);
     }
     if (r == ncclSuccess && d.g.hasR) {
-        r = N.send(d.sendR.base, d.sendR.bytes, ncclUint8, c->rank + 1, c->comm, c->stream);
-        if (r == ncclSuccess) r = N.recv(d.recvR.base, d.recvR.bytes, ncclUint8, c->rank + 1, c->comm, c->stream);
+        r = N.send(d.sendR.base, d.sendR.bytes, ncclUint8, c->rank + 1, c->comm, st);
+        if (r == ncclSuccess) r = N.recv(d.recvR.base, d.recvR.bytes, ncclUint8, c->rank + 1, c->comm, st);
     }
     ncclResult_t r2 = N.groupEnd();
     if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
@@ -681,30 +712,58 @@ orca_status enqueue_exchange(orca_ctx* c) {
 // One step body for every strip: reset per-step counters -> k_step (query, half-planes,
 // LP2, integrate, route) -> k_lp3 (queued infeasible agents) -> exchange -> k_receive ->
 // scan -> scatter.  ev (nullable): events around the stages for orca_step_timed.
+void enqueue_receive(orca_ctx* c, cudaStream_t st) {
+    for (Domain& d : c->doms) {
+        if (d.g.hasL || d.g.hasR) {
+            StepArgs a = make_args(c, d);
+            const int capX = (d.g.hasL ? d.recvL.b.capM + d.recvL.b.capH : 0) +
+                             (d.g.hasR ? d.recvR.b.capM + d.recvR.b.capH : 0);
+            k_receive<<<cap_blocks(capX, 256), 256, 0, st>>>(a, d.recvL.b, d.recvL1.b, d.recvR.b, d.recvR1.b,
+                                                             c->transport == 0 ? 1 : 0);
+        }
+    }
+}
+
 orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
     if (ev) CK(cudaEventRecord(ev[0], c->stream));
+    bool anyOverlap = false;
     for (Domain& d : c->doms) {
         if (c->transport != 0) {  // (the peer-memory k_push empties the send buffers itself)
             if (d.g.hasL) CK(cudaMemsetAsync(d.sendL.b.hdr, 0, 16, c->stream));
             if (d.g.hasR) CK(cudaMemsetAsync(d.sendR.b.hdr, 0, 16, c->stream));
         }
         StepArgs a = make_args(c, d);
+        if (overlap_on(c, d)) {  // the boundary columns first
+            a.phase = 1;
+            anyOverlap = true;
+        }
         launch_step<false>(c, d, a);
         launch_lp3<false>(c, d, a);
     }
     CK(cudaGetLastError());
     if (ev) CK(cudaEventRecord(ev[1], c->stream));
-    CKS(enqueue_exchange(c));
-    for (Domain& d : c->doms) {
-        if (d.g.hasL || d.g.hasR) {
+    if (anyOverlap) {
+        // fork: exchange + k_receive on the side stream, the interior columns here; join
+        // before the binning of the next step
+        CK(cudaEventRecord(c->evFork, c->stream));
+        CK(cudaStreamWaitEvent(c->side, c->evFork, 0));
+        CKS(enqueue_exchange(c, c->side));
+        enqueue_receive(c, c->side);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(c->evJoin, c->side));
+        for (Domain& d : c->doms) {
+            if (!overlap_on(c, d)) continue;
             StepArgs a = make_args(c, d);
-            const int capX = (d.g.hasL ? d.recvL.b.capM + d.recvL.b.capH : 0) +
-                             (d.g.hasR ? d.recvR.b.capM + d.recvR.b.capH : 0);
-            k_receive<<<cap_blocks(capX, 256), 256, 0, c->stream>>>(a, d.recvL.b, d.recvL1.b, d.recvR.b,
-                                                                    d.recvR1.b, c->transport == 0 ? 1 : 0);
+            a.phase = 2;
+            launch_step<false>(c, d, a);
         }
+        CK(cudaGetLastError());
+        CK(cudaStreamWaitEvent(c->stream, c->evJoin, 0));
+    } else {
+        CKS(enqueue_exchange(c, c->stream));
+        enqueue_receive(c, c->stream);
+        CK(cudaGetLastError());
     }
-    CK(cudaGetLastError());
     if (ev) CK(cudaEventRecord(ev[2], c->stream));
     for (Domain& d : c->doms) CK(enqueue_scan(c, d, false));
     if (ev) CK(cudaEventRecord(ev[3], c->stream));
@@ -770,6 +829,9 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
     c->p = *params;
     *cp = c;
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMalloc(&c->partial, 1024 * 5 * sizeof(float));
     if (e == cudaSuccess) e = cudaHostAlloc(&c->gridFlagHost, sizeof(int), cudaHostAllocMapped);
     if (e == cudaSuccess) {
@@ -782,7 +844,8 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
     const void* stepFns[] = {(const void*)k_step<false, 0>,  (const void*)k_step<true, 0>,
                              (const void*)k_step<false, 10>, (const void*)k_step<true, 10>,
                              (const void*)k_step<false, 16>, (const void*)k_step<true, 16>,
-                             (const void*)k_step<false, 0, true>, (const void*)k_step<true, 0, true>};
+                             (const void*)k_step<false, 0, true>, (const void*)k_step<true, 0, true>,
+                             (const void*)k_step<false, 0, false, true>, (const void*)k_step<true, 0, false, true>};
     const int stepSmemMax = c->smemBytes + 3 * std::max(params->maxNeighbors, 1) * 4 * kStepThreads;  // + inline LP3
     for (const void* f : stepFns)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, stepSmemMax);
@@ -803,6 +866,9 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step<false, 0, false>, kStepThreads, smemInl);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         c->inlineBelow = (int64_t)blocks * sms * kStepThreads;
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step<false, 0, false, true>, kStepThreads, smemInl);
+        c->pairBelow = (int64_t)blocks * sms * (kStepThreads / 2);
     }
     if (e != cudaSuccess) return cuda_fail(e, "orca_create");
     return ORCA_OK;
@@ -1408,6 +1474,7 @@ void orca_destroy(orca_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->side) cudaStreamSynchronize(c->side);
     drop_graph(c);
     for (Domain& d : c->doms) d.release();
     dfree(c->stage);
@@ -1448,6 +1515,9 @@ void orca_destroy(orca_ctx* c) {
         if (e) cudaEventDestroy(e);
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->evFork) cudaEventDestroy(c->evFork);
+    if (c->evJoin) cudaEventDestroy(c->evJoin);
     delete c;
 }
 
@@ -2120,6 +2190,7 @@ orca_status orca_get_launch_info(orca_ctx* c, int32_t info[4]) {
     int n = 0;
     for (const Domain& d : c->doms) {
         n += pick_lp3_inline(c, d) ? 3 : 4;
+        if (overlap_on(c, d)) n += 1;  // the step kernel twice: boundary, then interior columns
         if (d.g.hasL || d.g.hasR) {  // strips: k_receive, and k_push per neighbour (peer memory)
             n += 1;
             if (c->transport == 0) n += (d.g.hasL ? 1 : 0) + (d.g.hasR ? 1 : 0);
@@ -2138,6 +2209,15 @@ orca_status orca_get_comm_info(orca_ctx* c, int32_t info[3]) {
     info[0] = c->world;
     info[1] = c->rank;
     info[2] = c->world > 1 ? c->commRanks : 1;
+    return ORCA_OK;
+}
+
+orca_status orca_set_overlap(orca_ctx* c, int32_t mode) {
+    if (!c || mode < -1 || mode > 1) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be -1 (auto), 0 or 1");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    drop_graph(c);
+    c->overlapMode = mode;
     return ORCA_OK;
 }
 
@@ -2208,7 +2288,7 @@ orca_status orca_get_active(orca_ctx* c, uint8_t* active) {
 }
 
 orca_status orca_set_variant(orca_ctx* c, int32_t variant) {
-    if (!c || variant < -1 || variant > 3) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be -1, 0, 1, 2 or 3");
+    if (!c || variant < -1 || variant > 4) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be -1, 0, 1, 2, 3 or 4");
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->variant = variant;

@@ -18,6 +18,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <climits>
 
 namespace orca {
 
@@ -710,6 +711,115 @@ __device__ __forceinline__ int lp2_greedy(const Lines& L, int T, int n, int kmax
     return failed;
 }
 
+// ---- LP2 on a lane pair (variant 4): the two lanes of an agent split the
+// greedy violation scan and LP1's earlier lines; max/min combines are exact and the tie rule
+// (lowest slot) is kept, so the result is lp2_greedy's bit for bit.  An LP1 failure (rare:
+// once per infeasible agent) is redone serially by the pair's first lane, so the g2 flags and
+// the work counters are exactly those of the serial LP1 (which stops at the failing line).
+// Both lanes call it with identical arguments; `pm` is the pair's two lanes, h = lane & 1;
+// only lane 0's fl / work counters are meaningful.
+template <bool CNT>
+__device__ __forceinline__ bool lp1_pair(const Lines& L, int T, int no, float r, float optx, float opty, float& vx,
+                                         float& vy, uint32_t& fl, WorkT& w, unsigned pm, int h) {
+    const float2 ni = L.n[no * T];
+    const float nix = ni.x, niy = ni.y, si = L.s[no * T];
+    const float disc = (r - si) * (r + si);
+    if (disc < 0.0f) return false;  // (both lanes: the serial lp1 fails before any line)
+    const float sq = sqrtf(disc);
+    float tL = -sq, tR = sq;
+    const float Dx = niy, Dy = -nix;
+    bool failp = false;
+    uint32_t g2 = 0;
+    for (int j = h; j < no; j += 2) {
+        const float2 nj = L.n[j * T];
+        const float njx = nj.x, njy = nj.y, sj = L.s[j * T];
+        const float den = fmaf(njx, Dx, njy * Dy);
+        const float num = sj - si * fmaf(njx, nix, njy * niy);
+        if (fabsf(den) <= kEps) {
+            if (fabsf(num) <= 2e-5f * r + 1e-6f) g2 = FL_G2;
+            if (num > 0.0f) failp = true;
+            continue;
+        }
+        const float t = num / den;
+        if (den > 0.0f)
+            tL = fmaxf(tL, t);
+        else
+            tR = fminf(tR, t);
+    }
+    tL = fmaxf(tL, __shfl_xor_sync(pm, tL, 1));
+    tR = fminf(tR, __shfl_xor_sync(pm, tR, 1));
+    const int ofail = __shfl_xor_sync(pm, (int)failp, 1);  // (not inside || : both lanes must shuffle)
+    failp = failp || ofail != 0;
+    g2 |= __shfl_xor_sync(pm, g2, 1);
+    if (failp || tL > tR) {
+        if (h == 0) {  // exact flags and counters of the serial lp1 (which fails too)
+            float ux = vx, uy = vy;
+            lp1<CNT>(L, T, no, r, optx, opty, false, ux, uy, fl, w);
+        }
+        return false;
+    }
+    if (CNT && h == 0) w.lp1 += (uint32_t)no;
+    fl |= g2;
+    const float od = fmaf(optx, Dx, opty * Dy);
+    const float t = fminf(fmaxf(od, tL), tR);
+    vx = fmaf(t, Dx, si * nix);
+    vy = fmaf(t, Dy, si * niy);
+    return true;
+}
+
+template <bool CNT>
+__device__ __forceinline__ int lp2_greedy_pair(const Lines& L, int T, int n, int kmax, float r, float optx,
+                                               float opty, float& vx, float& vy, uint32_t& fl, WorkT& w,
+                                               unsigned mask, unsigned pm, int h) {
+    const float l2 = fmaf(optx, optx, opty * opty);
+    if (l2 > r * r) {
+        const float sc = r / sqrtf(l2);
+        vx = optx * sc;
+        vy = opty * sc;
+    } else {
+        vx = optx;
+        vy = opty;
+    }
+    int failed = n;
+    bool done = n == 0;
+    for (int t = 0; t < kmax; ++t) {
+        if (!__any_sync(mask, !done)) break;  // (both lanes of a pair share `done`)
+        if (done) continue;
+        float best = 0.0f;
+        int bi = -1;
+        for (int q = t + h; q < n; q += 2) {
+            if (CNT) ++w.checks;
+            const float2 nq = L.n[q * T];
+            const float pen = L.s[q * T] - fmaf(nq.x, vx, nq.y * vy);
+            if (pen > best) {
+                best = pen;
+                bi = q;
+            }
+        }
+        // the larger penetration; equal ones -> the lower slot (the serial scan's first)
+        const float ob = __shfl_xor_sync(pm, best, 1);
+        const int oi = __shfl_xor_sync(pm, bi, 1);
+        if (oi >= 0 && (ob > best || (ob == best && (bi < 0 || oi < bi)))) {
+            best = ob;
+            bi = oi;
+        }
+        if (bi < 0) {
+            done = true;
+            continue;
+        }
+        if (bi != t && h == 0) line_swap(L, T, t, bi);
+        __syncwarp(pm);
+        const float tx = vx, ty = vy;
+        if (!lp1_pair<CNT>(L, T, t, r, optx, opty, vx, vy, fl, w, pm, h)) {
+            vx = tx;
+            vy = ty;
+            failed = t;
+            done = true;
+        }
+    }
+    return failed;
+}
+
 // Warp-synchronised LP2 / LP3: the same arithmetic as lp2 / lp3, but every
 // lane in `mask` runs the same number (kmax) of constraint iterations -- lines it does not
 // have are skipped -- with a reconvergence point after each, so the lanes that re-solve on
@@ -1085,7 +1195,9 @@ struct StepArgs {
     unsigned long long* stats;
     int* ctr;   // per-domain counters (CT_*)
     int capW;   // work / sorted array capacity
-    int pad0;   // explicit (no implicit padding: the host compares the bytes, graph_key)
+    int phase;  // strips' halo overlap: 0 every owned agent; 1 the agents of the
+                // two boundary columns on each side (everything that can end in an edge
+                // column or leave the strip); 2 the interior columns [c0 + 2, c1 - 2)
     ExBuf sendL, sendR;
     // outputs of a dry (debug) step, indexed by global id
     float2* dbgV;
@@ -1398,6 +1510,41 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
     }
 }
 
+// ---- shared-memory staging of the warp's candidate runs by cp.async.bulk (ablation,
+// ORCA_STAGE=1).  Per warp, the union of its 32 agents' first-pass windows --
+// one contiguous run of the sorted positions per fine column -- is copied into shared memory
+// by the bulk-copy engine (one elected lane issues one copy per run and arms the warp's
+// mbarrier with the byte count), and the lanes scan their own windows from there.  Windows
+// that do not fit kStageEntries fall back to the direct reads.
+#ifndef ORCA_STAGE
+#define ORCA_STAGE 0
+#endif
+constexpr int kStageEntries = 256;  // float2 per warp (2 KB)
+constexpr int kStageCols = 6;       // fine columns per warp union
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
 // warp reconvergence points in k_step at the once-per-agent phase
 // boundaries (PHASES); the one before the final merge is always on
 #ifndef ORCA_SYNC_PHASES
@@ -1414,7 +1561,12 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
 #endif
 // KR > 0: the top-k selection runs in a register list (k <= KR); KR = 0: shared memory.
 // WU: LP2 with the paper's work units (lp2_wu) instead of per-lane re-solves.
-template <bool DRY, int KR, bool WU = false>
+// PAIR (variant 4; KR = 0, k <= 14, LP3 on the block queue or k_lp3): two lanes per agent --
+// each scans every other candidate of the runs into its own top-k list, the first lane merges
+// the two lists (exact order) into the second lane's buffer column, the lanes build every
+// other half-plane and run lp2_greedy_pair; half the per-warp dependency chain of variant 0
+// for latency-bound strips.
+template <bool DRY, int KR, bool WU = false, bool PAIR = false>
 __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(StepArgs a) {
     pdl_entry();
     constexpr bool CNT = DRY;  // only the debug variant counts work
@@ -1432,14 +1584,43 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     // owned agents are the contiguous sorted range of columns [c0, c1)
     const int o0 = (int)a.binStart[(a.g.c0 - a.g.e0) * a.g.colBins];
     const int o1 = (int)a.binStart[(a.g.c1 - a.g.e0) * a.g.colBins];
-    const int ws = blockIdx.x * T + tid;  // work slot
-    const int i = o0 + ws;                // sorted index
-    const bool active = i < o1;
-    const unsigned activeMask = __ballot_sync(0xffffffffu, active);  // lanes that step an agent
-    if (!DRY && blockIdx.x == 0 && tid == 0) {  // per-step counters (k_receive appends after CT_NOWN)
+    constexpr int APB = PAIR ? T / 2 : T;        // agents per block
+    const int h = PAIR ? (tid & 1) : 0;          // lane in the agent's pair
+    const bool lead = h == 0;                    // the lane that owns the agent's results
+    const unsigned pm = PAIR ? (3u << (tid & 30)) : (1u << (tid & 31));  // the pair's lanes
+    if (!DRY && a.phase != 2 && blockIdx.x == 0 && tid == 0) {  // per-step counters (k_receive appends after CT_NOWN)
         a.ctr[CT_NOWN] = o1 - o0;
         a.ctr[CT_EXTRA] = 0;
     }
+    // this launch's agents: [ia, ib) then [ja, jb) of the sorted order (phase 1: the two
+    // boundary columns at either side; 2: the interior; 0: all owned agents)
+    int ia = o0, ib = o1, ja = 0, jb = 0;
+    if (a.phase != 0) {
+        const int bL = (int)a.binStart[(a.g.c0 + 2 - a.g.e0) * a.g.colBins];
+        const int bR = (int)a.binStart[(a.g.c1 - 2 - a.g.e0) * a.g.colBins];
+        if (a.phase == 1) {
+            ib = bL;
+            ja = bR;
+            jb = o1;
+        } else {
+            ia = bL;
+            ib = bR;
+        }
+    }
+    const int nPh = (ib - ia) + (jb - ja);
+    if ((int)blockIdx.x * APB >= nPh) return;  // (block-uniform, before any barrier)
+    auto agent_of = [&](int wl) { return wl < ib - ia ? ia + wl : ja + (wl - (ib - ia)); };
+    const int wlin = blockIdx.x * APB + (PAIR ? (tid >> 1) : tid);
+    const int i = agent_of(wlin);          // sorted index
+    const int ws = i - o0;                 // work slot
+    const bool active = wlin < nPh;
+    // PAIR: the agent's half-planes live in the lead lane's columns; the merged neighbour
+    // list (fp32 d2 at word 2q, j at 2q + 1) in the second lane's buffer column
+    uint2* Lst0 = Lst - h;
+    uint32_t* Bf0 = Bf - h;
+    uint32_t* Bf1 = Bf0 + 1;
+    const Lines L0{reinterpret_cast<float2*>(Lst0), reinterpret_cast<float*>(Bf0)};
+    const unsigned activeMask = __ballot_sync(0xffffffffu, active);  // lanes that step an agent
     uint32_t fl = 0;
     int nColl = 0;
     bool deferred = false;
@@ -1453,6 +1634,16 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     if (blockQ) __syncthreads();
     bool queued = false;
     int cInfX = 0, cDegX = 0, cG1X = 0, cG2X = 0, cG3X = 0;  // agents this thread finished from the queue
+#if ORCA_STAGE
+    __shared__ __align__(16) float2 sStage[T / 32][kStageEntries];
+    __shared__ __align__(8) uint64_t sBar[T / 32];
+    __shared__ int sStageOff[T / 32][kStageCols + 1];
+    __shared__ int sStageS[T / 32][kStageCols];  // per column: staged position of index j = j - S
+    if (!PAIR && (tid & 31) == 0) mbar_init(&sBar[tid >> 5]);
+    __syncwarp();
+    bool staged = false;
+    int stF0 = 0;  // the union's first fine column
+#endif
     if (active) {
         const float2 pi = a.posS[i];
         const float2 vi = a.velS[i];
@@ -1551,20 +1742,73 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                     fb = min(fb, (int)fmin(fmax(floor(tx + rsx), 0.0), (double)((a.g.nx << lgC) - 1)));
                 }
                 int nb = 0;
+#if ORCA_STAGE
+                if (!PAIR && pass == 0 && mode == ((KR > 0) ? 0 : 1)) {
+                    // the warp's union window, one run per fine column, into shared memory
+                    __syncwarp(activeMask);
+                    const int w5 = tid >> 5;
+                    const int F0 = __reduce_min_sync(activeMask, fa), F1 = __reduce_max_sync(activeMask, fb);
+                    int tot = 0;
+                    bool oob = false;
+                    const bool lw = (tid & 31) == __ffs(activeMask) - 1;  // the warp's first active lane
+                    if (F1 - F0 + 1 <= kStageCols) {
+                        for (int c = 0; c <= F1 - F0; ++c) {
+                            const int fc = F0 + c;
+                            const bool mine = fa <= fc && fc <= fb;
+                            const int sb = mine ? (int)a.binStart[(fc - fe0) * nyS + lo] : INT_MAX;
+                            const int se = mine ? (int)a.binStart[(fc - fe0) * nyS + hi + 1] : INT_MIN;
+                            int S = __reduce_min_sync(activeMask, sb), E = __reduce_max_sync(activeMask, se);
+                            if (E <= S) S = E = 0;
+                            S &= ~1;               // 16-byte aligned source (even index)
+                            E = (E + 1) & ~1;      // whole 16-byte units
+                            oob |= E > a.capW + 2; // (the sorted arrays carry 2 spare entries)
+                            if (lw) {
+                                sStageOff[w5][c] = E - S;
+                                sStageS[w5][c] = S - tot;
+                            }
+                            tot += E - S;
+                        }
+                    }
+                    staged = tot > 0 && tot <= kStageEntries && F1 - F0 + 1 <= kStageCols && !oob;
+                    if (staged) {
+                        stF0 = F0;
+                        if (lw) {
+                            mbar_expect_tx(&sBar[w5], (uint32_t)tot * 8u);
+                            int off = 0;
+                            for (int c = 0; c <= F1 - F0; ++c) {
+                                const int len = sStageOff[w5][c];
+                                if (len > 0)
+                                    bulk_g2s(&sStage[w5][off], a.posS + (off + sStageS[w5][c]), (uint32_t)len * 8u,
+                                             &sBar[w5]);
+                                off += len;
+                            }
+                        }
+                        mbar_wait(&sBar[w5], 0);
+                    }
+                }
+#endif
                 for (int fc = fa; fc <= fb; ++fc) {  // one run per fine column
                     const int b = (int)a.binStart[(fc - fe0) * nyS + lo];
                     const int e = (int)a.binStart[(fc - fe0) * nyS + hi + 1];
-                    if (CNT) w.cand += (uint32_t)(e - b);
-                    int j = b;
-                    for (; j + 1 < e; j += 2) {  // 2-way unrolled: two loads in flight
-                        const float2 p0 = a.posS[j];
-                        const float2 p1 = a.posS[j + 1];
+#if ORCA_STAGE
+                    // this run's positions: staged (pass 0) or the sorted array
+                    const float2* __restrict__ psrc =
+                        (staged && pass == 0) ? &sStage[tid >> 5][0] - sStageS[tid >> 5][fc - stF0] : a.posS;
+#else
+                    const float2* __restrict__ psrc = a.posS;
+#endif
+                    if (CNT && lead) w.cand += (uint32_t)(e - b);
+                    constexpr int st = PAIR ? 2 : 1;  // PAIR: each lane every other candidate
+                    int j = b + h;
+                    for (; j + st < e; j += 2 * st) {  // 2-way unrolled: two loads in flight
+                        const float2 p0 = psrc[j];
+                        const float2 p1 = psrc[j + st];
                         const float dx0 = p0.x - pi.x, dy0 = p0.y - pi.y;
                         const float dx1 = p1.x - pi.x, dy1 = p1.y - pi.y;
                         const float d20 = fmaf(dx0, dx0, dy0 * dy0);
                         const float d21 = fmaf(dx1, dx1, dy1 * dy1);
                         const bool a0 = d20 <= thr && j != i;
-                        const bool a1 = d21 <= thr && j + 1 != i;
+                        const bool a1 = d21 <= thr && j + st != i;
                         if (a0 | a1) {
                             if (a0) {
                                 Bf[nb * T] = (uint32_t)j;
@@ -1572,7 +1816,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                                 ++nb;
                             }
                             if (a1) {
-                                Bf[nb * T] = (uint32_t)(j + 1);
+                                Bf[nb * T] = (uint32_t)(j + st);
                                 if (!ORCA_BUF1) Bff[nb * T] = d21;
                                 ++nb;
                             }
@@ -1585,7 +1829,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                         }
                     }
                     if (j < e) {
-                        const float2 p0 = a.posS[j];
+                        const float2 p0 = psrc[j];
                         const float dx0 = p0.x - pi.x, dy0 = p0.y - pi.y;
                         const float d20 = fmaf(dx0, dx0, dy0 * dy0);
                         if (d20 <= thr && j != i) {
@@ -1606,12 +1850,41 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 // exactly once (rescans / exact redos are per-lane and rare).
                 if (pass == 0 && mode == ((KR > 0) ? 0 : 1)) __syncwarp(activeMask);
                 merge(nb);
+                if (PAIR) {
+                    // the lead lane merges the two lanes' sorted lists (exact (kappa, id) order;
+                    // disjoint candidate sets) into the second lane's buffer column
+                    __syncwarp(pm);
+                    const int cA = __shfl_sync(pm, cnt, tid & 30), cB = __shfl_sync(pm, cnt, (tid & 30) + 1);
+                    const int cM = min(k, cA + cB);
+                    if (lead) {
+                        const uint2* B = Lst + 1;
+                        int ia = 0, ib = 0;
+                        for (int q = 0; q < cM; ++q) {
+                            bool takeA;
+                            if (ia >= cA) {
+                                takeA = false;
+                            } else if (ib >= cB) {
+                                takeA = true;
+                            } else {
+                                const uint2 ea = Lst[ia * T], eb = B[ib * T];
+                                takeA = cand_less(__uint_as_float(ea.x), ea.y, __uint_as_float(eb.x), eb.y, pi,
+                                                  a.posS, a.idS);
+                            }
+                            const uint2 e2 = takeA ? Lst[(ia++) * T] : B[(ib++) * T];
+                            Bf1[(2 * q) * T] = e2.x;
+                            Bf1[(2 * q + 1) * T] = e2.y;
+                        }
+                    }
+                    __syncwarp(pm);
+                    cnt = cM;
+                }
                 if (!guessed) break;
                 // Exact only if every candidate not kept -- rejected by the guessed radius
                 // (key > thrPass (1 - 2^-22)) or pruned geometrically (distance > rg) -- is
                 // strictly beyond the k-th key.
                 // kappa_k <= fk (1 + 2^-22) < thrPass (1 - 2^-22) < any rejected kappa
-                if (cnt >= k && (double)kth() < (double)thrPass * (1.0 - 0x1p-20)) break;
+                const float kthM = PAIR ? __uint_as_float(Bf1[(2 * (k - 1)) * T]) : (cnt >= k ? kth() : 0.0f);
+                if (cnt >= k && (double)kthM < (double)thrPass * (1.0 - 0x1p-20)) break;
                 // Too few within the guess (cnt < k): widen it once to ~1.5 k expected
                 // agents at the observed density, else rescan the full stencil at r_obs.
                 const float wid = (pass == 0 && cnt < k)
@@ -1631,7 +1904,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             thr = thr0;
             guessed = guessed0;
           }
-            if (cnt >= k) fk = kth();
+            if (cnt >= k) fk = PAIR ? __uint_as_float(Bf1[(2 * (k - 1)) * T]) : kth();
             cnt = min(cnt, k);
             if (KR > 0 && mode == 0) {  // neighbour indices into the shared list slots
 #pragma unroll
@@ -1639,20 +1912,23 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                     if (q < cnt) Lst[q * T] = make_uint2(__float_as_uint(R.f[q]), R.j[q]);
             }
         }
-        if (!DRY) a.rk2W[ws] = fk;  // next step's search bound (read back by k_lp3 for queued agents)
+        if (!DRY && lead) a.rk2W[ws] = fk;  // next step's search bound (read back by k_lp3 for queued agents)
 
         // Reconvergence points: each phase below runs exactly once per active lane, so the
         // warp re-forms here after the data-dependent selection (r01l).
         if (ORCA_SYNC_PHASES) __syncwarp(activeMask);
         // ---- 3. one ORCA half-plane per neighbour, nearest first (Fig. 1) -----
-        if (DRY && a.dbgNbr)  // neighbours in (distance, id) order
-            for (int q = 0; q < cnt; ++q) a.dbgNbr[(size_t)idi * k + q] = (int32_t)a.idS[Lst[q * T].y];
+        // the neighbour j's: list slots (j in .y, stride 2T words) or, PAIR, the merged list
+        uint32_t* nbrJ = PAIR ? Bf1 + T : reinterpret_cast<uint32_t*>(Lst) + 1;
+        if (DRY && a.dbgNbr && lead)  // neighbours in (distance, id) order
+            for (int q = 0; q < cnt; ++q) a.dbgNbr[(size_t)idi * k + q] = (int32_t)a.idS[nbrJ[q * 2 * T]];
         // optional randomized LP order (P:82 Seidel, reading Q8): permute the list first
-        if (a.m.lpRandom && cnt > 1)  // (the j of each 64-bit slot: stride 2T words)
-            lp_shuffle(reinterpret_cast<uint32_t*>(Lst) + 1, 2 * T, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
-        // (half-plane q overwrites list slot q in place: j is read before the write)
-        for (int q = 0; q < cnt; ++q) {
-            const uint32_t j = Lst[q * T].y;
+        if (a.m.lpRandom && cnt > 1 && lead) lp_shuffle(nbrJ, 2 * T, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
+        if (PAIR) __syncwarp(pm);
+        // (half-plane q overwrites list slot q in place: j is read before the write; PAIR: the
+        // lanes build every other half-plane into the lead lane's columns)
+        for (int q = h; q < cnt; q += (PAIR ? 2 : 1)) {
+            const uint32_t j = nbrJ[q * 2 * T];
             const float2 pj = a.posS[j];
             const float2 vj = a.velS[j];
             float nx, ny, s;
@@ -1667,8 +1943,12 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             }
             fl |= orca_line(pi.x, pi.y, vi.x, vi.y, pj.x, pj.y, vj.x, vj.y, idi, a.idS, j, Rp, R2p, a.m, nx, ny, s, coll);
             nColl += coll;
-            L.n[q * T] = make_float2(nx, ny);
-            L.s[q * T] = s;
+            L0.n[q * T] = make_float2(nx, ny);
+            L0.s[q * T] = s;
+        }
+        if (PAIR) {
+            __syncwarp(pm);
+            fl |= __shfl_xor_sync(pm, fl, 1);  // the second lane's coincidence flags (g1)
         }
 
         if (ORCA_SYNC_PHASES) __syncwarp(activeMask);
@@ -1685,14 +1965,23 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             py = aux.y;
         }
         float vx, vy;
-        if (CNT) w.lines += (uint32_t)cnt;
+        if (CNT && lead) w.lines += (uint32_t)cnt;
         // LP order (reading Q8): greedy (mode 0, default) or the sequential incremental LP over
-        // the neighbour / randomized order (modes 2 / 1; the work-unit variant's own loop)
-        const int f = a.m.lpGreedy ? lp2_greedy<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
+        // the neighbour / randomized order (modes 2 / 1; the work-unit variant's own loop);
+        // PAIR runs the greedy order only (the host falls back to variant 0 otherwise)
+#ifndef ORCA_PAIR_SERIAL_LP
+#define ORCA_PAIR_SERIAL_LP 0  // debug: the lead lane alone runs lp2_greedy
+#endif
+        const int f = (PAIR && ORCA_PAIR_SERIAL_LP)
+                          ? (lead ? lp2_greedy<CNT>(L0, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask & 0x55555555u) : 0)
+                      : PAIR ? lp2_greedy_pair<CNT>(L0, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask, pm, h)
+                      : a.m.lpGreedy ? lp2_greedy<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                       : WU         ? lp2_wu<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                       : ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                                      : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
-        if (blockQ) {
+        if (!lead) {
+            fl = 0;  // PAIR: the second lane's part is done; the lead lane finishes the agent
+        } else if (blockQ) {
             if (f < cnt) {
                 // infeasible: into the block's queue; the least-penetration LP runs after
                 // the block barrier below on a compacted set of lanes.  The LP2 point waits in
@@ -1717,7 +2006,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             // small strips (latency bound, spare issue slots): the least-penetration LP
             // runs here on the half-planes in shared memory -- the same lp3 as k_lp3, so the
             // same result -- and the agent is finished below like a feasible one
-            const unsigned lmask = __ballot_sync(activeMask, f < cnt);
+            const unsigned lmask = __ballot_sync(PAIR ? (activeMask & 0x55555555u) : activeMask, f < cnt);
             if (f < cnt) {
                 fl |= FL_INFEASIBLE;
                 // projected half-planes in the 3k words per thread the launch adds after the
@@ -1758,8 +2047,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
 
         if (ORCA_SYNC_PHASES) __syncwarp(activeMask);
         // ---- 5. integrate (explicit Euler) + next step's binning ----------------------
-        if (deferred || queued) {
-            // finished by k_lp3 / by the block queue below
+        if (deferred || queued || !lead) {
+            // finished by k_lp3 / by the block queue below (PAIR: by the lead lane)
         } else if (DRY) {
             if (a.dbgV) a.dbgV[idi] = make_float2(vx, vy);
             if (a.dbgFlags) a.dbgFlags[idi] = (uint8_t)fl;
@@ -1815,8 +2104,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                                      : Lines{reinterpret_cast<float2*>(scratch) + pcol, scratch + 2 * k * TP + pcol};
                 float vx = sw[3 * k * T + owner];  // the LP2 point stashed after s
                 float vy = sw[(3 * k + 1) * T + owner];
-                const int wso = blockIdx.x * T + owner;
-                const int io = o0 + wso;
+                const int io = agent_of(blockIdx.x * APB + (PAIR ? (owner >> 1) : owner));
+                const int wso = io - o0;
                 const float4 pr = a.propS ? a.propS[io] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
                 if (a.m.lpGreedy)
                     lp3_greedy<CNT>(Lo, P, T, TP, cnt, f, k, pr.y, vx, vy, fl2, w, xmask);

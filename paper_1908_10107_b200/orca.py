@@ -30,7 +30,7 @@ EXPORTS = [
     "orca_nccl_unique_id", "orca_create_dist", "orca_get_local_state", "orca_debug_work",
     "orca_create_strips", "orca_partition_columns", "orca_get_strips", "orca_set_variant",
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
-    "orca_set_lp_order", "orca_set_lp3_lanes", "orca_set_lp3_inline", "orca_rebalance", "orca_set_transport",
+    "orca_set_lp_order", "orca_set_lp3_lanes", "orca_set_lp3_inline", "orca_set_overlap", "orca_rebalance", "orca_set_transport",
     "orca_get_transport", "orca_set_state", "orca_set_state_async", "orca_get_state_async",
     "orca_io_wait", "orca_get_launch_info", "orca_probe_alu", "orca_get_comm_info",
 ]
@@ -96,6 +96,7 @@ def _load():
         "orca_set_lp_order": [vp, i32, ctypes.c_uint64, i64],
         "orca_set_lp3_lanes": [vp, i32],
         "orca_set_lp3_inline": [vp, i32],
+        "orca_set_overlap": [vp, i32],
         "orca_rebalance": [vp],
         "orca_set_transport": [vp, i32],
         "orca_get_transport": [vp, P(i32)],
@@ -378,6 +379,11 @@ class Orca:
         """Re-partition the strips from the current state (automatic when a strip nears its
         capacities; every rank must call it together)."""
         _check(_lib.orca_rebalance(self._ctx))
+
+    def set_overlap(self, mode: int):
+        """Strips: -1 automatic, 0 off, 1 on -- boundary columns first, exchange concurrent
+        with the interior columns."""
+        _check(_lib.orca_set_overlap(self._ctx, mode))
 
     def set_lp3_inline(self, mode: int):
         """-1 automatic, 0 always queue for k_lp3, 1 inside the step kernel per thread, 2 inside

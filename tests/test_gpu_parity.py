@@ -475,6 +475,39 @@ def test_strips_bit_identical(orca, strips, config, n):
     b.close()
 
 
+@pytest.mark.parametrize("strips,transport", [(2, 0), (4, 0), (4, 1), (8, 0)])
+def test_strips_overlap_bit_identical(orca, strips, transport):
+    """Halo overlap (orca_set_overlap): boundary columns first, the exchange and
+    k_receive on a second stream while the interior columns step -- bit-identical to the
+    un-overlapped strips and to one strip, with both transports; the step launches the step
+    kernel twice per overlapping strip."""
+    w = W.make("uniform", n=80000)
+    a, p = _ctx(orca, w)
+    runs = []
+    for mode in (0, 1):
+        b = orca.Orca(p, strips=strips)
+        b.set_agents(w["pos"], w["vel"], w["pref"])
+        b.set_transport(transport)
+        b.set_overlap(mode)
+        runs.append(b)
+    k0, k1 = runs[0].launch_info()["kernels_per_step"], runs[1].launch_info()["kernels_per_step"]
+    assert k1 == k0 + strips  # every strip here has >= 4 columns
+    for chunk in (1, 9, 30):
+        a.step(chunk)
+        ref = a.get_state()
+        for b in runs:
+            b.step(chunk)
+            st = b.get_state()
+            assert np.array_equal(ref[0], st[0]) and np.array_equal(ref[1], st[1]), chunk
+    sa = a.stats()
+    for b in runs:
+        sb = b.stats()
+        for key in ("infeasible", "degenerate", "collision_pairs"):
+            assert sa[key] == sb[key], key
+        b.close()
+    a.close()
+
+
 def test_strips_goals_circle(orca):
     """Goal seeking through the strips (the circle's agents cross every strip)."""
     w = W.make("circle")
@@ -495,29 +528,34 @@ def test_strips_goals_circle(orca):
 @pytest.mark.parametrize("config,n,rho", [("uniform", 20000, 0.25), ("dense", 20000, None), ("uniform", 5000, 0.02)])
 def test_variants_bit_identical(orca, config, n, rho, order):
     """Thread-per-agent with a shared-memory (0) or register (2) top-k list, the
-    8-lane-group-per-agent kernel (1) and the work-unit LP2 (3): same neighbours, velocities
+    8-lane-group-per-agent kernel (1), the work-unit LP2 (3) and two lanes per agent (4): same
+    neighbours, velocities
     and trajectories bit for bit (exact comparators; the group and work-unit LPs use exact
     min/max reductions), in the greedy LP order (0, default) and the sequential neighbour
     order (2, where variant 3 runs the work units).  The work-unit LP also reproduces every
     flag and work counter."""
     w = W.make(config, n=n, rho=rho) if rho else W.make(config, n=n)
     ctxs = []
-    for v in (0, 1, 2, 3):
+    for v in (0, 1, 2, 3, 4):
         o, p = _ctx(orca, w)
         o.set_variant(v)
         o.set_lp_order(order)
         ctxs.append(o)
     r = [o.debug_step() for o in ctxs]
-    for q in (1, 2, 3):
+    for q in (1, 2, 3, 4):
         assert np.array_equal(r[0][2], r[q][2]) and np.array_equal(r[0][3], r[q][3])
         assert np.array_equal(r[0][0], r[q][0])
         assert np.array_equal(r[0][1] & 1, r[q][1] & 1)
     assert np.array_equal(r[0][1], r[3][1])
     assert ctxs[0].work() == ctxs[3].work()
+    # the lane-pair variant (4; greedy order only, else it runs as 0) reproduces every flag and
+    # work counter too
+    assert np.array_equal(r[0][1], r[4][1])
+    assert ctxs[0].work() == ctxs[4].work()
     for o in ctxs:
         o.step(25)
     s = [o.get_state() for o in ctxs]
-    for q in (1, 2, 3):
+    for q in (1, 2, 3, 4):
         assert np.array_equal(s[0][0], s[q][0]) and np.array_equal(s[0][1], s[q][1])
     for o in ctxs:
         o.close()
@@ -830,15 +868,15 @@ def test_lp3_lanes_bit_identical(orca, config, n, k):
                                             ("uniform", 3001, 3, False), ("dense", 40000, 10, True)])
 def test_lp3_modes_bit_identical(orca, config, n, k, het):
     """Where LP3 runs -- the k_lp3 kernel (0), per thread inside k_step (1), k_step's block-local
-    compacted queue (2, two rounds when more than half a block is infeasible) -- changes
-    nothing: dry-step velocities / flags / lists / work counters and 15 real steps (state and
+    compacted queue (2, several rounds when more than half a block is infeasible) -- changes
+    nothing, for the thread-per-agent (0) and the lane-pair (4; k <= 14) kernels: dry-step velocities / flags / lists / work counters and 15 real steps (state and
     statistics) bit for bit, with heterogeneous agents and goals too."""
     w = W.make(config, n=n) if config == "dense" else W.make(config, n=n, rho=0.6)
     rng = np.random.default_rng(3)
     ctxs = []
-    for mode in (0, 1, 2):
+    for mode, variant in ((0, 0), (1, 0), (2, 0), (0, 4), (2, 4)):
         o, _ = _ctx(orca, w, maxNeighbors=k)
-        o.set_variant(0)
+        o.set_variant(variant)
         if het:
             props = _het_props(n, seed=21)
             o.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
@@ -850,7 +888,7 @@ def test_lp3_modes_bit_identical(orca, config, n, k, het):
     r = [o.debug_step() for o in ctxs]
     assert np.count_nonzero(r[0][1] & 1) > 0
     wk = [o.work() for o in ctxs]
-    for q in (1, 2):
+    for q in range(1, len(ctxs)):
         for x, y in zip(r[0], r[q]):
             assert np.array_equal(x, y), q
         assert wk[0] == wk[q], q
@@ -858,7 +896,7 @@ def test_lp3_modes_bit_identical(orca, config, n, k, het):
         o.step(15)
     s = [o.get_state() for o in ctxs]
     st = [o.stats() for o in ctxs]
-    for q in (1, 2):
+    for q in range(1, len(ctxs)):
         assert np.array_equal(s[0][0], s[q][0]) and np.array_equal(s[0][1], s[q][1]), q
         assert st[0] == st[q], q
     for o in ctxs:
