@@ -1229,6 +1229,9 @@ constexpr int kStepThreads = ORCA_STEP_THREADS;
 #define ORCA_BUF_EXTRA 14  // candidate buffer = k + this many entries
 #endif
 __host__ __device__ constexpr int step_buf_words(int k) { return k + ORCA_BUF_EXTRA; }
+#ifndef ORCA_SCAN_UNROLL
+#define ORCA_SCAN_UNROLL 2  // candidates per scan iteration (2: r01; see DESIGN.md §12 r02)
+#endif
 #ifndef ORCA_BUF1
 #define ORCA_BUF1 1  // 1: the buffer keeps j only; the merge recomputes the fp32 d2 (r01o: -8 %)
 #endif
@@ -1364,14 +1367,17 @@ __device__ __forceinline__ bool exact_less(uint32_t ja, uint32_t jb, float2 pi, 
 #endif
 // List entries are (fp32 d2 bits, j) pairs in one 64-bit shared-memory slot each: a shift
 // step of the insertion is one 64-bit load and one 64-bit store.
+// allIn: every buffered candidate has fp32 d2 <= a pass threshold below nd2Lo, i.e. is surely
+// strictly within r_obs (in_radius would return true at its first compare).
 __device__ __forceinline__ int merge_candidates(uint2* Lst, int cnt, int k, const uint32_t* Bf,
                                                 const float* Bff, int nb, float2 pi, const Model& m,
-                                                const float2* __restrict__ posS, const uint32_t* __restrict__ idS) {
+                                                const float2* __restrict__ posS, const uint32_t* __restrict__ idS,
+                                                bool allIn = false) {
     constexpr int T = kStepThreads;
     for (int b = 0; b < nb; ++b) {
         const uint32_t j = Bf[b * T];
         const float f = buf_d2(Bff, b, j, pi, posS);
-        if (!in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
+        if (!allIn && !in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
         if (ORCA_FAST_MERGE && f > 1e-30f) {
             const float fhi = f * (1.0f + 0x1p-19f), flo = f * (1.0f - 0x1p-19f);
             int p = cnt;
@@ -1609,9 +1615,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     }
     const int nPh = (ib - ia) + (jb - ja);
     if ((int)blockIdx.x * APB >= nPh) return;  // (block-uniform, before any barrier)
-    auto agent_of = [&](int wl) { return wl < ib - ia ? ia + wl : ja + (wl - (ib - ia)); };
     const int wlin = blockIdx.x * APB + (PAIR ? (tid >> 1) : tid);
-    const int i = agent_of(wlin);          // sorted index
+    const int i = wlin < ib - ia ? ia + wlin : ja + (wlin - (ib - ia));  // sorted index
     const int ws = i - o0;                 // work slot
     const bool active = wlin < nPh;
     // PAIR: the agent's half-planes live in the lead lane's columns; the merged neighbour
@@ -1709,11 +1714,12 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             const float thr0 = thr;
             const bool guessed0 = guessed;
             int mode = (KR > 0) ? 0 : 1;
+            bool allIn = false;  // this pass's threshold is below nd2Lo (set at each pass start)
             auto merge = [&](int nb) {
                 if (KR > 0 && mode == 0)
                     reg_merge<(KR > 0 ? KR : 1)>(R, cnt, Bf, Bff, nb, pi, a.m, a.posS, tie);
                 else
-                    cnt = merge_candidates(Lst, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS);
+                    cnt = merge_candidates(Lst, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS, allIn);
             };
             auto kth = [&]() -> float {  // fp32 d2 of the k-th (valid when cnt >= k)
                 if (KR > 0 && mode == 0) return reg_f<(KR > 0 ? KR : 1)>(R, k - 1);
@@ -1723,6 +1729,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             if (KR > 0 && mode == 0) reg_clear<(KR > 0 ? KR : 1)>(R);
             for (int pass = 0; pass < 3; ++pass) {
                 const float thrPass = thr;
+                allIn = thr < a.m.nd2Lo;
                 // sub-row window and fine-column range for this pass
                 int lo = rlo, hi = rhi - 1, fa = f0, fb = f1;
                 if (guessed) {
@@ -1799,28 +1806,32 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
 #endif
                     if (CNT && lead) w.cand += (uint32_t)(e - b);
                     constexpr int st = PAIR ? 2 : 1;  // PAIR: each lane every other candidate
+                    constexpr int U = ORCA_SCAN_UNROLL;  // candidates per iteration (loads in flight)
                     int j = b + h;
-                    for (; j + st < e; j += 2 * st) {  // 2-way unrolled: two loads in flight
-                        const float2 p0 = psrc[j];
-                        const float2 p1 = psrc[j + st];
-                        const float dx0 = p0.x - pi.x, dy0 = p0.y - pi.y;
-                        const float dx1 = p1.x - pi.x, dy1 = p1.y - pi.y;
-                        const float d20 = fmaf(dx0, dx0, dy0 * dy0);
-                        const float d21 = fmaf(dx1, dx1, dy1 * dy1);
-                        const bool a0 = d20 <= thr && j != i;
-                        const bool a1 = d21 <= thr && j + st != i;
-                        if (a0 | a1) {
-                            if (a0) {
-                                Bf[nb * T] = (uint32_t)j;
-                                if (!ORCA_BUF1) Bff[nb * T] = d20;
-                                ++nb;
+                    for (; j + (U - 1) * st < e; j += U * st) {
+                        float2 pu[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) pu[u] = psrc[j + u * st];
+                        bool hit[U];
+                        float d2u[U];
+                        bool any = false;
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const float dx = pu[u].x - pi.x, dy = pu[u].y - pi.y;
+                            d2u[u] = fmaf(dx, dx, dy * dy);
+                            hit[u] = d2u[u] <= thr && j + u * st != i;
+                            any |= hit[u];
+                        }
+                        if (any) {
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                if (hit[u]) {
+                                    Bf[nb * T] = (uint32_t)(j + u * st);
+                                    if (!ORCA_BUF1) Bff[nb * T] = d2u[u];
+                                    ++nb;
+                                }
                             }
-                            if (a1) {
-                                Bf[nb * T] = (uint32_t)(j + st);
-                                if (!ORCA_BUF1) Bff[nb * T] = d21;
-                                ++nb;
-                            }
-                            if (nb >= capB - 1) {  // buffer (nearly) full: merge, tighten
+                            if (nb > capB - U) {  // buffer (nearly) full: merge, tighten
                                 merge(nb);
                                 nb = 0;
                                 if (cnt >= k)  // any key <= the k-th has fp32 d2 <= fk (1 + 2^-20)
@@ -1828,7 +1839,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                             }
                         }
                     }
-                    if (j < e) {
+                    for (; j < e; j += st) {  // the remainder (< U candidates)
                         const float2 p0 = psrc[j];
                         const float dx0 = p0.x - pi.x, dy0 = p0.y - pi.y;
                         const float d20 = fmaf(dx0, dx0, dy0 * dy0);
@@ -1837,7 +1848,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                             if (!ORCA_BUF1) Bff[nb * T] = d20;
                             ++nb;
                         }
-                        if (nb >= capB - 1) {
+                        if (nb > capB - U) {
                             merge(nb);
                             nb = 0;
                             if (cnt >= k) thr = fminf(thr, __fmul_ru(kth(), 1.0f + 0x1p-20f));
@@ -1990,6 +2001,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 queued = true;
                 Bf[k * T] = __float_as_uint(vx);
                 Bf[(k + 1) * T] = __float_as_uint(vy);
+                Bf[(k + 2) * T] = (uint32_t)ws;  // (the executor finds the agent from its column)
                 const unsigned mask = __activemask();
                 const int lane = tid & 31;
                 const int leader = __ffs(mask) - 1;
@@ -2104,8 +2116,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                                      : Lines{reinterpret_cast<float2*>(scratch) + pcol, scratch + 2 * k * TP + pcol};
                 float vx = sw[3 * k * T + owner];  // the LP2 point stashed after s
                 float vy = sw[(3 * k + 1) * T + owner];
-                const int io = agent_of(blockIdx.x * APB + (PAIR ? (owner >> 1) : owner));
-                const int wso = io - o0;
+                const int wso = (int)reinterpret_cast<uint32_t*>(sw)[(3 * k + 2) * T + owner];
+                const int io = o0 + wso;
                 const float4 pr = a.propS ? a.propS[io] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
                 if (a.m.lpGreedy)
                     lp3_greedy<CNT>(Lo, P, T, TP, cnt, f, k, pr.y, vx, vy, fl2, w, xmask);
