@@ -1169,6 +1169,40 @@ __device__ __forceinline__ void lp3_sync(const Lines& L, const Lines& P, int T, 
     }
 }
 
+// The least-penetration LP as an out-of-line call inside k_step (ORCA_COLD_NOINLINE): it runs
+// once per infeasible agent, so a call costs little, while inlining it (twice: the per-thread
+// and the block-queue placements, each in both LP orders) roughly doubles k_step's code and its
+// instruction-cache footprint around the hot selection loops.
+#ifndef ORCA_COLD_NOINLINE
+#define ORCA_COLD_NOINLINE 0
+#endif
+template <bool CNT>
+__device__ __noinline__ void lp3_call(Lines L, Lines P, int T, int TP, int n, int begin, int kmax, float r, float* vxy,
+                                      uint32_t* fl, WorkT* w, unsigned mask, bool greedy) {
+    float vx = vxy[0], vy = vxy[1];
+    if (greedy)
+        lp3_greedy<CNT>(L, P, T, TP, n, begin, kmax, r, vx, vy, *fl, *w, mask);
+    else
+        lp3_sync<CNT>(L, P, T, TP, n, begin, kmax, r, vx, vy, *fl, *w, mask);
+    vxy[0] = vx;
+    vxy[1] = vy;
+}
+template <bool CNT>
+__device__ __forceinline__ void lp3_dispatch(const Lines& L, const Lines& P, int T, int TP, int n, int begin, int kmax,
+                                             float r, float& vx, float& vy, uint32_t& fl, WorkT& w, unsigned mask,
+                                             bool greedy) {
+    if (ORCA_COLD_NOINLINE) {
+        float vxy[2] = {vx, vy};
+        lp3_call<CNT>(L, P, T, TP, n, begin, kmax, r, vxy, &fl, &w, mask, greedy);
+        vx = vxy[0];
+        vy = vxy[1];
+    } else if (greedy) {
+        lp3_greedy<CNT>(L, P, T, TP, n, begin, kmax, r, vx, vy, fl, w, mask);
+    } else {
+        lp3_sync<CNT>(L, P, T, TP, n, begin, kmax, r, vx, vy, fl, w, mask);
+    }
+}
+
 // --------------------------------------------------------------------- fused step
 struct StepArgs {
     Grid g;
@@ -2026,10 +2060,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 // threads still selecting stay untouched)
                 float* Pb = reinterpret_cast<float*>(smem) + (2 * k + capB) * T;
                 const Lines P{reinterpret_cast<float2*>(Pb) + tid, Pb + 2 * k * T + tid};
-                if (a.m.lpGreedy)
-                    lp3_greedy<CNT>(L, P, T, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask);
-                else
-                    lp3_sync<CNT>(L, P, T, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask);
+                lp3_dispatch<CNT>(L, P, T, T, cnt, f, k, vmaxi, vx, vy, fl, w, lmask, a.m.lpGreedy != 0);
                 float dl = 0.0f;
                 for (int m = 0; m < cnt; ++m) {
                     const float2 nm = L.n[m * T];
@@ -2119,10 +2150,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 const int wso = (int)reinterpret_cast<uint32_t*>(sw)[(3 * k + 2) * T + owner];
                 const int io = o0 + wso;
                 const float4 pr = a.propS ? a.propS[io] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
-                if (a.m.lpGreedy)
-                    lp3_greedy<CNT>(Lo, P, T, TP, cnt, f, k, pr.y, vx, vy, fl2, w, xmask);
-                else
-                    lp3_sync<CNT>(Lo, P, T, TP, cnt, f, k, pr.y, vx, vy, fl2, w, xmask);
+                lp3_dispatch<CNT>(Lo, P, T, TP, cnt, f, k, pr.y, vx, vy, fl2, w, xmask, a.m.lpGreedy != 0);
                 float dl = 0.0f;
                 for (int m = 0; m < cnt; ++m) {
                     const float2 nm = Lo.n[m * T];
