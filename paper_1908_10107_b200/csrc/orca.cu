@@ -266,6 +266,10 @@ struct orca_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
     int overlapMode = -1;  // -1 auto (on for strips), 0 off, 1 on
+    // loopback strips: one stream per strip (fork / join by events), so the strips' kernels
+    // run concurrently like ranks on their own GPUs (peer-memory transport only)
+    std::vector<cudaStream_t> stripStream;
+    std::vector<cudaEvent_t> stripDone;
     orca_params p{};
     bool ready = false, goals = false;
     float prefSpeed = 0.0f;
@@ -520,12 +524,15 @@ int pick_lp3_lanes(const orca_ctx* c, const Domain& d) {
 // 0: queued for k_lp3, 1: inside k_step per thread, 2: inside k_step on the block's
 // compacted queue (orca_set_lp3_inline)
 bool overlap_on(const orca_ctx* c, const Domain& d);
+bool strip_streams_on(const orca_ctx* c);
 int pick_lp3_mode(const orca_ctx* c, const Domain& d) {
     const int v = pick_variant(c, d);
     if (v == 1) return 0;  // the group kernel always queues
     if (overlap_on(c, d)) return 2;  // the boundary agents' LP3 must finish inside their launch
     if (c->lp3InlineMode >= 0) return (v == 4 && c->lp3InlineMode == 1) ? 2 : c->lp3InlineMode;
-    return d.popBuild <= std::min<int64_t>(c->inlineBelow, ORCA_AUTO_LP3_INLINE_BELOW) ? 2 : 0;
+    // loopback strips on their own streams share ONE GPU: the wave rule applies to the whole crowd
+    const int64_t pop = strip_streams_on(c) ? c->nGlobal : d.popBuild;
+    return pop <= std::min<int64_t>(c->inlineBelow, ORCA_AUTO_LP3_INLINE_BELOW) ? 2 : 0;
 }
 bool pick_lp3_inline(const orca_ctx* c, const Domain& d) { return pick_lp3_mode(c, d) != 0; }
 
@@ -533,9 +540,14 @@ bool pick_lp3_inline(const orca_ctx* c, const Domain& d) { return pick_lp3_mode(
 // that can end the step in an edge column or leave the strip, since maxSpeed dt < one
 // column) step first, then their exchange and k_receive run on the side stream while the
 // interior columns step.  Needs >= 4 owned columns and the thread-per-agent kernels.
+bool strip_streams_on(const orca_ctx* c);
 bool overlap_on(const orca_ctx* c, const Domain& d) {
     if (c->world == 1 || c->overlapMode == 0 || !(d.g.hasL || d.g.hasR)) return false;
     if (pick_variant(c, d) == 1 || d.g.c1 - d.g.c0 < 4) return false;
+    if (strip_streams_on(c)) return false;  // loopback strips already overlap on their own streams
+    // automatic: only where LP3 runs inside k_step anyway (a strip within one wave of blocks);
+    // a bigger strip's k_lp3 placement is faster, and its exchange a small part of its step
+    if (c->overlapMode < 0 && d.popBuild > std::min<int64_t>(c->inlineBelow, ORCA_AUTO_LP3_INLINE_BELOW)) return false;
     return true;
 }
 
@@ -724,7 +736,53 @@ void enqueue_receive(orca_ctx* c, cudaStream_t st) {
     }
 }
 
+// Loopback strips with the peer-memory exchange on one stream per strip: each strip's whole step
+// body (k_step, k_lp3, k_push into its neighbours' receive buffers, k_receive waiting on their
+// arrival flags, scan, scatter) runs on its own stream, forked from and joined back into the
+// context stream, so the strips overlap on the GPU as ranks do on their own GPUs.  The arrival
+// flags and the step-parity receive buffers order the exchange across streams exactly as
+// across ranks; results are the single-stream ones bit for bit.
+bool strip_streams_on(const orca_ctx* c) {
+    return c->loopback && c->transport == 0 && c->stripStream.size() == c->doms.size() && c->doms.size() > 1 &&
+           !std::getenv("ORCA_ONE_STREAM");
+}
+
+orca_status enqueue_step_streams(orca_ctx* c) {
+    cudaStream_t main = c->stream;
+    CK(cudaEventRecord(c->evFork, main));
+    orca_status st = ORCA_OK;
+    for (size_t q = 0; q < c->doms.size() && st == ORCA_OK; ++q) {
+        Domain& d = c->doms[q];
+        cudaStream_t ss = c->stripStream[q];
+        cudaError_t e = cudaStreamWaitEvent(ss, c->evFork, 0);
+        if (e != cudaSuccess) {
+            st = cuda_fail(e, "cudaStreamWaitEvent");
+            break;
+        }
+        c->stream = ss;  // every enqueue below (launch_k, scan, scatter) goes to the strip's stream
+        StepArgs a = make_args(c, d);
+        launch_step<false>(c, d, a);
+        launch_lp3<false>(c, d, a);
+        if (d.g.hasL)
+            k_push<<<kPushBlocks, 256, 0, ss>>>(d.sendL.b, d.peerL[0], d.peerL[1], d.ctr, d.pushDone);
+        if (d.g.hasR)
+            k_push<<<kPushBlocks, 256, 0, ss>>>(d.sendR.b, d.peerR[0], d.peerR[1], d.ctr, d.pushDone + 1);
+        const int capX = (d.g.hasL ? d.recvL.b.capM + d.recvL.b.capH : 0) + (d.g.hasR ? d.recvR.b.capM + d.recvR.b.capH : 0);
+        k_receive<<<cap_blocks(capX, 256), 256, 0, ss>>>(a, d.recvL.b, d.recvL1.b, d.recvR.b, d.recvR1.b, 1);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = enqueue_scan(c, d, false);
+        if (e == cudaSuccess) e = enqueue_scatter(c, d, 1);
+        if (e == cudaSuccess) e = cudaEventRecord(c->stripDone[q], ss);
+        if (e != cudaSuccess) st = cuda_fail(e, "strip step");
+    }
+    c->stream = main;
+    if (st != ORCA_OK) return st;
+    for (size_t q = 0; q < c->doms.size(); ++q) CK(cudaStreamWaitEvent(main, c->stripDone[q], 0));
+    return ORCA_OK;
+}
+
 orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
+    if (!ev && strip_streams_on(c)) return enqueue_step_streams(c);
     if (ev) CK(cudaEventRecord(ev[0], c->stream));
     bool anyOverlap = false;
     for (Domain& d : c->doms) {
@@ -1416,6 +1474,19 @@ orca_status orca_create_strips(const orca_params* params, int32_t device, int32_
     c->doms.resize(nstrips);
     c->world = nstrips;
     c->loopback = true;
+    if (nstrips > 1) {
+        c->stripStream.resize(nstrips);
+        c->stripDone.resize(nstrips);
+        for (int q = 0; q < nstrips; ++q) {
+            cudaError_t e = cudaStreamCreateWithFlags(&c->stripStream[q], cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->stripDone[q], cudaEventDisableTiming);
+            if (e != cudaSuccess) {
+                orca_destroy(c);
+                *out = nullptr;
+                return cuda_fail(e, "orca_create_strips streams");
+            }
+        }
+    }
     *out = c;
     return ORCA_OK;
 }
@@ -1475,6 +1546,8 @@ void orca_destroy(orca_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->side) cudaStreamSynchronize(c->side);
+    for (cudaStream_t st : c->stripStream)
+        if (st) cudaStreamSynchronize(st);
     drop_graph(c);
     for (Domain& d : c->doms) d.release();
     dfree(c->stage);
@@ -1516,6 +1589,10 @@ void orca_destroy(orca_ctx* c) {
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->side) cudaStreamDestroy(c->side);
+    for (cudaStream_t st : c->stripStream)
+        if (st) cudaStreamDestroy(st);
+    for (cudaEvent_t ev : c->stripDone)
+        if (ev) cudaEventDestroy(ev);
     if (c->evFork) cudaEventDestroy(c->evFork);
     if (c->evJoin) cudaEventDestroy(c->evJoin);
     delete c;

@@ -1263,6 +1263,9 @@ constexpr int kStepThreads = ORCA_STEP_THREADS;
 #define ORCA_BUF_EXTRA 14  // candidate buffer = k + this many entries
 #endif
 __host__ __device__ constexpr int step_buf_words(int k) { return k + ORCA_BUF_EXTRA; }
+#ifndef ORCA_SHIFT2
+#define ORCA_SHIFT2 0  // insertion shift loop two entries per iteration (r02 sweep)
+#endif
 #ifndef ORCA_SCAN_UNROLL
 #define ORCA_SCAN_UNROLL 2  // candidates per scan iteration (2: r01; see DESIGN.md §12 r02)
 #endif
@@ -1423,6 +1426,20 @@ __device__ __forceinline__ int merge_candidates(uint2* Lst, int cnt, int k, cons
             }
             uint2* q = Lst + p * T;
             // fast path: shift while the entry below is surely farther (one fp32 compare)
+#if ORCA_SHIFT2
+            // two entries per iteration: both loads in flight before the first compare
+            while (p > 1) {
+                const uint2 o1 = q[-T], o2 = q[-2 * T];
+                if (!(fhi < __uint_as_float(o1.x))) break;
+                *q = o1;
+                q -= T;
+                --p;
+                if (!(fhi < __uint_as_float(o2.x))) break;
+                *q = o2;
+                q -= T;
+                --p;
+            }
+#endif
             while (p > 0) {
                 const uint2 o = q[-T];
                 if (!(fhi < __uint_as_float(o.x))) break;

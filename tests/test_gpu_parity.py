@@ -481,24 +481,29 @@ def test_strips_overlap_bit_identical(orca, strips, transport):
     k_receive on a second stream while the interior columns step -- bit-identical to the
     un-overlapped strips and to one strip, with both transports; the step launches the step
     kernel twice per overlapping strip."""
+    import os
     w = W.make("uniform", n=80000)
     a, p = _ctx(orca, w)
     runs = []
-    for mode in (0, 1):
-        b = orca.Orca(p, strips=strips)
-        b.set_agents(w["pos"], w["vel"], w["pref"])
-        b.set_transport(transport)
-        b.set_overlap(mode)
-        runs.append(b)
-    k0, k1 = runs[0].launch_info()["kernels_per_step"], runs[1].launch_info()["kernels_per_step"]
-    assert k1 == k0 + strips  # every strip here has >= 4 columns
-    for chunk in (1, 9, 30):
-        a.step(chunk)
-        ref = a.get_state()
-        for b in runs:
-            b.step(chunk)
-            st = b.get_state()
-            assert np.array_equal(ref[0], st[0]) and np.array_equal(ref[1], st[1]), chunk
+    os.environ["ORCA_ONE_STREAM"] = "1"  # loopback strips on one stream (else they overlap anyway)
+    try:
+        for mode in (0, 1):
+            b = orca.Orca(p, strips=strips)
+            b.set_agents(w["pos"], w["vel"], w["pref"])
+            b.set_transport(transport)
+            b.set_overlap(mode)
+            runs.append(b)
+        k0, k1 = runs[0].launch_info()["kernels_per_step"], runs[1].launch_info()["kernels_per_step"]
+        assert k1 == k0 + strips  # every strip here has >= 4 columns
+        for chunk in (1, 9, 30):
+            a.step(chunk)
+            ref = a.get_state()
+            for b in runs:
+                b.step(chunk)
+                st = b.get_state()
+                assert np.array_equal(ref[0], st[0]) and np.array_equal(ref[1], st[1]), chunk
+    finally:
+        del os.environ["ORCA_ONE_STREAM"]
     sa = a.stats()
     for b in runs:
         sb = b.stats()
@@ -506,6 +511,35 @@ def test_strips_overlap_bit_identical(orca, strips, transport):
             assert sa[key] == sb[key], key
         b.close()
     a.close()
+
+
+@pytest.mark.parametrize("strips", [2, 4, 8])
+def test_strips_own_streams_bit_identical(orca, strips):
+    """Loopback strips on one stream per strip (peer-memory exchange ordered by the arrival
+    flags and step-parity buffers across streams) equal one strip and the
+    single-stream strips bit for bit, over steps that cross a 64-step graph chunk."""
+    import os
+    w = W.make("uniform", n=60000)
+    a, p = _ctx(orca, w)
+    b = orca.Orca(p, strips=strips)
+    b.set_agents(w["pos"], w["vel"], w["pref"])
+    os.environ["ORCA_ONE_STREAM"] = "1"
+    try:
+        c = orca.Orca(p, strips=strips)
+        c.set_agents(w["pos"], w["vel"], w["pref"])
+        for chunk in (1, 70):
+            c.step(chunk)
+    finally:
+        del os.environ["ORCA_ONE_STREAM"]
+    for chunk in (1, 70):
+        a.step(chunk)
+        b.step(chunk)
+    ra, rb, rc = a.get_state(), b.get_state(), c.get_state()
+    assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[1], rb[1])
+    assert np.array_equal(ra[0], rc[0]) and np.array_equal(ra[1], rc[1])
+    assert a.stats()["infeasible"] == b.stats()["infeasible"]
+    for o in (a, b, c):
+        o.close()
 
 
 def test_strips_goals_circle(orca):
