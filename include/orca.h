@@ -220,6 +220,19 @@ orca_status orca_set_state_async(orca_ctx *ctx, const float *pos, const float *v
 orca_status orca_get_state_async(orca_ctx *ctx, float *pos, float *vel);
 orca_status orca_io_wait(orca_ctx *ctx);
 
+/* One frame of the per-frame loop in one call: upload pos_in / vel_in (float[2n] by id, like
+ * orca_set_state_async), step once, and read the stepped positions / velocities back into
+ * pos_out / vel_out (float[2n] by id, either may be NULL; like orca_get_state_async) -- no host
+ * synchronisation; complete after orca_io_wait.  Results equal orca_set_state_async ->
+ * orca_step(1) -> orca_get_state_async bit for bit.  On one strip it skips work those three
+ * calls repeat: the step's own next-step binning is left undone, the next frame bins its upload
+ * in place in the work arrays, the read-back un-permutes the work arrays, and any other call
+ * first completes the pending binning.  Strips, n = 0 or a pending grid re-derivation take the
+ * three calls.  The buffers must stay untouched until orca_io_wait (pinned host memory for the
+ * overlap).  Errors: as the three calls. */
+orca_status orca_step_io_async(orca_ctx *ctx, const float *pos_in, const float *vel_in, float *pos_out,
+                               float *vel_out);
+
 /* Number of agents currently held (multi-GPU: held by this rank). */
 orca_status orca_get_count(orca_ctx *ctx, int64_t *n);
 

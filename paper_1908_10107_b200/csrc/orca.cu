@@ -266,6 +266,9 @@ struct orca_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t evFork = nullptr, evJoin = nullptr;
     int overlapMode = -1;  // -1 auto (on for strips), 0 off, 1 on
+    // orca_step_io_async left its step's binning undone: the work arrays hold the state, the
+    // sorted arrays are stale; flush_deferred() sorts them before anything else reads them
+    bool deferred = false;
     // loopback strips: one stream per strip (fork / join by events), so the strips' kernels
     // run concurrently like ranks on their own GPUs (peer-memory transport only)
     std::vector<cudaStream_t> stripStream;
@@ -678,6 +681,19 @@ cudaError_t enqueue_scatter(orca_ctx* c, Domain& d, int bump, bool props = true)
 // Neighbour exchange of one step: every strip sends its L/R buffers and receives its
 // neighbours'.  Loopback: device copies between the strips of this context.  NCCL: one
 // group of send/recv with ranks +-1.
+// The binning orca_step_io_async skipped: scan + scatter of the work arrays the last step wrote
+// (bump: that step is complete).  No-op unless deferred.
+cudaError_t flush_deferred(orca_ctx* c) {
+    if (!c->deferred) return cudaSuccess;
+    c->deferred = false;
+    for (Domain& d : c->doms) {
+        cudaError_t e = enqueue_scan(c, d, false);
+        if (e == cudaSuccess) e = enqueue_scatter(c, d, 1);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 orca_status enqueue_exchange(orca_ctx* c, cudaStream_t st) {
     if (c->world == 1) return ORCA_OK;
     if (c->transport == 0) {  // peer memory: exact-size remote stores + arrival flags
@@ -1603,6 +1619,7 @@ orca_status orca_set_agents(orca_ctx* c, int64_t n, const float* pos, const floa
     if (n < 0 || n > ((int64_t)1 << 30)) return fail(ORCA_ERR_INVALID_ARGUMENT, "n out of range");
     if (n > 0 && (!pos || !vel || !pref)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
     CK(cudaSetDevice(c->device));
+    if (c->ready) CK(flush_deferred(c));  // (the radius hints below are read in sorted order)
     CK(cudaStreamSynchronize(c->stream));
     if (c->ioBadHost) *c->ioBadHost = 0;  // a refused asynchronous upload is superseded
     *c->gridFlagHost = 0;  // a new grid is derived below
@@ -1649,6 +1666,7 @@ orca_status orca_set_state(orca_ctx* c, const float* pos, const float* vel) {
     const int64_t n = c->nGlobal;
     if (n > 0 && (!pos || !vel)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     CK(cudaStreamSynchronize(c->stream));
     if (n == 0) return ORCA_OK;
     // everything but the kinematic state stays: preferred velocities or goals, per-agent
@@ -1684,6 +1702,7 @@ orca_status orca_set_state_async(orca_ctx* c, const float* pos, const float* vel
     if (c->world > 1 || c->doms.size() != 1) return orca_set_state(c, pos, vel);  // strips: synchronous
     if (n == 0) return ORCA_OK;
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     CKS(io_init(c));
     const int b = c->inSlot;
     c->inSlot ^= 1;
@@ -1706,12 +1725,90 @@ orca_status orca_set_state_async(orca_ctx* c, const float* pos, const float* vel
     return ORCA_OK;
 }
 
+// One frame of the per-frame loop in one call (single strip; strips fall back to the three
+// calls): upload pos_in / vel_in (copy stream 1), bin them, one step, and read the stepped state
+// back into pos_out / vel_out (copy stream 2), without host synchronisation.  Since the next
+// frame uploads a new state anyway, the step's own next-step binning is skipped: the upload is
+// binned in place in the work arrays the previous frame's step left (k_reload_work), and the
+// read-back un-permutes those work arrays (k_unpermute_work).  Any other call first completes
+// the skipped binning (flush_deferred), so results equal orca_set_state_async -> orca_step(1)
+// -> orca_get_state_async bit for bit.
+orca_status orca_step_io_async(orca_ctx* c, const float* pos_in, const float* vel_in, float* pos_out,
+                               float* vel_out) {
+    if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
+    if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    const int64_t n = c->nGlobal;
+    if (n > 0 && (!pos_in || !vel_in)) return fail(ORCA_ERR_INVALID_ARGUMENT, "null array");
+    if (c->world > 1 || c->doms.size() != 1 || n == 0 || *c->gridFlagHost) {
+        // strips, an empty crowd, or a pending grid re-derivation: the three calls
+        CKS(orca_set_state_async(c, pos_in, vel_in));
+        CKS(orca_step(c, 1));
+        return orca_get_state_async(c, pos_out, vel_out);
+    }
+    CK(cudaSetDevice(c->device));
+    CKS(io_init(c));
+    Domain& d = c->doms[0];
+    const int b = c->inSlot;
+    c->inSlot ^= 1;
+    float2* buf = c->inBuf[b];
+    CK(cudaStreamWaitEvent(c->ioIn, c->inFree[b], 0));
+    CK(cudaMemcpyAsync(buf, pos_in, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->ioIn));
+    CK(cudaMemcpyAsync(buf + n, vel_in, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->ioIn));
+    CK(cudaEventRecord(c->inReady[b], c->ioIn));
+    CK(cudaStreamWaitEvent(c->stream, c->inReady[b], 0));
+    const bool prevStep = c->deferred;  // the previous frame's step is complete once binned
+    if (c->deferred) {
+        // the previous frame's step left its agents in the work arrays: bin the upload there
+        CK(cudaMemsetAsync(d.count, 0, (size_t)d.nbins * sizeof(uint32_t), c->stream));
+        k_reload_work<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.ctr, d.capW, d.g, buf, buf + n, d.posW,
+                                                                      d.velW, d.idW, d.cellW, d.rankW, d.count,
+                                                                      c->gridFlagDev, c->ioBadDev);
+    } else {
+        k_reload<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(
+            d.binStart, d.g, d.idS, d.auxS, d.rk2S, c->het ? d.propS : nullptr, buf, buf + n, d.posW, d.velW, d.auxW,
+            d.idW, d.rk2W, c->het ? d.propW : nullptr, d.cellW, d.rankW, d.count, d.ctr, c->gridFlagDev, c->ioBadDev);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->inFree[b], c->stream));
+    CK(enqueue_scan(c, d, false));
+    CK(enqueue_scatter(c, d, prevStep ? 1 : 0));
+    // the step without its trailing binning
+    StepArgs a = make_args(c, d);
+    launch_step<false>(c, d, a);
+    launch_lp3<false>(c, d, a);
+    CK(cudaGetLastError());
+    c->deferred = true;
+    c->host_steps += 1;
+    c->steps_total += 1;
+    c->host_updates += n;
+    // read-back of the work arrays
+    if (pos_out || vel_out) {
+        const int ob_i = c->outSlot;
+        c->outSlot ^= 1;
+        float2* ob = c->outBuf[ob_i];
+        CK(cudaStreamWaitEvent(c->stream, c->outFree[ob_i], 0));
+        if (c->removeR > 0.0f)  // agents removed at their goal read as NaN
+            k_fill2<<<cap_blocks(2 * n, 256), 256, 0, c->stream>>>((int)(2 * n), ob, NAN);
+        k_unpermute_work<<<cap_blocks(d.capW, 256), 256, 0, c->stream>>>(d.ctr, d.capW, d.cellW, d.idW, d.posW, d.velW,
+                                                                         pos_out ? ob : nullptr,
+                                                                         vel_out ? ob + n : nullptr);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(c->outReady[ob_i], c->stream));
+        CK(cudaStreamWaitEvent(c->ioOut, c->outReady[ob_i], 0));
+        if (pos_out) CK(cudaMemcpyAsync(pos_out, ob, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->ioOut));
+        if (vel_out) CK(cudaMemcpyAsync(vel_out, ob + n, (size_t)n * sizeof(float2), cudaMemcpyDefault, c->ioOut));
+        CK(cudaEventRecord(c->outFree[ob_i], c->ioOut));
+    }
+    return ORCA_OK;
+}
+
 orca_status orca_set_goals(orca_ctx* c, const float* goal, float prefSpeed) {
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     if (!(prefSpeed >= 0.0f) || !std::isfinite(prefSpeed)) return fail(ORCA_ERR_INVALID_ARGUMENT, "prefSpeed");
     if (c->nGlobal > 0 && !goal) return fail(ORCA_ERR_INVALID_ARGUMENT, "null goal");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     const int64_t n = c->nGlobal;
     if (n > 0) {
         // goals arrive in id order (global): check finiteness, gather into sorted order
@@ -1737,6 +1834,7 @@ orca_status orca_step(orca_ctx* c, int32_t n_steps) {
     if (n_steps < 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "n_steps < 0");
     if (n_steps == 0) return ORCA_OK;
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     // one graph of up to kChunk step bodies, replayed
     const int kChunk = 64;
     int remaining = n_steps;
@@ -1820,6 +1918,7 @@ orca_status orca_step_timed(orca_ctx* c, int32_t n_steps, double ms[4]) {
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     if (n_steps < 0) return fail(ORCA_ERR_INVALID_ARGUMENT, "n_steps < 0");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     for (int q = 0; q < 4; ++q) ms[q] = 0.0;
     for (int s = 0; s < n_steps; ++s) {
         if (s % 64 == 0) CKS(maybe_rebalance(c));
@@ -1847,6 +1946,7 @@ orca_status orca_get_state(orca_ctx* c, float* pos, float* vel) {
     if (c->world > 1 && !c->loopback)
         return fail(ORCA_ERR_INVALID_ARGUMENT, "multi-rank context: use orca_get_local_state");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     CKS(check_overflow(c));
     const int64_t n = c->nGlobal;
     if (n > 0 && (pos || vel)) {
@@ -1875,6 +1975,7 @@ orca_status orca_get_state_async(orca_ctx* c, float* pos, float* vel) {
     const int64_t n = c->nGlobal;
     if (n == 0 || (!pos && !vel)) return ORCA_OK;
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     CKS(io_init(c));
     const int b = c->outSlot;
     c->outSlot ^= 1;
@@ -1918,6 +2019,7 @@ orca_status orca_get_count(orca_ctx* c, int64_t* n) {
         return ORCA_OK;
     }
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     int64_t t = 0;
     for (Domain& d : c->doms) {
         int o0, o1;
@@ -1932,6 +2034,7 @@ orca_status orca_get_local_state(orca_ctx* c, int32_t* ids, float* pos, float* v
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     CKS(check_overflow(c));
     size_t off = 0;
     for (Domain& d : c->doms) {
@@ -1978,6 +2081,7 @@ orca_status orca_debug_cells(orca_ctx* c, int32_t* cx, int32_t* cy) {
     if (!c || !cx || !cy) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     const int64_t n = c->nGlobal;
     if (n > 0) {
         int32_t* d0 = reinterpret_cast<int32_t*>(c->outA);  // 2 x int32 per agent
@@ -1996,6 +2100,7 @@ orca_status orca_debug_step(orca_ctx* c, float* vnew, uint8_t* flags, int32_t* n
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     const int64_t n = c->nGlobal;
     if (n == 0) return ORCA_OK;
     const int k = c->p.maxNeighbors;
@@ -2040,6 +2145,7 @@ orca_status orca_debug_work(orca_ctx* c, int64_t out[6]) {
     if (!c || !out) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     for (int q = 0; q < 6; ++q) out[q] = 0;
     if (c->nGlobal == 0) return ORCA_OK;
     Work* dW = nullptr;
@@ -2110,6 +2216,7 @@ orca_status orca_set_agent_props(orca_ctx* c, const float* radius, const float* 
     if (!c) return fail(ORCA_ERR_INVALID_ARGUMENT, "null context");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     CK(cudaStreamSynchronize(c->stream));
     const int64_t n = c->nGlobal;
     drop_graph(c);
@@ -2174,6 +2281,7 @@ orca_status orca_step_trace(orca_ctx* c, int32_t n_steps, float* frames, float* 
     if (c->world > 1 && !c->loopback)
         return fail(ORCA_ERR_INVALID_ARGUMENT, "multi-rank context: trace each rank with orca_get_local_state");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     const int64_t n = c->nGlobal;
     if (n == 0 || n_steps == 0) return orca_step(c, n_steps);
     if (!c->copyStream) {
@@ -2216,6 +2324,7 @@ orca_status orca_step_trace(orca_ctx* c, int32_t n_steps, float* frames, float* 
 orca_status orca_set_goal_removal(orca_ctx* c, float radius) {
     if (!c || !(radius >= 0.0f) || !std::isfinite(radius)) return fail(ORCA_ERR_INVALID_ARGUMENT, "radius");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->removeR = radius;
@@ -2237,6 +2346,7 @@ cudaError_t write_lp_step(orca_ctx* c) {
 orca_status orca_set_transport(orca_ctx* c, int32_t mode) {
     if (!c || (mode != 0 && mode != 1)) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     CK(cudaStreamSynchronize(c->stream));
     if (mode == c->transport) return ORCA_OK;
     c->transport = mode;
@@ -2312,6 +2422,7 @@ orca_status orca_rebalance(orca_ctx* c) {
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     if (c->world == 1) return ORCA_OK;
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     CK(cudaStreamSynchronize(c->stream));
     CKS(check_overflow(c));
     if (c->reportCap < 3 * (int)c->doms.size() + 4) {
@@ -2351,6 +2462,7 @@ orca_status orca_get_active(orca_ctx* c, uint8_t* active) {
     if (!c || !active) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
     if (!c->ready) return fail(ORCA_ERR_NOT_READY, "set_agents first");
     CK(cudaSetDevice(c->device));
+    CK(flush_deferred(c));  // (orca_step_io_async left the binning to the next reader)
     const int64_t n = c->nGlobal;
     if (n > 0) {
         uint8_t* d = reinterpret_cast<uint8_t*>(c->outA);

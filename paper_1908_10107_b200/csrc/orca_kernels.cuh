@@ -2474,6 +2474,51 @@ __global__ void k_reload(const uint32_t* __restrict__ binStart, Grid g, const ui
     if (__any_sync(0xffffffffu, ring) && (threadIdx.x & 31) == 0) *gridFlag = 1;
 }
 
+// orca_step_io_async (single strip): the upload is binned IN PLACE in the work arrays the last
+// step left behind (its own next-step binning was skipped): every valid work slot takes its new
+// pos / vel by id, keeps its id, preferred velocity / goal, radius hint and properties, and gets
+// its bin and rank.  count[] must be zero.
+__global__ void k_reload_work(const int* __restrict__ ctr, int capW, Grid g, const float2* __restrict__ pos,
+                              const float2* __restrict__ vel, float2* __restrict__ posW, float2* __restrict__ velW,
+                              const uint32_t* __restrict__ idW, uint32_t* __restrict__ cellW,
+                              uint32_t* __restrict__ rankW, uint32_t* __restrict__ count, int* gridFlag, int* bad) {
+    const int nW = min(ctr[CT_NOWN] + ctr[CT_EXTRA], capW);
+    bool nonfinite = false, ring = false;
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nW; w += gridDim.x * blockDim.x) {
+        if (cellW[w] == kInvalid) continue;  // removed at its goal
+        const uint32_t id = idW[w];
+        const float2 p = pos[id];
+        const float2 v = vel[id];
+        nonfinite |= !(isfinite(p.x) && isfinite(p.y) && isfinite(v.x) && isfinite(v.y));
+        const int fx = finecol_coord(p.x, g);
+        const int cx = fx >> g.lgC;
+        const int sy = subrow_coord(p.y, g);
+        const int cyc = sy >> g.lgS;
+        ring |= cx == 0 || cx == g.nx - 1 || cyc == 0 || cyc == g.ny - 1;
+        const uint32_t c = bin_of(fx, sy, g);
+        posW[w] = p;
+        velW[w] = v;
+        cellW[w] = c;
+        rankW[w] = atomicAdd(&count[c], 1u);
+    }
+    if (__any_sync(0xffffffffu, nonfinite) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+    if (__any_sync(0xffffffffu, ring) && (threadIdx.x & 31) == 0) *gridFlag = 1;
+}
+
+// The state after a step whose binning was skipped, by id, from the work arrays.
+__global__ void k_unpermute_work(const int* __restrict__ ctr, int capW, const uint32_t* __restrict__ cellW,
+                                 const uint32_t* __restrict__ idW, const float2* __restrict__ posW,
+                                 const float2* __restrict__ velW, float2* __restrict__ posOut,
+                                 float2* __restrict__ velOut) {
+    const int nW = min(ctr[CT_NOWN] + ctr[CT_EXTRA], capW);
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nW; w += gridDim.x * blockDim.x) {
+        if (cellW[w] == kInvalid) continue;
+        const uint32_t id = idW[w];
+        if (posOut) posOut[id] = posW[w];
+        if (velOut) velOut[id] = velW[w];
+    }
+}
+
 __global__ void k_fill1(int n, float* __restrict__ out, float v) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = v;
 }

@@ -32,7 +32,7 @@ EXPORTS = [
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
     "orca_set_lp_order", "orca_set_lp3_lanes", "orca_set_lp3_inline", "orca_set_overlap", "orca_rebalance", "orca_set_transport",
     "orca_get_transport", "orca_set_state", "orca_set_state_async", "orca_get_state_async",
-    "orca_io_wait", "orca_get_launch_info", "orca_probe_alu", "orca_get_comm_info",
+    "orca_io_wait", "orca_step_io_async", "orca_get_launch_info", "orca_probe_alu", "orca_get_comm_info",
 ]
 
 
@@ -102,6 +102,7 @@ def _load():
         "orca_get_transport": [vp, P(i32)],
         "orca_set_state": [vp, vp, vp],
         "orca_set_state_async": [vp, vp, vp],
+        "orca_step_io_async": [vp, vp, vp, vp, vp],
         "orca_get_state_async": [vp, vp, vp],
         "orca_io_wait": [vp],
         "orca_get_launch_info": [vp, P(i32)],
@@ -247,6 +248,12 @@ class Orca:
         pos / vel (float32 C-contiguous, either None); valid after io_wait()."""
         self._io_keep.extend((_io_arg(pos), _io_arg(vel)))
         _check(_lib.orca_get_state_async(self._ctx, _ptr(pos), _ptr(vel)))
+
+    def step_io_async(self, pos_in, vel_in, pos_out=None, vel_out=None):
+        """orca_step_io_async: upload, one step and read-back in one enqueued call (float32
+        C-contiguous buffers, pinned for the overlap, untouched until io_wait())."""
+        self._io_keep.extend((_io_arg(pos_in), _io_arg(vel_in), _io_arg(pos_out), _io_arg(vel_out)))
+        _check(_lib.orca_step_io_async(self._ctx, _ptr(pos_in), _ptr(vel_in), _ptr(pos_out), _ptr(vel_out)))
 
     def io_wait(self):
         """orca_io_wait: every enqueued upload, step and read-back is complete."""

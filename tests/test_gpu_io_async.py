@@ -175,3 +175,61 @@ def test_async_empty_and_strips_fallback(orca):
     assert np.array_equal(ra[0], pos) and np.array_equal(ra[1], vel)
     a.close()
     s.close()
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_step_io_equals_three_calls(orca, full):
+    """orca_step_io_async (upload + step + read-back in one call; the step's own binning is
+    deferred to the next frame's in-place reload or to whatever call reads the state next)
+    gives the synchronous loop's states bit for bit -- with goals, removal at the goal,
+    per-agent properties, the randomized LP order and an upload 400 m off the grid -- and the
+    context stays consistent for the other calls afterwards (step, get_state, stats)."""
+    import torch
+    w = W.make("uniform", n=30000 if full else 6000, rho=0.3)
+    n = len(w["pos"])
+    rng = np.random.default_rng(3)
+    goals = (w["pos"] + rng.uniform(-30, 30, w["pos"].shape)).astype(np.float32)
+    props = _props(n, 8)
+
+    def make():
+        o = orca.Orca(w["params"])
+        o.set_agents(w["pos"], w["vel"], w["pref"])
+        if full:
+            o.set_goals(goals, 1.0)
+            o.set_goal_removal(2.0)
+            o.set_agent_props(*props)
+            o.set_lp_order(True, 5, 0)
+        return o
+
+    K = 12
+    ups = _states(w, K, seed=11, far_step=7)
+    a, b = make(), make()
+    ref = []
+    for p, v in ups:
+        a.set_state(p, v)
+        a.step(1)
+        ref.append(a.get_state())
+    hp = [torch.from_numpy(p).pin_memory() for p, _ in ups]
+    hv = [torch.from_numpy(v).pin_memory() for _, v in ups]
+    op = [torch.empty((n, 2), dtype=torch.float32).pin_memory() for _ in range(K)]
+    ov = [torch.empty((n, 2), dtype=torch.float32).pin_memory() for _ in range(K)]
+    for s in range(K):
+        b.step_io_async(hp[s], hv[s], op[s], ov[s])
+        if s == 4:  # an ordinary call in between completes the pending binning first
+            b.io_wait()
+            mid = b.get_state()
+            assert np.array_equal(mid[0], ref[s][0], equal_nan=True)
+    b.io_wait()
+    for s in range(K):
+        assert np.array_equal(ref[s][0], op[s].numpy(), equal_nan=True), s
+        assert np.array_equal(ref[s][1], ov[s].numpy(), equal_nan=True), s
+    b.step(2)
+    a.step(2)
+    sa, sb = a.get_state(), b.get_state()
+    assert np.array_equal(sa[0], sb[0], equal_nan=True) and np.array_equal(sa[1], sb[1], equal_nan=True)
+    assert a.count() == b.count()
+    ta, tb = a.stats(), b.stats()
+    for key in ("steps", "infeasible", "collision_pairs", "removed"):
+        assert ta[key] == tb[key], key
+    a.close()
+    b.close()
