@@ -70,6 +70,8 @@ def parse():
                     help="--impl reference: time budget of the timed full oracle steps")
     ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--no-suite", action="store_true", help="skip the other BASELINE workloads (N=1 only)")
+    ap.add_argument("--only-timed", action="store_true",
+                    help="profiling: stop after the timed steps (no A/B sweeps, e2e, baselines); prints a short line")
     ap.add_argument("--shared-gpu", action="store_true",
                     help="test only: all ranks on GPU 0 (gloo for torch, ORCA_NCCL_LIB=tests/fake_nccl for liborca)")
     ap.add_argument("--lp3-lanes", type=int, default=-1, help="lanes per infeasible agent in the LP3 kernel (-1: auto)")
@@ -433,6 +435,14 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0].item())
         per_step_stats = [float(x) for x in t[1:].tolist()]
+    if args.only_timed:  # (ncu launch lists: the step's own kernels only)
+        if rank == 0:
+            print(json.dumps({"metric": "agent-updates/s", "ms_per_step": ms / args.steps, "only_timed": True,
+                              "launch_info": ctx.launch_info(), "config": {"workload": w["name"]}}), flush=True)
+        ctx.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
     st = ctx.stats()
     st["maintenance_in_timed_region"] = {k: st[k] - maint0[k] for k in ("rebalances", "regrids")}
     launch_info = ctx.launch_info()  # kernels per step as launched in the timed region

@@ -22,13 +22,14 @@ if [[ $WHAT == all || $WHAT == bench ]]; then
 fi
 if [[ $WHAT == all || $WHAT == ncu ]]; then
   B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-suite --e2e-steps 1"
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $B > $OUT/ncu_launch_$TAG.txt 2>&1
+  T="python bench.py --steps 10 --warmup 3 --only-timed"
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $T > $OUT/ncu_launch_$TAG.txt 2>&1
   echo "ncu launches exit $?"
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches100k_$TAG.csv $B --config uniform > /dev/null 2>&1
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches100k_$TAG.csv $T --config uniform > /dev/null 2>&1
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_step|k_lp3" -s 16 -c 2 -o $OUT/prof_kstep_$TAG $B > $OUT/ncu_full_$TAG.txt 2>&1
   echo "ncu full exit $?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_step" -s 16 -c 1 -o $OUT/prof_kstep100k_$TAG $B --config uniform > /dev/null 2>&1
-  timeout 900 ncu --set full --clock-control none -k regex:"k_scatter|k_scan" -s 4 -c 2 -o $OUT/prof_bin_$TAG $B > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none -k regex:"k_scatter|k_scan" -s 16 -c 2 -o $OUT/prof_bin_$TAG $T > /dev/null 2>&1
   echo "ncu rest exit $?"
 fi
 if [[ $WHAT == all || $WHAT == sanitize ]]; then
