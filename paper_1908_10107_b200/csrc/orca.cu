@@ -50,6 +50,10 @@ int cap_blocks(int64_t n, int threads) {
 #define ORCA_LP3_WAVES 4
 #endif
 constexpr int kPushBlocks = 64;  // k_push grid (last-block completion)
+#ifndef ORCA_REGRID_REACH
+#define ORCA_REGRID_REACH 512.0f  // steps of maxSpeed walking a re-derived grid's margin covers (r01: 128)
+#endif
+constexpr float kRegridReach = ORCA_REGRID_REACH;
 
 int lp3_blocks(int64_t n) {
     const int64_t need = (n + kStepThreads - 1) / kStepThreads;
@@ -1286,8 +1290,10 @@ orca_status rebalance(orca_ctx* c, bool regrid) {
             mn[1] = mx[1] = c->gg.oy + c->gg.cs;
         }
         // margin: agents move up to 128 maxSpeed dt before the next check sees them (a chunk of
-        // <= 64 steps is checked once the chunk after it is queued, orca_step)
-        const float reach = 128.0f * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
+        // <= 64 steps is checked once the chunk after it is queued, orca_step); the margin covers
+        // kRegridReach steps of walking, so a spreading crowd re-grids rarely (empty margin bins
+        // cost the latency-bound scan next to nothing)
+        const float reach = kRegridReach * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
         CKS(derive_grid(c, n, mn, mx, 1 + (int)std::ceil(reach / c->p.neighborDist)));
         c->regrids += 1;
     } else {
@@ -1683,7 +1689,7 @@ orca_status orca_set_state(orca_ctx* c, const float* pos, const float* vel) {
                         (mn[0] >= g.ox + g.cs && mn[1] >= g.oy + g.cs && (double)mx[0] < g.ox + (double)g.cs * (g.nx - 1) &&
                          (double)mx[1] < g.oy + (double)g.cs * (g.ny - 1));
     if (!inside) {  // the new state leaves the grid's interior: re-derive it (reading Q12)
-        const float reach = 128.0f * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
+        const float reach = kRegridReach * std::max(c->maxSpeedAll, c->p.maxSpeed) * c->p.timeStep;
         CKS(derive_grid(c, n, mn, mx, 1 + (int)std::ceil(reach / c->p.neighborDist)));
         c->regrids += 1;
     }

@@ -1146,7 +1146,7 @@ def test_long_step_call_regrids_while_running(orca):
     long_call = time.perf_counter() - t0
     for _ in range(10):
         b.step(60)
-    assert a.stats()["regrids"] >= 2
+    assert a.stats()["regrids"] >= 1  # (a re-derived grid keeps ~512 steps of walking as margin)
     sa, sb = a.get_state(), b.get_state()
     assert np.array_equal(sa[0], sb[0]) and np.array_equal(sa[1], sb[1])
     assert long_call < 0.6, long_call  # ~0.05 ms per step; an unre-gridded run took ~0.3 ms
