@@ -2408,6 +2408,10 @@ orca_status orca_get_comm_info(orca_ctx* c, int32_t info[3]) {
 orca_status orca_set_overlap(orca_ctx* c, int32_t mode) {
     if (!c || mode < -1 || mode > 1) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be -1 (auto), 0 or 1");
     CK(cudaSetDevice(c->device));
+    if (c->ready && c->deferred) {  // a pending step completes before the change
+        CK(cudaSetDevice(c->device));
+        CK(flush_deferred(c));
+    }
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->overlapMode = mode;
@@ -2417,6 +2421,10 @@ orca_status orca_set_overlap(orca_ctx* c, int32_t mode) {
 orca_status orca_set_lp3_inline(orca_ctx* c, int32_t mode) {
     if (!c || mode < -1 || mode > 2) return fail(ORCA_ERR_INVALID_ARGUMENT, "mode must be -1 (auto), 0, 1 or 2");
     CK(cudaSetDevice(c->device));
+    if (c->ready && c->deferred) {  // a pending step completes before the change
+        CK(cudaSetDevice(c->device));
+        CK(flush_deferred(c));
+    }
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->lp3InlineMode = mode;
@@ -2443,6 +2451,10 @@ orca_status orca_set_lp3_lanes(orca_ctx* c, int32_t lanes) {
     if (!c || (lanes != -1 && lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16))
         return fail(ORCA_ERR_INVALID_ARGUMENT, "lanes must be -1 (auto), 1, 4, 8 or 16");
     CK(cudaSetDevice(c->device));
+    if (c->ready && c->deferred) {  // a pending step completes before the change
+        CK(cudaSetDevice(c->device));
+        CK(flush_deferred(c));
+    }
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->lp3Lanes = lanes;
@@ -2454,6 +2466,10 @@ orca_status orca_set_lp_order(orca_ctx* c, int32_t mode, uint64_t seed, int64_t 
     if (first_step < 0 || first_step >= ((int64_t)1 << 31) - ((int64_t)1 << 24))
         return fail(ORCA_ERR_INVALID_ARGUMENT, "first_step out of range");
     CK(cudaSetDevice(c->device));
+    if (c->ready && c->deferred) {  // a pending step completes before the change
+        CK(cudaSetDevice(c->device));
+        CK(flush_deferred(c));
+    }
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->lpMode = mode;
@@ -2484,6 +2500,10 @@ orca_status orca_get_active(orca_ctx* c, uint8_t* active) {
 
 orca_status orca_set_variant(orca_ctx* c, int32_t variant) {
     if (!c || variant < -1 || variant > 4) return fail(ORCA_ERR_INVALID_ARGUMENT, "variant must be -1, 0, 1, 2, 3 or 4");
+    if (c->ready && c->deferred) {  // a pending step completes before the change
+        CK(cudaSetDevice(c->device));
+        CK(flush_deferred(c));
+    }
     CK(cudaStreamSynchronize(c->stream));
     drop_graph(c);
     c->variant = variant;

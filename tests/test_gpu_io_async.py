@@ -223,6 +223,13 @@ def test_step_io_equals_three_calls(orca, full):
     for s in range(K):
         assert np.array_equal(ref[s][0], op[s].numpy(), equal_nan=True), s
         assert np.array_equal(ref[s][1], ov[s].numpy(), equal_nan=True), s
+    # a configuration change right after a one-call frame (the pending binning completes first,
+    # so the LP-order step index the change sets is the one the next step sees)
+    b.step_io_async(hp[0], hv[0], op[0], ov[0])
+    a.set_state(*ups[0])
+    a.step(1)
+    for o in (a, b):
+        o.set_lp_order(True, 9, 77)
     b.step(2)
     a.step(2)
     sa, sb = a.get_state(), b.get_state()
