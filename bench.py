@@ -365,6 +365,10 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    if world > 1:
+        # NCCL's own init lines (communicator size per rank) on stderr, for the driver's checks
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if world != args.gpus:
         sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
         sys.exit(2)
