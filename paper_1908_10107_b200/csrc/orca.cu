@@ -568,8 +568,8 @@ std::vector<unsigned char> graph_key(orca_ctx* c) {
         const unsigned char* b = static_cast<const unsigned char*>(p);
         k.insert(k.end(), b, b + n);
     };
-    const int hdr[8] = {c->variant, c->lp3Lanes, c->smemBytes, c->world, c->loopback ? 1 : 0, (int)c->doms.size(),
-                        c->transport, c->overlapMode};
+    const int hdr[9] = {c->variant, c->lp3Lanes, c->smemBytes, c->world, c->loopback ? 1 : 0, (int)c->doms.size(),
+                        c->transport, c->overlapMode, strip_streams_on(c) ? 1 : 0};
     put(hdr, sizeof hdr);
     for (Domain& d : c->doms) {
         const StepArgs a = make_args(c, d);
