@@ -381,8 +381,9 @@ orca_status orca_get_transport(orca_ctx *ctx, int32_t *mode);
  * info[0] = step kernel variant of the first strip (0, 1, 2 or 3), info[1] = lanes per
  * agent of the first strip's least-penetration kernel (0 = LP3 runs inside the step kernel,
  * no k_lp3 launch), info[2] = this library's CUDA kernels launched per step, summed over
- * the strips this context holds (per strip: step kernel, k_lp3 unless inline, k_scan,
- * k_scatter, plus k_receive and one k_push per neighbour with the peer-memory exchange;
+ * the strips this context holds (per strip: step kernel, k_lp3 unless inline, k_scan and
+ * k_scatter -- one fused cooperative k_bin for a one-strip context -- plus k_receive and
+ * one k_push per neighbour with the peer-memory exchange;
  * NCCL's own kernels under transport 1 are not counted), info[3] = the transport.
  * Errors: INVALID_ARGUMENT, NOT_READY. */
 orca_status orca_get_launch_info(orca_ctx *ctx, int32_t info[4]);

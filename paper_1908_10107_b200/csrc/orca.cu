@@ -54,6 +54,10 @@ constexpr int kPushBlocks = 64;  // k_push grid (last-block completion)
 #define ORCA_REGRID_REACH 512.0f  // steps of maxSpeed walking a re-derived grid's margin covers (r01: 128)
 #endif
 constexpr float kRegridReach = ORCA_REGRID_REACH;
+constexpr int kBinMaxGrid = 4096;  // k_bin blocks at most (one resident wave)
+#ifndef ORCA_FUSED_BIN
+#define ORCA_FUSED_BIN 0  // 1: single-strip steps bin with the cooperative k_bin (scan + scatter fused); measured neutral/slower (r02ac), off
+#endif
 
 int lp3_blocks(int64_t n) {
     const int64_t need = (n + kStepThreads - 1) / kStepThreads;
@@ -219,6 +223,7 @@ struct Domain {
     uint32_t *idS = nullptr, *idW = nullptr, *cellW = nullptr, *rankW = nullptr;
     uint32_t *count = nullptr, *binStart = nullptr;
     unsigned long long* scanStatus = nullptr;  // look-back status + ticket + LP3 queue count
+    uint32_t* binPartial = nullptr;            // k_bin's per-block chunk totals (kBinMaxGrid)
     int4* qEntry = nullptr;
     float4* qLines = nullptr;
     int* ctr = nullptr;
@@ -252,6 +257,7 @@ struct Domain {
         dfree(propS);
         dfree(propW);
         dfree(scanStatus);
+        dfree(binPartial);
         dfree(qEntry);
         dfree(qLines);
         dfree(ctr);
@@ -320,6 +326,7 @@ struct orca_ctx {
     int lp3InlineMode = -1;  // orca_set_lp3_inline: -1 auto (strips up to inlineBelow agents), 0 queue, 1 inline
     int64_t inlineBelow = 0;  // one wave of k_step blocks with the inline-LP3 shared memory (orca_create)
     int64_t pairBelow = 0;    // one wave of the lane-pair k_step (variant 4) blocks (orca_create)
+    int binGrid = 0;          // k_bin blocks that are co-resident (cooperative launch limit)
     // strip rebalance: by-id active flags, all-gather records, fill reports
     uint8_t* activeBuf = nullptr;
     int64_t activeCap = 0;
@@ -448,6 +455,7 @@ orca_status dom_alloc(orca_ctx* c, Domain& d, int capW, int64_t nbins, int capM,
         CK(cudaMalloc(&d.count, (nbins + 4) * sizeof(uint32_t)));
         CK(cudaMalloc(&d.binStart, (nbins + 1) * sizeof(uint32_t)));
         CK(cudaMalloc(&d.scanStatus, (scan_tiles(nbins) + 2) * sizeof(unsigned long long)));
+        if (!d.binPartial) CK(cudaMalloc(&d.binPartial, kBinMaxGrid * sizeof(uint32_t)));
         d.binCap = nbins;
     }
     if (!d.ctr) {
@@ -682,6 +690,29 @@ cudaError_t enqueue_scatter(orca_ctx* c, Domain& d, int bump, bool props = true)
     return cudaGetLastError();
 }
 
+// Scan + scatter of one strip as ONE cooperative launch (k_bin); the grid is at most one
+// resident wave, sized to the work (~1024 bins or agents per block).  Same result as
+// enqueue_scan + enqueue_scatter.
+cudaError_t enqueue_bin(orca_ctx* c, Domain& d, int bump) {
+    const int64_t work = std::max<int64_t>(d.capW, d.nbins);
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(c->binGrid, (work + 4 * kBinThreads - 1) / (4 * kBinThreads)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kBinThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_bin, d.ctr, bump, d.count, d.binStart, (int)d.nbins, d.binPartial, d.cellW,
+                              d.rankW, d.posW, d.velW, d.auxW, d.idW, d.rk2W, d.posS, d.velS, d.auxS, d.idS, d.rk2S,
+                              d.capW, c->het ? d.propW : nullptr, c->het ? d.propS : nullptr, d.scanStatus,
+                              scan_tiles(d.nbins) + 2);
+}
+bool fused_bin(const orca_ctx* c) { return ORCA_FUSED_BIN && c->doms.size() == 1 && c->binGrid > 0; }
+
 // Neighbour exchange of one step: every strip sends its L/R buffers and receives its
 // neighbours'.  Loopback: device copies between the strips of this context.  NCCL: one
 // group of send/recv with ranks +-1.
@@ -691,8 +722,8 @@ cudaError_t flush_deferred(orca_ctx* c) {
     if (!c->deferred) return cudaSuccess;
     c->deferred = false;
     for (Domain& d : c->doms) {
-        cudaError_t e = enqueue_scan(c, d, false);
-        if (e == cudaSuccess) e = enqueue_scatter(c, d, 1);
+        cudaError_t e = fused_bin(c) ? enqueue_bin(c, d, 1) : enqueue_scan(c, d, false);
+        if (e == cudaSuccess && !fused_bin(c)) e = enqueue_scatter(c, d, 1);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -843,6 +874,10 @@ orca_status enqueue_step(orca_ctx* c, cudaEvent_t* ev) {
         CK(cudaGetLastError());
     }
     if (ev) CK(cudaEventRecord(ev[2], c->stream));
+    if (!ev && fused_bin(c)) {  // (orca_step_timed keeps the two kernels for its stage times)
+        CK(enqueue_bin(c, c->doms[0], 1));
+        return ORCA_OK;
+    }
     for (Domain& d : c->doms) CK(enqueue_scan(c, d, false));
     if (ev) CK(cudaEventRecord(ev[3], c->stream));
     for (Domain& d : c->doms) CK(enqueue_scatter(c, d, 1));
@@ -947,6 +982,8 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
         if (e == cudaSuccess)
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step<false, 0, false, true>, kStepThreads, smemInl);
         c->pairBelow = (int64_t)blocks * sms * (kStepThreads / 2);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_bin, kBinThreads, 0);
+        c->binGrid = std::min(kBinMaxGrid, blocks * sms);
     }
     if (e != cudaSuccess) return cuda_fail(e, "orca_create");
     return ORCA_OK;
@@ -1776,8 +1813,12 @@ orca_status orca_step_io_async(orca_ctx* c, const float* pos_in, const float* ve
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->inFree[b], c->stream));
-    CK(enqueue_scan(c, d, false));
-    CK(enqueue_scatter(c, d, prevStep ? 1 : 0));
+    if (fused_bin(c)) {
+        CK(enqueue_bin(c, d, prevStep ? 1 : 0));
+    } else {
+        CK(enqueue_scan(c, d, false));
+        CK(enqueue_scatter(c, d, prevStep ? 1 : 0));
+    }
     // the step without its trailing binning
     StepArgs a = make_args(c, d);
     launch_step<false>(c, d, a);
@@ -2382,7 +2423,7 @@ orca_status orca_get_launch_info(orca_ctx* c, int32_t info[4]) {
     // the inline-LP3 choice); NCCL's own kernels (transport 1) are not ours and not counted
     int n = 0;
     for (const Domain& d : c->doms) {
-        n += pick_lp3_inline(c, d) ? 3 : 4;
+        n += (pick_lp3_inline(c, d) ? 3 : 4) - (fused_bin(c) ? 1 : 0);  // (k_bin = k_scan + k_scatter)
         if (overlap_on(c, d)) n += 1;  // the step kernel twice: boundary, then interior columns
         if (d.g.hasL || d.g.hasR) {  // strips: k_receive, and k_push per neighbour (peer memory)
             n += 1;

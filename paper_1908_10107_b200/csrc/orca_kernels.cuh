@@ -17,9 +17,11 @@
 //     well conditioned.
 #pragma once
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <stdint.h>
 #include <climits>
 
+namespace cg = cooperative_groups;
 namespace orca {
 
 constexpr int kMaxK = 32;
@@ -401,6 +403,97 @@ __global__ void k_scatter(int* __restrict__ ctr, int bump, const uint32_t* __res
         ctr[CT_XSTEP] += 1;
     }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t c = cell[i];
+        if (c == kInvalid) continue;
+        const uint32_t dst = binStart[c] + rank[i];
+        posS[dst] = posW[i];
+        velS[dst] = velW[i];
+        auxS[dst] = auxW[i];
+        idS[dst] = idW[i];
+        rk2S[dst] = rk2W[i];
+        if (propW) propS[dst] = propW[i];
+    }
+}
+
+// Fused binning of one strip (the step graph's single-strip path): the exclusive scan of the
+// bin counts and the counting-sort scatter in ONE cooperative launch of at most one resident
+// wave, with two grid-wide barriers instead of a kernel boundary and a decoupled look-back:
+//   (a) every block sums its contiguous chunk of bins into partial[block];
+//   (b) every block adds up the partials before it (its exclusive offset) and scans its own
+//       chunk (a thread per contiguous segment, one block scan), writing binStart and
+//       re-zeroing the counts (binStart[C] = the total);
+//   (c) the scatter of k_scatter, grid-stride over the work slots.
+// The result is k_scan + k_scatter's bit for bit (integer sums).
+constexpr int kBinThreads = 256;
+__device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* sm) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) sm[wid] = v;
+    __syncthreads();
+    uint32_t t = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += sm[q];
+    return t;
+}
+
+__global__ void __launch_bounds__(kBinThreads) k_bin(int* __restrict__ ctr, int bump, uint32_t* __restrict__ count,
+                                                      uint32_t* __restrict__ binStart, int C, uint32_t* __restrict__ partial,
+                                                      const uint32_t* __restrict__ cell, const uint32_t* __restrict__ rank,
+                                                      const float2* __restrict__ posW, const float2* __restrict__ velW,
+                                                      const float2* __restrict__ auxW, const uint32_t* __restrict__ idW,
+                                                      const float* __restrict__ rk2W, float2* __restrict__ posS,
+                                                      float2* __restrict__ velS, float2* __restrict__ auxS,
+                                                      uint32_t* __restrict__ idS, float* __restrict__ rk2S, int capW,
+                                                      const float4* __restrict__ propW, float4* __restrict__ propS,
+                                                      unsigned long long* __restrict__ scanStatus, int nStatus) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint32_t sm[kBinThreads / 32];
+    __shared__ uint32_t sScan[kBinThreads];
+    const int G = gridDim.x, b = blockIdx.x, t = threadIdx.x;
+    const int per = (C + G - 1) / G;
+    const int lo = min(C, b * per), hi = min(C, lo + per);
+    // (a) the block's chunk total
+    uint32_t s = 0;
+    for (int q = lo + t; q < hi; q += kBinThreads) s += count[q];
+    s = block_sum_u32(s, sm);
+    if (t == 0) partial[b] = s;
+    if (b == 0)  // k_scan's status words / ticket and the LP3 queue count for the next step
+        for (int q = t; q < nStatus; q += kBinThreads) scanStatus[q] = 0ull;
+    grid.sync();
+    // (b) offset of this chunk, then its scan
+    uint32_t o = 0;
+    for (int q = t; q < b; q += kBinThreads) o += partial[q];
+    o = block_sum_u32(o, sm);
+    const int L = (hi - lo + kBinThreads - 1) / kBinThreads;  // bins per thread (contiguous)
+    const int s0 = min(hi, lo + t * L), s1 = min(hi, s0 + L);
+    uint32_t mine = 0;
+    for (int q = s0; q < s1; ++q) mine += count[q];
+    sScan[t] = mine;
+    __syncthreads();
+    for (int d = 1; d < kBinThreads; d <<= 1) {  // inclusive Hillis-Steele scan of the thread sums
+        const uint32_t v = (t >= d) ? sScan[t - d] : 0u;
+        __syncthreads();
+        sScan[t] += v;
+        __syncthreads();
+    }
+    uint32_t run = o + sScan[t] - mine;
+    for (int q = s0; q < s1; ++q) {
+        const uint32_t c = count[q];
+        binStart[q] = run;
+        count[q] = 0u;
+        run += c;
+    }
+    if (hi == C && lo < C && t == kBinThreads - 1) binStart[C] = o + sScan[kBinThreads - 1];
+    if (C == 0 && b == 0 && t == 0) binStart[0] = 0u;
+    grid.sync();
+    // (c) the scatter
+    const int n = min(ctr[CT_NOWN] + ctr[CT_EXTRA], capW);
+    if (bump && b == 0 && t == 0) {  // the step is complete
+        ctr[CT_STEP] += 1;
+        ctr[CT_XSTEP] += 1;
+    }
+    for (int i = b * kBinThreads + t; i < n; i += G * kBinThreads) {
         const uint32_t c = cell[i];
         if (c == kInvalid) continue;
         const uint32_t dst = binStart[c] + rank[i];
