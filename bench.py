@@ -68,7 +68,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=6.0, help="single-thread oracle sample (cpu_baseline)")
     ap.add_argument("--ref-seconds", type=float, default=150.0,
                     help="--impl reference: time budget of the timed full oracle steps")
-    ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--no-suite", action="store_true", help="skip the other BASELINE workloads (N=1 only)")
     ap.add_argument("--only-timed", action="store_true",
                     help="profiling: stop after the timed steps (no A/B sweeps, e2e, baselines); prints a short line")
