@@ -12,18 +12,47 @@ import torch  # noqa: E402
 from paper_1908_10107_b200 import orca as O, workloads as W  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "uniform"
-ne = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+ne = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 40
 w = W.make(cfg)
 n = len(w["pos"])
 c = O.Orca(w["params"])
 c.set_agents(w["pos"], w["vel"], w["pref"])
-c.step(30)
+c.step(int(os.environ.get("PRE_STEPS", "30")))
 p, v = c.get_state()
 hp, hv = torch.from_numpy(p).pin_memory(), torch.from_numpy(v).pin_memory()
 hq = torch.from_numpy(w["pref"]).pin_memory()
 outs = [(torch.empty((n, 2)).pin_memory(), torch.empty((n, 2)).pin_memory()) for _ in range(2)]
+if "--churn" in sys.argv:  # the bench's A/B section before its e2e part
+    for v in (0, 1, 2, 3):
+        c.set_variant(v)
+        c.step(2)
+        for _ in range(5):
+            c.step_timed(1)
+    c.set_variant(-1)
+    for mode, v in ((0, 0), (2, 0), (1, 0), (2, 3)):
+        c.set_variant(v)
+        c.set_lp_order(mode, 1, 0)
+        c.step(2)
+        for _ in range(5):
+            c.step_timed(1)
+    c.set_lp_order(0)
+    c.set_variant(-1)
+    for lanes in (1, 4, 8, 16, "inline"):
+        c.set_lp3_inline(1 if lanes == "inline" else 0)
+        c.set_lp3_lanes(1 if lanes == "inline" else lanes)
+        c.step(2)
+        for _ in range(5):
+            c.step_timed(1)
+    c.set_lp3_lanes(-1)
+    c.set_lp3_inline(-1)
+    print("churned", c.launch_info(), flush=True)
 c.set_agents(hp, hv, hq)
 c.step(1)
+if "--sync" in sys.argv:
+    for _ in range(20):
+        c.set_state(hp, hv)
+        c.step(1)
+        c.get_state()
 for name in ("step_io", "three", "step_io", "three"):
     for s in range(3):
         if name == "step_io":
