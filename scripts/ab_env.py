@@ -1,4 +1,4 @@
-"""A/B of an environment switch read by liborca (e.g. ORCA_LP3_SPLIT): per config, a hash of the
+"""A/B of an environment switch or of library builds (ORCA_LIB=vlibs/...): per config, a hash of the
 state after 12 steps (bit-identity across runs) and the median whole-step device time (L2
 flushed between steps).  python scripts/ab_env.py <configs> ; run once per setting."""
 import hashlib, json, os, sys
@@ -26,6 +26,12 @@ for cfg in sys.argv[1].split(","):
             e1.record(s)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
-    print(cfg, json.dumps(dict(hash=h, step_ms=round(float(np.median(ts)), 4), launch=c.launch_info(),
+    stg = []
+    for it in range(15):
+        with torch.cuda.stream(s):
+            flush.zero_()
+        stg.append(c.step_timed(1))
+    stage = [round(float(x), 4) for x in np.median(np.array(stg), axis=0)]  # step+lp3, exchange, scan, scatter
+    print(cfg, json.dumps(dict(hash=h, step_ms=round(float(np.median(ts)), 4), stages=stage, launch=c.launch_info(),
                                 stats_inf=c.stats()["infeasible"])), flush=True)
     c.close()
