@@ -659,6 +659,8 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     else if (variant == 4)  // two lanes per agent: 64 agents per block
         launch_k(c, k_step<DRY, 0, false, true>, dim3((d.capW + kStepThreads / 2 - 1) / (kStepThreads / 2)),
                  dim3(kStepThreads), smem, a);
+    else if ((variant != 2 || k < 1 || k > 16) && a.lp3Inline == 0 && a.m.lpGreedy && !a.m.lpRandom)  // (QONLY)
+        launch_k(c, k_step<DRY, 0, false, false, true>, dim3(blocks), dim3(kStepThreads), smem, a);
     else if (variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
         launch_k(c, k_step<DRY, 0, false>, dim3(blocks), dim3(kStepThreads), smem, a);
     else if (k <= 10)  // register top-k list
@@ -958,7 +960,9 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
                              (const void*)k_step<false, 10>, (const void*)k_step<true, 10>,
                              (const void*)k_step<false, 16>, (const void*)k_step<true, 16>,
                              (const void*)k_step<false, 0, true>, (const void*)k_step<true, 0, true>,
-                             (const void*)k_step<false, 0, false, true>, (const void*)k_step<true, 0, false, true>};
+                             (const void*)k_step<false, 0, false, true>, (const void*)k_step<true, 0, false, true>,
+                             (const void*)k_step<false, 0, false, false, true>,
+                             (const void*)k_step<true, 0, false, false, true>};
     const int stepSmemMax = c->smemBytes + 3 * std::max(params->maxNeighbors, 1) * 4 * kStepThreads;  // + inline LP3
     for (const void* f : stepFns)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, stepSmemMax);

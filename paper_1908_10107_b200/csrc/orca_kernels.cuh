@@ -1716,7 +1716,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // the two lists (exact order) into the second lane's buffer column, the lanes build every
 // other half-plane and run lp2_greedy_pair; half the per-warp dependency chain of variant 0
 // for latency-bound strips.
-template <bool DRY, int KR, bool WU = false, bool PAIR = false>
+// QONLY: compiled for the default configuration of strips above one wave of blocks -- LP3 in
+// k_lp3 only (lp3Inline == 0) and the greedy LP order (lpGreedy, no lpRandom): the block-queue
+// and per-thread LP3 placements and the sequential LP orders are not in this kernel's code
+// (half the SASS of the general kernel; r02ai: 1M -2.8 %).
+template <bool DRY, int KR, bool WU = false, bool PAIR = false, bool QONLY = false>
 __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(StepArgs a) {
     pdl_entry();
     constexpr bool CNT = DRY;  // only the debug variant counts work
@@ -1778,7 +1782,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     __shared__ uint32_t sQ[T];
     __shared__ uint8_t sFree[T];
     __shared__ int sQn;
-    const bool blockQ = a.lp3Inline == 2;
+    const int lp3Mode = QONLY ? 0 : a.lp3Inline;
+    const bool blockQ = lp3Mode == 2;
     if (blockQ && tid == 0) sQn = 0;
     if (blockQ) __syncthreads();
     bool queued = false;
@@ -2078,7 +2083,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         if (DRY && a.dbgNbr && lead)  // neighbours in (distance, id) order
             for (int q = 0; q < cnt; ++q) a.dbgNbr[(size_t)idi * k + q] = (int32_t)a.idS[nbrJ[q * 2 * T]];
         // optional randomized LP order (P:82 Seidel, reading Q8): permute the list first
-        if (a.m.lpRandom && cnt > 1 && lead) lp_shuffle(nbrJ, 2 * T, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
+        if (!QONLY && a.m.lpRandom && cnt > 1 && lead) lp_shuffle(nbrJ, 2 * T, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
         if (PAIR) __syncwarp(pm);
         // (half-plane q overwrites list slot q in place: j is read before the write; PAIR: the
         // lanes build every other half-plane into the lead lane's columns)
@@ -2130,7 +2135,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         const int f = (PAIR && ORCA_PAIR_SERIAL_LP)
                           ? (lead ? lp2_greedy<CNT>(L0, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask & 0x55555555u) : 0)
                       : PAIR ? lp2_greedy_pair<CNT>(L0, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask, pm, h)
-                      : a.m.lpGreedy ? lp2_greedy<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
+                      : (QONLY || a.m.lpGreedy) ? lp2_greedy<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                       : WU         ? lp2_wu<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                       : ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                                      : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
@@ -2158,7 +2163,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 if (DRY && a.dbgNbr)
                     for (int q2 = cnt; q2 < k; ++q2) a.dbgNbr[(size_t)idi * k + q2] = -1;
             }
-        } else if (a.lp3Inline) {
+        } else if (lp3Mode) {
             // small strips (latency bound, spare issue slots): the least-penetration LP
             // runs here on the half-planes in shared memory -- the same lp3 as k_lp3, so the
             // same result -- and the agent is finished below like a feasible one
