@@ -651,16 +651,27 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
                         (a.lp3Inline == 1   ? (size_t)3 * k * 4 * kStepThreads
                          : a.lp3Inline == 2 ? (size_t)step_lp3q_scratch_bytes(k)
                                             : 0);
+    // the default configurations run kernels compiled for them (k_step's LM / MONO): the greedy
+    // LP order, LP3 in k_lp3 or on the block queue, and (mono) one strip of homogeneous agents
+    const bool spec = a.m.lpGreedy && !a.m.lpRandom;
+    const bool mono = !a.g.hasL && !a.g.hasR && !a.propS;
     if (variant == 1)  // 8-lane group per agent
         launch_k(c, k_step_group<DRY>, dim3((d.capW + kGroupAgents - 1) / kGroupAgents), dim3(kGroupThreads),
                  (size_t)c->groupSmem, a);
     else if (variant == 3)  // work-unit LP2 (P:84-89 ablation)
         launch_k(c, k_step<DRY, 0, true>, dim3(blocks), dim3(kStepThreads), smem, a);
+    else if (variant == 4 && spec && a.lp3Inline == 2)  // two lanes per agent, specialised (LM = 2)
+        launch_k(c, mono ? k_step<DRY, 0, false, true, 2, true> : k_step<DRY, 0, false, true, 2, false>,
+                 dim3((d.capW + kStepThreads / 2 - 1) / (kStepThreads / 2)), dim3(kStepThreads), smem, a);
     else if (variant == 4)  // two lanes per agent: 64 agents per block
         launch_k(c, k_step<DRY, 0, false, true>, dim3((d.capW + kStepThreads / 2 - 1) / (kStepThreads / 2)),
                  dim3(kStepThreads), smem, a);
-    else if ((variant != 2 || k < 1 || k > 16) && a.lp3Inline == 0 && a.m.lpGreedy && !a.m.lpRandom)  // (QONLY)
-        launch_k(c, k_step<DRY, 0, false, false, true>, dim3(blocks), dim3(kStepThreads), smem, a);
+    else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 0)  // specialised: LM = 0
+        launch_k(c, mono ? k_step<DRY, 0, false, false, 0, true> : k_step<DRY, 0, false, false, 0, false>,
+                 dim3(blocks), dim3(kStepThreads), smem, a);
+    else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 2)  // specialised: LM = 2
+        launch_k(c, mono ? k_step<DRY, 0, false, false, 2, true> : k_step<DRY, 0, false, false, 2, false>,
+                 dim3(blocks), dim3(kStepThreads), smem, a);
     else if (variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
         launch_k(c, k_step<DRY, 0, false>, dim3(blocks), dim3(kStepThreads), smem, a);
     else if (k <= 10)  // register top-k list
@@ -961,8 +972,18 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
                              (const void*)k_step<false, 16>, (const void*)k_step<true, 16>,
                              (const void*)k_step<false, 0, true>, (const void*)k_step<true, 0, true>,
                              (const void*)k_step<false, 0, false, true>, (const void*)k_step<true, 0, false, true>,
-                             (const void*)k_step<false, 0, false, false, true>,
-                             (const void*)k_step<true, 0, false, false, true>};
+                             (const void*)k_step<false, 0, false, false, 0, false>,
+                             (const void*)k_step<true, 0, false, false, 0, false>,
+                             (const void*)k_step<false, 0, false, false, 0, true>,
+                             (const void*)k_step<true, 0, false, false, 0, true>,
+                             (const void*)k_step<false, 0, false, false, 2, false>,
+                             (const void*)k_step<true, 0, false, false, 2, false>,
+                             (const void*)k_step<false, 0, false, false, 2, true>,
+                             (const void*)k_step<true, 0, false, false, 2, true>,
+                             (const void*)k_step<false, 0, false, true, 2, false>,
+                             (const void*)k_step<true, 0, false, true, 2, false>,
+                             (const void*)k_step<false, 0, false, true, 2, true>,
+                             (const void*)k_step<true, 0, false, true, 2, true>};
     const int stepSmemMax = c->smemBytes + 3 * std::max(params->maxNeighbors, 1) * 4 * kStepThreads;  // + inline LP3
     for (const void* f : stepFns)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, stepSmemMax);

@@ -1609,6 +1609,8 @@ __device__ __forceinline__ void append_work(const StepArgs& a, int nOwn, int fx,
 // sits in an edge column), or emigrates (exchange buffer, plus a local ghost entry since
 // it now sits in this strip's ghost column).  Single-GPU: always stays.  pr: the agent's
 // (radius, maxSpeed, prefSpeed, 0) when heterogeneous.
+// MONO: one strip (every agent stays: no halo copies, no emigration) of homogeneous agents.
+template <bool MONO = false>
 __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn, float2 pi, float vx, float vy,
                                              float2 aux, uint32_t id, float rk2, float4 pr) {
     const float2 pn = make_float2(fmaf(a.m.dt, vx, pi.x), fmaf(a.m.dt, vy, pi.y));
@@ -1630,18 +1632,18 @@ __device__ __forceinline__ void finish_agent(const StepArgs& a, int w, int nOwn,
         const int cyc = sy >> a.g.lgS;
         if (cx == 0 || cx == a.g.nx - 1 || cyc == 0 || cyc == a.g.ny - 1) *a.gridFlag = 1;
     }
-    if (cx >= a.g.c0 && cx < a.g.c1) {
+    if (MONO || (cx >= a.g.c0 && cx < a.g.c1)) {
         const uint32_t c = bin_of(fx, sy, a.g);
         a.posW[w] = pn;
         a.velW[w] = vn;
         a.auxW[w] = aux;
         a.idW[w] = id;
         a.rk2W[w] = rk2;
-        if (a.propW) a.propW[w] = pr;
+        if (!MONO && a.propW) a.propW[w] = pr;
         a.cellW[w] = c;
         a.rankW[w] = atomicAdd(&a.count[c], 1u);
-        if (cx == a.g.c0 && a.g.hasL) push_halo(a.sendL, a.ctr, pn, vn, id, pr.x);
-        if (cx == a.g.c1 - 1 && a.g.hasR) push_halo(a.sendR, a.ctr, pn, vn, id, pr.x);
+        if (!MONO && cx == a.g.c0 && a.g.hasL) push_halo(a.sendL, a.ctr, pn, vn, id, pr.x);
+        if (!MONO && cx == a.g.c1 - 1 && a.g.hasR) push_halo(a.sendR, a.ctr, pn, vn, id, pr.x);
     } else {
         a.cellW[w] = kInvalid;
         const ExBuf& x = (cx < a.g.c0) ? a.sendL : a.sendR;
@@ -1716,11 +1718,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // the two lists (exact order) into the second lane's buffer column, the lanes build every
 // other half-plane and run lp2_greedy_pair; half the per-warp dependency chain of variant 0
 // for latency-bound strips.
-// QONLY: compiled for the default configuration of strips above one wave of blocks -- LP3 in
-// k_lp3 only (lp3Inline == 0) and the greedy LP order (lpGreedy, no lpRandom): the block-queue
-// and per-thread LP3 placements and the sequential LP orders are not in this kernel's code
-// (half the SASS of the general kernel; r02ai: 1M -2.8 %).
-template <bool DRY, int KR, bool WU = false, bool PAIR = false, bool QONLY = false>
+// LM >= 0: compiled for one LP3 placement (lp3Inline == LM: 0 = k_lp3, 2 = the block queue) and
+// the greedy LP order (lpGreedy, no lpRandom) -- the default configurations -- so the other
+// placements and the sequential LP orders are not in this kernel's code (less than half the
+// SASS of the general kernel; r02ai: 1M -2.8 %).  LM = -1: any (runtime).
+// MONO (with LM >= 0): one strip of homogeneous agents (finish_agent<true>, no per-agent props).
+template <bool DRY, int KR, bool WU = false, bool PAIR = false, int LM = -1, bool MONO = false>
 __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(StepArgs a) {
     pdl_entry();
     constexpr bool CNT = DRY;  // only the debug variant counts work
@@ -1782,7 +1785,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
     __shared__ uint32_t sQ[T];
     __shared__ uint8_t sFree[T];
     __shared__ int sQn;
-    const int lp3Mode = QONLY ? 0 : a.lp3Inline;
+    const int lp3Mode = LM >= 0 ? LM : a.lp3Inline;
     const bool blockQ = lp3Mode == 2;
     if (blockQ && tid == 0) sQn = 0;
     if (blockQ) __syncthreads();
@@ -1804,7 +1807,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         const float2 aux = a.auxS[i];
         const uint32_t idi = a.idS[i];
         // per-agent (radius, maxSpeed, prefSpeed) of heterogeneous crowds
-        const bool het = a.propS != nullptr;
+        const bool het = !MONO && a.propS != nullptr;
         const float4 pr = het ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
         const float ri = pr.x, vmaxi = pr.y, vprefi = (pr.z >= 0.0f) ? pr.z : a.m.prefSpeed;
         (void)ri;
@@ -2083,7 +2086,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         if (DRY && a.dbgNbr && lead)  // neighbours in (distance, id) order
             for (int q = 0; q < cnt; ++q) a.dbgNbr[(size_t)idi * k + q] = (int32_t)a.idS[nbrJ[q * 2 * T]];
         // optional randomized LP order (P:82 Seidel, reading Q8): permute the list first
-        if (!QONLY && a.m.lpRandom && cnt > 1 && lead) lp_shuffle(nbrJ, 2 * T, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
+        if (LM < 0 && a.m.lpRandom && cnt > 1 && lead) lp_shuffle(nbrJ, 2 * T, cnt, a.m.lpSeed, a.ctr[CT_STEP], idi);
         if (PAIR) __syncwarp(pm);
         // (half-plane q overwrites list slot q in place: j is read before the write; PAIR: the
         // lanes build every other half-plane into the lead lane's columns)
@@ -2135,7 +2138,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
         const int f = (PAIR && ORCA_PAIR_SERIAL_LP)
                           ? (lead ? lp2_greedy<CNT>(L0, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask & 0x55555555u) : 0)
                       : PAIR ? lp2_greedy_pair<CNT>(L0, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask, pm, h)
-                      : (QONLY || a.m.lpGreedy) ? lp2_greedy<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
+                      : (LM >= 0 || a.m.lpGreedy) ? lp2_greedy<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                       : WU         ? lp2_wu<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                       : ORCA_SYNC_LP ? lp2_sync<CNT>(L, T, cnt, k, vmaxi, px, py, vx, vy, fl, w, activeMask)
                                      : lp2<CNT>(L, T, cnt, vmaxi, px, py, false, vx, vy, fl, w);
@@ -2214,7 +2217,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             if (a.dbgNbr)
                 for (int q = cnt; q < k; ++q) a.dbgNbr[(size_t)idi * k + q] = -1;
         } else {
-            finish_agent(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk, pr);
+            finish_agent<MONO>(a, ws, o1 - o0, pi, vx, vy, aux, idi, fk, pr);
         }
     }
     if (blockQ) {
@@ -2264,8 +2267,8 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                 float vy = sw[(3 * k + 1) * T + owner];
                 const int wso = (int)reinterpret_cast<uint32_t*>(sw)[(3 * k + 2) * T + owner];
                 const int io = o0 + wso;
-                const float4 pr = a.propS ? a.propS[io] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
-                lp3_dispatch<CNT>(Lo, P, T, TP, cnt, f, k, pr.y, vx, vy, fl2, w, xmask, a.m.lpGreedy != 0);
+                const float4 pr = (!MONO && a.propS) ? a.propS[io] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
+                lp3_dispatch<CNT>(Lo, P, T, TP, cnt, f, k, pr.y, vx, vy, fl2, w, xmask, LM >= 0 || a.m.lpGreedy != 0);
                 float dl = 0.0f;
                 for (int m = 0; m < cnt; ++m) {
                     const float2 nm = Lo.n[m * T];
@@ -2277,7 +2280,7 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
                     if (a.dbgV) a.dbgV[ido] = make_float2(vx, vy);
                     if (a.dbgFlags) a.dbgFlags[ido] = (uint8_t)fl2;
                 } else {
-                    finish_agent(a, wso, o1b - o0, a.posS[io], vx, vy, a.auxS[io], ido, a.rk2W[wso], pr);
+                    finish_agent<MONO>(a, wso, o1b - o0, a.posS[io], vx, vy, a.auxS[io], ido, a.rk2W[wso], pr);
                 }
                 cInfX += 1;
                 cDegX += (fl2 & (FL_G1 | FL_G2)) != 0;
