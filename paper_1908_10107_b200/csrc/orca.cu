@@ -55,6 +55,12 @@ constexpr int kPushBlocks = 64;  // k_push grid (last-block completion)
 #endif
 constexpr float kRegridReach = ORCA_REGRID_REACH;
 constexpr int kBinMaxGrid = 4096;  // k_bin blocks at most (one resident wave)
+// threads per block of the specialised block-queue k_step (LP3 on the block queue, strips of at
+// most one wave; r02al: 100k 0.0614 -> 0.0585 ms with 256 instead of 128)
+#ifndef ORCA_STEP_BQ_THREADS
+#define ORCA_STEP_BQ_THREADS 256
+#endif
+constexpr int kStepBQ = ORCA_STEP_BQ_THREADS;
 #ifndef ORCA_FUSED_BIN
 #define ORCA_FUSED_BIN 0  // 1: single-strip steps bin with the cooperative k_bin (scan + scatter fused); measured neutral/slower (r02ac), off
 #endif
@@ -669,9 +675,10 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 0)  // specialised: LM = 0
         launch_k(c, mono ? k_step<DRY, 0, false, false, 0, true> : k_step<DRY, 0, false, false, 0, false>,
                  dim3(blocks), dim3(kStepThreads), smem, a);
-    else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 2)  // specialised: LM = 2
-        launch_k(c, mono ? k_step<DRY, 0, false, false, 2, true> : k_step<DRY, 0, false, false, 2, false>,
-                 dim3(blocks), dim3(kStepThreads), smem, a);
+    else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 2)  // specialised: LM = 2, 256 threads
+        launch_k(c, mono ? k_step<DRY, 0, false, false, 2, true, kStepBQ> : k_step<DRY, 0, false, false, 2, false, kStepBQ>,
+                 dim3((d.capW + kStepBQ - 1) / kStepBQ), dim3(kStepBQ),
+                 (size_t)step_smem_per_thread(k) * kStepBQ + (size_t)step_lp3q_scratch_bytes(k), a);
     else if (variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
         launch_k(c, k_step<DRY, 0, false>, dim3(blocks), dim3(kStepThreads), smem, a);
     else if (k <= 10)  // register top-k list
@@ -984,9 +991,16 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
                              (const void*)k_step<true, 0, false, true, 2, false>,
                              (const void*)k_step<false, 0, false, true, 2, true>,
                              (const void*)k_step<true, 0, false, true, 2, true>};
+    const void* stepFnsBQ[] = {(const void*)k_step<false, 0, false, false, 2, false, kStepBQ>,
+                               (const void*)k_step<true, 0, false, false, 2, false, kStepBQ>,
+                               (const void*)k_step<false, 0, false, false, 2, true, kStepBQ>,
+                               (const void*)k_step<true, 0, false, false, 2, true, kStepBQ>};
     const int stepSmemMax = c->smemBytes + 3 * std::max(params->maxNeighbors, 1) * 4 * kStepThreads;  // + inline LP3
     for (const void* f : stepFns)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, stepSmemMax);
+    const int stepSmemBQ = step_smem_per_thread(params->maxNeighbors) * kStepBQ + step_lp3q_scratch_bytes(params->maxNeighbors);
+    for (const void* f : stepFnsBQ)
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, stepSmemBQ);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
     if (e == cudaSuccess)

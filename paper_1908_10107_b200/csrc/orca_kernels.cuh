@@ -1455,6 +1455,7 @@ __device__ __forceinline__ float reg_f(const RegList<KR>& L, int q) {
 
 // fp32 d2 of buffered candidate b: stored, or (ORCA_BUF1) recomputed with the scan's
 // expression -- the same bits
+template <int T = kStepThreads>
 __device__ __forceinline__ float buf_d2(const float* Bff, int b, uint32_t j, float2 pi,
                                         const float2* __restrict__ posS) {
     if (ORCA_BUF1) {
@@ -1462,17 +1463,16 @@ __device__ __forceinline__ float buf_d2(const float* Bff, int b, uint32_t j, flo
         const float dx = p.x - pi.x, dy = p.y - pi.y;
         return fmaf(dx, dx, dy * dy);
     }
-    return Bff[b * kStepThreads];
+    return Bff[b * T];
 }
 
 // buffered (j, fp32 d2) candidates into the register list (inside r_obs only)
-template <int KR>
+template <int KR, int T = kStepThreads>
 __device__ __forceinline__ void reg_merge(RegList<KR>& L, int& cnt, const uint32_t* Bj, const float* Bff, int nb,
                                           float2 pi, const Model& m, const float2* __restrict__ posS, bool& tie) {
-    constexpr int T = kStepThreads;
     for (int b = 0; b < nb; ++b) {
         const uint32_t j = Bj[b * T];
-        const float f = buf_d2(Bff, b, j, pi, posS);
+        const float f = buf_d2<T>(Bff, b, j, pi, posS);
         if (!in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
         reg_insert<KR>(L, f, j, tie);
         cnt = min(cnt + 1, KR);
@@ -1499,14 +1499,14 @@ __device__ __forceinline__ bool exact_less(uint32_t ja, uint32_t jb, float2 pi, 
 // step of the insertion is one 64-bit load and one 64-bit store.
 // allIn: every buffered candidate has fp32 d2 <= a pass threshold below nd2Lo, i.e. is surely
 // strictly within r_obs (in_radius would return true at its first compare).
+template <int T = kStepThreads>
 __device__ __forceinline__ int merge_candidates(uint2* Lst, int cnt, int k, const uint32_t* Bf,
                                                 const float* Bff, int nb, float2 pi, const Model& m,
                                                 const float2* __restrict__ posS, const uint32_t* __restrict__ idS,
                                                 bool allIn = false) {
-    constexpr int T = kStepThreads;
     for (int b = 0; b < nb; ++b) {
         const uint32_t j = Bf[b * T];
-        const float f = buf_d2(Bff, b, j, pi, posS);
+        const float f = buf_d2<T>(Bff, b, j, pi, posS);
         if (!allIn && !in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
         if (ORCA_FAST_MERGE && f > 1e-30f) {
             const float fhi = f * (1.0f + 0x1p-19f), flo = f * (1.0f - 0x1p-19f);
@@ -1723,13 +1723,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // placements and the sequential LP orders are not in this kernel's code (less than half the
 // SASS of the general kernel; r02ai: 1M -2.8 %).  LM = -1: any (runtime).
 // MONO (with LM >= 0): one strip of homogeneous agents (finish_agent<true>, no per-agent props).
-template <bool DRY, int KR, bool WU = false, bool PAIR = false, int LM = -1, bool MONO = false>
-__global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(StepArgs a) {
+// TB: threads per block (kStepThreads, or 256 for the block-queue kernel: DESIGN.md §12 r02al).
+template <bool DRY, int KR, bool WU = false, bool PAIR = false, int LM = -1, bool MONO = false, int TB = kStepThreads>
+__global__ void __launch_bounds__(TB, ORCA_STEP_MINBLOCKS * kStepThreads / TB) k_step(StepArgs a) {
     pdl_entry();
     constexpr bool CNT = DRY;  // only the debug variant counts work
     WorkT w{0, 0, 0, 0, 0};
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int T = kStepThreads;
+    constexpr int T = TB;
     const int tid = threadIdx.x;
     const int k = a.m.k;
     const int capB = step_buf_words(k);
@@ -1869,9 +1870,9 @@ __global__ void __launch_bounds__(kStepThreads, ORCA_STEP_MINBLOCKS) k_step(Step
             bool allIn = false;  // this pass's threshold is below nd2Lo (set at each pass start)
             auto merge = [&](int nb) {
                 if (KR > 0 && mode == 0)
-                    reg_merge<(KR > 0 ? KR : 1)>(R, cnt, Bf, Bff, nb, pi, a.m, a.posS, tie);
+                    reg_merge<(KR > 0 ? KR : 1), T>(R, cnt, Bf, Bff, nb, pi, a.m, a.posS, tie);
                 else
-                    cnt = merge_candidates(Lst, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS, allIn);
+                    cnt = merge_candidates<T>(Lst, cnt, k, Bf, Bff, nb, pi, a.m, a.posS, a.idS, allIn);
             };
             auto kth = [&]() -> float {  // fp32 d2 of the k-th (valid when cnt >= k)
                 if (KR > 0 && mode == 0) return reg_f<(KR > 0 ? KR : 1)>(R, k - 1);
