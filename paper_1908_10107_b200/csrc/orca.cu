@@ -641,7 +641,11 @@ void launch_lp3(orca_ctx* c, Domain& d, StepArgs& a) {
         case 4: launch_lp3_grp<DRY, 4>(c, d, a); break;
         case 8: launch_lp3_grp<DRY, 8>(c, d, a); break;
         case 16: launch_lp3_grp<DRY, 16>(c, d, a); break;
-        default: launch_k(c, k_lp3<DRY>, dim3(lp3_blocks(d.capW)), dim3(kStepThreads), (size_t)c->lp3Smem, a);
+        default:
+            if (!a.g.hasL && !a.g.hasR && !a.propS)  // one strip of homogeneous agents
+                launch_k(c, k_lp3<DRY, true>, dim3(lp3_blocks(d.capW)), dim3(kStepThreads), (size_t)c->lp3Smem, a);
+            else
+                launch_k(c, k_lp3<DRY>, dim3(lp3_blocks(d.capW)), dim3(kStepThreads), (size_t)c->lp3Smem, a);
     }
 }
 
@@ -1005,6 +1009,8 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
         e = cudaFuncSetAttribute(k_lp3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_lp3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
+    for (const void* f : {(const void*)k_lp3<false, true>, (const void*)k_lp3<true, true>})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, c->lp3Smem);
     c->groupSmem = group_words(params->maxNeighbors) * 4 * kGroupAgents;
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_step_group<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->groupSmem);

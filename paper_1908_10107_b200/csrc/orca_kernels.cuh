@@ -2356,7 +2356,8 @@ __global__ void __launch_bounds__(TB, ORCA_STEP_MINBLOCKS * kStepThreads / TB) k
 #define ORCA_MAX_K_DEV 32  // = ORCA_MAX_K (include/orca.h); buckets 0..32 by failure index
 // One thread per queued (infeasible) agent, grid-stride over the device-side queue
 // count; same smem column layout as k_step (lines, then projected lines).
-template <bool DRY>
+// MONO: one strip of homogeneous agents (finish_agent<true>, no per-agent props)
+template <bool DRY, bool MONO = false>
 __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
     pdl_entry();
     constexpr bool CNT = DRY;
@@ -2429,7 +2430,7 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
             L.n[m * T] = make_float2(l.x, l.y);
             L.s[m * T] = l.z;
         }
-        const float4 pr = a.propS ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
+        const float4 pr = (!MONO && a.propS) ? a.propS[i] : make_float4(0.5f * a.m.R, a.m.maxSpeed, a.m.prefSpeed, 0.0f);
         if (a.m.lpGreedy)
             lp3_greedy<CNT>(L, P, T, T, cnt, f, k, pr.y, vx, vy, fl, w, qmask);
         else if (ORCA_SYNC_LP)
@@ -2448,7 +2449,7 @@ __global__ void __launch_bounds__(kStepThreads) k_lp3(StepArgs a) {
             if (a.dbgV) a.dbgV[idi] = make_float2(vx, vy);
             if (a.dbgFlags) a.dbgFlags[idi] = (uint8_t)fl;
         } else {
-            finish_agent(a, i - o0, nOwn, pi, vx, vy, a.auxS[i], idi, a.rk2W[i - o0], pr);
+            finish_agent<MONO>(a, i - o0, nOwn, pi, vx, vy, a.auxS[i], idi, a.rk2W[i - o0], pr);
         }
         cInf += 1;
         cDeg += (fl & (FL_G1 | FL_G2)) != 0;
