@@ -60,7 +60,9 @@ for lf, name in ((f"launches_{tag}.csv", "1M"), (f"launches100k_{tag}.csv", "100
             dd[r[ki].split("(")[0]].append(float(r[vi].replace(",", "")))
         except ValueError:
             pass
-    main = ["void orca::k_step<0, 0, 0, 0>", "void orca::k_lp3<0>", "orca::k_scan", "orca::k_scatter"]
+    # the step's own kernels: every non-debug k_step / k_lp3 instantiation, the scan, the scatter
+    main = [k for k in dd if (k.startswith("void orca::k_step<0,") or k.startswith("void orca::k_lp3<0"))] + \
+        ["orca::k_scan", "orca::k_scatter"]
     med = {k: sorted(v)[len(v) // 2] / 1000 for k, v in dd.items()}
     tot = sum(med.get(k, 0) for k in main)
     print(f"\n### ncu launch list, {name} (cold cache, serialised; median per launch)\n")
