@@ -32,6 +32,7 @@ if [[ $WHAT == all || $WHAT == ncu ]]; then
   timeout 900 ncu --set full --clock-control none -k regex:"k_scatter|k_scan" -s 16 -c 2 -o $OUT/prof_bin_$TAG $T > /dev/null 2>&1
   echo "ncu rest exit $?"
 fi
-if [[ $WHAT == all || $WHAT == sanitize ]]; then
+# compute-sanitizer is closed on the GPU pool since r02b1: only on request (what = sanitize)
+if [[ $WHAT == sanitize ]]; then
   bash scripts/sanitize.sh $TAG > $OUT/sanitize_${TAG}_summary.txt 2>&1; cat $OUT/sanitize_${TAG}_summary.txt
 fi
