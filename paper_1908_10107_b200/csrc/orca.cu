@@ -332,6 +332,7 @@ struct orca_ctx {
     int lp3InlineMode = -1;  // orca_set_lp3_inline: -1 auto (strips up to inlineBelow agents), 0 queue, 1 inline
     int64_t inlineBelow = 0;  // one wave of k_step blocks with the inline-LP3 shared memory (orca_create)
     int64_t pairBelow = 0;    // one wave of the lane-pair k_step (variant 4) blocks (orca_create)
+    int64_t bq3Below = 0;     // one wave of the 3-blocks/SM block-queue k_step (orca_create)
     int binGrid = 0;          // k_bin blocks that are co-resident (cooperative launch limit)
     // strip rebalance: by-id active flags, all-gather records, fill reports
     uint8_t* activeBuf = nullptr;
@@ -680,7 +681,10 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
         launch_k(c, mono ? k_step<DRY, 0, false, false, 0, true> : k_step<DRY, 0, false, false, 0, false>,
                  dim3(blocks), dim3(kStepThreads), smem, a);
     else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 2)  // specialised: LM = 2, 256 threads
-        launch_k(c, mono ? k_step<DRY, 0, false, false, 2, true, kStepBQ> : k_step<DRY, 0, false, false, 2, false, kStepBQ>,
+        launch_k(c,
+                 d.popBuild <= c->bq3Below
+                     ? (mono ? k_step<DRY, 0, false, false, 2, true, kStepBQ, 3> : k_step<DRY, 0, false, false, 2, false, kStepBQ, 3>)
+                     : (mono ? k_step<DRY, 0, false, false, 2, true, kStepBQ> : k_step<DRY, 0, false, false, 2, false, kStepBQ>),
                  dim3((d.capW + kStepBQ - 1) / kStepBQ), dim3(kStepBQ),
                  (size_t)step_smem_per_thread(k) * kStepBQ + (size_t)step_lp3q_scratch_bytes(k), a);
     else if (variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
@@ -998,7 +1002,11 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
     const void* stepFnsBQ[] = {(const void*)k_step<false, 0, false, false, 2, false, kStepBQ>,
                                (const void*)k_step<true, 0, false, false, 2, false, kStepBQ>,
                                (const void*)k_step<false, 0, false, false, 2, true, kStepBQ>,
-                               (const void*)k_step<true, 0, false, false, 2, true, kStepBQ>};
+                               (const void*)k_step<true, 0, false, false, 2, true, kStepBQ>,
+                               (const void*)k_step<false, 0, false, false, 2, false, kStepBQ, 3>,
+                               (const void*)k_step<true, 0, false, false, 2, false, kStepBQ, 3>,
+                               (const void*)k_step<false, 0, false, false, 2, true, kStepBQ, 3>,
+                               (const void*)k_step<true, 0, false, false, 2, true, kStepBQ, 3>};
     const int stepSmemMax = c->smemBytes + 3 * std::max(params->maxNeighbors, 1) * 4 * kStepThreads;  // + inline LP3
     for (const void* f : stepFns)
         if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, stepSmemMax);
@@ -1027,6 +1035,12 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
         if (e == cudaSuccess)
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step<false, 0, false, true>, kStepThreads, smemInl);
         c->pairBelow = (int64_t)blocks * sms * (kStepThreads / 2);
+        // the 3-blocks/SM block-queue kernel (85 registers) while a strip fits one wave of it (r02ao)
+        const size_t smemBQ = (size_t)step_smem_per_thread(k) * kStepBQ + (size_t)step_lp3q_scratch_bytes(k);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step<false, 0, false, false, 2, true, kStepBQ, 3>,
+                                                              kStepBQ, smemBQ);
+        c->bq3Below = (int64_t)blocks * sms * kStepBQ;
         if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_bin, kBinThreads, 0);
         c->binGrid = std::min(kBinMaxGrid, blocks * sms);
     }

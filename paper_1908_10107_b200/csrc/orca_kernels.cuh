@@ -1724,8 +1724,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // SASS of the general kernel; r02ai: 1M -2.8 %).  LM = -1: any (runtime).
 // MONO (with LM >= 0): one strip of homogeneous agents (finish_agent<true>, no per-agent props).
 // TB: threads per block (kStepThreads, or 256 for the block-queue kernel: DESIGN.md §12 r02al).
-template <bool DRY, int KR, bool WU = false, bool PAIR = false, int LM = -1, bool MONO = false, int TB = kStepThreads>
-__global__ void __launch_bounds__(TB, ORCA_STEP_MINBLOCKS * kStepThreads / TB) k_step(StepArgs a) {
+// MB > 0: blocks per SM the register budget is sized for (3 x 256 threads: 85 registers; the block-queue
+// kernel for strips within one wave of it, r02ao), else 1024 threads per SM (64 registers).
+template <bool DRY, int KR, bool WU = false, bool PAIR = false, int LM = -1, bool MONO = false, int TB = kStepThreads,
+          int MB = 0>
+__global__ void __launch_bounds__(TB, MB > 0 ? MB : ORCA_STEP_MINBLOCKS * kStepThreads / TB) k_step(StepArgs a) {
     pdl_entry();
     constexpr bool CNT = DRY;  // only the debug variant counts work
     WorkT w{0, 0, 0, 0, 0};
