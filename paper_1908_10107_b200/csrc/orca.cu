@@ -61,6 +61,10 @@ constexpr int kBinMaxGrid = 4096;  // k_bin blocks at most (one resident wave)
 #define ORCA_STEP_BQ_THREADS 256
 #endif
 constexpr int kStepBQ = ORCA_STEP_BQ_THREADS;
+// blocks/SM the k_lp3-placement k_step's register budget is sized for (0: 8 = 64 registers)
+#ifndef ORCA_LM0_MB
+#define ORCA_LM0_MB 0
+#endif
 #ifndef ORCA_FUSED_BIN
 #define ORCA_FUSED_BIN 0  // 1: single-strip steps bin with the cooperative k_bin (scan + scatter fused); measured neutral/slower (r02ac), off
 #endif
@@ -678,7 +682,8 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
         launch_k(c, k_step<DRY, 0, false, true>, dim3((d.capW + kStepThreads / 2 - 1) / (kStepThreads / 2)),
                  dim3(kStepThreads), smem, a);
     else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 0)  // specialised: LM = 0
-        launch_k(c, mono ? k_step<DRY, 0, false, false, 0, true> : k_step<DRY, 0, false, false, 0, false>,
+        launch_k(c, mono ? k_step<DRY, 0, false, false, 0, true, kStepThreads, ORCA_LM0_MB>
+                         : k_step<DRY, 0, false, false, 0, false, kStepThreads, ORCA_LM0_MB>,
                  dim3(blocks), dim3(kStepThreads), smem, a);
     else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 2)  // specialised: LM = 2, 256 threads
         launch_k(c,
@@ -987,10 +992,10 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
                              (const void*)k_step<false, 16>, (const void*)k_step<true, 16>,
                              (const void*)k_step<false, 0, true>, (const void*)k_step<true, 0, true>,
                              (const void*)k_step<false, 0, false, true>, (const void*)k_step<true, 0, false, true>,
-                             (const void*)k_step<false, 0, false, false, 0, false>,
-                             (const void*)k_step<true, 0, false, false, 0, false>,
-                             (const void*)k_step<false, 0, false, false, 0, true>,
-                             (const void*)k_step<true, 0, false, false, 0, true>,
+                             (const void*)k_step<false, 0, false, false, 0, false, kStepThreads, ORCA_LM0_MB>,
+                             (const void*)k_step<true, 0, false, false, 0, false, kStepThreads, ORCA_LM0_MB>,
+                             (const void*)k_step<false, 0, false, false, 0, true, kStepThreads, ORCA_LM0_MB>,
+                             (const void*)k_step<true, 0, false, false, 0, true, kStepThreads, ORCA_LM0_MB>,
                              (const void*)k_step<false, 0, false, false, 2, false>,
                              (const void*)k_step<true, 0, false, false, 2, false>,
                              (const void*)k_step<false, 0, false, false, 2, true>,
