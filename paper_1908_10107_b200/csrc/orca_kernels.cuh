@@ -1362,6 +1362,9 @@ __host__ __device__ constexpr int step_buf_words(int k) { return k + ORCA_BUF_EX
 #ifndef ORCA_SCAN_UNROLL
 #define ORCA_SCAN_UNROLL 2  // candidates per scan iteration (2: r01; see DESIGN.md §12 r02)
 #endif
+#ifndef ORCA_SCAN_UNROLL_LM0
+#define ORCA_SCAN_UNROLL_LM0 3  // r02ar: the k_lp3-placement kernel, 1M -0.7 %, dense -1 % vs 2 (4: +0.7 %)
+#endif
 #ifndef ORCA_BUF1
 #define ORCA_BUF1 1  // 1: the buffer keeps j only; the merge recomputes the fp32 d2 (r01o: -8 %)
 #endif
@@ -1962,7 +1965,9 @@ __global__ void __launch_bounds__(TB, MB > 0 ? MB : ORCA_STEP_MINBLOCKS * kStepT
 #endif
                     if (CNT && lead) w.cand += (uint32_t)(e - b);
                     constexpr int st = PAIR ? 2 : 1;  // PAIR: each lane every other candidate
-                    constexpr int U = ORCA_SCAN_UNROLL;  // candidates per iteration (loads in flight)
+                    // candidates per iteration (loads in flight); the k_lp3-placement kernel (large
+                    // strips, throughput bound) may take another unroll than the latency-bound ones
+                    constexpr int U = (LM == 0) ? ORCA_SCAN_UNROLL_LM0 : ORCA_SCAN_UNROLL;
                     int j = b + h;
                     for (; j + (U - 1) * st < e; j += U * st) {
                         float2 pu[U];
