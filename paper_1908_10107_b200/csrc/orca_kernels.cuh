@@ -1498,6 +1498,9 @@ __device__ __forceinline__ bool exact_less(uint32_t ja, uint32_t jb, float2 pi, 
 #ifndef ORCA_FAST_MERGE
 #define ORCA_FAST_MERGE 1
 #endif
+#ifndef ORCA_MERGE_PF
+#define ORCA_MERGE_PF 1  // r02at: 1M -0.7 %. 1: the merge loads the next buffered candidate during the current insertion
+#endif
 // List entries are (fp32 d2 bits, j) pairs in one 64-bit shared-memory slot each: a shift
 // step of the insertion is one 64-bit load and one 64-bit store.
 // allIn: every buffered candidate has fp32 d2 <= a pass threshold below nd2Lo, i.e. is surely
@@ -1507,9 +1510,25 @@ __device__ __forceinline__ int merge_candidates(uint2* Lst, int cnt, int k, cons
                                                 const float* Bff, int nb, float2 pi, const Model& m,
                                                 const float2* __restrict__ posS, const uint32_t* __restrict__ idS,
                                                 bool allIn = false) {
+#if ORCA_MERGE_PF && ORCA_BUF1
+    // the next buffered candidate's index and position are loaded while this one is inserted
+    uint32_t jn = (nb > 0) ? Bf[0] : 0u;
+    float2 pn = (nb > 0) ? posS[jn] : make_float2(0.0f, 0.0f);
+#endif
     for (int b = 0; b < nb; ++b) {
+#if ORCA_MERGE_PF && ORCA_BUF1
+        const uint32_t j = jn;
+        const float2 pj = pn;
+        if (b + 1 < nb) {
+            jn = Bf[(b + 1) * T];
+            pn = posS[jn];
+        }
+        const float dxm = pj.x - pi.x, dym = pj.y - pi.y;
+        const float f = fmaf(dxm, dxm, dym * dym);  // (buf_d2's expression: the scan's bits)
+#else
         const uint32_t j = Bf[b * T];
         const float f = buf_d2<T>(Bff, b, j, pi, posS);
+#endif
         if (!allIn && !in_radius(f, j, pi, m.nd2Lo, m.nd2Fup, m.nd2D, posS)) continue;
         if (ORCA_FAST_MERGE && f > 1e-30f) {
             const float fhi = f * (1.0f + 0x1p-19f), flo = f * (1.0f - 0x1p-19f);
