@@ -61,6 +61,10 @@ constexpr int kBinMaxGrid = 4096;  // k_bin blocks at most (one resident wave)
 #define ORCA_STEP_BQ_THREADS 256
 #endif
 constexpr int kStepBQ = ORCA_STEP_BQ_THREADS;
+// blocks/SM of the larger-register lane-pair k_step used while a strip fits one wave of it (0: off)
+#ifndef ORCA_PAIR_MB
+#define ORCA_PAIR_MB 6  // r02au: 85 registers; 55k -4 %, 20k / corridor 0-5 % (5 and 7 no better)
+#endif
 // blocks/SM the k_lp3-placement k_step's register budget is sized for (0: 8 = 64 registers)
 #ifndef ORCA_LM0_MB
 #define ORCA_LM0_MB 0
@@ -337,6 +341,7 @@ struct orca_ctx {
     int64_t inlineBelow = 0;  // one wave of k_step blocks with the inline-LP3 shared memory (orca_create)
     int64_t pairBelow = 0;    // one wave of the lane-pair k_step (variant 4) blocks (orca_create)
     int64_t bq3Below = 0;     // one wave of the 3-blocks/SM block-queue k_step (orca_create)
+    int64_t pairMBBelow = 0;  // one wave of the lane-pair k_step with the ORCA_PAIR_MB register budget
     int binGrid = 0;          // k_bin blocks that are co-resident (cooperative launch limit)
     // strip rebalance: by-id active flags, all-gather records, fill reports
     uint8_t* activeBuf = nullptr;
@@ -676,7 +681,11 @@ void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     else if (variant == 3)  // work-unit LP2 (P:84-89 ablation)
         launch_k(c, k_step<DRY, 0, true>, dim3(blocks), dim3(kStepThreads), smem, a);
     else if (variant == 4 && spec && a.lp3Inline == 2)  // two lanes per agent, specialised (LM = 2)
-        launch_k(c, mono ? k_step<DRY, 0, false, true, 2, true> : k_step<DRY, 0, false, true, 2, false>,
+        launch_k(c,
+                 d.popBuild <= c->pairMBBelow
+                     ? (mono ? k_step<DRY, 0, false, true, 2, true, kStepThreads, ORCA_PAIR_MB>
+                             : k_step<DRY, 0, false, true, 2, false, kStepThreads, ORCA_PAIR_MB>)
+                     : (mono ? k_step<DRY, 0, false, true, 2, true> : k_step<DRY, 0, false, true, 2, false>),
                  dim3((d.capW + kStepThreads / 2 - 1) / (kStepThreads / 2)), dim3(kStepThreads), smem, a);
     else if (variant == 4)  // two lanes per agent: 64 agents per block
         launch_k(c, k_step<DRY, 0, false, true>, dim3((d.capW + kStepThreads / 2 - 1) / (kStepThreads / 2)),
@@ -1003,7 +1012,11 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
                              (const void*)k_step<false, 0, false, true, 2, false>,
                              (const void*)k_step<true, 0, false, true, 2, false>,
                              (const void*)k_step<false, 0, false, true, 2, true>,
-                             (const void*)k_step<true, 0, false, true, 2, true>};
+                             (const void*)k_step<true, 0, false, true, 2, true>,
+                             (const void*)k_step<false, 0, false, true, 2, false, kStepThreads, ORCA_PAIR_MB>,
+                             (const void*)k_step<true, 0, false, true, 2, false, kStepThreads, ORCA_PAIR_MB>,
+                             (const void*)k_step<false, 0, false, true, 2, true, kStepThreads, ORCA_PAIR_MB>,
+                             (const void*)k_step<true, 0, false, true, 2, true, kStepThreads, ORCA_PAIR_MB>};
     const void* stepFnsBQ[] = {(const void*)k_step<false, 0, false, false, 2, false, kStepBQ>,
                                (const void*)k_step<true, 0, false, false, 2, false, kStepBQ>,
                                (const void*)k_step<false, 0, false, false, 2, true, kStepBQ>,
@@ -1046,6 +1059,11 @@ orca_status ctx_init(const orca_params* params, int32_t device, orca_ctx** out, 
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step<false, 0, false, false, 2, true, kStepBQ, 3>,
                                                               kStepBQ, smemBQ);
         c->bq3Below = (int64_t)blocks * sms * kStepBQ;
+        // the lane-pair kernel with a larger register budget while a strip fits one wave of it
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &blocks, k_step<false, 0, false, true, 2, true, kStepThreads, ORCA_PAIR_MB>, kStepThreads, smemInl);
+        c->pairMBBelow = ORCA_PAIR_MB > 0 ? (int64_t)blocks * sms * (kStepThreads / 2) : 0;
         if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_bin, kBinThreads, 0);
         c->binGrid = std::min(kBinMaxGrid, blocks * sms);
     }
