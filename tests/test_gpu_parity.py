@@ -595,6 +595,42 @@ def test_variants_bit_identical(orca, config, n, rho, order):
         o.close()
 
 
+@pytest.mark.parametrize("n,het", [(170000, False), (170000, True), (100000, False), (60000, False)])
+def test_specialised_kernels_bit_identical(orca, n, het):
+    """The default configurations run k_step instantiations compiled for them (DESIGN.md §10,
+    r02ai-au): LP3 placement fixed (k_lp3 above one wave, the block queue below it, 256-thread
+    blocks with an 85-register budget while one wave of those fits), one homogeneous strip
+    (MONO), the lane pair with its own register budget.  Each must equal the general kernels --
+    variant 2 (register top-k list) and variant 3 (work-unit template, greedy order) run the
+    general instantiation -- in dry-step velocities, flags and lists and in 12 real steps (state
+    and statistics), with per-agent properties too (the non-MONO specialisation)."""
+    w = W.make("uniform", n=n)
+    ctxs = []
+    for v in (-1, 2, 3):
+        o, _ = _ctx(orca, w)
+        o.set_variant(v)
+        if het:
+            props = _het_props(n, seed=9)
+            o.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
+        ctxs.append(o)
+    r = [o.debug_step() for o in ctxs]
+    assert np.count_nonzero(r[0][1] & 1) > 0  # infeasible agents: the LP3 placement is exercised
+    for q in (1, 2):
+        assert np.array_equal(r[0][0], r[q][0]), q  # velocities
+        assert np.array_equal(r[0][2], r[q][2]) and np.array_equal(r[0][3], r[q][3]), q  # lists
+        assert np.array_equal(r[0][1] & 1, r[q][1] & 1), q  # infeasible
+    assert np.array_equal(r[0][1], r[2][1])  # every flag (the same half-plane and LP code)
+    for o in ctxs:
+        o.step(12)
+    s = [o.get_state() for o in ctxs]
+    st = [o.stats() for o in ctxs]
+    for q in (1, 2):
+        assert np.array_equal(s[0][0], s[q][0]) and np.array_equal(s[0][1], s[q][1]), q
+        assert st[0] == st[q], q
+    for o in ctxs:
+        o.close()
+
+
 # ---------------------------------------------------- goals + removal (P:110, §8(f1))
 def test_removal_one_step_vs_oracle(orca, oracle):
     """After one step an agent is removed iff its new position is strictly within R of its
