@@ -450,6 +450,7 @@ def run_ours(args):
     st = ctx.stats()
     st["maintenance_in_timed_region"] = {k: st[k] - maint0[k] for k in ("rebalances", "regrids")}
     launch_info = ctx.launch_info()  # kernels per step as launched in the timed region
+    kernel_config = ctx.kernel_config()  # the step-kernel instantiation of the timed region
     ms_per_step = ms / args.steps
     value = n_total * args.steps / (ms / 1000.0)
 
@@ -701,6 +702,7 @@ def run_ours(args):
         # per step: k_step, k_lp3, k_scan, k_scatter (+ strips: k_receive and one k_push per
         # neighbour with the peer-memory exchange)
         "gpu_launches": launch_info["kernels_per_step"] * args.steps, "launch_info": launch_info,
+        "kernel_config": kernel_config,
         "kernel_variant": args.variant, "k_step_ms_by_variant": variant_ms, "k_step_ms_by_lp_order": order_ms,
         "lp3_lanes": args.lp3_lanes, "k_step_ms_by_lp3_lanes": lp3_ms,
         "roofline": roofline, "hbm_context": hbm, "comm": comm,

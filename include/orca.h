@@ -388,6 +388,17 @@ orca_status orca_get_transport(orca_ctx *ctx, int32_t *mode);
  * Errors: INVALID_ARGUMENT, NOT_READY. */
 orca_status orca_get_launch_info(orca_ctx *ctx, int32_t info[4]);
 
+/* The step-kernel instantiation the first strip runs (DESIGN.md §10, §12 r02ai-au): cfg[0] =
+ * kernel variant (0 thread per agent with the shared-memory top-k list, 1 8-lane group, 2
+ * register list, 3 work-unit LP2, 4 lane pair), cfg[1] = LP3 placement (0 k_lp3 kernel, 1 per
+ * thread inside the step kernel, 2 the step kernel's block queue), cfg[2] = -1 for the general
+ * instantiation, else the LP3 placement it is compiled for (0 or 2; greedy LP order), cfg[3] = 1
+ * if compiled for one strip of homogeneous agents, cfg[4] = threads per block, cfg[5] = the
+ * blocks per SM its register budget is sized for (0: 1024 threads per SM, 64 registers).
+ * Informational: every configuration gives the same results bit for bit.
+ * Errors: INVALID_ARGUMENT, NOT_READY. */
+orca_status orca_get_kernel_config(orca_ctx *ctx, int32_t cfg[6]);
+
 /* Owned column ranges of the strips held by this context: bounds int32[2 * strips held]
  * = (c0, c1) pairs.  Errors: INVALID_ARGUMENT, NOT_READY. */
 orca_status orca_get_strips(orca_ctx *ctx, int32_t *bounds);

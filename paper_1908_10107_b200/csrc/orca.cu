@@ -659,49 +659,75 @@ void launch_lp3(orca_ctx* c, Domain& d, StepArgs& a) {
     }
 }
 
-// fused step kernel of the selected variant (same results bit for bit)
+// The k_step instantiation a strip runs (one source of truth for launch_step and
+// orca_get_kernel_config): the default configurations -- greedy LP order, LP3 in k_lp3 (LM 0) or
+// on the block queue (LM 2), one strip of homogeneous agents (mono) -- run kernels compiled for
+// exactly that case, with their block size and register budget (min blocks per SM) chosen by the
+// strip's size (DESIGN.md §10, §12 r02ai-au); everything else runs the general instantiation.
+struct StepKernelCfg {
+    int variant;  // 0 thread per agent (shared-memory list), 1 8-lane group, 2 register list, 3 work units, 4 lane pair
+    int lm;       // -1 general; 0 / 2: compiled for that LP3 placement and the greedy order
+    int mono;     // compiled for one strip of homogeneous agents
+    int threads;  // threads per block
+    int mb;       // min blocks per SM of the register budget (0: 1024 threads per SM)
+};
+StepKernelCfg step_kernel_cfg(const orca_ctx* c, const Domain& d, const StepArgs& a) {
+    const int k = c->p.maxNeighbors;
+    const int v = pick_variant(c, d);
+    const bool spec = a.m.lpGreedy && !a.m.lpRandom;
+    const int mono = (!a.g.hasL && !a.g.hasR && !a.propS) ? 1 : 0;
+    if (v == 1) return {1, -1, 0, kGroupThreads, 0};
+    if (v == 3) return {3, -1, 0, kStepThreads, 0};
+    if (v == 4) {
+        if (spec && a.lp3Inline == 2) return {4, 2, mono, kStepThreads, d.popBuild <= c->pairMBBelow ? ORCA_PAIR_MB : 0};
+        return {4, -1, 0, kStepThreads, 0};
+    }
+    const bool shared = v != 2 || k < 1 || k > 16;
+    if (shared && spec && a.lp3Inline == 0) return {0, 0, mono, kStepThreads, ORCA_LM0_MB};
+    if (shared && spec && a.lp3Inline == 2) return {0, 2, mono, kStepBQ, d.popBuild <= c->bq3Below ? 3 : 0};
+    return {shared ? 0 : 2, -1, 0, kStepThreads, 0};
+}
+
+// fused step kernel of the selected configuration (same results bit for bit)
 template <bool DRY>
 void launch_step(orca_ctx* c, Domain& d, StepArgs& a) {
     const int blocks = (d.capW + kStepThreads - 1) / kStepThreads;
     const int k = c->p.maxNeighbors;
-    const int variant = pick_variant(c, d);
+    const StepKernelCfg kc = step_kernel_cfg(c, d, a);
     // per-thread inline LP3 (mode 1) needs the projected half-planes: 3k more words per thread
     // after the columns; the block queue (mode 2) only its small scratch area
     const size_t smem = (size_t)c->smemBytes +
                         (a.lp3Inline == 1   ? (size_t)3 * k * 4 * kStepThreads
                          : a.lp3Inline == 2 ? (size_t)step_lp3q_scratch_bytes(k)
                                             : 0);
-    // the default configurations run kernels compiled for them (k_step's LM / MONO): the greedy
-    // LP order, LP3 in k_lp3 or on the block queue, and (mono) one strip of homogeneous agents
-    const bool spec = a.m.lpGreedy && !a.m.lpRandom;
-    const bool mono = !a.g.hasL && !a.g.hasR && !a.propS;
-    if (variant == 1)  // 8-lane group per agent
+    const bool mono = kc.mono != 0;
+    if (kc.variant == 1)  // 8-lane group per agent
         launch_k(c, k_step_group<DRY>, dim3((d.capW + kGroupAgents - 1) / kGroupAgents), dim3(kGroupThreads),
                  (size_t)c->groupSmem, a);
-    else if (variant == 3)  // work-unit LP2 (P:84-89 ablation)
+    else if (kc.variant == 3)  // work-unit LP2 (P:84-89 ablation)
         launch_k(c, k_step<DRY, 0, true>, dim3(blocks), dim3(kStepThreads), smem, a);
-    else if (variant == 4 && spec && a.lp3Inline == 2)  // two lanes per agent, specialised (LM = 2)
+    else if (kc.variant == 4 && kc.lm == 2)  // two lanes per agent, specialised (LM = 2)
         launch_k(c,
-                 d.popBuild <= c->pairMBBelow
+                 kc.mb == ORCA_PAIR_MB && kc.mb > 0
                      ? (mono ? k_step<DRY, 0, false, true, 2, true, kStepThreads, ORCA_PAIR_MB>
                              : k_step<DRY, 0, false, true, 2, false, kStepThreads, ORCA_PAIR_MB>)
                      : (mono ? k_step<DRY, 0, false, true, 2, true> : k_step<DRY, 0, false, true, 2, false>),
                  dim3((d.capW + kStepThreads / 2 - 1) / (kStepThreads / 2)), dim3(kStepThreads), smem, a);
-    else if (variant == 4)  // two lanes per agent: 64 agents per block
+    else if (kc.variant == 4)  // two lanes per agent: 64 agents per block
         launch_k(c, k_step<DRY, 0, false, true>, dim3((d.capW + kStepThreads / 2 - 1) / (kStepThreads / 2)),
                  dim3(kStepThreads), smem, a);
-    else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 0)  // specialised: LM = 0
+    else if (kc.lm == 0)  // specialised: LM = 0
         launch_k(c, mono ? k_step<DRY, 0, false, false, 0, true, kStepThreads, ORCA_LM0_MB>
                          : k_step<DRY, 0, false, false, 0, false, kStepThreads, ORCA_LM0_MB>,
                  dim3(blocks), dim3(kStepThreads), smem, a);
-    else if ((variant != 2 || k < 1 || k > 16) && spec && a.lp3Inline == 2)  // specialised: LM = 2, 256 threads
+    else if (kc.lm == 2)  // specialised: LM = 2, 256 threads
         launch_k(c,
-                 d.popBuild <= c->bq3Below
+                 kc.mb == 3
                      ? (mono ? k_step<DRY, 0, false, false, 2, true, kStepBQ, 3> : k_step<DRY, 0, false, false, 2, false, kStepBQ, 3>)
                      : (mono ? k_step<DRY, 0, false, false, 2, true, kStepBQ> : k_step<DRY, 0, false, false, 2, false, kStepBQ>),
                  dim3((d.capW + kStepBQ - 1) / kStepBQ), dim3(kStepBQ),
                  (size_t)step_smem_per_thread(k) * kStepBQ + (size_t)step_lp3q_scratch_bytes(k), a);
-    else if (variant != 2 || k < 1 || k > 16)  // shared-memory top-k list (any k)
+    else if (kc.variant == 0)  // shared-memory top-k list (any k)
         launch_k(c, k_step<DRY, 0, false>, dim3(blocks), dim3(kStepThreads), smem, a);
     else if (k <= 10)  // register top-k list
         launch_k(c, k_step<DRY, 10, false>, dim3(blocks), dim3(kStepThreads), smem, a);
@@ -2517,6 +2543,21 @@ orca_status orca_get_launch_info(orca_ctx* c, int32_t info[4]) {
     info[1] = pick_lp3_inline(c, d) ? 0 : pick_lp3_lanes(c, d);
     info[2] = n;
     info[3] = c->transport;
+    return ORCA_OK;
+}
+
+orca_status orca_get_kernel_config(orca_ctx* c, int32_t cfg[6]) {
+    if (!c || !cfg) return fail(ORCA_ERR_INVALID_ARGUMENT, "null argument");
+    if (!c->ready || c->doms.empty()) return fail(ORCA_ERR_NOT_READY, "set_agents first");
+    Domain& d = c->doms[0];
+    const StepArgs a = make_args(c, d);
+    const StepKernelCfg kc = step_kernel_cfg(c, d, a);
+    cfg[0] = kc.variant;
+    cfg[1] = a.lp3Inline;
+    cfg[2] = kc.lm;
+    cfg[3] = kc.mono;
+    cfg[4] = kc.threads;
+    cfg[5] = kc.mb;
     return ORCA_OK;
 }
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "orca_set_goal_removal", "orca_get_active", "orca_set_agent_props", "orca_step_trace",
     "orca_set_lp_order", "orca_set_lp3_lanes", "orca_set_lp3_inline", "orca_set_overlap", "orca_rebalance", "orca_set_transport",
     "orca_get_transport", "orca_set_state", "orca_set_state_async", "orca_get_state_async",
-    "orca_io_wait", "orca_step_io_async", "orca_get_launch_info", "orca_probe_alu", "orca_get_comm_info",
+    "orca_io_wait", "orca_step_io_async", "orca_get_launch_info", "orca_get_kernel_config", "orca_probe_alu", "orca_get_comm_info",
 ]
 
 
@@ -106,6 +106,7 @@ def _load():
         "orca_get_state_async": [vp, vp, vp],
         "orca_io_wait": [vp],
         "orca_get_launch_info": [vp, P(i32)],
+        "orca_get_kernel_config": [vp, P(i32)],
         "orca_probe_alu": [i32, P(ctypes.c_double)],
         "orca_get_comm_info": [vp, P(i32)],
     }
@@ -375,6 +376,13 @@ class Orca:
         out = (ctypes.c_int32 * 4)()
         _check(_lib.orca_get_launch_info(self._ctx, out))
         return dict(variant=out[0], lp3_lanes=out[1], kernels_per_step=out[2], transport=out[3])
+
+    def kernel_config(self) -> dict:
+        """orca_get_kernel_config: the step-kernel instantiation the first strip runs."""
+        out = (ctypes.c_int32 * 6)()
+        _check(_lib.orca_get_kernel_config(self._ctx, out))
+        return dict(variant=out[0], lp3_placement=out[1], compiled_for_lp3=out[2], mono=out[3],
+                    threads=out[4], min_blocks_per_sm=out[5])
 
     def comm_info(self) -> dict:
         """orca_get_comm_info: world, rank and the rank count of liborca's NCCL communicator."""

@@ -613,6 +613,13 @@ def test_specialised_kernels_bit_identical(orca, n, het):
             props = _het_props(n, seed=9)
             o.set_agent_props(props["radius"], props["maxSpeed"], props["prefSpeed"])
         ctxs.append(o)
+    kc = [o.kernel_config() for o in ctxs]
+    exp = {170000: dict(variant=0, lp3_placement=0, compiled_for_lp3=0, threads=128),
+           100000: dict(variant=0, lp3_placement=2, compiled_for_lp3=2, threads=256, min_blocks_per_sm=3),
+           60000: dict(variant=4, lp3_placement=2, compiled_for_lp3=2, threads=128, min_blocks_per_sm=6)}[n]
+    assert {q: kc[0][q] for q in exp} == exp, kc[0]
+    assert kc[0]["mono"] == (0 if het else 1)
+    assert kc[1]["compiled_for_lp3"] == -1 and kc[2]["compiled_for_lp3"] == -1  # the general kernels
     r = [o.debug_step() for o in ctxs]
     assert np.count_nonzero(r[0][1] & 1) > 0  # infeasible agents: the LP3 placement is exercised
     for q in (1, 2):
